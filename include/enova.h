@@ -1,0 +1,191 @@
+/*
+ * enova.h -- C ABI of the B200-native ENOVA performance-detection hot path.
+ *
+ * ENOVA (arXiv 2407.09486) detects anomalous service performance with a VAE
+ * over normalised monitoring metrics, scores each input by the KL divergence
+ * of the posterior from the prior, sets the anomaly threshold with the
+ * peaks-over-threshold (POT) method, and uses the Mean Difference (MD) between
+ * the input and its reconstruction to decide scale-up vs scale-down
+ * (PAPER.md:282-297).  This library runs that path over a fleet's metric
+ * tensor [instances x T x M] with sliding windows of length W.
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R-n = reading n in
+ * DESIGN.md (where the paper is silent or ambiguous).
+ *
+ * Conventions (every entry point):
+ *  - All tensors are caller-owned.  Pointers documented "device" must be CUDA
+ *    device pointers on the current device; "host" pointers are host memory.
+ *    The library never allocates device memory on the hot path; scratch lives
+ *    in caller-provided workspaces sized by the *_workspace_bytes functions
+ *    (256-byte aligned; one workspace per concurrent stream).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    score/detect/stats/ring_push are stream-ordered and asynchronous;
+ *    enova_compute_stats synchronises only to return n_degenerate;
+ *    enova_fit_threshold is synchronous and returns with *out filled.
+ *  - Argument and shape errors are detected before any launch; outputs are
+ *    then untouched.  Sticky CUDA / NCCL errors surface as ENOVA_ERR_CUDA /
+ *    ENOVA_ERR_NCCL; enova_last_error() returns a thread-local detail string.
+ *    No C++ exception crosses the ABI.
+ *  - Fast-path envelope (else ENOVA_ERR_UNSUPPORTED, there is no fallback):
+ *    M == 8 or M % 16 == 0 (M <= 64); W even, 2 <= W <= 256; H in {32, 64, 128};
+ *    1 <= Z <= 16.
+ *  - Precision is part of the contract (R-17): the detector is defined on fp16
+ *    tensor-core operands.  enc_w1, enc_wmu, enc_wlv and dec_w1 are rounded to
+ *    fp16 (RNE) by enova_prepare_detector; the normalised input is
+ *    x = fp16_RNE(clamp(fp32((fp32(X - mean)) / std), +-1e4)).  Everything after
+ *    that is carried with fp32 accumulation (h and mu as hi+lo fp16 pairs).
+ */
+#ifndef ENOVA_H_
+#define ENOVA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENOVA_ABI_VERSION 1
+
+typedef enum {
+  ENOVA_OK = 0,
+  ENOVA_ERR_INVALID_ARGUMENT = 1,   /* null pointer, bad size, misalignment          */
+  ENOVA_ERR_UNSUPPORTED = 2,        /* shape outside the fast-path envelope           */
+  ENOVA_ERR_INSUFFICIENT_HISTORY = 3, /* T < W, or a window range needs t < W-1 */
+  ENOVA_ERR_TOO_FEW_EXCEEDANCES = 4,  /* fewer than 10 POT peaks       */
+  ENOVA_ERR_NONFINITE = 5,          /* NaN/Inf in the calibration horizon (R-18)       */
+  ENOVA_ERR_UNCALIBRATED = 6,       /* threshold missing or not finite         */
+  ENOVA_ERR_CUDA = 7,
+  ENOVA_ERR_NCCL = 8,
+  ENOVA_ERR_WORKSPACE = 9           /* workspace too small or misaligned               */
+} enova_status;
+
+/* Detector parameters (VAE; topology S:547, R-5).  Device pointers,
+ * fp32, row-major [out][in], read-only.  D = window * n_metrics, flattened
+ * time-major k = tau*M + j with tau = 0 the oldest sample of the window (R-1). */
+typedef struct {
+  int32_t window, n_metrics, hidden, latent;   /* W, M, H, Z                    */
+  const float *enc_w1, *enc_b1;    /* [H][D], [H]      encoder hidden layer    */
+  const float *enc_wmu, *enc_bmu;  /* [Z][H], [Z]      posterior mean head     */
+  const float *enc_wlv, *enc_blv;  /* [Z][H], [Z]      posterior log-variance  */
+  const float *dec_w1, *dec_b1;    /* [H][Z], [H]      decoder hidden layer    */
+  const float *dec_w2, *dec_b2;    /* [D][H], [D]      linear output m'        */
+} enova_detector;
+
+/* A fleet's metric tensor and the window range to score.
+ * metrics: device fp32, instance i occupies [i*ld_instance, i*ld_instance + T*M),
+ * row-major [T][M]; 16-byte aligned, ld_instance % 4 == 0, ld_instance >= T*M.
+ * Windows ENDING at t in [t_begin, t_end) are scored (window = samples
+ * t-W+1 .. t, R-2); requires W-1 <= t_begin <= t_end <= T.
+ * Per-window outputs are laid out [N][t_end - t_begin] (index t - t_begin).
+ * norm_mean / norm_std: device fp32 [N][M] from enova_compute_stats over the
+ * calibration horizon, frozen for detection and streaming (R-4);
+ * REQUIRED by score/detect. */
+typedef struct {
+  const float *metrics;
+  int64_t n_instances, n_steps, ld_instance;
+  int64_t t_begin, t_end;
+  const float *norm_mean, *norm_std;
+  int32_t n_metrics, reserved;     /* M; must equal detector.n_metrics */
+} enova_series;
+
+/* POT threshold (P:297 citing Siffer et al. 2017, R-11..R-13).
+ * t = initial threshold (order statistic), (gamma, sigma) = GPD MLE of the
+ * peaks, z_q = final threshold at risk q, n = scores used, n_peaks = N_t,
+ * method 0 = GPD root (gamma != 0), 1 = exponential candidate (gamma == 0). */
+typedef struct {
+  double init_quantile, risk_q, t, gamma, sigma, z_q;
+  int64_t n, n_peaks;
+  int32_t method, reserved;
+} enova_threshold;
+
+typedef struct enova_comm_s *enova_comm_t;
+
+/* ---------------------------------------------------------------- K0 ----
+ * Bytes of the prepared-detector image (fp16 canonical UMMA operand images of
+ * W1, [Wmu|Wlv], W3; fp32 biases; w_bar = 1^T W_dec2 and b_bar = sum b_dec2
+ * accumulated in fp64).  0 if the detector is outside the envelope. */
+size_t enova_detector_workspace_bytes(const enova_detector *det);
+
+/* Build the prepared-detector image into det_ws (device, caller-owned, must
+ * stay alive and unmodified while score/detect use it).  Asynchronous. */
+enova_status enova_prepare_detector(const enova_detector *det, void *det_ws,
+                                    size_t det_ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------- a-1 ----
+ * Per-(instance, metric) mean and population std over samples [0, t_cal_end)
+ * ("input metrics are normalized prior"; R-4), accumulated in
+ * fp64 and rounded to fp32; std floored at 1e-6.  mean/std: device fp32 [N][M].
+ * *n_degenerate (host, may be NULL): series whose std was floored.
+ * Reads series->metrics / n_instances / n_steps / ld_instance / n_metrics only.
+ * Returns ENOVA_ERR_NONFINITE if any sample in the horizon is NaN/Inf (R-18);
+ * synchronises the stream. */
+size_t enova_stats_workspace_bytes(int64_t n_instances, int32_t n_metrics);
+enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, float *mean, float *std,
+                                 int64_t *n_degenerate, void *ws, size_t ws_bytes,
+                                 void *stream);
+
+/* ------------------------------------------------------------ a-2..a-5 ----
+ * KL score (R-6) and MD (R-8) of every window in
+ * the series range.  scores, md: device fp32 [N][t_end - t_begin] (md may be
+ * NULL).  det_ws: the image from enova_prepare_detector for `det`. */
+enova_status enova_score_windows(const enova_series *series, const enova_detector *det,
+                                 const void *det_ws, size_t det_ws_bytes,
+                                 float *scores, float *md, void *stream);
+
+/* ------------------------------------------------------------ a-7..a-9 ----
+ * Fleet-wide POT threshold over calibration scores.  scores: device fp32
+ * [n_local] (this rank's shard).  comm == NULL: single GPU.  With a comm, all
+ * ranks call collectively; integer histograms are all-reduced and score tails
+ * all-gathered in rank order, so *out is bit-identical on every rank and for
+ * every world size.  n_global_max bounds sum(n_local) over ranks and must be
+ * the value the workspace was sized with.  out: host.  Synchronous.
+ * ENOVA_ERR_TOO_FEW_EXCEEDANCES if fewer than 10 scores exceed t. */
+size_t enova_threshold_workspace_bytes(int64_t n_global_max, double init_quantile);
+enova_status enova_fit_threshold(const float *scores, int64_t n_local, int64_t n_global_max,
+                                 double init_quantile, double risk_q, enova_comm_t comm,
+                                 enova_threshold *out, void *ws, size_t ws_bytes,
+                                 void *stream);
+
+/* ------------------------------------------------------------ a-2..a-6 ----
+ * Score every window of the series range and flag it ("An anomaly is
+ * detected if the KL-divergence ... exceeds this threshold", MD decides
+ * "scale up or down", R-9, R-10):
+ *   flag = 0 if score <= z_q; +1 (scale up) if MD >= 0; -1 (scale down) otherwise.
+ * flags: device int8 [N][t_end - t_begin]; scores_opt / md_opt may be NULL.
+ * thr: host; ENOVA_ERR_UNCALIBRATED if thr is NULL or z_q is not finite. */
+enova_status enova_detect(const enova_series *series, const enova_detector *det,
+                          const void *det_ws, size_t det_ws_bytes,
+                          const enova_threshold *thr, int8_t *flags,
+                          float *scores_opt, float *md_opt, void *stream);
+
+/* ----------------------------------------------------------------- a-10 ----
+ * Streaming ("executed in streaming computing framework"): a mirror
+ * ring of 2W samples per instance, device fp32 [N][2W][M].  enova_ring_push
+ * writes sample[N][M] (device) for tick `tick` at ring slots (tick mod W) and
+ * (tick mod W) + W.  After the push of tick k >= W-1, the window ending at
+ * tick k is the contiguous view ring + ((k+1) mod W)*M with ld_instance =
+ * 2*W*M, n_steps = W, t_begin = W-1, t_end = W: pass it to enova_detect. */
+enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window,
+                             int32_t n_metrics, const float *sample, int64_t tick,
+                             void *stream);
+
+/* ------------------------------------------------------------ comm (§8e) ----
+ * NCCL communicator for the fleet-wide threshold.  Rank 0 creates the 128-byte
+ * unique id; the caller broadcasts it (e.g. torch.distributed) and every rank
+ * calls enova_comm_create with its own device.  NCCL is loaded at run time
+ * (libnccl.so.2); ENOVA_ERR_NCCL if it is unavailable. */
+enova_status enova_comm_unique_id(void *out128);
+enova_status enova_comm_create(enova_comm_t *comm, int rank, int world, const void *id128,
+                               int device);
+void enova_comm_destroy(enova_comm_t comm);
+
+/* ------------------------------------------------------------- misc ---- */
+const char *enova_status_string(enova_status s);
+const char *enova_last_error(void);
+int enova_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENOVA_H_ */

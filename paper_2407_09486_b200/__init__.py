@@ -1,0 +1,18 @@
+"""B200-native ENOVA performance-detection hot path (arXiv 2407.09486).
+
+Public API (thin binding over libenova.so, include/enova.h):
+  PreparedDetector, compute_stats, score_windows, fit_threshold, detect,
+  ring_push, ring_view, Comm, ThresholdWorkspace, run_pipeline.
+Seeded synthetic inputs live in ``paper_2407_09486_b200.synth``.
+"""
+__all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold", "detect",
+           "ring_push", "ring_view", "Comm", "ThresholdWorkspace", "run_pipeline",
+           "EnovaError"]
+
+
+def __getattr__(name):
+    if name in __all__:
+        from . import api
+        from ._lib import EnovaError
+        return EnovaError if name == "EnovaError" else getattr(api, name)
+    raise AttributeError(name)

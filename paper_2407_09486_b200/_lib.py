@@ -1,0 +1,112 @@
+"""ctypes binding of libenova.so (include/enova.h).  Argument marshalling only:
+every step of the detection path runs in the library's CUDA kernels.  torch
+supplies device memory and streams.  There is no fallback: if the library is
+missing or the GPU is absent the calls raise."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libenova.so")
+
+ENOVA_OK = 0
+STATUS = {
+    0: "ENOVA_OK", 1: "ENOVA_ERR_INVALID_ARGUMENT", 2: "ENOVA_ERR_UNSUPPORTED",
+    3: "ENOVA_ERR_INSUFFICIENT_HISTORY", 4: "ENOVA_ERR_TOO_FEW_EXCEEDANCES",
+    5: "ENOVA_ERR_NONFINITE", 6: "ENOVA_ERR_UNCALIBRATED", 7: "ENOVA_ERR_CUDA",
+    8: "ENOVA_ERR_NCCL", 9: "ENOVA_ERR_WORKSPACE",
+}
+
+# every symbol include/enova.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "enova_detector_workspace_bytes", "enova_prepare_detector", "enova_stats_workspace_bytes",
+    "enova_compute_stats", "enova_score_windows", "enova_threshold_workspace_bytes",
+    "enova_fit_threshold", "enova_detect", "enova_ring_push", "enova_comm_unique_id",
+    "enova_comm_create", "enova_comm_destroy", "enova_status_string", "enova_last_error",
+    "enova_abi_version",
+)
+
+
+class EnovaError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {detail}")
+
+
+class Detector(C.Structure):
+    _fields_ = [("window", C.c_int32), ("n_metrics", C.c_int32), ("hidden", C.c_int32),
+                ("latent", C.c_int32),
+                ("enc_w1", C.c_void_p), ("enc_b1", C.c_void_p),
+                ("enc_wmu", C.c_void_p), ("enc_bmu", C.c_void_p),
+                ("enc_wlv", C.c_void_p), ("enc_blv", C.c_void_p),
+                ("dec_w1", C.c_void_p), ("dec_b1", C.c_void_p),
+                ("dec_w2", C.c_void_p), ("dec_b2", C.c_void_p)]
+
+
+class Series(C.Structure):
+    _fields_ = [("metrics", C.c_void_p), ("n_instances", C.c_int64), ("n_steps", C.c_int64),
+                ("ld_instance", C.c_int64), ("t_begin", C.c_int64), ("t_end", C.c_int64),
+                ("norm_mean", C.c_void_p), ("norm_std", C.c_void_p),
+                ("n_metrics", C.c_int32), ("reserved", C.c_int32)]
+
+
+class Threshold(C.Structure):
+    _fields_ = [("init_quantile", C.c_double), ("risk_q", C.c_double), ("t", C.c_double),
+                ("gamma", C.c_double), ("sigma", C.c_double), ("z_q", C.c_double),
+                ("n", C.c_int64), ("n_peaks", C.c_int64), ("method", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load libenova.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(python -m paper_2407_09486_b200.build)")
+        L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        vp, i64, i32, dbl, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_size_t
+        P = C.POINTER
+        sig = {
+            "enova_detector_workspace_bytes": (sz, [P(Detector)]),
+            "enova_prepare_detector": (C.c_int, [P(Detector), vp, sz, vp]),
+            "enova_stats_workspace_bytes": (sz, [i64, i32]),
+            "enova_compute_stats": (C.c_int, [P(Series), i64, vp, vp, P(i64), vp, sz, vp]),
+            "enova_score_windows": (C.c_int, [P(Series), P(Detector), vp, sz, vp, vp, vp]),
+            "enova_threshold_workspace_bytes": (sz, [i64, dbl]),
+            "enova_fit_threshold": (C.c_int, [vp, i64, i64, dbl, dbl, vp, P(Threshold), vp, sz, vp]),
+            "enova_detect": (C.c_int, [P(Series), P(Detector), vp, sz, P(Threshold), vp, vp, vp, vp]),
+            "enova_ring_push": (C.c_int, [vp, i64, i32, i32, vp, i64, vp]),
+            "enova_comm_unique_id": (C.c_int, [vp]),
+            "enova_comm_create": (C.c_int, [P(vp), C.c_int, C.c_int, vp, C.c_int]),
+            "enova_comm_destroy": (None, [vp]),
+            "enova_status_string": (C.c_char_p, [C.c_int]),
+            "enova_last_error": (C.c_char_p, []),
+            "enova_abi_version": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+        return _lib
+
+
+def check(status: int) -> None:
+    if status != ENOVA_OK:
+        detail = lib().enova_last_error()
+        raise EnovaError(status, detail.decode() if detail else "")

@@ -1,0 +1,252 @@
+"""Python surface of the ENOVA detection hot path (same names as the C ABI in
+include/enova.h).  Tensors are CUDA fp32; torch provides memory, streams and
+process groups; libenova.so does all the work."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Detector, Series, Threshold, check, lib
+
+_WEIGHT_KEYS = ("enc_w1", "enc_b1", "enc_wmu", "enc_bmu", "enc_wlv", "enc_blv",
+                "dec_w1", "dec_b1", "dec_w2", "dec_b2")
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(t: torch.Tensor, name: str, dtype=torch.float32):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}")
+
+
+class PreparedDetector:
+    """Detector weights on the GPU plus their prepared fp16 operand image (K0)."""
+
+    def __init__(self, weights: dict, device=None, stream=None):
+        device = torch.device(device or "cuda")
+        self.window = int(weights["window"])
+        self.n_metrics = int(weights["n_metrics"])
+        self.hidden = int(weights["hidden"])
+        self.latent = int(weights["latent"])
+        self.tensors = {}
+        for k in _WEIGHT_KEYS:
+            v = weights[k]
+            if isinstance(v, np.ndarray):
+                v = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32))
+            self.tensors[k] = v.to(device=device, dtype=torch.float32).contiguous()
+        self.struct = Detector(self.window, self.n_metrics, self.hidden, self.latent,
+                               *[self.tensors[k].data_ptr() for k in _WEIGHT_KEYS])
+        self.ws_bytes = int(lib().enova_detector_workspace_bytes(C.byref(self.struct)))
+        if self.ws_bytes == 0:
+            raise _lib.EnovaError(2, "detector shape outside the fast-path envelope")
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        check(lib().enova_prepare_detector(C.byref(self.struct), C.c_void_p(self.ws.data_ptr()),
+                                           self.ws_bytes, _stream_ptr(stream)))
+
+
+def _series(metrics: torch.Tensor, mean=None, std=None, t_begin=0, t_end=0) -> Series:
+    _require_cuda(metrics, "metrics")
+    if metrics.dim() != 3:
+        raise ValueError("metrics must be [instances, T, M]")
+    N, T, M = metrics.shape
+    if metrics.stride(2) != 1 or metrics.stride(1) != M:
+        raise ValueError("metrics rows must be contiguous [T][M] per instance")
+    ld = metrics.stride(0) if N > 1 else T * M
+    s = Series(metrics.data_ptr(), N, T, ld, int(t_begin), int(t_end),
+               mean.data_ptr() if mean is not None else None,
+               std.data_ptr() if std is not None else None, M, 0)
+    return s
+
+
+def compute_stats(metrics: torch.Tensor, t_cal_end: int, stream=None):
+    """a-1: per-(instance, metric) mean / std over [0, t_cal_end)."""
+    N, T, M = metrics.shape
+    s = _series(metrics)
+    mean = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+    std = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+    nb = int(lib().enova_stats_workspace_bytes(N, M))
+    ws = torch.empty(nb, dtype=torch.uint8, device=metrics.device)
+    ndeg = C.c_int64(0)
+    check(lib().enova_compute_stats(C.byref(s), int(t_cal_end), C.c_void_p(mean.data_ptr()),
+                                    C.c_void_p(std.data_ptr()), C.byref(ndeg),
+                                    C.c_void_p(ws.data_ptr()), nb, _stream_ptr(stream)))
+    return mean, std, int(ndeg.value)
+
+
+def score_windows(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tensor,
+                  std: torch.Tensor, t_begin: int | None = None, t_end: int | None = None,
+                  *, with_md: bool = True, out=None, stream=None):
+    """a-2..a-5: KL scores and MD of every window ending in [t_begin, t_end)."""
+    N, T, M = metrics.shape
+    tb = det.window - 1 if t_begin is None else int(t_begin)
+    te = T if t_end is None else int(t_end)
+    s = _series(metrics, mean, std, tb, te)
+    nw = max(te - tb, 0)
+    if out is None:
+        scores = torch.empty((N, nw), dtype=torch.float32, device=metrics.device)
+        md = torch.empty((N, nw), dtype=torch.float32, device=metrics.device) if with_md else None
+    else:
+        scores, md = out
+    check(lib().enova_score_windows(C.byref(s), C.byref(det.struct), C.c_void_p(det.ws.data_ptr()),
+                                    det.ws_bytes, C.c_void_p(scores.data_ptr()),
+                                    C.c_void_p(md.data_ptr() if md is not None else None),
+                                    _stream_ptr(stream)))
+    return scores, md
+
+
+class ThresholdWorkspace:
+    """Scratch for enova_fit_threshold, sized for up to n_global_max scores."""
+
+    def __init__(self, n_global_max: int, init_quantile: float = 0.98, device=None):
+        self.n_global_max = int(n_global_max)
+        self.init_quantile = float(init_quantile)
+        self.nbytes = int(lib().enova_threshold_workspace_bytes(self.n_global_max,
+                                                                self.init_quantile))
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device or "cuda")
+
+
+def fit_threshold(scores: torch.Tensor, init_quantile: float = 0.98, risk_q: float = 1e-3,
+                  comm: "Comm | None" = None, n_global_max: int | None = None,
+                  workspace: ThresholdWorkspace | None = None, stream=None) -> dict:
+    """a-7..a-9: fleet-wide POT threshold (synchronous; identical on all ranks)."""
+    _require_cuda(scores, "scores")
+    flat = scores.reshape(-1)
+    if not flat.is_contiguous():
+        flat = flat.contiguous()
+    n_local = flat.numel()
+    if workspace is None:
+        nmax = int(n_global_max if n_global_max is not None else
+                   n_local * (comm.world if comm is not None else 1))
+        workspace = ThresholdWorkspace(nmax, init_quantile, scores.device)
+    out = Threshold()
+    check(lib().enova_fit_threshold(C.c_void_p(flat.data_ptr()), n_local, workspace.n_global_max,
+                                    float(init_quantile), float(risk_q),
+                                    C.c_void_p(comm.handle if comm is not None else None),
+                                    C.byref(out), C.c_void_p(workspace.buf.data_ptr()),
+                                    workspace.nbytes, _stream_ptr(stream)))
+    return out.as_dict()
+
+
+def _thr_struct(thr: dict) -> Threshold:
+    t = Threshold()
+    for k, _ in Threshold._fields_:
+        if k in thr:
+            setattr(t, k, thr[k])
+    return t
+
+
+def detect(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tensor, std: torch.Tensor,
+           threshold: dict, t_begin: int | None = None, t_end: int | None = None, *,
+           return_scores: bool = False, out=None, stream=None):
+    """a-2..a-6: flags (+1 scale up / -1 scale down / 0) of every window."""
+    N, T, M = metrics.shape
+    tb = det.window - 1 if t_begin is None else int(t_begin)
+    te = T if t_end is None else int(t_end)
+    s = _series(metrics, mean, std, tb, te)
+    nw = max(te - tb, 0)
+    if out is None:
+        flags = torch.empty((N, nw), dtype=torch.int8, device=metrics.device)
+        sc = torch.empty((N, nw), dtype=torch.float32, device=metrics.device) if return_scores else None
+        md = torch.empty((N, nw), dtype=torch.float32, device=metrics.device) if return_scores else None
+    else:
+        flags, sc, md = out
+    thr = _thr_struct(threshold)
+    check(lib().enova_detect(C.byref(s), C.byref(det.struct), C.c_void_p(det.ws.data_ptr()),
+                             det.ws_bytes, C.byref(thr), C.c_void_p(flags.data_ptr()),
+                             C.c_void_p(sc.data_ptr() if sc is not None else None),
+                             C.c_void_p(md.data_ptr() if md is not None else None),
+                             _stream_ptr(stream)))
+    if return_scores:
+        return flags, sc, md
+    return flags
+
+
+def ring_push(ring: torch.Tensor, sample: torch.Tensor, tick: int, stream=None):
+    """a-10: append one sample per instance to the mirror ring [N][2W][M]."""
+    _require_cuda(ring, "ring")
+    _require_cuda(sample, "sample")
+    N, W2, M = ring.shape
+    check(lib().enova_ring_push(C.c_void_p(ring.data_ptr()), N, W2 // 2, M,
+                                C.c_void_p(sample.data_ptr()), int(tick), _stream_ptr(stream)))
+
+
+def ring_view(ring: torch.Tensor, tick: int) -> torch.Tensor:
+    """The W samples ending at `tick` as a [N, W, M] strided view of the ring."""
+    N, W2, M = ring.shape
+    W = W2 // 2
+    off = ((tick + 1) % W)
+    return ring.as_strided((N, W, M), (W2 * M, M, 1), ring.storage_offset() + off * M)
+
+
+class Comm:
+    """NCCL communicator for the fleet-wide threshold (one per rank)."""
+
+    def __init__(self, handle: int, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    @staticmethod
+    def create(rank: int, world: int, device: int, group=None) -> "Comm":
+        import torch.distributed as dist
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib().enova_comm_unique_id(buf))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.is_initialized() and world > 1:
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+                dist.broadcast(t, 0, group=group)
+                t = t.cpu()
+            else:
+                dist.broadcast(t, 0, group=group)
+        raw = (C.c_uint8 * 128)(*t.tolist())
+        h = C.c_void_p()
+        check(lib().enova_comm_create(C.byref(h), rank, world, raw, device))
+        return Comm(h.value, rank, world)
+
+    def destroy(self):
+        if self.handle:
+            lib().enova_comm_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+
+@dataclass
+class PipelineResult:
+    mean: torch.Tensor
+    std: torch.Tensor
+    n_degenerate: int
+    cal_scores: torch.Tensor
+    threshold: dict
+    flags: torch.Tensor
+    scores: torch.Tensor | None
+    md: torch.Tensor | None
+
+
+def run_pipeline(metrics: torch.Tensor, det: PreparedDetector, t_cal_end: int,
+                 init_quantile: float = 0.98, risk_q: float = 1e-3, comm: Comm | None = None,
+                 workspace: ThresholdWorkspace | None = None, return_scores: bool = True,
+                 stream=None) -> PipelineResult:
+    """One pass of the whole hot path: stats over [0, t_cal_end) -> scores of the
+    calibration windows (ending in [W-1, t_cal_end)) -> fleet-wide POT threshold
+    -> flags (and scores/MD) of the windows ending in [t_cal_end, T)."""
+    T = metrics.shape[1]
+    mean, std, nd = compute_stats(metrics, t_cal_end, stream)
+    cal, _ = score_windows(metrics, det, mean, std, det.window - 1, t_cal_end, with_md=False,
+                           stream=stream)
+    thr = fit_threshold(cal, init_quantile, risk_q, comm=comm, workspace=workspace, stream=stream)
+    res = detect(metrics, det, mean, std, thr, t_cal_end, T, return_scores=return_scores,
+                 stream=stream)
+    if return_scores:
+        flags, sc, md = res
+    else:
+        flags, sc, md = res, None, None
+    return PipelineResult(mean, std, nd, cal, thr, flags, sc, md)

@@ -1,0 +1,283 @@
+// abi.cu -- the C ABI of libenova (include/enova.h): argument validation,
+// workspace sizing and launch sequencing.  No allocation on the hot path.
+#include <math.h>
+
+#include <string>
+
+#include "comm.h"
+#include "common.cuh"
+#include "layout.h"
+
+namespace enova {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+enova_status cuda_status(cudaError_t e, const char *what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return ENOVA_ERR_CUDA;
+}
+
+enova_status prepare_detector(const enova_detector *det, const DetLayout &L, void *ws,
+                              cudaStream_t st);
+enova_status compute_stats(const enova_series *s, int64_t t_cal_end, float *mean, float *stdv,
+                           int64_t *n_degenerate, void *ws, cudaStream_t st);
+enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
+                          float *scores, float *md, int8_t *flags, double z_q, cudaStream_t st);
+enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
+                           enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
+                           int64_t n_global_max, cudaStream_t st);
+size_t threshold_workspace_bytes(int64_t n_max, double q0);
+enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
+                       cudaStream_t st);
+
+static inline bool aligned(const void *p, size_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+
+static enova_status check_detector(const enova_detector *det, DetLayout *L) {
+  if (!det) {
+    set_error("detector is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_layout(det->window, det->n_metrics, det->hidden, det->latent, L)) {
+    set_error("detector shape outside the fast-path envelope (M==8 or M%16==0<=64, W even "
+              "2..256, H in {32,64,128}, 1<=Z<=16)");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  return ENOVA_OK;
+}
+
+static enova_status check_det_ptrs(const enova_detector *d) {
+  if (!d->enc_w1 || !d->enc_b1 || !d->enc_wmu || !d->enc_bmu || !d->enc_wlv || !d->enc_blv ||
+      !d->dec_w1 || !d->dec_b1 || !d->dec_w2 || !d->dec_b2) {
+    set_error("detector weight pointer is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  return ENOVA_OK;
+}
+
+static enova_status check_series_base(const enova_series *s) {
+  if (!s || !s->metrics) {
+    set_error("series or series->metrics is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (s->n_instances < 0 || s->n_steps < 0 || s->n_metrics <= 0 || (s->n_metrics % 8) != 0) {
+    set_error("bad series sizes (n_metrics must be a positive multiple of 8)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (s->ld_instance < s->n_steps * (int64_t)s->n_metrics || (s->ld_instance % 4) != 0) {
+    set_error("ld_instance must be >= n_steps*n_metrics and a multiple of 4");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!aligned(s->metrics, 16)) {
+    set_error("metrics must be 16-byte aligned");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  return ENOVA_OK;
+}
+
+static enova_status check_series_windows(const enova_series *s, const DetLayout &L) {
+  enova_status r = check_series_base(s);
+  if (r) return r;
+  if (s->n_metrics != L.M) {
+    set_error("series n_metrics != detector n_metrics");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (s->n_steps < L.W) {
+    set_error("insufficient history: n_steps < window");
+    return ENOVA_ERR_INSUFFICIENT_HISTORY;
+  }
+  if (s->t_begin < L.W - 1) {
+    set_error("insufficient history: t_begin < window - 1");
+    return ENOVA_ERR_INSUFFICIENT_HISTORY;
+  }
+  if (s->t_end < s->t_begin || s->t_end > s->n_steps) {
+    set_error("window range must satisfy t_begin <= t_end <= n_steps");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!s->norm_mean || !s->norm_std || !aligned(s->norm_mean, 16) || !aligned(s->norm_std, 16)) {
+    set_error("norm_mean / norm_std are required and must be 16-byte aligned");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  return ENOVA_OK;
+}
+
+static enova_status sticky() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_status(e, "pending CUDA error");
+  return ENOVA_OK;
+}
+
+}  // namespace enova
+
+using namespace enova;
+
+extern "C" {
+
+int enova_abi_version(void) { return ENOVA_ABI_VERSION; }
+
+const char *enova_last_error(void) { return g_last_error.c_str(); }
+
+const char *enova_status_string(enova_status s) {
+  switch (s) {
+    case ENOVA_OK: return "ENOVA_OK";
+    case ENOVA_ERR_INVALID_ARGUMENT: return "ENOVA_ERR_INVALID_ARGUMENT";
+    case ENOVA_ERR_UNSUPPORTED: return "ENOVA_ERR_UNSUPPORTED";
+    case ENOVA_ERR_INSUFFICIENT_HISTORY: return "ENOVA_ERR_INSUFFICIENT_HISTORY";
+    case ENOVA_ERR_TOO_FEW_EXCEEDANCES: return "ENOVA_ERR_TOO_FEW_EXCEEDANCES";
+    case ENOVA_ERR_NONFINITE: return "ENOVA_ERR_NONFINITE";
+    case ENOVA_ERR_UNCALIBRATED: return "ENOVA_ERR_UNCALIBRATED";
+    case ENOVA_ERR_CUDA: return "ENOVA_ERR_CUDA";
+    case ENOVA_ERR_NCCL: return "ENOVA_ERR_NCCL";
+    case ENOVA_ERR_WORKSPACE: return "ENOVA_ERR_WORKSPACE";
+  }
+  return "ENOVA_ERR_UNKNOWN";
+}
+
+size_t enova_detector_workspace_bytes(const enova_detector *det) {
+  DetLayout L;
+  if (!det || !det_layout(det->window, det->n_metrics, det->hidden, det->latent, &L)) return 0;
+  return L.total;
+}
+
+enova_status enova_prepare_detector(const enova_detector *det, void *det_ws, size_t det_ws_bytes,
+                                    void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if ((r = check_det_ptrs(det))) return r;
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("detector workspace missing, too small or not 256-byte aligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  return prepare_detector(det, L, det_ws, static_cast<cudaStream_t>(stream));
+}
+
+size_t enova_stats_workspace_bytes(int64_t n_instances, int32_t n_metrics) {
+  (void)n_instances;
+  (void)n_metrics;
+  return 256;
+}
+
+enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, float *mean,
+                                 float *std, int64_t *n_degenerate, void *ws, size_t ws_bytes,
+                                 void *stream) {
+  enova_status r = check_series_base(series);
+  if (r) return r;
+  if (series->n_metrics > 256) {
+    set_error("n_metrics > 256");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (t_cal_end < 1 || t_cal_end > series->n_steps) {
+    set_error("t_cal_end must be in [1, n_steps]");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!mean || !std) {
+    set_error("mean / std outputs are NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!ws || ws_bytes < 256 || !aligned(ws, 256)) {
+    set_error("stats workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  if (series->n_instances == 0) {
+    if (n_degenerate) *n_degenerate = 0;
+    return ENOVA_OK;
+  }
+  return compute_stats(series, t_cal_end, mean, std, n_degenerate, ws,
+                       static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_score_windows(const enova_series *series, const enova_detector *det,
+                                 const void *det_ws, size_t det_ws_bytes, float *scores,
+                                 float *md, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if ((r = check_series_windows(series, L))) return r;
+  const bool empty = series->n_instances == 0 || series->t_end == series->t_begin;
+  if (!scores && !empty) {
+    set_error("scores output is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  if (empty) return ENOVA_OK;
+  return launch_score(series, L, det_ws, scores, md, nullptr, 0.0,
+                      static_cast<cudaStream_t>(stream));
+}
+
+size_t enova_threshold_workspace_bytes(int64_t n_global_max, double init_quantile) {
+  if (n_global_max < 1) n_global_max = 1;
+  return threshold_workspace_bytes(n_global_max, init_quantile);
+}
+
+enova_status enova_fit_threshold(const float *scores, int64_t n_local, int64_t n_global_max,
+                                 double init_quantile, double risk_q, enova_comm_t comm,
+                                 enova_threshold *out, void *ws, size_t ws_bytes, void *stream) {
+  if (!out || n_local < 0 || (n_local > 0 && !scores)) {
+    set_error("bad fit_threshold arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!(init_quantile >= 0.0 && init_quantile < 1.0) || !(risk_q > 0.0 && risk_q < 1.0)) {
+    set_error("init_quantile must be in [0,1) and risk_q in (0,1)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (n_global_max < n_local) n_global_max = n_local;
+  if (!ws || !aligned(ws, 256)) {
+    set_error("threshold workspace missing or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return fit_threshold(scores, n_local, init_quantile, risk_q, comm, out, ws, ws_bytes,
+                       n_global_max, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_detect(const enova_series *series, const enova_detector *det,
+                          const void *det_ws, size_t det_ws_bytes, const enova_threshold *thr,
+                          int8_t *flags, float *scores_opt, float *md_opt, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if ((r = check_series_windows(series, L))) return r;
+  if (!thr || !isfinite(thr->z_q)) {
+    set_error("threshold missing or not finite");
+    return ENOVA_ERR_UNCALIBRATED;
+  }
+  const bool empty = series->n_instances == 0 || series->t_end == series->t_begin;
+  if (!flags && !empty) {
+    set_error("flags output is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  if (empty) return ENOVA_OK;
+  return launch_score(series, L, det_ws, scores_opt, md_opt, flags, thr->z_q,
+                      static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window, int32_t n_metrics,
+                             const float *sample, int64_t tick, void *stream) {
+  if (!ring || !sample || n_instances < 0 || window < 1 || n_metrics < 1 || tick < 0 ||
+      (n_metrics % 4) != 0 || !aligned(ring, 16) || !aligned(sample, 16)) {
+    set_error("bad ring_push arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return ring_push(ring, n_instances, window, n_metrics, sample, tick,
+                   static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

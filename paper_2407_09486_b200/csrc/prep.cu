@@ -1,0 +1,113 @@
+// prep.cu -- K0: build the prepared-detector image.
+//
+// The detector's tensor-core operands are defined in fp16 (R-17):
+// W1 [H][D], [Wmu | Wlv] [2Z][H] and W3 [H][Z] are rounded RNE to fp16 and
+// written as K-major, no-swizzle canonical UMMA B images (layout.h), so the
+// score kernel can bulk-copy them into shared memory unchanged.  The decoder
+// output layer is only needed through the column-sum identity
+//   mean_k (x_k - m'_k) = (sum_k x_k - w_bar . a3 - b_bar) / D,
+//   w_bar = 1^T W_dec2,  b_bar = sum_k b_dec2          (R-8, exact algebra)
+// whose sums are accumulated in fp64 in a fixed order (deterministic).
+#include "common.cuh"
+#include "layout.h"
+
+namespace enova {
+
+__global__ void k_pack_w1(const float *__restrict__ w1, __half *__restrict__ img, int H, int D) {
+  size_t total = (size_t)H * D;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    int n = (int)(e / D), k = (int)(e % D);
+    img[kmajor_step_offset(n, k, H) / 2] = __float2half_rn(w1[e]);
+  }
+}
+
+// heads: rows n < ZP -> Wmu[n] (zero if n >= Z); rows ZP + z -> Wlv[z]
+__global__ void k_pack_heads(const float *__restrict__ wmu, const float *__restrict__ wlv,
+                             __half *__restrict__ img, int H, int Z, int ZP) {
+  int N2 = 2 * ZP;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N2 * H; e += gridDim.x * blockDim.x) {
+    int n = e / H, k = e % H;
+    float v = 0.f;
+    if (n < ZP) {
+      if (n < Z) v = wmu[n * H + k];
+    } else if (n - ZP < Z) {
+      v = wlv[(n - ZP) * H + k];
+    }
+    img[kmajor_step_offset(n, k, N2) / 2] = __float2half_rn(v);
+  }
+}
+
+// W3 [H][Z] -> B image N = H, K = 16 (z >= Z zero padded)
+__global__ void k_pack_w3(const float *__restrict__ w3, __half *__restrict__ img, int H, int Z) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < H * 16; e += gridDim.x * blockDim.x) {
+    int n = e / 16, k = e % 16;
+    float v = k < Z ? w3[n * Z + k] : 0.f;
+    img[kmajor_step_offset(n, k, H) / 2] = __float2half_rn(v);
+  }
+}
+
+__global__ void k_pack_vectors(const float *__restrict__ b1, const float *__restrict__ bmu,
+                               const float *__restrict__ blv, const float *__restrict__ b3,
+                               float *__restrict__ ob1, float *__restrict__ obml,
+                               float *__restrict__ ob3, int H, int Z, int ZP) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < H) {
+    ob1[i] = b1[i];
+    ob3[i] = b3[i];
+  }
+  if (i < 2 * ZP) {
+    float v = 0.f;
+    if (i < ZP) {
+      if (i < Z) v = bmu[i];
+    } else if (i - ZP < Z) {
+      v = blv[i - ZP];
+    }
+    obml[i] = v;
+  }
+}
+
+// block h < H: w_bar[h] = sum_k W_dec2[k][h]; block H: b_bar = sum_k b_dec2[k].
+// fp64, fixed-order strided partials then a fixed tree.
+__global__ void k_colsum(const float *__restrict__ w2, const float *__restrict__ b2,
+                         float *__restrict__ wbar, double *__restrict__ bbar, int H, int D) {
+  __shared__ double red[256];
+  int h = blockIdx.x;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < D; k += blockDim.x)
+    s += (h < H) ? (double)w2[(size_t)k * H + h] : (double)b2[k];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (h < H)
+      wbar[h] = (float)red[0];
+    else
+      *bbar = red[0];
+  }
+}
+
+enova_status prepare_detector(const enova_detector *det, const DetLayout &L, void *ws,
+                              cudaStream_t st) {
+  char *base = static_cast<char *>(ws);
+  k_pack_w1<<<296, 256, 0, st>>>(det->enc_w1, reinterpret_cast<__half *>(base + L.off_w1), L.H,
+                                 L.D);
+  k_pack_heads<<<16, 256, 0, st>>>(det->enc_wmu, det->enc_wlv,
+                                   reinterpret_cast<__half *>(base + L.off_heads), L.H, L.Z, L.ZP);
+  k_pack_w3<<<8, 256, 0, st>>>(det->dec_w1, reinterpret_cast<__half *>(base + L.off_w3), L.H,
+                               L.Z);
+  k_pack_vectors<<<1, 256, 0, st>>>(det->enc_b1, det->enc_bmu, det->enc_blv, det->dec_b1,
+                                    reinterpret_cast<float *>(base + L.off_b1),
+                                    reinterpret_cast<float *>(base + L.off_bml),
+                                    reinterpret_cast<float *>(base + L.off_b3), L.H, L.Z, L.ZP);
+  k_colsum<<<L.H + 1, 256, 0, st>>>(det->dec_w2, det->dec_b2,
+                                    reinterpret_cast<float *>(base + L.off_wbar),
+                                    reinterpret_cast<double *>(base + L.off_bbar), L.H, L.D);
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
+}
+
+}  // namespace enova

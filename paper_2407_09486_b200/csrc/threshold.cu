@@ -1,0 +1,669 @@
+// threshold.cu -- K3..K5: fleet-wide peaks-over-threshold calibration (a-7..a-9).
+//
+// "The threshold for detecting anomalies is automatically set using the
+// peaks-over-threshold method" (citing Siffer et al. 2017;
+// SPEC.md:232-240, 254, 260; R-11..R-13):
+//   t   = S_(k), k = floor(q0 n): exact order statistic by a 3-pass radix select
+//         over order-preserving uint32 keys of the fp32 scores (11/11/10-bit
+//         digits, integer histograms -> all-reduced across ranks, exact);
+//   Y   = {s - t : s > t} in fp64, compacted stably in index order (and
+//         all-gathered in rank order), so every rank holds the same Y;
+//   GPD = maximum likelihood by Grimshaw's reduction: the roots of
+//         w(x) = u(x) v(x) - 1 (u = mean 1/(1+xY), v = 1 + mean log1p(xY)) are
+//         bracketed on the fixed 64-point grids of both intervals and refined by
+//         k-section (bisection when S = 1) to a 2^-60 bracket; every root gives
+//         gamma = v - 1, sigma = gamma / x, log-likelihood -N (ln sigma + gamma + 1);
+//         the exponential candidate (gamma = 0, sigma = Ybar) is always present;
+//   z_q = t + sigma/gamma * expm1(-gamma ln(q n / N_t))  (t - sigma ln(.) at gamma = 0).
+// All reductions use a fixed block partition and a fixed combine order, so the
+// result is deterministic and identical on every rank.
+#include <math.h>
+
+#include <vector>
+
+#include "comm.h"
+#include "common.cuh"
+
+namespace enova {
+
+constexpr int kBins = 2048;
+constexpr int kSelThreads = 1024;
+constexpr int kCompactBlocks = 1184;  // 8 per SM
+constexpr int kCompactThreads = 256;
+constexpr int kFitBlocks = 296;
+constexpr int kFitThreads = 256;
+constexpr int kMaxPts = 128;
+constexpr int kMaxSlots = 64;
+constexpr int kGrid = 64;
+
+enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
+
+struct SelState {
+  unsigned int prefix, mask;
+  unsigned long long k_rem;
+  float t;
+  int pad;
+};
+
+struct FitState {
+  int64_t nt, n;
+  double t, q, ybar, ymin, ymax;
+  int phase, npts, nslots, S, iters, overflow;
+  unsigned int counter, pad;
+  double xs[kMaxPts], w[kMaxPts], L[kMaxPts];
+  double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots];
+  int exact[kMaxSlots];
+  int refine_idx[kMaxSlots];   // slot of the k-th refined bracket
+  int nrefine;
+  // result
+  double gamma, sigma, z_q;
+  int method, nroots;
+};
+
+struct ThrLayout {
+  size_t hist, sel, fit, partials, counts, counts_all, nbuf, ylocal, yall, total;
+  int64_t cap;
+};
+
+static inline ThrLayout thr_layout(int64_t n_max, double q0) {
+  ThrLayout L;
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 255) / 256 * 256; return r; };
+  double tail = (1.0 - q0) * (double)n_max;
+  if (tail < 0) tail = 0;
+  L.cap = (int64_t)ceil(tail) + 16;
+  if (L.cap > n_max) L.cap = n_max;
+  if (L.cap < 16) L.cap = 16;
+  L.hist = take(kBins * 8);
+  L.sel = take(sizeof(SelState));
+  L.fit = take(sizeof(FitState));
+  L.partials = take((size_t)kFitBlocks * kMaxPts * 2 * 8);
+  L.counts = take((kCompactBlocks + 1) * 8);
+  L.counts_all = take(1024 * 8);
+  L.nbuf = take(16);
+  L.ylocal = take((size_t)L.cap * 8);
+  L.yall = take((size_t)L.cap * 8);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ unsigned int f2key(float f) {
+  unsigned int b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned int k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// ---------------------------------------------------------------- K3 ----
+__global__ void k_sel_init(SelState *s, unsigned long long k) {
+  s->prefix = 0;
+  s->mask = 0;
+  s->k_rem = k;
+  s->t = 0.f;
+}
+
+__global__ void k_hist(const float *__restrict__ x, int64_t n, const SelState *__restrict__ sel,
+                       unsigned long long *__restrict__ hist, int shift, int nbins) {
+  __shared__ unsigned int h[kBins];
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const unsigned int prefix = sel->prefix, mask = sel->mask;
+  const int64_t n4 = n / 4;
+  const float4 *x4 = reinterpret_cast<const float4 *>(x);
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto add = [&](float f) {
+    unsigned int k = f2key(f);
+    if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & (nbins - 1)], 1u);
+  };
+  if (aligned) {
+    for (int64_t i = i0; i < n4; i += stride) {
+      float4 v = __ldg(x4 + i);
+      add(v.x); add(v.y); add(v.z); add(v.w);
+    }
+    for (int64_t i = 4 * n4 + i0; i < n; i += stride) add(__ldg(x + i));
+  } else {
+    for (int64_t i = i0; i < n; i += stride) add(__ldg(x + i));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, (unsigned long long)h[i]);
+}
+
+// one block of 1024 threads, 2 bins per thread: find the digit holding rank k_rem
+__global__ void k_select(unsigned long long *__restrict__ hist, SelState *__restrict__ sel,
+                         int shift, int nbins) {
+  __shared__ unsigned long long warp_tot[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long c0 = 0, c1 = 0;
+  if (2 * tid < nbins) c0 = hist[2 * tid];
+  if (2 * tid + 1 < nbins) c1 = hist[2 * tid + 1];
+  unsigned long long v = c0 + c1, incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long wv = warp_tot[lane], wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    warp_tot[lane] = wi - wv;  // exclusive warp offsets
+  }
+  __syncthreads();
+  const unsigned long long before = warp_tot[warp] + incl - v;  // exclusive prefix of bin 2*tid
+  const unsigned long long k = sel->k_rem;
+  __syncthreads();
+  int digit = -1;
+  unsigned long long below = 0;
+  if (c0 && k >= before && k < before + c0) {
+    digit = 2 * tid;
+    below = before;
+  } else if (c1 && k >= before + c0 && k < before + c0 + c1) {
+    digit = 2 * tid + 1;
+    below = before + c0;
+  }
+  if (digit >= 0) {
+    sel->prefix |= (unsigned int)digit << shift;
+    sel->mask |= (unsigned int)(nbins - 1) << shift;
+    sel->k_rem = k - below;
+    if (shift == 0) sel->t = key2f(sel->prefix);
+  }
+  __syncthreads();
+  if (2 * tid < nbins) hist[2 * tid] = 0;
+  if (2 * tid + 1 < nbins) hist[2 * tid + 1] = 0;
+}
+
+// ---------------------------------------------------------------- K4 ----
+__device__ __forceinline__ void chunk_of(int64_t n, int64_t *b0, int64_t *b1) {
+  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  chunk = (chunk + 255) / 256 * 256;
+  *b0 = min(n, (int64_t)blockIdx.x * chunk);
+  *b1 = min(n, *b0 + chunk);
+}
+
+__global__ void k_count_peaks(const float *__restrict__ x, int64_t n,
+                              const SelState *__restrict__ sel,
+                              long long *__restrict__ counts) {
+  __shared__ int wsum[32];
+  int64_t b0, b1;
+  chunk_of(n, &b0, &b1);
+  const double t = (double)sel->t;
+  int c = 0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += ((double)__ldg(x + i) > t);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wsum[w];
+    counts[blockIdx.x] = s;
+  }
+}
+
+// exclusive scan of nblk counts in place; total at counts[nblk]
+__global__ void k_scan_counts(long long *counts, int nblk) {
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int b = 0; b < nblk; ++b) {
+      long long c = counts[b];
+      counts[b] = run;
+      run += c;
+    }
+    counts[nblk] = run;
+  }
+}
+
+__global__ void k_scatter_peaks(const float *__restrict__ x, int64_t n,
+                                const SelState *__restrict__ sel,
+                                const long long *__restrict__ offsets, double *__restrict__ Y) {
+  __shared__ int woff[kCompactThreads / 32 + 1];
+  int64_t b0, b1;
+  chunk_of(n, &b0, &b1);
+  const double t = (double)sel->t;
+  long long base = offsets[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t i0 = b0; i0 < b1; i0 += blockDim.x) {
+    int64_t i = i0 + threadIdx.x;
+    double s = (i < b1) ? (double)__ldg(x + i) : 0.0;
+    bool f = (i < b1) && (s > t);
+    unsigned int bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) woff[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int w = 0; w < nw; ++w) {
+        int c = woff[w];
+        woff[w] = run;
+        run += c;
+      }
+      woff[nw] = run;
+    }
+    __syncthreads();
+    if (f) Y[base + woff[warp] + __popc(bal & ((1u << lane) - 1u))] = s - t;
+    base += woff[nw];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K5 ----
+__device__ bool last_block_done(unsigned int *counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int ticket = atomicAdd(counter, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+template <typename T, typename Op>
+__device__ T block_reduce(T v, Op op, T *scratch) {
+  // fixed-order tree: warp xor-shuffle, then warp totals in order
+  for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  T r = scratch[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = op(r, scratch[w]);
+  return r;
+}
+
+__device__ void setup_grid(FitState *f) {
+  // the fixed scan grids of R-13 (same formulas as the oracle)
+  const double ymax = f->ymax, ymin = f->ymin, ybar = f->ybar;
+  for (int k = 0; k < kGrid; ++k) {
+    double th = 1e-8 + k * ((1.0 - 2e-8) / (kGrid - 1));
+    f->xs[k] = (-1.0 / ymax) * (1.0 - th);
+  }
+  double a = 1e-12 / ybar;
+  double b = 2.0 * (ybar - ymin) / (ymin * ymin);
+  int np = kGrid;
+  if (b > a) {
+    double la = log(a), lb = log(b);
+    for (int k = 0; k < kGrid; ++k) f->xs[kGrid + k] = exp(la + k * ((lb - la) / (kGrid - 1)));
+    np = 2 * kGrid;
+  }
+  f->npts = np;
+  f->phase = PH_GRID;
+}
+
+__global__ void k_ystats(const double *__restrict__ Y, int64_t nt, FitState *f,
+                         double *__restrict__ partials) {
+  __shared__ double scratch[32];
+  int64_t b0, b1;
+  chunk_of(nt, &b0, &b1);
+  double s = 0.0, mn = INFINITY, mx = -INFINITY;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    double y = Y[i];
+    s += y;
+    mn = fmin(mn, y);
+    mx = fmax(mx, y);
+  }
+  s = block_reduce(s, [](double a, double b) { return a + b; }, scratch);
+  mn = block_reduce(mn, [](double a, double b) { return fmin(a, b); }, scratch);
+  mx = block_reduce(mx, [](double a, double b) { return fmax(a, b); }, scratch);
+  if (threadIdx.x == 0) {
+    partials[3 * blockIdx.x + 0] = s;
+    partials[3 * blockIdx.x + 1] = mn;
+    partials[3 * blockIdx.x + 2] = mx;
+  }
+  if (last_block_done(&f->counter)) {
+    if (threadIdx.x == 0) {
+      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        ts += partials[3 * b];
+        tmn = fmin(tmn, partials[3 * b + 1]);
+        tmx = fmax(tmx, partials[3 * b + 2]);
+      }
+      f->ybar = ts / (double)nt;
+      f->ymin = tmn;
+      f->ymax = tmx;
+      f->counter = 0;
+      setup_grid(f);
+    }
+  }
+}
+
+__device__ void controller(FitState *f) {
+  if (f->phase == PH_GRID) {
+    // sign changes of w on each grid, in scan order (left grid, then right)
+    int ns = 0;
+    auto push = [&](double lo, double hi, double wlo, int exact) {
+      if (ns >= kMaxSlots) {
+        f->overflow = 1;
+        return;
+      }
+      f->lo[ns] = lo;
+      f->hi[ns] = hi;
+      f->wlo[ns] = wlo;
+      f->exact[ns] = exact;
+      ++ns;
+    };
+    for (int g = 0; g * kGrid < f->npts; ++g) {
+      const double *x = f->xs + g * kGrid;
+      const double *w = f->w + g * kGrid;
+      for (int k = 0; k < kGrid - 1; ++k) {
+        if (w[k] == 0.0)
+          push(x[k], x[k], 0.0, 1);
+        else if (w[k] * w[k + 1] < 0.0)
+          push(x[k], x[k + 1], w[k], 0);
+      }
+      if (w[kGrid - 1] == 0.0) push(x[kGrid - 1], x[kGrid - 1], 0.0, 1);
+    }
+    f->nslots = ns;
+    int nr = 0;
+    for (int s = 0; s < ns; ++s)
+      if (!f->exact[s]) f->refine_idx[nr++] = s;
+    f->nrefine = nr;
+    if (nr > 0) {
+      double work = (double)f->nt * nr;
+      int S = work <= 262144.0 ? 31 : (work <= 2097152.0 ? 7 : 1);
+      if (S * nr > kMaxPts) S = kMaxPts / nr;
+      if (S < 1) S = 1;
+      int it = 0;
+      double red = 1.0;
+      while (red < 1152921504606846976.0) {  // 2^60, the oracle's 60 halvings
+        red *= (double)(S + 1);
+        ++it;
+      }
+      f->S = S;
+      f->iters = it;
+      f->phase = PH_REFINE;
+    } else {
+      f->S = 0;
+      f->iters = 0;
+      f->phase = PH_FINAL;
+    }
+  } else if (f->phase == PH_REFINE) {
+    const int S = f->S;
+    for (int r = 0; r < f->nrefine; ++r) {
+      const int s = f->refine_idx[r];
+      const double lo = f->lo[s], hi = f->hi[s], wl = f->wlo[s];
+      const bool pos = wl > 0;
+      double nlo = lo, nhi = hi, nwl = wl;
+      int j;
+      for (j = 0; j < S; ++j) {
+        const double wj = f->w[r * S + j];
+        if ((wj > 0) != pos) break;
+      }
+      if (j < S) {
+        nhi = f->xs[r * S + j];
+        if (j > 0) {
+          nlo = f->xs[r * S + j - 1];
+          nwl = f->w[r * S + j - 1];
+        }
+      } else {
+        nlo = f->xs[r * S + S - 1];
+        nwl = f->w[r * S + S - 1];
+      }
+      f->lo[s] = nlo;
+      f->hi[s] = nhi;
+      f->wlo[s] = nwl;
+    }
+    f->iters -= 1;
+    if (f->iters <= 0) f->phase = PH_FINAL;
+  } else if (f->phase == PH_FINAL) {
+    const double N = (double)f->nt;
+    double bg = 0.0, bs = f->ybar, bll = -N * (log(f->ybar) + 1.0);
+    int method = 1, nroots = 0;
+    for (int s = 0; s < f->nslots; ++s) {
+      const double x = f->xs[s];
+      const double g = f->L[s];
+      if (x == 0.0 || g == 0.0) continue;
+      const double sg = g / x;
+      if (!(sg > 0.0)) continue;
+      ++nroots;
+      const double ll = -N * (log(sg) + g + 1.0);
+      if (ll > bll || (ll == bll && fabs(g) < fabs(bg))) {
+        bll = ll;
+        bg = g;
+        bs = sg;
+        method = 0;
+      }
+    }
+    const double r = f->q * (double)f->n / N;
+    const double lr = log(r);
+    f->gamma = bg;
+    f->sigma = bs;
+    f->method = method;
+    f->nroots = nroots;
+    f->z_q = (bg == 0.0) ? f->t - bs * lr : f->t + (bs / bg) * expm1(-bg * lr);
+    f->phase = PH_DONE;
+    return;
+  }
+  // next evaluation points
+  if (f->phase == PH_REFINE) {
+    const int S = f->S;
+    for (int r = 0; r < f->nrefine; ++r) {
+      const int s = f->refine_idx[r];
+      const double lo = f->lo[s], hi = f->hi[s];
+      if (S == 1) {
+        f->xs[r] = 0.5 * (lo + hi);
+      } else {
+        for (int j = 0; j < S; ++j) f->xs[r * S + j] = lo + (hi - lo) * (double)(j + 1) / (double)(S + 1);
+      }
+    }
+    f->npts = S * f->nrefine;
+  } else if (f->phase == PH_FINAL) {
+    for (int s = 0; s < f->nslots; ++s)
+      f->xs[s] = f->exact[s] ? f->lo[s] : 0.5 * (f->lo[s] + f->hi[s]);
+    f->npts = f->nslots;
+  }
+}
+
+// evaluate P(x) = mean(-xY/(1+xY)) and L(x) = mean(log1p(xY)) at state->xs; the
+// last block combines the per-block partials in block order and runs the controller
+__global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, int64_t nt,
+                                                          FitState *f,
+                                                          double *__restrict__ partials) {
+  __shared__ double xs[kMaxPts];
+  __shared__ double scratch[32];
+  if (f->phase == PH_DONE) return;
+  const int npts = f->npts;
+  for (int i = threadIdx.x; i < npts; i += blockDim.x) xs[i] = f->xs[i];
+  __syncthreads();
+  int64_t b0, b1;
+  chunk_of(nt, &b0, &b1);
+  for (int pt = 0; pt < npts; ++pt) {
+    const double x = xs[pt];
+    double P = 0.0, L = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const double xy = x * Y[i];
+      P += -xy / (1.0 + xy);
+      L += log1p(xy);
+    }
+    P = block_reduce(P, [](double a, double b) { return a + b; }, scratch);
+    L = block_reduce(L, [](double a, double b) { return a + b; }, scratch);
+    if (threadIdx.x == 0) {
+      partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 0] = P;
+      partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 1] = L;
+    }
+  }
+  if (last_block_done(&f->counter)) {
+    const double N = (double)nt;
+    for (int pt = threadIdx.x; pt < npts; pt += blockDim.x) {
+      double P = 0.0, L = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        P += partials[((size_t)b * kMaxPts + pt) * 2 + 0];
+        L += partials[((size_t)b * kMaxPts + pt) * 2 + 1];
+      }
+      P /= N;
+      L /= N;
+      f->w[pt] = P + L + P * L;
+      f->L[pt] = L;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      f->counter = 0;
+      controller(f);
+    }
+  }
+}
+
+__global__ void k_fit_init(FitState *f, int64_t nt, int64_t n, const SelState *sel, double q) {
+  f->nt = nt;
+  f->n = n;
+  f->t = (double)sel->t;
+  f->q = q;
+  f->counter = 0;
+  f->overflow = 0;
+  f->phase = PH_GRID;
+  f->npts = 0;
+}
+
+// ------------------------------------------------------------- driver ----
+enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
+                           enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
+                           int64_t n_global_max, cudaStream_t st) {
+  char *b = static_cast<char *>(ws);
+  // global n
+  int64_t n = n_local;
+  unsigned long long *nbuf = reinterpret_cast<unsigned long long *>(b + 0);  // placeholder
+  ThrLayout L = thr_layout(n_global_max, q0);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  nbuf = reinterpret_cast<unsigned long long *>(b + L.nbuf);
+  if (comm) {
+    unsigned long long hn = (unsigned long long)n_local;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(nbuf, &hn, 8, cudaMemcpyHostToDevice, st));
+    enova_status s = comm_allreduce_u64_sum(comm, nbuf, nbuf, 1, st);
+    if (s) return s;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(&hn, nbuf, 8, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+    n = (int64_t)hn;
+  }
+  if (n <= 0) {
+    set_error("no scores");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (n > n_global_max) {
+    set_error("total score count exceeds n_global_max used to size the workspace");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  const int64_t k = (int64_t)floor(q0 * (double)n);
+  if (k < 0 || k >= n) {
+    set_error("init_quantile out of range");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  unsigned long long *hist = reinterpret_cast<unsigned long long *>(b + L.hist);
+  SelState *sel = reinterpret_cast<SelState *>(b + L.sel);
+  FitState *fit = reinterpret_cast<FitState *>(b + L.fit);
+  double *partials = reinterpret_cast<double *>(b + L.partials);
+  long long *counts = reinterpret_cast<long long *>(b + L.counts);
+  long long *counts_all = reinterpret_cast<long long *>(b + L.counts_all);
+  double *ylocal = reinterpret_cast<double *>(b + L.ylocal);
+  double *yall = reinterpret_cast<double *>(b + L.yall);
+
+  // K3: radix select of the k-th smallest key (3 digit passes)
+  ENOVA_CUDA_TRY(cudaMemsetAsync(hist, 0, kBins * 8, st));
+  k_sel_init<<<1, 1, 0, st>>>(sel, (unsigned long long)k);
+  const int shifts[3] = {21, 10, 0};
+  const int nbins[3] = {2048, 2048, 1024};
+  const int hblocks = 148 * 4;
+  for (int pass = 0; pass < 3; ++pass) {
+    if (n_local > 0) k_hist<<<hblocks, 512, 0, st>>>(scores, n_local, sel, hist, shifts[pass], nbins[pass]);
+    if (comm) {
+      enova_status s = comm_allreduce_u64_sum(comm, hist, hist, (size_t)nbins[pass], st);
+      if (s) return s;
+    }
+    k_select<<<1, kSelThreads, 0, st>>>(hist, sel, shifts[pass], nbins[pass]);
+  }
+  ENOVA_CUDA_TRY(cudaGetLastError());
+
+  // K4: stable compaction of the peaks
+  double *ydst = comm ? ylocal : yall;
+  int64_t nt_local = 0;
+  if (n_local > 0) {
+    k_count_peaks<<<kCompactBlocks, kCompactThreads, 0, st>>>(scores, n_local, sel, counts);
+    k_scan_counts<<<1, 32, 0, st>>>(counts, kCompactBlocks);
+    long long h_tot = 0;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(&h_tot, counts + kCompactBlocks, 8, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+    nt_local = h_tot;
+    if (nt_local > L.cap) {
+      set_error("peak count exceeds workspace capacity");
+      return ENOVA_ERR_WORKSPACE;
+    }
+    k_scatter_peaks<<<kCompactBlocks, kCompactThreads, 0, st>>>(scores, n_local, sel, counts, ydst);
+    ENOVA_CUDA_TRY(cudaGetLastError());
+  }
+  int64_t nt = nt_local;
+  if (comm) {
+    long long *my = counts + kCompactBlocks;  // device copy of nt_local
+    if (n_local == 0) ENOVA_CUDA_TRY(cudaMemsetAsync(my, 0, 8, st));
+    enova_status s = comm_allgather_i64(comm, my, counts_all, st);
+    if (s) return s;
+    std::vector<int64_t> hc(comm->world), off(comm->world);
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts_all, 8 * comm->world, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+    nt = 0;
+    for (int r = 0; r < comm->world; ++r) {
+      off[r] = nt;
+      nt += hc[r];
+    }
+    if (nt > L.cap) {
+      set_error("peak count exceeds workspace capacity");
+      return ENOVA_ERR_WORKSPACE;
+    }
+    s = comm_allgatherv_f64(comm, ylocal, yall, hc.data(), off.data(), st);
+    if (s) return s;
+  }
+  if (nt < 10) {
+    set_error("fewer than 10 exceedances above the initial threshold");
+    return ENOVA_ERR_TOO_FEW_EXCEEDANCES;
+  }
+
+  // K5: GPD fit (replicated, deterministic)
+  k_fit_init<<<1, 1, 0, st>>>(fit, nt, n, sel, q);
+  k_ystats<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);
+  k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);  // grid scan
+  int iters = 0;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&iters, &fit->iters, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int overflow = 0;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&overflow, &fit->overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  if (overflow) {
+    set_error("more than 64 Grimshaw roots");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  for (int i = 0; i < iters; ++i) k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);
+  k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);  // final candidates
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  struct {
+    double gamma, sigma, z_q;
+    int method, nroots;
+  } res;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&res, &fit->gamma, sizeof(res), cudaMemcpyDeviceToHost, st));
+  float t = 0.f;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&t, &sel->t, 4, cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  out->init_quantile = q0;
+  out->risk_q = q;
+  out->t = (double)t;
+  out->gamma = res.gamma;
+  out->sigma = res.sigma;
+  out->z_q = res.z_q;
+  out->n = n;
+  out->n_peaks = nt;
+  out->method = res.method;
+  out->reserved = 0;
+  return ENOVA_OK;
+}
+
+size_t threshold_workspace_bytes(int64_t n_max, double q0) { return thr_layout(n_max, q0).total; }
+
+}  // namespace enova

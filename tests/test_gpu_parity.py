@@ -1,0 +1,329 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances (north_star):
+  scores  |d| <= 1e-3 |ref| + 1e-6         (every window)
+  md      |d| <= 1e-4 + 1e-3 |ref|
+  flags   identical outside |score_ref - z_q| <= 1e-3 z_q and |md_ref| <= 1e-4
+  stats   bitwise (fp64-accumulated, rounded to fp32) up to 1 fp32 ulp
+  z_q     |d| <= 1e-9 z_q on identical scores
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import enova_oracle as O
+from paper_2407_09486_b200 import synth
+from tests import detectors
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL, SCORE_ATOL = 1e-3, 1e-6
+MD_ATOL, MD_RTOL = 1e-4, 1e-3
+
+
+@pytest.fixture(scope="module")
+def E():
+    from paper_2407_09486_b200 import build as B
+    B.build()
+    import paper_2407_09486_b200 as P
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return P
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def assert_scores(gpu, ref, what="scores"):
+    gpu = np.asarray(gpu, np.float64)
+    err = np.abs(gpu - ref)
+    tol = SCORE_RTOL * np.abs(ref) + SCORE_ATOL
+    bad = np.count_nonzero(err > tol)
+    assert bad == 0, f"{what}: {bad} windows outside tolerance; max rel {np.max(err / (np.abs(ref) + 1e-12)):.3e}"
+    return float(np.max(err / (np.abs(ref) + 1e-12)))
+
+
+def assert_md(gpu, ref):
+    err = np.abs(np.asarray(gpu, np.float64) - ref)
+    bad = np.count_nonzero(err > MD_ATOL + MD_RTOL * np.abs(ref))
+    assert bad == 0, f"md: {bad} windows outside tolerance; max abs {err.max():.3e}"
+
+
+def assert_flags(gpu_flags, ref_flags, ref_scores, ref_md, z_q):
+    band = (np.abs(ref_scores - z_q) <= 1e-3 * abs(z_q)) | (
+        (np.abs(ref_md) <= 1e-4) & (ref_scores > z_q * (1 - 1e-3)))
+    g = np.asarray(gpu_flags)
+    mism = (g != ref_flags) & ~band
+    assert not mism.any(), f"{mism.sum()} flag mismatches outside the band"
+    return int(band.sum())
+
+
+# ------------------------------------------------------------------ a-1 ----
+def test_stats_match_oracle(E):
+    X = synth.metric_trace(8, 3000, 16, seed=21)
+    X[5, :, 7] = 3.5                                    # degenerate series
+    mean, std, nd = E.compute_stats(cuda(X), 1500)
+    om, os_, ond = O.series_stats(X, 1500)
+    gm, gs = mean.cpu().numpy(), std.cpu().numpy()
+    assert nd == ond == 1
+    assert np.max(np.abs(gm.view(np.int32) - om.view(np.int32))) <= 1
+    assert np.max(np.abs(gs.view(np.int32) - os_.view(np.int32))) <= 1
+
+
+def test_stats_nonfinite_rejected(E):
+    X = synth.metric_trace(2, 300, 8, seed=22)
+    X[1, 100, 2] = np.nan
+    with pytest.raises(E.EnovaError) as ei:
+        E.compute_stats(cuda(X), 300)
+    assert ei.value.name == "ENOVA_ERR_NONFINITE"
+    X[1, 100, 2] = 0.0
+    X[0, 250, 0] = np.inf          # outside the horizon [0, 200): accepted
+    E.compute_stats(cuda(X), 200)
+
+
+# ------------------------------------------------------------ a-2..a-5 ----
+SHAPES = [  # (W, M, H, Z)
+    (32, 8, 32, 4),       # c1 "tiny" (SPEC sizes)
+    (64, 16, 128, 16),    # c2..c5 benchmark detector
+    (16, 32, 64, 8),
+    (8, 64, 32, 16),
+    (64, 16, 64, 5),
+    (2, 8, 32, 1),
+    (10, 16, 128, 9),
+]
+
+
+@pytest.mark.parametrize("W,M,H,Z", SHAPES, ids=lambda v: str(v))
+def test_scores_match_oracle_shapes(E, W, M, H, Z):
+    N, T = 3, 700 + W                          # ragged last tile per instance
+    X = synth.metric_trace(N, T, M, seed=W * 1000 + M + H + Z)
+    wts = synth.detector_weights(W, M, H, Z, seed=H + Z)
+    mean, std, _ = O.series_stats(X, T // 2)
+    det = E.PreparedDetector(wts)
+    for tb, te in ((W - 1, T), (W - 1 + 37, T - 11), (T - 5, T), (W + 3, W + 3)):
+        sc, md = E.score_windows(cuda(X), det, cuda(mean), cuda(std), tb, te)
+        rs, rmd = O.score_windows(X, wts, mean, std, tb, te)
+        assert sc.shape == (N, te - tb)
+        if te > tb:
+            assert_scores(sc.cpu().numpy(), rs)
+            assert_md(md.cpu().numpy(), rmd)
+
+
+def test_strided_instances_and_large_values(E):
+    W, M, H, Z = 64, 16, 128, 16
+    N, T = 4, 900
+    X = synth.metric_trace(N, T, M, seed=5)
+    X[2, 300:340, :] *= 50.0                    # far outliers -> clamp region / saturation
+    pad = np.zeros((N, T * M + 64), np.float32)
+    pad[:, :T * M] = X.reshape(N, -1)
+    Xt = cuda(pad)[:, :T * M].view(N, T, M)      # ld_instance = T*M + 64
+    wts = synth.detector_weights(W, M, H, Z)
+    mean, std, _ = O.series_stats(X, 450)
+    det = E.PreparedDetector(wts)
+    sc, md = E.score_windows(Xt, det, cuda(mean), cuda(std))
+    rs, rmd = O.score_windows(X, wts, mean, std, W - 1, T)
+    assert_scores(sc.cpu().numpy(), rs)
+    assert_md(md.cpu().numpy(), rmd)
+
+
+def test_constructed_detectors(E):
+    W, M, H, Z = 32, 8, 32, 4
+    r = np.random.default_rng(3)
+    X = r.standard_normal((2, 300, M)).astype(np.float16).astype(np.float32)
+    zeros_m, ones_s = cuda(np.zeros((2, M), np.float32)), cuda(np.ones((2, M), np.float32))
+    d = detectors.zeros(W, M, H, Z)
+    d["enc_bmu"][:] = [0.5, -0.25, 1.0, 0.0]
+    d["enc_blv"][:] = [0.125, -0.5, 0.0, 1.0]
+    sc, _ = E.score_windows(cuda(X), E.PreparedDetector(d), zeros_m, ones_s)
+    expect = 0.5 * sum(b * b + math.expm1(l) - l for b, l in zip(d["enc_bmu"], d["enc_blv"]))
+    assert np.allclose(sc.cpu().numpy(), expect, rtol=1e-6, atol=0)
+    for tau, j in ((0, 0), (5, 3), (31, 7)):
+        d = detectors.tap_selector(W, M, H, Z, tau, j, a=0.75)
+        sc, _ = E.score_windows(cuda(X), E.PreparedDetector(d), zeros_m, ones_s)
+        t = np.arange(W - 1, 300)
+        v = X[:, t - W + 1 + tau, j].astype(np.float64)
+        assert_scores(sc.cpu().numpy(), 0.5 * np.tanh(0.75 * v) ** 2, f"tap {tau},{j}")
+    d = detectors.zeros(W, M, H, Z)
+    d["dec_b2"][:] = 0.625
+    Xc = np.full((1, 80, M), 0.625, np.float32)
+    _, md = E.score_windows(cuda(Xc), E.PreparedDetector(d), zeros_m[:1], ones_s[:1])
+    assert np.all(md.cpu().numpy() == 0.0)           # perfect reconstruction -> MD = 0
+
+
+# ------------------------------------------------------------ a-7..a-9 ----
+@pytest.mark.parametrize("kind,n", [("mixture", 2_000_000), ("exp", 100_000), ("gpd_neg", 300_000),
+                                    ("ties", 50_001), ("small", 600)])
+def test_threshold_on_identical_scores(E, kind, n):
+    r = np.random.default_rng(7)
+    if kind == "mixture":
+        s = synth.score_mixture(n, seed=77)
+    elif kind == "exp":
+        s = r.exponential(1.0, n).astype(np.float32)
+    elif kind == "gpd_neg":
+        s = (2.0 / -0.2 * (r.uniform(size=n) ** 0.2 - 1.0)).astype(np.float32)
+    elif kind == "ties":
+        s = np.round(r.exponential(1.0, n), 2).astype(np.float32)
+    else:
+        s = r.exponential(1.0, n).astype(np.float32)
+    g = E.fit_threshold(cuda(s), 0.98, 1e-3)
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    assert g["t"] == o["t"]
+    assert g["n"] == o["n"] and g["n_peaks"] == o["n_peaks"]
+    assert g["method"] == o["method"]
+    assert abs(g["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
+    assert abs(g["gamma"] - o["gamma"]) <= 1e-7 * max(1.0, abs(o["gamma"]))
+    assert abs(g["sigma"] - o["sigma"]) <= 1e-9 * o["sigma"]
+
+
+def test_threshold_too_few_exceedances(E):
+    s = np.random.default_rng(1).exponential(1.0, 400).astype(np.float32)
+    with pytest.raises(E.EnovaError) as ei:
+        E.fit_threshold(cuda(s), 0.98, 1e-3)
+    assert ei.value.name == "ENOVA_ERR_TOO_FEW_EXCEEDANCES"
+
+
+def test_threshold_c5_full_size(E):
+    n = synth.CONFIGS["c5"]["n_scores"]
+    s = synth.score_mixture(n)
+    g = E.fit_threshold(cuda(s), 0.98, 1e-3)
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    assert g["t"] == o["t"] and g["n_peaks"] == o["n_peaks"]
+    assert abs(g["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
+
+
+def test_comm_world1_matches_single_gpu(E):
+    s = synth.score_mixture(500_000, seed=3)
+    comm = E.Comm.create(0, 1, torch.cuda.current_device())
+    try:
+        a = E.fit_threshold(cuda(s), 0.98, 1e-3, comm=comm)
+    finally:
+        comm.destroy()
+    b = E.fit_threshold(cuda(s), 0.98, 1e-3)
+    assert a == b
+
+
+# ------------------------------------------------------ whole path ----
+def test_c1_pipeline_matches_oracle(E):
+    cfg = synth.CONFIGS["c1"]
+    W, M, H, Z = cfg["window"], cfg["n_metrics"], cfg["hidden"], cfg["latent"]
+    X = synth.metric_trace(cfg["n_instances"], cfg["n_steps"], M, seed=synth.DEFAULT_SEED + 1)
+    wts = synth.detector_weights(W, M, H, Z, seed=synth.DEFAULT_SEED + 1)
+    T = X.shape[1]
+    tcal = T // 2
+    det = E.PreparedDetector(wts)
+    res = E.run_pipeline(cuda(X), det, tcal)
+    ref = O.detect_pipeline(X, wts, tcal)
+    assert np.array_equal(res.mean.cpu().numpy(), ref["mean"])
+    assert_scores(res.cal_scores.cpu().numpy(), ref["cal_scores"], "calibration scores")
+    assert_scores(res.scores.cpu().numpy(), ref["scores"])
+    assert_md(res.md.cpu().numpy(), ref["md"])
+    # end to end: threshold fitted on GPU scores vs on oracle scores
+    assert res.threshold["n"] == ref["threshold"]["n"]
+    assert abs(res.threshold["z_q"] - ref["threshold"]["z_q"]) <= 1e-3 * ref["threshold"]["z_q"]
+    assert_flags(res.flags.cpu().numpy(), ref["flags"], ref["scores"], ref["md"],
+                 ref["threshold"]["z_q"])
+
+
+def test_c2_full_size_sampled(E):
+    """c2 at full size in the bench's launch configuration; the oracle checks a
+    seeded sample of windows one by one, and flags are checked everywhere."""
+    cfg = synth.CONFIGS["c2"]
+    N, T, M = cfg["n_instances"], cfg["n_steps"], cfg["n_metrics"]
+    W, H, Z = cfg["window"], cfg["hidden"], cfg["latent"]
+    X = synth.metric_trace(N, T, M, seed=synth.DEFAULT_SEED + 2)
+    wts = synth.detector_weights(W, M, H, Z, seed=synth.DEFAULT_SEED + 2)
+    tcal = T // 2
+    det = E.PreparedDetector(wts)
+    res = E.run_pipeline(cuda(X), det, tcal)
+    mean32, std32 = res.mean.cpu().numpy(), res.std.cpu().numpy()
+    om, os_, _ = O.series_stats(X, tcal)
+    assert np.max(np.abs(mean32.view(np.int32) - om.view(np.int32))) <= 1
+    r = np.random.default_rng(11)
+    gs, gmd = res.scores.cpu().numpy(), res.md.cpu().numpy()
+    inst = r.integers(0, N, 400)
+    for i in np.unique(inst):
+        ts = np.sort(r.choice(np.arange(tcal, T), 4, replace=False))
+        for t in ts:
+            rs, rmd = O.score_windows(X[i:i + 1], wts, om[i:i + 1], os_[i:i + 1], t, t + 1)
+            assert_scores(gs[i, t - tcal:t - tcal + 1], rs[0], f"inst {i} t {t}")
+            assert_md(gmd[i, t - tcal:t - tcal + 1], rmd[0])
+    # fleet threshold from the GPU's own calibration scores equals the oracle fit of them
+    o = O.pot_threshold(res.cal_scores.cpu().numpy(), 0.98, 1e-3)
+    assert abs(res.threshold["z_q"] - o["z_q"]) <= 1e-9 * o["z_q"]
+    # flags are exactly the rule applied to the GPU's scores/MD
+    f = O.flags(gs, gmd, res.threshold["z_q"])
+    assert np.array_equal(res.flags.cpu().numpy(), f)
+
+
+def test_detect_invariants(E):
+    W, M, H, Z = 64, 16, 128, 16
+    X = synth.metric_trace(6, 2500, M, seed=31)
+    wts = synth.detector_weights(W, M, H, Z, seed=31)
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    mean, std, _ = E.compute_stats(Xc, 1250)
+    sc, md = E.score_windows(Xc, det, mean, std)
+    s_np = sc.cpu().numpy()
+    zq = float(np.quantile(s_np, 0.99))
+    prev = None
+    for z in (zq, zq * 1.1, zq * 1.5):
+        f = E.detect(Xc, det, mean, std, {"z_q": z}).cpu().numpy()
+        assert np.array_equal(f != 0, s_np > z)                    # direction != 0 iff anomaly
+        assert np.array_equal(f[f != 0], np.where(md.cpu().numpy() >= 0, 1, -1)[f != 0])
+        if prev is not None:
+            assert np.all((f != 0) <= (prev != 0))                  # monotone in the threshold
+        prev = f
+    perm = [3, 1, 5, 0, 2, 4]
+    sp, mp = E.score_windows(cuda(X[perm]), det, mean[perm].contiguous(), std[perm].contiguous())
+    assert torch.equal(sp, sc[perm]) and torch.equal(mp, md[perm])  # bitwise equivariance
+    sc2, md2 = E.score_windows(Xc, det, mean, std)
+    assert torch.equal(sc2, sc) and torch.equal(md2, md)           # deterministic
+    X2 = X.copy()
+    X2[2, 1000, 4] += 7 * float(std[2, 4])
+    s3, _ = E.score_windows(cuda(X2), det, mean, std)
+    ch = torch.nonzero((s3 != sc).any(dim=0)).flatten().cpu().numpy() + W - 1
+    assert ch.min() >= 1000 and ch.max() <= 1000 + W - 1            # window locality
+    with pytest.raises(E.EnovaError) as ei:
+        E.detect(Xc, det, mean, std, {"z_q": float("nan")})
+    assert ei.value.name == "ENOVA_ERR_UNCALIBRATED"
+    with pytest.raises(E.EnovaError) as ei:
+        E.score_windows(Xc[:, :50], det, mean, std)
+    assert ei.value.name == "ENOVA_ERR_INSUFFICIENT_HISTORY"
+
+
+def test_surge_and_drop_flags(E):                 # S:527-529 with a constructed detector
+    W, M, H, Z = 32, 8, 32, 4
+    d = detectors.mean_detector(W, M, H, Z, alpha=1.0, beta=2.0)
+    r = np.random.default_rng(12)
+    T = 4000
+    X = r.standard_normal((1, T, M)).astype(np.float32)
+    X[0, 3000:3000 + W, :] += 5.0
+    X[0, 3500:3500 + W, :] -= 3.0
+    det = E.PreparedDetector(d)
+    res = E.run_pipeline(cuda(X), det, 2000)
+    f = res.flags.cpu().numpy()[0]
+    assert f[3000 + W - 1 - 2000] == 1 and f[3500 + W - 1 - 2000] == -1
+    ref = O.detect_pipeline(X, d, 2000)
+    assert_flags(f[None], ref["flags"], ref["scores"], ref["md"], ref["threshold"]["z_q"])
+
+
+# ----------------------------------------------------------------- a-10 ----
+def test_streaming_ring_matches_batch(E):
+    W, M, H, Z = 64, 16, 128, 16
+    N, T = 300, 200
+    X = synth.metric_trace(N, T, M, seed=41)
+    wts = synth.detector_weights(W, M, H, Z, seed=41)
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    mean, std, _ = E.compute_stats(Xc, 150)
+    thr = {"z_q": 2.0}
+    fb, sb, mb = E.detect(Xc, det, mean, std, thr, return_scores=True)
+    ring = torch.zeros((N, 2 * W, M), dtype=torch.float32, device="cuda")
+    for k in range(T):
+        E.ring_push(ring, Xc[:, k, :].contiguous(), k)
+        if k >= W - 1:
+            view = E.ring_view(ring, k)
+            f, s, m = E.detect(view, det, mean, std, thr, W - 1, W, return_scores=True)
+            assert torch.equal(s[:, 0], sb[:, k - W + 1])
+            assert torch.equal(f[:, 0], fb[:, k - W + 1])
