@@ -182,6 +182,9 @@ void enova_comm_destroy(enova_comm_t comm);
 
 /* ------------------------------------------------------------- misc ---- */
 const char *enova_status_string(enova_status s);
+/* Number of CUDA kernels this library has launched in this process (all
+ * devices, monotonically increasing; diagnostic for benchmarks). */
+uint64_t enova_kernel_launches(void);
 const char *enova_last_error(void);
 int enova_abi_version(void);
 

@@ -25,7 +25,7 @@ EXPORTS = (
     "enova_compute_stats", "enova_score_windows", "enova_threshold_workspace_bytes",
     "enova_fit_threshold", "enova_detect", "enova_ring_push", "enova_comm_unique_id",
     "enova_comm_create", "enova_comm_destroy", "enova_status_string", "enova_last_error",
-    "enova_abi_version",
+    "enova_abi_version", "enova_kernel_launches",
 )
 
 
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
             "enova_status_string": (C.c_char_p, [C.c_int]),
             "enova_last_error": (C.c_char_p, []),
             "enova_abi_version": (C.c_int, []),
+            "enova_kernel_launches": (C.c_uint64, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

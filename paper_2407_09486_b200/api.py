@@ -68,12 +68,15 @@ def _series(metrics: torch.Tensor, mean=None, std=None, t_begin=0, t_end=0) -> S
     return s
 
 
-def compute_stats(metrics: torch.Tensor, t_cal_end: int, stream=None):
+def compute_stats(metrics: torch.Tensor, t_cal_end: int, *, out=None, stream=None):
     """a-1: per-(instance, metric) mean / std over [0, t_cal_end)."""
     N, T, M = metrics.shape
     s = _series(metrics)
-    mean = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
-    std = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+    if out is None:
+        mean = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+        std = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+    else:
+        mean, std = out
     nb = int(lib().enova_stats_workspace_bytes(N, M))
     ws = torch.empty(nb, dtype=torch.uint8, device=metrics.device)
     ndeg = C.c_int64(0)
@@ -239,7 +242,7 @@ def run_pipeline(metrics: torch.Tensor, det: PreparedDetector, t_cal_end: int,
     calibration windows (ending in [W-1, t_cal_end)) -> fleet-wide POT threshold
     -> flags (and scores/MD) of the windows ending in [t_cal_end, T)."""
     T = metrics.shape[1]
-    mean, std, nd = compute_stats(metrics, t_cal_end, stream)
+    mean, std, nd = compute_stats(metrics, t_cal_end, stream=stream)
     cal, _ = score_windows(metrics, det, mean, std, det.window - 1, t_cal_end, with_md=False,
                            stream=stream)
     thr = fit_threshold(cal, init_quantile, risk_q, comm=comm, workspace=workspace, stream=stream)

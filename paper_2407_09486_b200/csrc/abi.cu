@@ -2,6 +2,7 @@
 // workspace sizing and launch sequencing.  No allocation on the hot path.
 #include <math.h>
 
+#include <atomic>
 #include <string>
 
 #include "comm.h"
@@ -11,6 +12,9 @@
 namespace enova {
 
 static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -117,6 +121,8 @@ using namespace enova;
 extern "C" {
 
 int enova_abi_version(void) { return ENOVA_ABI_VERSION; }
+
+uint64_t enova_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char *enova_last_error(void) { return g_last_error.c_str(); }
 

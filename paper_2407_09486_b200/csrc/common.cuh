@@ -31,6 +31,11 @@ enova_status cuda_status(cudaError_t e, const char *what);
     }                                                                     \
   } while (0)
 
+void count_launch();
+// kernel launch + diagnostic launch counter (enova_kernel_launches)
+#define ENOVA_LAUNCH(kern, grid, block, smem, stream, ...) \
+  (::enova::count_launch(), kern<<<grid, block, smem, stream>>>(__VA_ARGS__))
+
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ---------------------------------------------------------------- device ----

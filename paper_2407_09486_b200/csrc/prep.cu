@@ -93,17 +93,17 @@ __global__ void k_colsum(const float *__restrict__ w2, const float *__restrict__
 enova_status prepare_detector(const enova_detector *det, const DetLayout &L, void *ws,
                               cudaStream_t st) {
   char *base = static_cast<char *>(ws);
-  k_pack_w1<<<296, 256, 0, st>>>(det->enc_w1, reinterpret_cast<__half *>(base + L.off_w1), L.H,
+  ENOVA_LAUNCH(k_pack_w1, 296, 256, 0, st, det->enc_w1, reinterpret_cast<__half *>(base + L.off_w1), L.H,
                                  L.D);
-  k_pack_heads<<<16, 256, 0, st>>>(det->enc_wmu, det->enc_wlv,
+  ENOVA_LAUNCH(k_pack_heads, 16, 256, 0, st, det->enc_wmu, det->enc_wlv,
                                    reinterpret_cast<__half *>(base + L.off_heads), L.H, L.Z, L.ZP);
-  k_pack_w3<<<8, 256, 0, st>>>(det->dec_w1, reinterpret_cast<__half *>(base + L.off_w3), L.H,
+  ENOVA_LAUNCH(k_pack_w3, 8, 256, 0, st, det->dec_w1, reinterpret_cast<__half *>(base + L.off_w3), L.H,
                                L.Z);
-  k_pack_vectors<<<1, 256, 0, st>>>(det->enc_b1, det->enc_bmu, det->enc_blv, det->dec_b1,
+  ENOVA_LAUNCH(k_pack_vectors, 1, 256, 0, st, det->enc_b1, det->enc_bmu, det->enc_blv, det->dec_b1,
                                     reinterpret_cast<float *>(base + L.off_b1),
                                     reinterpret_cast<float *>(base + L.off_bml),
                                     reinterpret_cast<float *>(base + L.off_b3), L.H, L.Z, L.ZP);
-  k_colsum<<<L.H + 1, 256, 0, st>>>(det->dec_w2, det->dec_b2,
+  ENOVA_LAUNCH(k_colsum, L.H + 1, 256, 0, st, det->dec_w2, det->dec_b2,
                                     reinterpret_cast<float *>(base + L.off_wbar),
                                     reinterpret_cast<double *>(base + L.off_bbar), L.H, L.D);
   ENOVA_CUDA_TRY(cudaGetLastError());

@@ -28,7 +28,7 @@ enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample
   int64_t total = n * (M / 4);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_ring_push<<<blocks, 256, 0, st>>>(ring, n, W, M, sample, tick);
+  ENOVA_LAUNCH(k_ring_push, blocks, 256, 0, st, ring, n, W, M, sample, tick);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }

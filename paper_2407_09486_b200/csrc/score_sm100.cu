@@ -391,7 +391,7 @@ static enova_status launch_score_t(const ScoreParams &p, cudaStream_t st) {
     set_error("too many tiles for one launch");
     return ENOVA_ERR_UNSUPPORTED;
   }
-  kern<<<(unsigned)grid, 128, smem, st>>>(p);
+  ENOVA_LAUNCH(kern, (unsigned)grid, 128, smem, st, p);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }

@@ -570,17 +570,17 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
 
   // K3: radix select of the k-th smallest key (3 digit passes)
   ENOVA_CUDA_TRY(cudaMemsetAsync(hist, 0, kBins * 8, st));
-  k_sel_init<<<1, 1, 0, st>>>(sel, (unsigned long long)k);
+  ENOVA_LAUNCH(k_sel_init, 1, 1, 0, st, sel, (unsigned long long)k);
   const int shifts[3] = {21, 10, 0};
   const int nbins[3] = {2048, 2048, 1024};
   const int hblocks = 148 * 4;
   for (int pass = 0; pass < 3; ++pass) {
-    if (n_local > 0) k_hist<<<hblocks, 512, 0, st>>>(scores, n_local, sel, hist, shifts[pass], nbins[pass]);
+    if (n_local > 0) ENOVA_LAUNCH(k_hist, hblocks, 512, 0, st, scores, n_local, sel, hist, shifts[pass], nbins[pass]);
     if (comm) {
       enova_status s = comm_allreduce_u64_sum(comm, hist, hist, (size_t)nbins[pass], st);
       if (s) return s;
     }
-    k_select<<<1, kSelThreads, 0, st>>>(hist, sel, shifts[pass], nbins[pass]);
+    ENOVA_LAUNCH(k_select, 1, kSelThreads, 0, st, hist, sel, shifts[pass], nbins[pass]);
   }
   ENOVA_CUDA_TRY(cudaGetLastError());
 
@@ -588,8 +588,8 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   double *ydst = comm ? ylocal : yall;
   int64_t nt_local = 0;
   if (n_local > 0) {
-    k_count_peaks<<<kCompactBlocks, kCompactThreads, 0, st>>>(scores, n_local, sel, counts);
-    k_scan_counts<<<1, 32, 0, st>>>(counts, kCompactBlocks);
+    ENOVA_LAUNCH(k_count_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel, counts);
+    ENOVA_LAUNCH(k_scan_counts, 1, 32, 0, st, counts, kCompactBlocks);
     long long h_tot = 0;
     ENOVA_CUDA_TRY(cudaMemcpyAsync(&h_tot, counts + kCompactBlocks, 8, cudaMemcpyDeviceToHost, st));
     ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
@@ -598,7 +598,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
       set_error("peak count exceeds workspace capacity");
       return ENOVA_ERR_WORKSPACE;
     }
-    k_scatter_peaks<<<kCompactBlocks, kCompactThreads, 0, st>>>(scores, n_local, sel, counts, ydst);
+    ENOVA_LAUNCH(k_scatter_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel, counts, ydst);
     ENOVA_CUDA_TRY(cudaGetLastError());
   }
   int64_t nt = nt_local;
@@ -628,9 +628,9 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   }
 
   // K5: GPD fit (replicated, deterministic)
-  k_fit_init<<<1, 1, 0, st>>>(fit, nt, n, sel, q);
-  k_ystats<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);
-  k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);  // grid scan
+  ENOVA_LAUNCH(k_fit_init, 1, 1, 0, st, fit, nt, n, sel, q);
+  ENOVA_LAUNCH(k_ystats, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);
+  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);  // grid scan
   int iters = 0;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&iters, &fit->iters, sizeof(int), cudaMemcpyDeviceToHost, st));
   int overflow = 0;
@@ -640,8 +640,8 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     set_error("more than 64 Grimshaw roots");
     return ENOVA_ERR_UNSUPPORTED;
   }
-  for (int i = 0; i < iters; ++i) k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);
-  k_fit_eval<<<kFitBlocks, kFitThreads, 0, st>>>(yall, nt, fit, partials);  // final candidates
+  for (int i = 0; i < iters; ++i) ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);
+  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);  // final candidates
   ENOVA_CUDA_TRY(cudaGetLastError());
   struct {
     double gamma, sigma, z_q;
