@@ -10,11 +10,11 @@
 
 namespace enova {
 
-__global__ void k_series_stats(const float *__restrict__ X, int64_t ld, int M, int64_t T_cal,
+__global__ void __launch_bounds__(1024) k_series_stats(const float *__restrict__ X, int64_t ld, int M, int64_t T_cal,
                                float *__restrict__ mean_out, float *__restrict__ std_out,
                                unsigned long long *__restrict__ counters) {
   extern __shared__ double red[];  // [nslots][M]
-  __shared__ double mean_s[64];
+  __shared__ double mean_s[256];
   const int G = M / 4;
   const int g = threadIdx.x % G;
   const int slot = threadIdx.x / G;
@@ -24,7 +24,18 @@ __global__ void k_series_stats(const float *__restrict__ X, int64_t ld, int M, i
 
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   int bad = 0;
-  for (int64_t t = slot; t < T_cal; t += nslots) {
+  int64_t t = slot;
+  for (; t + 3 * nslots < T_cal; t += 4 * nslots) {   // 4 independent 128-bit loads in flight
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(base + (t + u * nslots) * G + g);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= !(isfinite(v[u].x) && isfinite(v[u].y) && isfinite(v[u].z) && isfinite(v[u].w));
+      s0 += v[u].x; s1 += v[u].y; s2 += v[u].z; s3 += v[u].w;
+    }
+  }
+  for (; t < T_cal; t += nslots) {
     float4 v = __ldg(base + t * G + g);
     bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
     s0 += v.x; s1 += v.y; s2 += v.z; s3 += v.w;
@@ -43,7 +54,17 @@ __global__ void k_series_stats(const float *__restrict__ X, int64_t ld, int M, i
   const double m0 = mean_s[4 * g], m1 = mean_s[4 * g + 1], m2 = mean_s[4 * g + 2],
                m3 = mean_s[4 * g + 3];
   s0 = s1 = s2 = s3 = 0;
-  for (int64_t t = slot; t < T_cal; t += nslots) {
+  for (t = slot; t + 3 * nslots < T_cal; t += 4 * nslots) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(base + (t + u * nslots) * G + g);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double d0 = v[u].x - m0, d1 = v[u].y - m1, d2 = v[u].z - m2, d3 = v[u].w - m3;
+      s0 += d0 * d0; s1 += d1 * d1; s2 += d2 * d2; s3 += d3 * d3;
+    }
+  }
+  for (; t < T_cal; t += nslots) {
     float4 v = __ldg(base + t * G + g);
     double d0 = v.x - m0, d1 = v.y - m1, d2 = v.z - m2, d3 = v.w - m3;
     s0 += d0 * d0; s1 += d1 * d1; s2 += d2 * d2; s3 += d3 * d3;
@@ -72,7 +93,7 @@ enova_status compute_stats(const enova_series *s, int64_t t_cal_end, float *mean
                            int64_t *n_degenerate, void *ws, cudaStream_t st) {
   const int M = s->n_metrics;
   const int G = M / 4;
-  const int nthreads = G * (256 / G);
+  const int nthreads = G * (1024 / G);
   const int nslots = nthreads / G;
   unsigned long long *counters = static_cast<unsigned long long *>(ws);
   ENOVA_CUDA_TRY(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));

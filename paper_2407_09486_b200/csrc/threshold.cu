@@ -208,22 +208,41 @@ __global__ void k_count_peaks(const float *__restrict__ x, int64_t n,
   }
 }
 
-// exclusive scan of nblk counts in place; total at counts[nblk]
+// exclusive scan of nblk (<= 2048) counts in place; total at counts[nblk].
+// One block of 1024 threads, two counts per thread (warp shuffles + warp totals).
 __global__ void k_scan_counts(long long *counts, int nblk) {
-  if (threadIdx.x == 0) {
-    long long run = 0;
-    for (int b = 0; b < nblk; ++b) {
-      long long c = counts[b];
-      counts[b] = run;
-      run += c;
-    }
-    counts[nblk] = run;
+  __shared__ long long warp_tot[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long c0 = (2 * tid < nblk) ? counts[2 * tid] : 0;
+  long long c1 = (2 * tid + 1 < nblk) ? counts[2 * tid + 1] : 0;
+  long long v = c0 + c1, incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    long long wv = warp_tot[lane], wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    warp_tot[lane] = wi - wv;
+    if (lane == 31) counts[nblk] = wi;
+  }
+  __syncthreads();
+  const long long before = warp_tot[warp] + incl - v;
+  if (2 * tid < nblk) counts[2 * tid] = before;
+  if (2 * tid + 1 < nblk) counts[2 * tid + 1] = before + c0;
 }
 
 __global__ void k_scatter_peaks(const float *__restrict__ x, int64_t n,
                                 const SelState *__restrict__ sel,
-                                const long long *__restrict__ offsets, double *__restrict__ Y) {
+                                const long long *__restrict__ offsets, double *__restrict__ Y,
+                                int64_t cap) {
   __shared__ int woff[kCompactThreads / 32 + 1];
   int64_t b0, b1;
   chunk_of(n, &b0, &b1);
@@ -247,7 +266,10 @@ __global__ void k_scatter_peaks(const float *__restrict__ x, int64_t n,
       woff[nw] = run;
     }
     __syncthreads();
-    if (f) Y[base + woff[warp] + __popc(bal & ((1u << lane) - 1u))] = s - t;
+    if (f) {
+      const long long o = base + woff[warp] + __popc(bal & ((1u << lane) - 1u));
+      if (o < cap) Y[o] = s - t;
+    }
     base += woff[nw];
     __syncthreads();
   }
@@ -299,9 +321,11 @@ __device__ void setup_grid(FitState *f) {
   f->phase = PH_GRID;
 }
 
-__global__ void k_ystats(const double *__restrict__ Y, int64_t nt, FitState *f,
+__global__ void k_ystats(const double *__restrict__ Y, FitState *f,
                          double *__restrict__ partials) {
   __shared__ double scratch[32];
+  const int64_t nt = f->nt;
+  if (f->phase == PH_DONE) return;
   int64_t b0, b1;
   chunk_of(nt, &b0, &b1);
   double s = 0.0, mn = INFINITY, mx = -INFINITY;
@@ -463,30 +487,35 @@ __device__ void controller(FitState *f) {
   }
 }
 
-// evaluate P(x) = mean(-xY/(1+xY)) and L(x) = mean(log1p(xY)) at state->xs; the
-// last block combines the per-block partials in block order and runs the controller
-__global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, int64_t nt,
-                                                          FitState *f,
+// evaluate P(x) = mean(-xY/(1+xY)) and L(x) = mean(log1p(xY)) at state->xs.
+// Each warp owns a subset of the points and sweeps the block's chunk of Y with
+// its 32 lanes (fixed order, xor-shuffle reduce); the last block combines the
+// per-block partials in block order and runs the controller.
+__global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, FitState *f,
                                                           double *__restrict__ partials) {
   __shared__ double xs[kMaxPts];
-  __shared__ double scratch[32];
-  if (f->phase == PH_DONE) return;
+  const int64_t nt = f->nt;
+  if (f->phase == PH_DONE || nt < 10) return;
   const int npts = f->npts;
   for (int i = threadIdx.x; i < npts; i += blockDim.x) xs[i] = f->xs[i];
   __syncthreads();
   int64_t b0, b1;
   chunk_of(nt, &b0, &b1);
-  for (int pt = 0; pt < npts; ++pt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int pt = warp; pt < npts; pt += nwarps) {
     const double x = xs[pt];
     double P = 0.0, L = 0.0;
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    for (int64_t i = b0 + lane; i < b1; i += 32) {
       const double xy = x * Y[i];
       P += -xy / (1.0 + xy);
       L += log1p(xy);
     }
-    P = block_reduce(P, [](double a, double b) { return a + b; }, scratch);
-    L = block_reduce(L, [](double a, double b) { return a + b; }, scratch);
-    if (threadIdx.x == 0) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      P += __shfl_xor_sync(0xffffffffu, P, o);
+      L += __shfl_xor_sync(0xffffffffu, L, o);
+    }
+    if (lane == 0) {
       partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 0] = P;
       partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 1] = L;
     }
@@ -512,31 +541,45 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restri
   }
 }
 
-__global__ void k_fit_init(FitState *f, int64_t nt, int64_t n, const SelState *sel, double q) {
-  f->nt = nt;
+__global__ void k_fit_init(FitState *f, const long long *nt, int64_t n, const SelState *sel,
+                           double q, int64_t cap) {
+  f->nt = *nt;
   f->n = n;
   f->t = (double)sel->t;
   f->q = q;
   f->counter = 0;
   f->overflow = 0;
-  f->phase = PH_GRID;
+  f->phase = (f->nt < 10 || f->nt > cap) ? PH_DONE : PH_GRID;
   f->npts = 0;
+  f->iters = 0;
 }
 
 // ------------------------------------------------------------- driver ----
+// Host syncs: single GPU 2 (after the grid scan: N_t, iteration count; at the
+// end: the result).  With a communicator 2 more (global n; tail counts for the
+// rank-ordered allgatherv).
 enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
                            enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
                            int64_t n_global_max, cudaStream_t st) {
   char *b = static_cast<char *>(ws);
-  // global n
-  int64_t n = n_local;
-  unsigned long long *nbuf = reinterpret_cast<unsigned long long *>(b + 0);  // placeholder
-  ThrLayout L = thr_layout(n_global_max, q0);
+  const ThrLayout L = thr_layout(n_global_max, q0);
   if (ws_bytes < L.total) {
     set_error("threshold workspace too small");
     return ENOVA_ERR_WORKSPACE;
   }
-  nbuf = reinterpret_cast<unsigned long long *>(b + L.nbuf);
+  unsigned long long *nbuf = reinterpret_cast<unsigned long long *>(b + L.nbuf);
+  unsigned long long *hist = reinterpret_cast<unsigned long long *>(b + L.hist);
+  SelState *sel = reinterpret_cast<SelState *>(b + L.sel);
+  FitState *fit = reinterpret_cast<FitState *>(b + L.fit);
+  double *partials = reinterpret_cast<double *>(b + L.partials);
+  long long *counts = reinterpret_cast<long long *>(b + L.counts);
+  long long *counts_all = reinterpret_cast<long long *>(b + L.counts_all);
+  double *ylocal = reinterpret_cast<double *>(b + L.ylocal);
+  double *yall = reinterpret_cast<double *>(b + L.yall);
+  long long *nt_dev = counts + kCompactBlocks;  // total written by k_scan_counts
+
+  // global n
+  int64_t n = n_local;
   if (comm) {
     unsigned long long hn = (unsigned long long)n_local;
     ENOVA_CUDA_TRY(cudaMemcpyAsync(nbuf, &hn, 8, cudaMemcpyHostToDevice, st));
@@ -559,89 +602,90 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     set_error("init_quantile out of range");
     return ENOVA_ERR_INVALID_ARGUMENT;
   }
-  unsigned long long *hist = reinterpret_cast<unsigned long long *>(b + L.hist);
-  SelState *sel = reinterpret_cast<SelState *>(b + L.sel);
-  FitState *fit = reinterpret_cast<FitState *>(b + L.fit);
-  double *partials = reinterpret_cast<double *>(b + L.partials);
-  long long *counts = reinterpret_cast<long long *>(b + L.counts);
-  long long *counts_all = reinterpret_cast<long long *>(b + L.counts_all);
-  double *ylocal = reinterpret_cast<double *>(b + L.ylocal);
-  double *yall = reinterpret_cast<double *>(b + L.yall);
 
-  // K3: radix select of the k-th smallest key (3 digit passes)
+  // K3: radix select of the k-th smallest key (3 digit passes, exact)
   ENOVA_CUDA_TRY(cudaMemsetAsync(hist, 0, kBins * 8, st));
   ENOVA_LAUNCH(k_sel_init, 1, 1, 0, st, sel, (unsigned long long)k);
   const int shifts[3] = {21, 10, 0};
   const int nbins[3] = {2048, 2048, 1024};
   const int hblocks = 148 * 4;
   for (int pass = 0; pass < 3; ++pass) {
-    if (n_local > 0) ENOVA_LAUNCH(k_hist, hblocks, 512, 0, st, scores, n_local, sel, hist, shifts[pass], nbins[pass]);
+    if (n_local > 0)
+      ENOVA_LAUNCH(k_hist, hblocks, 512, 0, st, scores, n_local, sel, hist, shifts[pass],
+                   nbins[pass]);
     if (comm) {
       enova_status s = comm_allreduce_u64_sum(comm, hist, hist, (size_t)nbins[pass], st);
       if (s) return s;
     }
     ENOVA_LAUNCH(k_select, 1, kSelThreads, 0, st, hist, sel, shifts[pass], nbins[pass]);
   }
-  ENOVA_CUDA_TRY(cudaGetLastError());
 
-  // K4: stable compaction of the peaks
+  // K4: stable compaction of the peaks (bounded by the workspace capacity)
   double *ydst = comm ? ylocal : yall;
-  int64_t nt_local = 0;
   if (n_local > 0) {
-    ENOVA_LAUNCH(k_count_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel, counts);
-    ENOVA_LAUNCH(k_scan_counts, 1, 32, 0, st, counts, kCompactBlocks);
-    long long h_tot = 0;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(&h_tot, counts + kCompactBlocks, 8, cudaMemcpyDeviceToHost, st));
-    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-    nt_local = h_tot;
-    if (nt_local > L.cap) {
-      set_error("peak count exceeds workspace capacity");
-      return ENOVA_ERR_WORKSPACE;
-    }
-    ENOVA_LAUNCH(k_scatter_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel, counts, ydst);
-    ENOVA_CUDA_TRY(cudaGetLastError());
+    ENOVA_LAUNCH(k_count_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel,
+                 counts);
+    ENOVA_LAUNCH(k_scan_counts, 1, 1024, 0, st, counts, kCompactBlocks);
+    ENOVA_LAUNCH(k_scatter_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel,
+                 counts, ydst, L.cap);
+  } else {
+    ENOVA_CUDA_TRY(cudaMemsetAsync(nt_dev, 0, 8, st));
   }
-  int64_t nt = nt_local;
+  ENOVA_CUDA_TRY(cudaGetLastError());
   if (comm) {
-    long long *my = counts + kCompactBlocks;  // device copy of nt_local
-    if (n_local == 0) ENOVA_CUDA_TRY(cudaMemsetAsync(my, 0, 8, st));
-    enova_status s = comm_allgather_i64(comm, my, counts_all, st);
+    enova_status s = comm_allgather_i64(comm, nt_dev, counts_all, st);
     if (s) return s;
     std::vector<int64_t> hc(comm->world), off(comm->world);
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts_all, 8 * comm->world, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts_all, 8 * comm->world,
+                                   cudaMemcpyDeviceToHost, st));
     ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-    nt = 0;
+    int64_t tot = 0;
     for (int r = 0; r < comm->world; ++r) {
-      off[r] = nt;
-      nt += hc[r];
+      off[r] = tot;
+      if (hc[r] > L.cap) {
+        set_error("peak count exceeds workspace capacity");
+        return ENOVA_ERR_WORKSPACE;
+      }
+      tot += hc[r];
     }
-    if (nt > L.cap) {
+    if (tot > L.cap) {
       set_error("peak count exceeds workspace capacity");
       return ENOVA_ERR_WORKSPACE;
     }
     s = comm_allgatherv_f64(comm, ylocal, yall, hc.data(), off.data(), st);
     if (s) return s;
+    long long tl = tot;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(nbuf + 1, &tl, 8, cudaMemcpyHostToDevice, st));
+    nt_dev = reinterpret_cast<long long *>(nbuf + 1);
   }
-  if (nt < 10) {
+
+  // K5: GPD fit (replicated, deterministic); N_t read on the device
+  ENOVA_LAUNCH(k_fit_init, 1, 1, 0, st, fit, nt_dev, n, sel, q, L.cap);
+  ENOVA_LAUNCH(k_ystats, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
+  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // grid scan
+  struct {
+    int64_t nt;
+    int iters, overflow;
+  } h;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.nt, &fit->nt, 8, cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.iters, &fit->iters, 4, cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.overflow, &fit->overflow, 4, cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h.nt > L.cap) {
+    set_error("peak count exceeds workspace capacity");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if (h.nt < 10) {
     set_error("fewer than 10 exceedances above the initial threshold");
     return ENOVA_ERR_TOO_FEW_EXCEEDANCES;
   }
-
-  // K5: GPD fit (replicated, deterministic)
-  ENOVA_LAUNCH(k_fit_init, 1, 1, 0, st, fit, nt, n, sel, q);
-  ENOVA_LAUNCH(k_ystats, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);
-  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);  // grid scan
-  int iters = 0;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&iters, &fit->iters, sizeof(int), cudaMemcpyDeviceToHost, st));
-  int overflow = 0;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&overflow, &fit->overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-  if (overflow) {
+  if (h.overflow) {
     set_error("more than 64 Grimshaw roots");
     return ENOVA_ERR_UNSUPPORTED;
   }
-  for (int i = 0; i < iters; ++i) ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);
-  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, nt, fit, partials);  // final candidates
+  for (int i = 0; i < h.iters; ++i)
+    ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
+  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // candidates
   ENOVA_CUDA_TRY(cudaGetLastError());
   struct {
     double gamma, sigma, z_q;
@@ -658,7 +702,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   out->sigma = res.sigma;
   out->z_q = res.z_q;
   out->n = n;
-  out->n_peaks = nt;
+  out->n_peaks = h.nt;
   out->method = res.method;
   out->reserved = 0;
   return ENOVA_OK;
