@@ -17,6 +17,9 @@ struct DetLayout {
   size_t off_w1, off_heads, off_w3;        // fp16 canonical UMMA B images
   size_t off_b1, off_bml, off_b3, off_wbar; // fp32 vectors
   size_t off_bbar;                           // fp64 scalar
+  // CTA-pair (cta_group::2) images: rank r holds B rows [r*N/2, (r+1)*N/2)
+  size_t off_w1p, off_headsp, off_w3p;
+  bool pair_ok;                              // W1 half fits in shared memory
   size_t total;
 };
 
@@ -41,6 +44,10 @@ static inline bool det_layout(int W, int M, int H, int Z, DetLayout *L) {
   L->off_b3 = take((size_t)H * 4);
   L->off_wbar = take((size_t)H * 4);
   L->off_bbar = take(8);
+  L->off_w1p = take((size_t)H * L->D * 2);
+  L->off_headsp = take((size_t)L->N2 * H * 2);
+  L->off_w3p = take((size_t)H * 16 * 2);
+  L->pair_ok = ((size_t)(H / 2) * L->D * 2) <= 128 * 1024;
   L->total = o;
   return true;
 }
@@ -52,6 +59,14 @@ __host__ __device__ static inline size_t kmajor_step_offset(int n, int k, int N)
   int q = k >> 4, kk = k & 15;
   return (size_t)q * 32 * N + (size_t)(kk >> 3) * 16 * N + (size_t)(n >> 3) * 128 +
          (size_t)(n & 7) * 16 + (size_t)(kk & 7) * 2;
+}
+
+// Pair image: B rows split in two halves of N/2 (one per CTA of a cta_group::2
+// pair); each half is a back-to-back K-step image with N/2 rows.
+__host__ __device__ static inline size_t pair_offset(int n, int k, int N, int K) {
+  const int half = N / 2;
+  const int r = n / half, nl = n - r * half;
+  return (size_t)r * half * K * 2 + kmajor_step_offset(nl, k, half);
 }
 
 }  // namespace enova

@@ -90,6 +90,38 @@ __global__ void k_colsum(const float *__restrict__ w2, const float *__restrict__
   }
 }
 
+// CTA-pair images (pair_offset): W1 [H][D], heads [N2][H] (mu rows | lv rows),
+// W3 [H][16] (z >= Z zero padded)
+__global__ void k_pack_pair(const float *__restrict__ w1, const float *__restrict__ wmu,
+                            const float *__restrict__ wlv, const float *__restrict__ w3,
+                            __half *__restrict__ w1p, __half *__restrict__ hp,
+                            __half *__restrict__ w3p, int H, int D, int Z, int ZP) {
+  const int N2 = 2 * ZP;
+  const size_t n1 = (size_t)H * D, n2 = (size_t)N2 * H, n3 = (size_t)H * 16;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n1 + n2 + n3;
+       e += (size_t)gridDim.x * blockDim.x) {
+    if (e < n1) {
+      int n = (int)(e / D), k = (int)(e % D);
+      w1p[pair_offset(n, k, H, D) / 2] = __float2half_rn(w1[e]);
+    } else if (e < n1 + n2) {
+      int f = (int)(e - n1);
+      int n = f / H, k = f % H;
+      float v = 0.f;
+      if (n < ZP) {
+        if (n < Z) v = wmu[n * H + k];
+      } else if (n - ZP < Z) {
+        v = wlv[(n - ZP) * H + k];
+      }
+      hp[pair_offset(n, k, N2, H) / 2] = __float2half_rn(v);
+    } else {
+      int f = (int)(e - n1 - n2);
+      int n = f / 16, k = f % 16;
+      float v = k < Z ? w3[n * Z + k] : 0.f;
+      w3p[pair_offset(n, k, H, 16) / 2] = __float2half_rn(v);
+    }
+  }
+}
+
 enova_status prepare_detector(const enova_detector *det, const DetLayout &L, void *ws,
                               cudaStream_t st) {
   char *base = static_cast<char *>(ws);
@@ -106,6 +138,10 @@ enova_status prepare_detector(const enova_detector *det, const DetLayout &L, voi
   ENOVA_LAUNCH(k_colsum, L.H + 1, 256, 0, st, det->dec_w2, det->dec_b2,
                                     reinterpret_cast<float *>(base + L.off_wbar),
                                     reinterpret_cast<double *>(base + L.off_bbar), L.H, L.D);
+  ENOVA_LAUNCH(k_pack_pair, 296, 256, 0, st, det->enc_w1, det->enc_wmu, det->enc_wlv, det->dec_w1,
+               reinterpret_cast<__half *>(base + L.off_w1p),
+               reinterpret_cast<__half *>(base + L.off_headsp),
+               reinterpret_cast<__half *>(base + L.off_w3p), L.H, L.D, L.Z, L.ZP);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }

@@ -24,6 +24,9 @@
 //
 // Two CTAs share an SM (<= ~95 KB smem, 256 TMEM columns each) so one CTA's
 // epilogue overlaps the other's GEMM1.
+#include <stdlib.h>
+#include <string.h>
+
 #include "common.cuh"
 #include "layout.h"
 
@@ -396,8 +399,27 @@ static enova_status launch_score_t(const ScoreParams &p, cudaStream_t st) {
   return ENOVA_OK;
 }
 
+bool pair_path_ok(const DetLayout &L);
+enova_status launch_score_pair(const enova_series *s, const DetLayout &L, const void *det_ws,
+                               float *scores, float *md, int8_t *flags, double z_q,
+                               cudaStream_t st);
+
+// Kernel choice by shape: the weight-stationary CTA-pair kernel whenever half of
+// W1 fits in shared memory (all BASELINE configs), else the W1-streaming kernel.
+// ENOVA_SCORE_KERNEL=stream forces the streaming kernel (diagnostic / A-B tests).
+static bool force_stream() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("ENOVA_SCORE_KERNEL");
+    v = (e && strcmp(e, "stream") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
                           float *scores, float *md, int8_t *flags, double z_q, cudaStream_t st) {
+  if (!force_stream() && pair_path_ok(L))
+    return launch_score_pair(s, L, det_ws, scores, md, flags, z_q, st);
   ScoreParams p{};
   const uint8_t *b = static_cast<const uint8_t *>(det_ws);
   p.X = s->metrics;

@@ -91,6 +91,7 @@ SHAPES = [  # (W, M, H, Z)
     (64, 16, 64, 5),
     (2, 8, 32, 1),
     (10, 16, 128, 9),
+    (128, 32, 128, 16),   # W1 half > 128 KB: W1-streaming kernel
 ]
 
 
@@ -108,6 +109,34 @@ def test_scores_match_oracle_shapes(E, W, M, H, Z):
         if te > tb:
             assert_scores(sc.cpu().numpy(), rs)
             assert_md(md.cpu().numpy(), rmd)
+
+
+def test_streaming_kernel_matches_oracle_c2_slice():
+    """The W1-streaming kernel (forced by ENOVA_SCORE_KERNEL=stream) on the
+    benchmark detector, in a fresh process (the switch is read once)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2407_09486_b200 as E\n"
+        "from paper_2407_09486_b200 import synth\n"
+        "from oracle import enova_oracle as O\n"
+        "X = synth.metric_trace(4, 800, 16, seed=9)\n"
+        "w = synth.detector_weights(64, 16, 128, 16, seed=9)\n"
+        "m, s, _ = O.series_stats(X, 400)\n"
+        "d = E.PreparedDetector(w)\n"
+        "sc, md = E.score_windows(torch.from_numpy(X).cuda(), d, torch.from_numpy(m).cuda(), torch.from_numpy(s).cuda())\n"
+        "rs, rmd = O.score_windows(X, w, m, s, 63, 800)\n"
+        "e = np.abs(sc.cpu().numpy() - rs) / (np.abs(rs) + 1e-6)\n"
+        "f = np.abs(md.cpu().numpy() - rmd)\n"
+        "assert e.max() < 1e-3 and f.max() < 1e-4, (e.max(), f.max())\n"
+        "print('ok', e.max())\n")
+    import os
+    env = dict(os.environ, ENOVA_SCORE_KERNEL="stream")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 def test_strided_instances_and_large_values(E):
