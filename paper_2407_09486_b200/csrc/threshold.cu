@@ -30,7 +30,7 @@ constexpr int kBins = 2048;
 constexpr int kSelThreads = 1024;
 constexpr int kCompactBlocks = 1184;  // 8 per SM
 constexpr int kCompactThreads = 256;
-constexpr int kFitBlocks = 296;
+constexpr int kFitBlocks = 592;   // 4 per SM; blocks beyond ceil(N_t/256) only join the ticket
 constexpr int kFitThreads = 256;
 constexpr int kMaxPts = 128;
 constexpr int kMaxSlots = 64;
@@ -77,7 +77,7 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.hist = take(kBins * 8);
   L.sel = take(sizeof(SelState));
   L.fit = take(sizeof(FitState));
-  L.partials = take((size_t)kFitBlocks * kMaxPts * 2 * 8);
+  L.partials = take((size_t)kFitBlocks * kMaxPts * 2 * 8 + (size_t)kFitBlocks * 3 * 8);
   L.counts = take((kCompactBlocks + 1) * 8);
   L.counts_all = take(1024 * 8);
   L.nbuf = take(16);
@@ -321,41 +321,77 @@ __device__ void setup_grid(FitState *f) {
   f->phase = PH_GRID;
 }
 
-__global__ void k_ystats(const double *__restrict__ Y, FitState *f,
-                         double *__restrict__ partials) {
-  __shared__ double scratch[32];
-  const int64_t nt = f->nt;
+// blocks that hold Y elements: one element per thread per 256-wide sweep
+__device__ __forceinline__ int fit_active_blocks(int64_t nt) {
+  const int64_t a = (nt + 255) / 256;
+  return (int)(a < (int64_t)gridDim.x ? (a < 1 ? 1 : a) : gridDim.x);
+}
+
+// Ybar, Ymin, Ymax with a fixed reduction order (thread partial -> xor tree ->
+// warps in order -> blocks summed by lanes in order -> xor tree)
+__global__ void __launch_bounds__(kFitThreads) k_ystats(const double *__restrict__ Y, FitState *f,
+                                                        double *__restrict__ part) {
+  __shared__ double ws[3][kFitThreads / 32];
   if (f->phase == PH_DONE) return;
-  int64_t b0, b1;
-  chunk_of(nt, &b0, &b1);
-  double s = 0.0, mn = INFINITY, mx = -INFINITY;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    double y = Y[i];
-    s += y;
-    mn = fmin(mn, y);
-    mx = fmax(mx, y);
-  }
-  s = block_reduce(s, [](double a, double b) { return a + b; }, scratch);
-  mn = block_reduce(mn, [](double a, double b) { return fmin(a, b); }, scratch);
-  mx = block_reduce(mx, [](double a, double b) { return fmax(a, b); }, scratch);
-  if (threadIdx.x == 0) {
-    partials[3 * blockIdx.x + 0] = s;
-    partials[3 * blockIdx.x + 1] = mn;
-    partials[3 * blockIdx.x + 2] = mx;
-  }
-  if (last_block_done(&f->counter)) {
+  const int64_t nt = f->nt;
+  const int active = fit_active_blocks(nt);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *pS = part, *pMn = part + kFitBlocks, *pMx = part + 2 * kFitBlocks;
+  if ((int)blockIdx.x < active) {
+    const int64_t chunk = (nt + active - 1) / active;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(nt, b0 + chunk);
+    double s = 0.0, mn = INFINITY, mx = -INFINITY;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const double y = Y[i];
+      s += y;
+      mn = fmin(mn, y);
+      mx = fmax(mx, y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      ws[0][warp] = s;
+      ws[1][warp] = mn;
+      ws[2][warp] = mx;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
       double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
-      for (int b = 0; b < (int)gridDim.x; ++b) {
-        ts += partials[3 * b];
-        tmn = fmin(tmn, partials[3 * b + 1]);
-        tmx = fmax(tmx, partials[3 * b + 2]);
+      for (int w = 0; w < kFitThreads / 32; ++w) {
+        ts += ws[0][w];
+        tmn = fmin(tmn, ws[1][w]);
+        tmx = fmax(tmx, ws[2][w]);
       }
-      f->ybar = ts / (double)nt;
-      f->ymin = tmn;
-      f->ymax = tmx;
-      f->counter = 0;
-      setup_grid(f);
+      pS[blockIdx.x] = ts;
+      pMn[blockIdx.x] = tmn;
+      pMx[blockIdx.x] = tmx;
+    }
+  }
+  if (last_block_done(&f->counter)) {
+    if (warp == 0) {
+      double s = 0.0, mn = INFINITY, mx = -INFINITY;
+      for (int b = lane; b < active; b += 32) {
+        s += pS[b];
+        mn = fmin(mn, pMn[b]);
+        mx = fmax(mx, pMx[b]);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) {
+        f->ybar = s / (double)nt;
+        f->ymin = mn;
+        f->ymax = mx;
+        f->counter = 0;
+        setup_grid(f);
+      }
     }
   }
 }
@@ -488,50 +524,85 @@ __device__ void controller(FitState *f) {
 }
 
 // evaluate P(x) = mean(-xY/(1+xY)) and L(x) = mean(log1p(xY)) at state->xs.
-// Each warp owns a subset of the points and sweeps the block's chunk of Y with
-// its 32 lanes (fixed order, xor-shuffle reduce); the last block combines the
-// per-block partials in block order and runs the controller.
+// Each thread owns elements of Y and sweeps the points four at a time (four
+// independent fp64 chains); per point: xor tree over the warp, warps in order,
+// blocks in order (lanes over blocks + xor tree) -- fixed order, deterministic.
+// The last block finishes the sums and runs the controller.
 __global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, FitState *f,
-                                                          double *__restrict__ partials) {
+                                                          double *__restrict__ part) {
   __shared__ double xs[kMaxPts];
+  __shared__ double wP[kFitThreads / 32][kMaxPts], wL[kFitThreads / 32][kMaxPts];
+  if (f->phase == PH_DONE) return;
   const int64_t nt = f->nt;
-  if (f->phase == PH_DONE || nt < 10) return;
   const int npts = f->npts;
-  for (int i = threadIdx.x; i < npts; i += blockDim.x) xs[i] = f->xs[i];
-  __syncthreads();
-  int64_t b0, b1;
-  chunk_of(nt, &b0, &b1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int pt = warp; pt < npts; pt += nwarps) {
-    const double x = xs[pt];
-    double P = 0.0, L = 0.0;
-    for (int64_t i = b0 + lane; i < b1; i += 32) {
-      const double xy = x * Y[i];
-      P += -xy / (1.0 + xy);
-      L += log1p(xy);
-    }
+  const int active = fit_active_blocks(nt);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *pP = part, *pL = part + (size_t)kMaxPts * kFitBlocks;
+  if ((int)blockIdx.x < active) {
+    for (int i = threadIdx.x; i < npts; i += blockDim.x) xs[i] = f->xs[i];
+    __syncthreads();
+    const int64_t chunk = (nt + active - 1) / active;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(nt, b0 + chunk);
+    for (int pt0 = 0; pt0 < npts; pt0 += 4) {
+      double P[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
+      double x[4];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      P += __shfl_xor_sync(0xffffffffu, P, o);
-      L += __shfl_xor_sync(0xffffffffu, L, o);
+      for (int u = 0; u < 4; ++u) x[u] = (pt0 + u < npts) ? xs[pt0 + u] : 0.0;
+      for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        const double y = Y[i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double xy = x[u] * y;
+          P[u] += -xy / (1.0 + xy);
+          L[u] += log1p(xy);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          P[u] += __shfl_xor_sync(0xffffffffu, P[u], o);
+          L[u] += __shfl_xor_sync(0xffffffffu, L[u], o);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pt0 + u < npts) {
+            wP[warp][pt0 + u] = P[u];
+            wL[warp][pt0 + u] = L[u];
+          }
+      }
     }
-    if (lane == 0) {
-      partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 0] = P;
-      partials[((size_t)blockIdx.x * kMaxPts + pt) * 2 + 1] = L;
+    __syncthreads();
+    for (int pt = threadIdx.x; pt < npts; pt += blockDim.x) {
+      double sP = 0.0, sL = 0.0;
+      for (int w = 0; w < kFitThreads / 32; ++w) {
+        sP += wP[w][pt];
+        sL += wL[w][pt];
+      }
+      pP[(size_t)pt * kFitBlocks + blockIdx.x] = sP;
+      pL[(size_t)pt * kFitBlocks + blockIdx.x] = sL;
     }
   }
   if (last_block_done(&f->counter)) {
     const double N = (double)nt;
-    for (int pt = threadIdx.x; pt < npts; pt += blockDim.x) {
-      double P = 0.0, L = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) {
-        P += partials[((size_t)b * kMaxPts + pt) * 2 + 0];
-        L += partials[((size_t)b * kMaxPts + pt) * 2 + 1];
+    for (int pt = warp; pt < npts; pt += kFitThreads / 32) {
+      double sP = 0.0, sL = 0.0;
+      for (int b = lane; b < active; b += 32) {
+        sP += pP[(size_t)pt * kFitBlocks + b];
+        sL += pL[(size_t)pt * kFitBlocks + b];
       }
-      P /= N;
-      L /= N;
-      f->w[pt] = P + L + P * L;
-      f->L[pt] = L;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        sP += __shfl_xor_sync(0xffffffffu, sP, o);
+        sL += __shfl_xor_sync(0xffffffffu, sL, o);
+      }
+      if (lane == 0) {
+        const double Pm = sP / N, Lm = sL / N;
+        f->w[pt] = Pm + Lm + Pm * Lm;
+        f->L[pt] = Lm;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
