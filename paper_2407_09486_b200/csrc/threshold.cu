@@ -50,8 +50,9 @@ struct FitState {
   double t, q, ybar, ymin, ymax;
   int phase, npts, nslots, S, iters, overflow;
   unsigned int counter, pad;
-  double xs[kMaxPts], w[kMaxPts], L[kMaxPts];
+  double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts];
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots];
+  int converged;
   int exact[kMaxSlots];
   int refine_idx[kMaxSlots];   // slot of the k-th refined bracket
   int nrefine;
@@ -77,7 +78,7 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.hist = take(kBins * 8);
   L.sel = take(sizeof(SelState));
   L.fit = take(sizeof(FitState));
-  L.partials = take((size_t)kFitBlocks * kMaxPts * 2 * 8 + (size_t)kFitBlocks * 3 * 8);
+  L.partials = take((size_t)kFitBlocks * kMaxPts * 4 * 8 + (size_t)kFitBlocks * 3 * 8);
   L.counts = take((kCompactBlocks + 1) * 8);
   L.counts_all = take(1024 * 8);
   L.nbuf = take(16);
@@ -396,9 +397,16 @@ __global__ void __launch_bounds__(kFitThreads) k_ystats(const double *__restrict
   }
 }
 
+// Phase machine run by the last block of each evaluation launch.
+//  GRID  : w at the fixed scan grids -> one slot per sign change (or exact zero);
+//  REFINE: safeguarded Newton on every bracket: w(x), w'(x) from the same pass;
+//          the bracket shrinks with the sign of w(x); the Newton iterate is kept
+//          if it falls strictly inside the bracket, else the bracket midpoint is
+//          used; converged when every step is <= 1e-15 |x| (the oracle bisects
+//          to a 2^-60 bracket: both land on the same root of the fp64 w);
+//  FINAL : L(x) at the roots -> gamma, sigma, log-likelihood; pick; z_q.
 __device__ void controller(FitState *f) {
   if (f->phase == PH_GRID) {
-    // sign changes of w on each grid, in scan order (left grid, then right)
     int ns = 0;
     auto push = [&](double lo, double hi, double wlo, int exact) {
       if (ns >= kMaxSlots) {
@@ -427,54 +435,56 @@ __device__ void controller(FitState *f) {
     for (int s = 0; s < ns; ++s)
       if (!f->exact[s]) f->refine_idx[nr++] = s;
     f->nrefine = nr;
+    f->converged = 0;
     if (nr > 0) {
-      double work = (double)f->nt * nr;
-      int S = work <= 262144.0 ? 31 : (work <= 2097152.0 ? 7 : 1);
-      if (S * nr > kMaxPts) S = kMaxPts / nr;
-      if (S < 1) S = 1;
-      int it = 0;
-      double red = 1.0;
-      while (red < 1152921504606846976.0) {  // 2^60, the oracle's 60 halvings
-        red *= (double)(S + 1);
-        ++it;
+      for (int r = 0; r < nr; ++r) {
+        const int s = f->refine_idx[r];
+        f->xs[r] = 0.5 * (f->lo[s] + f->hi[s]);
       }
-      f->S = S;
-      f->iters = it;
+      f->npts = nr;
       f->phase = PH_REFINE;
     } else {
-      f->S = 0;
-      f->iters = 0;
       f->phase = PH_FINAL;
+      f->converged = 1;
+      for (int s = 0; s < ns; ++s) f->xs[s] = f->lo[s];
+      f->npts = ns;
     }
-  } else if (f->phase == PH_REFINE) {
-    const int S = f->S;
+    return;
+  }
+  if (f->phase == PH_REFINE) {
+    bool all_conv = true;
     for (int r = 0; r < f->nrefine; ++r) {
       const int s = f->refine_idx[r];
-      const double lo = f->lo[s], hi = f->hi[s], wl = f->wlo[s];
-      const bool pos = wl > 0;
-      double nlo = lo, nhi = hi, nwl = wl;
-      int j;
-      for (j = 0; j < S; ++j) {
-        const double wj = f->w[r * S + j];
-        if ((wj > 0) != pos) break;
-      }
-      if (j < S) {
-        nhi = f->xs[r * S + j];
-        if (j > 0) {
-          nlo = f->xs[r * S + j - 1];
-          nwl = f->w[r * S + j - 1];
-        }
+      const double x = f->xs[r], w = f->w[r], dw = f->dw[r];
+      double lo = f->lo[s], hi = f->hi[s];
+      if (w == 0.0) {
+        lo = hi = x;
+      } else if ((w > 0) == (f->wlo[s] > 0)) {
+        lo = x;
+        f->wlo[s] = w;
       } else {
-        nlo = f->xs[r * S + S - 1];
-        nwl = f->w[r * S + S - 1];
+        hi = x;
       }
-      f->lo[s] = nlo;
-      f->hi[s] = nhi;
-      f->wlo[s] = nwl;
+      f->lo[s] = lo;
+      f->hi[s] = hi;
+      double xn = (dw != 0.0) ? x - w / dw : 0.5 * (lo + hi);
+      const double a = fmin(lo, hi), b = fmax(lo, hi);
+      if (!(xn > a && xn < b)) xn = 0.5 * (lo + hi);
+      if (lo == hi) xn = lo;
+      if (!(fabs(xn - x) <= 1e-15 * fabs(x))) all_conv = false;
+      f->xs[r] = xn;
     }
-    f->iters -= 1;
-    if (f->iters <= 0) f->phase = PH_FINAL;
-  } else if (f->phase == PH_FINAL) {
+    if (all_conv) {
+      // every slot's root estimate is final (exact grid zeros keep lo)
+      for (int r = 0; r < f->nrefine; ++r) f->lo[f->refine_idx[r]] = f->xs[r];
+      for (int s = 0; s < f->nslots; ++s) f->xs[s] = f->lo[s];
+      f->npts = f->nslots;
+      f->phase = PH_FINAL;
+      f->converged = 1;
+    }
+    return;
+  }
+  if (f->phase == PH_FINAL) {
     const double N = (double)f->nt;
     double bg = 0.0, bs = f->ybar, bll = -N * (log(f->ybar) + 1.0);
     int method = 1, nroots = 0;
@@ -501,60 +511,57 @@ __device__ void controller(FitState *f) {
     f->nroots = nroots;
     f->z_q = (bg == 0.0) ? f->t - bs * lr : f->t + (bs / bg) * expm1(-bg * lr);
     f->phase = PH_DONE;
-    return;
-  }
-  // next evaluation points
-  if (f->phase == PH_REFINE) {
-    const int S = f->S;
-    for (int r = 0; r < f->nrefine; ++r) {
-      const int s = f->refine_idx[r];
-      const double lo = f->lo[s], hi = f->hi[s];
-      if (S == 1) {
-        f->xs[r] = 0.5 * (lo + hi);
-      } else {
-        for (int j = 0; j < S; ++j) f->xs[r * S + j] = lo + (hi - lo) * (double)(j + 1) / (double)(S + 1);
-      }
-    }
-    f->npts = S * f->nrefine;
-  } else if (f->phase == PH_FINAL) {
-    for (int s = 0; s < f->nslots; ++s)
-      f->xs[s] = f->exact[s] ? f->lo[s] : 0.5 * (f->lo[s] + f->hi[s]);
-    f->npts = f->nslots;
   }
 }
 
-// evaluate P(x) = mean(-xY/(1+xY)) and L(x) = mean(log1p(xY)) at state->xs.
-// Each thread owns elements of Y and sweeps the points four at a time (four
-// independent fp64 chains); per point: xor tree over the warp, warps in order,
-// blocks in order (lanes over blocks + xor tree) -- fixed order, deterministic.
-// The last block finishes the sums and runs the controller.
+// evaluate at state->xs: P = mean(-xY/(1+xY)), L = mean(log1p(xY)) and, in the
+// REFINE phase, their x-derivatives dP = mean(-Y/(1+xY)^2), dL = mean(Y/(1+xY)).
+// Blocks are (element block, group of 16 points); each thread sweeps its
+// elements four points at a time.  Per point: xor tree over the warp, warps in
+// order, element blocks in order (lanes over blocks + xor tree) -- a fixed
+// order, so the result is deterministic.  The last block runs the controller.
+constexpr int kPtsPerGroup = 16;
 __global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, FitState *f,
                                                           double *__restrict__ part) {
   __shared__ double xs[kMaxPts];
-  __shared__ double wP[kFitThreads / 32][kMaxPts], wL[kFitThreads / 32][kMaxPts];
-  if (f->phase == PH_DONE) return;
+  __shared__ double wS[4][kFitThreads / 32][kPtsPerGroup];
+  const int phase = f->phase;
+  if (phase == PH_DONE) return;
   const int64_t nt = f->nt;
   const int npts = f->npts;
-  const int active = fit_active_blocks(nt);
+  const bool deriv = (phase == PH_REFINE);
+  const int npg = npts > 0 ? (npts + kPtsPerGroup - 1) / kPtsPerGroup : 1;
+  const int64_t e_need = (nt + 255) / 256, e_max = (int64_t)(gridDim.x / npg);
+  int E = (int)(e_need < e_max ? e_need : e_max);
+  if (E < 1) E = 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *pP = part, *pL = part + (size_t)kMaxPts * kFitBlocks;
-  if ((int)blockIdx.x < active) {
-    for (int i = threadIdx.x; i < npts; i += blockDim.x) xs[i] = f->xs[i];
+  double *pq[4];
+  for (int k = 0; k < 4; ++k) pq[k] = part + (size_t)k * kMaxPts * kFitBlocks;
+  if ((int)blockIdx.x < E * npg && npts > 0) {
+    const int eb = blockIdx.x / npg, pg = blockIdx.x % npg;
+    const int pt_lo = pg * kPtsPerGroup, pt_hi = min(npts, pt_lo + kPtsPerGroup);
+    for (int i = threadIdx.x; i < pt_hi - pt_lo; i += blockDim.x) xs[i] = f->xs[pt_lo + i];
     __syncthreads();
-    const int64_t chunk = (nt + active - 1) / active;
-    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(nt, b0 + chunk);
-    for (int pt0 = 0; pt0 < npts; pt0 += 4) {
-      double P[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t chunk = (nt + E - 1) / E;
+    const int64_t b0 = (int64_t)eb * chunk, b1 = min(nt, b0 + chunk);
+    for (int q0 = 0; q0 < pt_hi - pt_lo; q0 += 4) {
+      double P[4] = {0, 0, 0, 0}, L[4] = {0, 0, 0, 0}, dP[4] = {0, 0, 0, 0}, dL[4] = {0, 0, 0, 0};
       double x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = (pt0 + u < npts) ? xs[pt0 + u] : 0.0;
+      for (int u = 0; u < 4; ++u) x[u] = (q0 + u < pt_hi - pt_lo) ? xs[q0 + u] : 0.0;
       for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
         const double y = Y[i];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const double xy = x[u] * y;
-          P[u] += -xy / (1.0 + xy);
+          const double r = 1.0 / (1.0 + xy);
+          P[u] -= xy * r;
           L[u] += log1p(xy);
+          if (deriv) {
+            const double yr = y * r;
+            dL[u] += yr;
+            dP[u] -= yr * r;
+          }
         }
       }
 #pragma unroll
@@ -563,45 +570,47 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restri
         for (int o = 16; o; o >>= 1) {
           P[u] += __shfl_xor_sync(0xffffffffu, P[u], o);
           L[u] += __shfl_xor_sync(0xffffffffu, L[u], o);
+          if (deriv) {
+            dP[u] += __shfl_xor_sync(0xffffffffu, dP[u], o);
+            dL[u] += __shfl_xor_sync(0xffffffffu, dL[u], o);
+          }
         }
       }
       if (lane == 0) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (pt0 + u < npts) {
-            wP[warp][pt0 + u] = P[u];
-            wL[warp][pt0 + u] = L[u];
+          if (q0 + u < pt_hi - pt_lo) {
+            wS[0][warp][q0 + u] = P[u];
+            wS[1][warp][q0 + u] = L[u];
+            wS[2][warp][q0 + u] = dP[u];
+            wS[3][warp][q0 + u] = dL[u];
           }
       }
     }
     __syncthreads();
-    for (int pt = threadIdx.x; pt < npts; pt += blockDim.x) {
-      double sP = 0.0, sL = 0.0;
-      for (int w = 0; w < kFitThreads / 32; ++w) {
-        sP += wP[w][pt];
-        sL += wL[w][pt];
-      }
-      pP[(size_t)pt * kFitBlocks + blockIdx.x] = sP;
-      pL[(size_t)pt * kFitBlocks + blockIdx.x] = sL;
+    for (int i = threadIdx.x; i < 4 * (pt_hi - pt_lo); i += blockDim.x) {
+      const int k = i / (pt_hi - pt_lo), q = i % (pt_hi - pt_lo);
+      double sum = 0.0;
+      for (int w = 0; w < kFitThreads / 32; ++w) sum += wS[k][w][q];
+      pq[k][(size_t)(pt_lo + q) * kFitBlocks + eb] = sum;
     }
   }
   if (last_block_done(&f->counter)) {
     const double N = (double)nt;
     for (int pt = warp; pt < npts; pt += kFitThreads / 32) {
-      double sP = 0.0, sL = 0.0;
-      for (int b = lane; b < active; b += 32) {
-        sP += pP[(size_t)pt * kFitBlocks + b];
-        sL += pL[(size_t)pt * kFitBlocks + b];
-      }
+      double a[4] = {0, 0, 0, 0};
+      for (int b = lane; b < E; b += 32)
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        sP += __shfl_xor_sync(0xffffffffu, sP, o);
-        sL += __shfl_xor_sync(0xffffffffu, sL, o);
-      }
+        for (int k = 0; k < 4; ++k) a[k] += pq[k][(size_t)pt * kFitBlocks + b];
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
       if (lane == 0) {
-        const double Pm = sP / N, Lm = sL / N;
+        const double Pm = a[0] / N, Lm = a[1] / N, dPm = a[2] / N, dLm = a[3] / N;
         f->w[pt] = Pm + Lm + Pm * Lm;
         f->L[pt] = Lm;
+        f->dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
       }
     }
     __syncthreads();
@@ -736,10 +745,9 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // grid scan
   struct {
     int64_t nt;
-    int iters, overflow;
+    int overflow, converged;
   } h;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.nt, &fit->nt, 8, cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.iters, &fit->iters, 4, cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.overflow, &fit->overflow, 4, cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
   if (h.nt > L.cap) {
@@ -754,8 +762,19 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     set_error("more than 64 Grimshaw roots");
     return ENOVA_ERR_UNSUPPORTED;
   }
-  for (int i = 0; i < h.iters; ++i)
-    ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
+  // Newton passes in rounds of 6 until every root has converged (<= 20 rounds);
+  // converged launches are no-ops until the final candidate pass
+  h.converged = 0;
+  for (int round = 0; round < 20 && !h.converged; ++round) {
+    for (int i = 0; i < 6; ++i)
+      ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.converged, &fit->converged, 4, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (!h.converged) {
+    set_error("GPD root refinement did not converge");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
   ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // candidates
   ENOVA_CUDA_TRY(cudaGetLastError());
   struct {
