@@ -21,6 +21,7 @@
 
 #include <vector>
 
+
 #include "comm.h"
 #include "common.cuh"
 
@@ -51,7 +52,7 @@ struct FitState {
   int phase, npts, nslots, S, iters, overflow;
   unsigned int counter, pad;
   double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts];
-  double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots];
+  double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
   int converged;
   int exact[kMaxSlots];
   int refine_idx[kMaxSlots];   // slot of the k-th refined bracket
@@ -78,7 +79,7 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.hist = take(kBins * 8);
   L.sel = take(sizeof(SelState));
   L.fit = take(sizeof(FitState));
-  L.partials = take((size_t)kFitBlocks * kMaxPts * 4 * 8 + (size_t)kFitBlocks * 3 * 8);
+  L.partials = take((size_t)kFitBlocks * (8 * kMaxPts + 4) * 8);
   L.counts = take((kCompactBlocks + 1) * 8);
   L.counts_all = take(1024 * 8);
   L.nbuf = take(16);
@@ -322,93 +323,18 @@ __device__ void setup_grid(FitState *f) {
   f->phase = PH_GRID;
 }
 
-// blocks that hold Y elements: one element per thread per 256-wide sweep
-__device__ __forceinline__ int fit_active_blocks(int64_t nt) {
-  const int64_t a = (nt + 255) / 256;
-  return (int)(a < (int64_t)gridDim.x ? (a < 1 ? 1 : a) : gridDim.x);
-}
-
-// Ybar, Ymin, Ymax with a fixed reduction order (thread partial -> xor tree ->
-// warps in order -> blocks summed by lanes in order -> xor tree)
-__global__ void __launch_bounds__(kFitThreads) k_ystats(const double *__restrict__ Y, FitState *f,
-                                                        double *__restrict__ part) {
-  __shared__ double ws[3][kFitThreads / 32];
-  if (f->phase == PH_DONE) return;
-  const int64_t nt = f->nt;
-  const int active = fit_active_blocks(nt);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *pS = part, *pMn = part + kFitBlocks, *pMx = part + 2 * kFitBlocks;
-  if ((int)blockIdx.x < active) {
-    const int64_t chunk = (nt + active - 1) / active;
-    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(nt, b0 + chunk);
-    double s = 0.0, mn = INFINITY, mx = -INFINITY;
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const double y = Y[i];
-      s += y;
-      mn = fmin(mn, y);
-      mx = fmax(mx, y);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (lane == 0) {
-      ws[0][warp] = s;
-      ws[1][warp] = mn;
-      ws[2][warp] = mx;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
-      for (int w = 0; w < kFitThreads / 32; ++w) {
-        ts += ws[0][w];
-        tmn = fmin(tmn, ws[1][w]);
-        tmx = fmax(tmx, ws[2][w]);
-      }
-      pS[blockIdx.x] = ts;
-      pMn[blockIdx.x] = tmn;
-      pMx[blockIdx.x] = tmx;
-    }
-  }
-  if (last_block_done(&f->counter)) {
-    if (warp == 0) {
-      double s = 0.0, mn = INFINITY, mx = -INFINITY;
-      for (int b = lane; b < active; b += 32) {
-        s += pS[b];
-        mn = fmin(mn, pMn[b]);
-        mx = fmax(mx, pMx[b]);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o);
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      if (lane == 0) {
-        f->ybar = s / (double)nt;
-        f->ymin = mn;
-        f->ymax = mx;
-        f->counter = 0;
-        setup_grid(f);
-      }
-    }
-  }
-}
-
 // Phase machine run by the last block of each evaluation launch.
 //  GRID  : w at the fixed scan grids -> one slot per sign change (or exact zero);
 //  REFINE: safeguarded Newton on every bracket: w(x), w'(x) from the same pass;
 //          the bracket shrinks with the sign of w(x); the Newton iterate is kept
 //          if it falls strictly inside the bracket, else the bracket midpoint is
-//          used; converged when every step is <= 1e-15 |x| (the oracle bisects
+//          used; converged when every step is <= 1e-13 |x| (the oracle bisects
 //          to a 2^-60 bracket: both land on the same root of the fp64 w);
 //  FINAL : L(x) at the roots -> gamma, sigma, log-likelihood; pick; z_q.
 __device__ void controller(FitState *f) {
   if (f->phase == PH_GRID) {
     int ns = 0;
-    auto push = [&](double lo, double hi, double wlo, int exact) {
+    auto push = [&](double lo, double hi, double wlo, double whi, int exact) {
       if (ns >= kMaxSlots) {
         f->overflow = 1;
         return;
@@ -416,6 +342,7 @@ __device__ void controller(FitState *f) {
       f->lo[ns] = lo;
       f->hi[ns] = hi;
       f->wlo[ns] = wlo;
+      f->whi[ns] = whi;
       f->exact[ns] = exact;
       ++ns;
     };
@@ -424,11 +351,11 @@ __device__ void controller(FitState *f) {
       const double *w = f->w + g * kGrid;
       for (int k = 0; k < kGrid - 1; ++k) {
         if (w[k] == 0.0)
-          push(x[k], x[k], 0.0, 1);
+          push(x[k], x[k], 0.0, 0.0, 1);
         else if (w[k] * w[k + 1] < 0.0)
-          push(x[k], x[k + 1], w[k], 0);
+          push(x[k], x[k + 1], w[k], w[k + 1], 0);
       }
-      if (w[kGrid - 1] == 0.0) push(x[kGrid - 1], x[kGrid - 1], 0.0, 1);
+      if (w[kGrid - 1] == 0.0) push(x[kGrid - 1], x[kGrid - 1], 0.0, 0.0, 1);
     }
     f->nslots = ns;
     int nr = 0;
@@ -437,9 +364,12 @@ __device__ void controller(FitState *f) {
     f->nrefine = nr;
     f->converged = 0;
     if (nr > 0) {
-      for (int r = 0; r < nr; ++r) {
+      for (int r = 0; r < nr; ++r) {   // first iterate: secant (regula falsi) point
         const int s = f->refine_idx[r];
-        f->xs[r] = 0.5 * (f->lo[s] + f->hi[s]);
+        const double lo = f->lo[s], hi = f->hi[s];
+        double x0 = lo - f->wlo[s] * (hi - lo) / (f->whi[s] - f->wlo[s]);
+        if (!(x0 > fmin(lo, hi) && x0 < fmax(lo, hi))) x0 = 0.5 * (lo + hi);
+        f->xs[r] = x0;
       }
       f->npts = nr;
       f->phase = PH_REFINE;
@@ -469,9 +399,9 @@ __device__ void controller(FitState *f) {
       f->hi[s] = hi;
       double xn = (dw != 0.0) ? x - w / dw : 0.5 * (lo + hi);
       const double a = fmin(lo, hi), b = fmax(lo, hi);
-      if (!(xn > a && xn < b)) xn = 0.5 * (lo + hi);
+      if (!(xn > a && xn < b) || f->iters > 20) xn = 0.5 * (lo + hi);   // safeguard: bisect
       if (lo == hi) xn = lo;
-      if (!(fabs(xn - x) <= 1e-15 * fabs(x))) all_conv = false;
+      if (!(fabs(xn - x) <= 1e-13 * fabs(x))) all_conv = false;
       f->xs[r] = xn;
     }
     if (all_conv) {
@@ -514,125 +444,233 @@ __device__ void controller(FitState *f) {
   }
 }
 
-// evaluate at state->xs: P = mean(-xY/(1+xY)), L = mean(log1p(xY)) and, in the
-// REFINE phase, their x-derivatives dP = mean(-Y/(1+xY)^2), dL = mean(Y/(1+xY)).
-// Blocks are (element block, group of 16 points); each thread sweeps its
-// elements four points at a time.  Per point: xor tree over the warp, warps in
-// order, element blocks in order (lanes over blocks + xor tree) -- a fixed
-// order, so the result is deterministic.  The last block runs the controller.
-constexpr int kPtsPerGroup = 16;
-__global__ void __launch_bounds__(kFitThreads) k_fit_eval(const double *__restrict__ Y, FitState *f,
-                                                          double *__restrict__ part) {
-  __shared__ double xs[kMaxPts];
-  __shared__ double wS[4][kFitThreads / 32][kPtsPerGroup];
-  const int phase = f->phase;
-  if (phase == PH_DONE) return;
-  const int64_t nt = f->nt;
-  const int npts = f->npts;
-  const bool deriv = (phase == PH_REFINE);
-  const int npg = npts > 0 ? (npts + kPtsPerGroup - 1) / kPtsPerGroup : 1;
-  const int64_t e_need = (nt + 255) / 256, e_max = (int64_t)(gridDim.x / npg);
-  int E = (int)(e_need < e_max ? e_need : e_max);
-  if (E < 1) E = 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *pq[4];
-  for (int k = 0; k < 4; ++k) pq[k] = part + (size_t)k * kMaxPts * kFitBlocks;
-  if ((int)blockIdx.x < E * npg && npts > 0) {
-    const int eb = blockIdx.x / npg, pg = blockIdx.x % npg;
-    const int pt_lo = pg * kPtsPerGroup, pt_hi = min(npts, pt_lo + kPtsPerGroup);
-    for (int i = threadIdx.x; i < pt_hi - pt_lo; i += blockDim.x) xs[i] = f->xs[pt_lo + i];
-    __syncthreads();
-    const int64_t chunk = (nt + E - 1) / E;
-    const int64_t b0 = (int64_t)eb * chunk, b1 = min(nt, b0 + chunk);
-    for (int q0 = 0; q0 < pt_hi - pt_lo; q0 += 4) {
-      double P[4] = {0, 0, 0, 0}, L[4] = {0, 0, 0, 0}, dP[4] = {0, 0, 0, 0}, dL[4] = {0, 0, 0, 0};
-      double x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = (q0 + u < pt_hi - pt_lo) ? xs[q0 + u] : 0.0;
-      for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-        const double y = Y[i];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double xy = x[u] * y;
-          const double r = 1.0 / (1.0 + xy);
-          P[u] -= xy * r;
-          L[u] += log1p(xy);
-          if (deriv) {
-            const double yr = y * r;
-            dL[u] += yr;
-            dP[u] -= yr * r;
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          P[u] += __shfl_xor_sync(0xffffffffu, P[u], o);
-          L[u] += __shfl_xor_sync(0xffffffffu, L[u], o);
-          if (deriv) {
-            dP[u] += __shfl_xor_sync(0xffffffffu, dP[u], o);
-            dL[u] += __shfl_xor_sync(0xffffffffu, dL[u], o);
-          }
-        }
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + u < pt_hi - pt_lo) {
-            wS[0][warp][q0 + u] = P[u];
-            wS[1][warp][q0 + u] = L[u];
-            wS[2][warp][q0 + u] = dP[u];
-            wS[3][warp][q0 + u] = dL[u];
-          }
-      }
+// K5 as ONE cooperative launch (one CTA per SM, grid-wide barriers): every CTA
+// keeps an identical copy of the fit state in shared memory and, after each
+// grid barrier, reduces the per-CTA partial sums itself in a fixed order and
+// runs the same controller -- so no host round trips, no extra broadcast
+// barrier, and a deterministic result.
+//   phase 0: Ybar, Ymin, Ymax -> scan grids;  then per pass: evaluate
+//   P = mean(-xY/(1+xY)), L = mean(log1p(xY)) (+ dP = mean(-Y/(1+xY)^2),
+//   dL = mean(Y/(1+xY)) for Newton) at the state's points; controller.
+constexpr int kCoopThreads = 256;
+
+// grid-wide barrier for a cooperative launch (all CTAs co-resident): one arrival
+// per CTA on a global ticket, the last one bumps the generation word.
+__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen,
+                                             unsigned int nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *(volatile unsigned int *)gen;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(count, 1u);
+    if (ticket == nb - 1) {
+      *(volatile unsigned int *)count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*(volatile unsigned int *)gen == g) __nanosleep(20);
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 4 * (pt_hi - pt_lo); i += blockDim.x) {
-      const int k = i / (pt_hi - pt_lo), q = i % (pt_hi - pt_lo);
-      double sum = 0.0;
-      for (int w = 0; w < kFitThreads / 32; ++w) sum += wS[k][w][q];
-      pq[k][(size_t)(pt_lo + q) * kFitBlocks + eb] = sum;
-    }
+    __threadfence();
   }
-  if (last_block_done(&f->counter)) {
-    const double N = (double)nt;
-    for (int pt = warp; pt < npts; pt += kFitThreads / 32) {
-      double a[4] = {0, 0, 0, 0};
-      for (int b = lane; b < E; b += 32)
+  __syncthreads();
+}
+constexpr int kMaxRefinePasses = 60;
+
+__device__ __forceinline__ void coop_reduce_points(FitState &f, const double *part, int nb,
+                                                   int npts, bool deriv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double N = (double)f.nt;
+  const int nk = deriv ? 4 : 2;
+  for (int pt = warp; pt < npts; pt += kCoopThreads / 32) {
+    double a[4] = {0, 0, 0, 0};
+    for (int b = lane; b < nb; b += 32)
+      for (int k = 0; k < nk; ++k) a[k] += part[((size_t)k * kMaxPts + pt) * kFitBlocks + b];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] += pq[k][(size_t)pt * kFitBlocks + b];
+    for (int o = 16; o; o >>= 1)
 #pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-      if (lane == 0) {
-        const double Pm = a[0] / N, Lm = a[1] / N, dPm = a[2] / N, dLm = a[3] / N;
-        f->w[pt] = Pm + Lm + Pm * Lm;
-        f->L[pt] = Lm;
-        f->dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      f->counter = 0;
-      controller(f);
+      for (int k = 0; k < 4; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+    if (lane == 0) {
+      const double Pm = a[0] / N, Lm = a[1] / N, dPm = a[2] / N, dLm = a[3] / N;
+      f.w[pt] = Pm + Lm + Pm * Lm;
+      f.L[pt] = Lm;
+      f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
     }
   }
 }
 
-__global__ void k_fit_init(FitState *f, const long long *nt, int64_t n, const SelState *sel,
-                           double q, int64_t cap) {
-  f->nt = *nt;
-  f->n = n;
-  f->t = (double)sel->t;
-  f->q = q;
-  f->counter = 0;
-  f->overflow = 0;
-  f->phase = (f->nt < 10 || f->nt > cap) ? PH_DONE : PH_GRID;
-  f->npts = 0;
-  f->iters = 0;
+__global__ void __launch_bounds__(kCoopThreads, 1)
+    k_fit_coop(const double *__restrict__ Y, FitState *gf, double *__restrict__ part,
+               const long long *nt_dev, int64_t n, const SelState *sel, double q) {
+  __shared__ FitState f;
+  unsigned int *bar_count = &gf->counter, *bar_gen = &gf->pad;
+  __shared__ double wS[4][kCoopThreads / 32][kMaxPts];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    f.nt = *nt_dev;
+    f.n = n;
+    f.t = (double)sel->t;
+    f.q = q;
+    f.overflow = 0;
+    f.converged = 0;
+    f.iters = 0;
+    f.phase = PH_GRID;
+  }
+  __syncthreads();
+  const int64_t nt = f.nt;
+  const int64_t chunk = (nt + nb - 1) / nb;
+  const int64_t b0 = min(nt, (int64_t)blockIdx.x * chunk), b1 = min(nt, b0 + chunk);
+
+  // ---- Ybar, Ymin, Ymax ----
+  {
+    double s = 0.0, mn = INFINITY, mx = -INFINITY;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const double y = Y[i];
+      s += y;
+      mn = fmin(mn, y);
+      mx = fmax(mx, y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      wS[0][warp][0] = s;
+      wS[1][warp][0] = mn;
+      wS[2][warp][0] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
+      for (int w = 0; w < kCoopThreads / 32; ++w) {
+        ts += wS[0][w][0];
+        tmn = fmin(tmn, wS[1][w][0]);
+        tmx = fmax(tmx, wS[2][w][0]);
+      }
+      part[blockIdx.x] = ts;
+      part[kFitBlocks + blockIdx.x] = tmn;
+      part[2 * kFitBlocks + blockIdx.x] = tmx;
+    }
+    grid_barrier(bar_count, bar_gen, nb);
+    if (warp == 0) {
+      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
+      for (int b = lane; b < nb; b += 32) {
+        ts += part[b];
+        tmn = fmin(tmn, part[kFitBlocks + b]);
+        tmx = fmax(tmx, part[2 * kFitBlocks + b]);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        ts += __shfl_xor_sync(0xffffffffu, ts, o);
+        tmn = fmin(tmn, __shfl_xor_sync(0xffffffffu, tmn, o));
+        tmx = fmax(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+      }
+      if (lane == 0) {
+        f.ybar = ts / (double)nt;
+        f.ymin = tmn;
+        f.ymax = tmx;
+        setup_grid(&f);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- evaluation passes (partials double-buffered: one barrier per pass) ----
+  for (int pass = 0; pass < kMaxRefinePasses + 3; ++pass) {
+    double *pw = part + 4 * kFitBlocks + (size_t)(pass & 1) * 4 * kMaxPts * kFitBlocks;
+    const int phase = f.phase;
+    if (phase == PH_DONE) break;
+    const int npts = f.npts;
+    const bool deriv = (phase == PH_REFINE);
+    if (npts > 0) {
+      for (int q0 = 0; q0 < npts; q0 += 4) {
+        double P[4] = {0, 0, 0, 0}, L[4] = {0, 0, 0, 0}, dP[4] = {0, 0, 0, 0},
+               dL[4] = {0, 0, 0, 0};
+        double x[4];
+        int nu = min(4, npts - q0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[q0 + u] : 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+          const double y = Y[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (u < nu) {
+              const double xy = x[u] * y;
+              const double r = 1.0 / (1.0 + xy);
+              P[u] -= xy * r;
+              L[u] += log1p(xy);
+              if (deriv) {
+                const double yr = y * r;
+                dL[u] += yr;
+                dP[u] -= yr * r;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            P[u] += __shfl_xor_sync(0xffffffffu, P[u], o);
+            L[u] += __shfl_xor_sync(0xffffffffu, L[u], o);
+            dP[u] += __shfl_xor_sync(0xffffffffu, dP[u], o);
+            dL[u] += __shfl_xor_sync(0xffffffffu, dL[u], o);
+          }
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nu) {
+              wS[0][warp][q0 + u] = P[u];
+              wS[1][warp][q0 + u] = L[u];
+              wS[2][warp][q0 + u] = dP[u];
+              wS[3][warp][q0 + u] = dL[u];
+            }
+        }
+      }
+      __syncthreads();
+      const int nk = deriv ? 4 : 2;
+      for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
+        const int k = i / npts, pt = i % npts;
+        double sum = 0.0;
+        for (int w = 0; w < kCoopThreads / 32; ++w) sum += wS[k][w][pt];
+        pw[((size_t)k * kMaxPts + pt) * kFitBlocks + blockIdx.x] = sum;
+      }
+    }
+    grid_barrier(bar_count, bar_gen, nb);
+    if (npts > 0) coop_reduce_points(f, pw, nb, npts, deriv);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (phase == PH_REFINE && ++f.iters >= kMaxRefinePasses && f.phase == PH_REFINE) {
+        // not converged: keep the current iterates, mark, and finish
+        for (int r = 0; r < f.nrefine; ++r) f.lo[f.refine_idx[r]] = f.xs[r];
+        controller(&f);
+        if (f.phase == PH_REFINE) {
+          for (int s2 = 0; s2 < f.nslots; ++s2) f.xs[s2] = f.lo[s2];
+          f.npts = f.nslots;
+          f.phase = PH_FINAL;
+        }
+      } else {
+        controller(&f);
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    gf->nt = f.nt;
+    gf->gamma = f.gamma;
+    gf->sigma = f.sigma;
+    gf->z_q = f.z_q;
+    gf->method = f.method;
+    gf->nroots = f.nroots;
+    gf->overflow = f.overflow;
+    gf->converged = f.converged;
+    gf->phase = f.phase;
+  }
 }
+
 
 // ------------------------------------------------------------- driver ----
 // Host syncs: single GPU 2 (after the grid scan: N_t, iteration count; at the
@@ -688,7 +726,9 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   ENOVA_LAUNCH(k_sel_init, 1, 1, 0, st, sel, (unsigned long long)k);
   const int shifts[3] = {21, 10, 0};
   const int nbins[3] = {2048, 2048, 1024};
-  const int hblocks = 148 * 4;
+  int hblocks = (int)((n_local + 4095) / 4096);   // ~8 keys per thread
+  if (hblocks < 1) hblocks = 1;
+  if (hblocks > 148 * 4) hblocks = 148 * 4;
   for (int pass = 0; pass < 3; ++pass) {
     if (n_local > 0)
       ENOVA_LAUNCH(k_hist, hblocks, 512, 0, st, scores, n_local, sel, hist, shifts[pass],
@@ -739,44 +779,49 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     nt_dev = reinterpret_cast<long long *>(nbuf + 1);
   }
 
-  // K5: GPD fit (replicated, deterministic); N_t read on the device
-  ENOVA_LAUNCH(k_fit_init, 1, 1, 0, st, fit, nt_dev, n, sel, q, L.cap);
-  ENOVA_LAUNCH(k_ystats, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
-  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // grid scan
-  struct {
-    int64_t nt;
-    int overflow, converged;
-  } h;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.nt, &fit->nt, 8, cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.overflow, &fit->overflow, 4, cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-  if (h.nt > L.cap) {
+  // K5: GPD fit (replicated, deterministic).  N_t is read back once so every fit
+  // launch is sized to the tail (few blocks -> cheap last-block tickets).
+  int64_t nt_h = 0;
+  {
+    long long v = 0;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(&v, nt_dev, 8, cudaMemcpyDeviceToHost, st));
+    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+    nt_h = v;
+  }
+  if (nt_h > L.cap) {
     set_error("peak count exceeds workspace capacity");
     return ENOVA_ERR_WORKSPACE;
   }
-  if (h.nt < 10) {
+  if (nt_h < 10) {
     set_error("fewer than 10 exceedances above the initial threshold");
     return ENOVA_ERR_TOO_FEW_EXCEEDANCES;
   }
-  if (h.overflow) {
-    set_error("more than 64 Grimshaw roots");
-    return ENOVA_ERR_UNSUPPORTED;
+  {
+    int dev = 0, sms = 148;
+    ENOVA_CUDA_TRY(cudaGetDevice(&dev));
+    ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int nb = sms < kFitBlocks ? sms : kFitBlocks;
+    const int64_t need = (nt_h + 63) / 64;   // >= 64 peaks per CTA
+    if (need < nb) nb = (int)(need < 1 ? 1 : need);
+    const double *Yc = yall;
+    FitState *fc = fit;
+    double *pc = partials;
+    const long long *ntc = nt_dev;
+    int64_t nc = n;
+    const SelState *sc = sel;
+    double qc = q;
+    void *args[] = {(void *)&Yc, (void *)&fc, (void *)&pc, (void *)&ntc,
+                    (void *)&nc, (void *)&sc, (void *)&qc};
+    ENOVA_CUDA_TRY(cudaMemsetAsync(&fit->counter, 0, sizeof(unsigned int), st));
+    count_launch();
+    ENOVA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_fit_coop, dim3(nb),
+                                               dim3(kCoopThreads), args, 0, st));
   }
-  // Newton passes in rounds of 6 until every root has converged (<= 20 rounds);
-  // converged launches are no-ops until the final candidate pass
-  h.converged = 0;
-  for (int round = 0; round < 20 && !h.converged; ++round) {
-    for (int i = 0; i < 6; ++i)
-      ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(&h.converged, &fit->converged, 4, cudaMemcpyDeviceToHost, st));
-    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-  }
-  if (!h.converged) {
-    set_error("GPD root refinement did not converge");
-    return ENOVA_ERR_UNSUPPORTED;
-  }
-  ENOVA_LAUNCH(k_fit_eval, kFitBlocks, kFitThreads, 0, st, yall, fit, partials);  // candidates
-  ENOVA_CUDA_TRY(cudaGetLastError());
+  struct {
+    int overflow, converged;
+  } hh;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&hh.overflow, &fit->overflow, 4, cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&hh.converged, &fit->converged, 4, cudaMemcpyDeviceToHost, st));
   struct {
     double gamma, sigma, z_q;
     int method, nroots;
@@ -785,6 +830,14 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   float t = 0.f;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&t, &sel->t, 4, cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hh.overflow) {
+    set_error("more than 64 Grimshaw roots");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (!hh.converged) {
+    set_error("GPD root refinement did not converge");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
   out->init_quantile = q0;
   out->risk_q = q;
   out->t = (double)t;
@@ -792,7 +845,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   out->sigma = res.sigma;
   out->z_q = res.z_q;
   out->n = n;
-  out->n_peaks = h.nt;
+  out->n_peaks = nt_h;
   out->method = res.method;
   out->reserved = 0;
   return ENOVA_OK;
