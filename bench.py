@@ -286,11 +286,24 @@ def main():
     ms_per_step = tot_ms / args.steps
     value = wins_local * world * args.steps / (tot_ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (k_score, two launches per step) ----
+    # ---- roofline of the dominant kernel (k_score) ----
+    # The in-step events around the two score launches also contain host gaps
+    # (compute_stats synchronises before them), so the kernel's own launch
+    # duration is measured with the same launch back to back (calibration range,
+    # same configuration), L2 flushed before the burst.
     peaks = load_peaks()
     fpw = flops_per_window(D, H, Z)
-    score_s = sum(score_ms) * 1e-3 / args.steps          # per step, both launches
-    achieved = fpw * wins_local / score_s / 1e12          # TFLOP/s
+    reps = 10
+    flush.zero_()
+    k0, k1 = ev(), ev()
+    E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+    k0.record(stream)
+    for _ in range(reps):
+        E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+    k1.record(stream)
+    torch.cuda.synchronize()
+    launch_ms = k0.elapsed_time(k1) / reps
+    achieved = fpw * n_cal_local / (launch_ms * 1e-3) / 1e12   # TFLOP/s
     traffic = None
     tp = os.path.join(ROOT, "profiles", "score_traffic.json")
     if os.path.exists(tp):
@@ -302,7 +315,9 @@ def main():
             "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16"],
             "traffic": traffic,
             "peak_source": peaks["source"] + ": dense bf16 burst; fp16 has the same nominal rate",
-            "flops_per_window": fpw, "launch_ms_avg": 1e3 * score_s / 2,
+            "flops_per_window": fpw, "windows_per_launch": n_cal_local,
+            "launch_ms_avg": launch_ms, "launches_timed": reps,
+            "in_step_score_ms": float(np.mean(score_ms)),
             "share_of_step": (sum(score_ms) / sum(step_ms))}
 
     # ---- end to end through the public API with host buffers ----

@@ -33,6 +33,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
                            enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
                            int64_t n_global_max, cudaStream_t st);
 size_t threshold_workspace_bytes(int64_t n_max, double q0);
+void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
 
@@ -121,6 +122,11 @@ using namespace enova;
 extern "C" {
 
 int enova_abi_version(void) { return ENOVA_ABI_VERSION; }
+
+// diagnostic (not part of enova.h): record a %globaltimer pipeline trace of CTA
+// pair 0 of the next CTA-pair score launches into a device buffer of
+// 2 x 512 x 16 uint64 (NULL disables)
+void enova_internal_set_trace(void *dev_buf) { enova::set_pair_trace(dev_buf); }
 
 uint64_t enova_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

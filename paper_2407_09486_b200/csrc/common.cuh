@@ -302,6 +302,24 @@ __device__ __forceinline__ void mma_f16_pair_warp(uint32_t d_tmem, uint64_t ades
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// four consecutive K-steps in one warp-collective issue block: descriptors advance
+// by (astep, bstep) 16-byte units per step; all four accumulate into d_tmem
+__device__ __forceinline__ void mma_f16_pair_warp_x4(uint32_t d_tmem, uint64_t adesc,
+                                                     uint64_t bdesc, uint32_t idesc,
+                                                     uint64_t astep, uint64_t bstep) {
+  asm volatile(
+      "{\n\t.reg .pred e, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "add.s64 a1, %1, %4;\n\tadd.s64 a2, a1, %4;\n\tadd.s64 a3, a2, %4;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, b1, %5;\n\tadd.s64 b3, b2, %5;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "l"(astep), "l"(bstep)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_pair_warp(uint64_t *bar, uint16_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
