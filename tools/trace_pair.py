@@ -45,3 +45,8 @@ for it in range(10, 12):
                 ev.append(((arr[it, k] - t0) / 1e3, f"c{cta} {names[k]} [tile/iter {it}]"))
     for x, nme in sorted(ev):
         print(f"   {x:8.3f}  {nme}")
+
+print("staging detail (CTA0), us: waits-done -> planes-loop-done -> planes_full -> sx done")
+for it in range(8, 16):
+    r = t[0, 256 + it]
+    print(f"  tile {it}: start {(t[0, it, 13] - t0) / 1e3:7.3f} waits-done {(r[0] - t0) / 1e3:7.3f} loop {(r[1] - t0) / 1e3:7.3f} full {(r[2] - t0) / 1e3:7.3f} sx {(t[0, it, 14] - t0) / 1e3:7.3f}")
