@@ -50,3 +50,9 @@ print("staging detail (CTA0), us: waits-done -> planes-loop-done -> planes_full 
 for it in range(8, 16):
     r = t[0, 256 + it]
     print(f"  tile {it}: start {(t[0, it, 13] - t0) / 1e3:7.3f} waits-done {(r[0] - t0) / 1e3:7.3f} loop {(r[1] - t0) / 1e3:7.3f} full {(r[2] - t0) / 1e3:7.3f} sx {(t[0, it, 14] - t0) / 1e3:7.3f}")
+print("per-tile summary (CTA0, us rel. to tile-10 MMA start):")
+print("  tile | mma start  planes  G1a   h     G1b   mu/dec | stg wait-done loop full | E1 acc  E1 done | E2 hf  E2 done | E3 df  E3 done")
+for it in range(8, 16):
+    a = t[0]; r = a[256 + it]
+    f = lambda v: f"{(v - t0) / 1e3:6.2f}"
+    print(f"  {it:4d} | {f(a[it,0])} {f(a[it,1])} {f(a[it,2])} {f(a[it,3])} {f(a[it,4])} {f(a[it,5])} | {f(r[0])} {f(r[1])} {f(r[2])} | {f(a[it,7])} {f(a[it,8])} | {f(a[it,11])} {f(a[it,12])} | {f(a[it,9])} {f(a[it,10])}")
