@@ -28,8 +28,8 @@ for c in range(4):
     first = t[c, 0, 0] if c % 2 == 0 else t[c, 0, 13]
     print(f"cta slot {c}: kernel body {(en - st) / 1e3:.1f} us, prologue to first iter {(t[c, 0, 1] - st) / 1e3 if c % 2 == 0 else 0:.1f} us, iterations {n}")
 gstart = min(t[c, 500, 15] for c in range(4)); gend = max(t[c, 501, 15] for c in range(4))
-names = {0: "mma: iter start", 1: "mma: planes ready", 2: "mma: G1a issued", 3: "mma: h ready(G2 i-1)",
-         4: "mma: G1b issued", 5: "mma: mu+dec ready (G3 i-2)", 6: "epi: E1 wait start", 7: "epi: E1 acc full",
+names = {0: "mma: iter start", 1: "mma: planes ready", 2: "mma: G1 issued", 3: "mma: h ready(G2 i-1)",
+         4: "mma: G2 issued", 5: "mma: mu+dec ready (G3 i-2)", 6: "epi: E1 wait start", 7: "epi: E1 acc full",
          8: "epi: E1 done", 9: "epi: E3 dec full", 10: "epi: E3 done", 11: "epi: E2 heads full",
          12: "epi: E2 done", 13: "stage: start wait", 14: "stage: sx done"}
 a = t[0]
@@ -51,7 +51,7 @@ for it in range(8, 16):
     r = t[0, 256 + it]
     print(f"  tile {it}: start {(t[0, it, 13] - t0) / 1e3:7.3f} waits-done {(r[0] - t0) / 1e3:7.3f} loop {(r[1] - t0) / 1e3:7.3f} full {(r[2] - t0) / 1e3:7.3f} sx {(t[0, it, 14] - t0) / 1e3:7.3f}")
 print("per-tile summary (CTA0, us rel. to tile-10 MMA start):")
-print("  tile | mma start  planes  G1a   h     G1b   mu/dec | stg wait-done loop full | E1 acc  E1 done | E2 hf  E2 done | E3 df  E3 done")
+print("  tile | mma start  planes  G1    h     G2    mu/dec | stg wait-done loop full | E1 acc  E1 done | E2 hf  E2 done | E3 df  E3 done")
 for it in range(8, 16):
     a = t[0]; r = a[256 + it]
     f = lambda v: f"{(v - t0) / 1e3:6.2f}"
