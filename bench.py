@@ -226,40 +226,32 @@ def main():
     n_cal_local = N * (tcal - (W - 1))
     n_det_local = N * (T - tcal)
     wins_local = n_cal_local + n_det_local
-    ws = E.ThresholdWorkspace(n_cal_local * world, 0.98, dev)
-    mean = torch.empty((N, M), dtype=torch.float32, device=dev)
-    std = torch.empty((N, M), dtype=torch.float32, device=dev)
-    cal = torch.empty((N, tcal - (W - 1)), dtype=torch.float32, device=dev)
-    flags = torch.empty((N, T - tcal), dtype=torch.int8, device=dev)
-    sc = torch.empty((N, T - tcal), dtype=torch.float32, device=dev)
-    md = torch.empty((N, T - tcal), dtype=torch.float32, device=dev)
+    pipe = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
+    cal, mean, std = pipe.cal, pipe.mean, pipe.std
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def step(Xd, kern_events=None):
-        E.compute_stats(Xd, tcal, out=(mean, std))
-        if kern_events is not None:
-            kern_events[0].record(stream)
-        E.score_windows(Xd, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
-        if kern_events is not None:
-            kern_events[1].record(stream)
-        thr = E.fit_threshold(cal, 0.98, 1e-3, comm=comm, workspace=ws)
-        if kern_events is not None:
-            kern_events[2].record(stream)
-        E.detect(Xd, det, mean, std, thr, tcal, T, return_scores=True, out=(flags, sc, md))
-        if kern_events is not None:
-            kern_events[3].record(stream)
-        return thr
-
-    for _ in range(args.warmup):
-        step(X)
+    # one step = pipe.enqueue(X): stats_async -> calibration scores -> POT threshold
+    # (device-resident on one GPU; collective + synchronous with a communicator)
+    # -> flags / scores / MD.  On one GPU the step is captured once into a CUDA
+    # graph and replayed (one graph launch per step).
+    use_graph = world == 1
+    l0 = _lib.lib().enova_kernel_launches()
+    pipe.enqueue(X)
     torch.cuda.synchronize()
+    launches_per_step = _lib.lib().enova_kernel_launches() - l0
+    if use_graph:
+        pipe.capture(X)
+    run_step = pipe.replay if use_graph else (lambda: pipe.enqueue(X))
+    for _ in range(args.warmup):
+        run_step()
+    torch.cuda.synchronize()
+    warm = pipe.result()                       # statuses checked (raises on failure)
 
     # ---- device-resident timed region ----
     starts = [ev() for _ in range(args.steps)]
     ends = [ev() for _ in range(args.steps)]
-    kev = [[ev() for _ in range(4)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -268,16 +260,17 @@ def main():
         for i in range(args.steps):
             flush.zero_()                              # untimed L2 flush between steps
             starts[i].record(stream)
-            thr = step(X, kev[i])
+            run_step()
             ends[i].record(stream)
         torch.cuda.synchronize()
-    launches = _lib.lib().enova_kernel_launches() - l0
+    launches = (launches_per_step * args.steps if use_graph
+                else _lib.lib().enova_kernel_launches() - l0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    score_ms = [k[0].elapsed_time(k[1]) + k[2].elapsed_time(k[3]) for k in kev]
-    fit_ms = [k[1].elapsed_time(k[2]) for k in kev]
+    res = pipe.result()
+    thr = res.threshold
+    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
     tot_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)
@@ -286,11 +279,30 @@ def main():
     ms_per_step = tot_ms / args.steps
     value = wins_local * world * args.steps / (tot_ms * 1e-3)
 
+    # ---- per-stage device times (eager, stream-ordered, events between stages) ----
+    stage = {"stats": [], "score_calibration": [], "fit_threshold": [], "detect": []}
+    if world == 1:
+        for _ in range(5):
+            flush.zero_()
+            k = [ev() for _ in range(5)]
+            k[0].record(stream)
+            E.compute_stats_async(X, tcal, out=(mean, std), diag=pipe.diag, workspace=pipe.stats_ws)
+            k[1].record(stream)
+            E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+            k[2].record(stream)
+            E.fit_threshold_async(cal, 0.98, 1e-3, workspace=pipe.thr_ws, out=pipe.thr)
+            k[3].record(stream)
+            E.detect_async(X, det, mean, std, pipe.thr, tcal, T, out=(pipe.flags, pipe.scores, pipe.md))
+            k[4].record(stream)
+            torch.cuda.synchronize()
+            for j, name in enumerate(stage):
+                stage[name].append(k[j].elapsed_time(k[j + 1]))
+    stage_ms = {k_: float(np.median(v_)) for k_, v_ in stage.items() if v_}
+
     # ---- roofline of the dominant kernel (k_score) ----
-    # The in-step events around the two score launches also contain host gaps
-    # (compute_stats synchronises before them), so the kernel's own launch
-    # duration is measured with the same launch back to back (calibration range,
-    # same configuration), L2 flushed before the burst.
+    # The kernel's own launch duration is measured with the same launch back to
+    # back (calibration range, the configuration the step uses), L2 flushed
+    # before the burst; its share of the step comes from the per-stage events.
     peaks = load_peaks()
     fpw = flops_per_window(D, H, Z)
     reps = 10
@@ -311,33 +323,37 @@ def main():
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
-    roof = {"kernel": "k_score<128,16>", "bound": "tensor", "achieved": achieved,
+    roof = {"kernel": "k_score_pair<128,16>", "bound": "tensor", "achieved": achieved,
             "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16"],
             "traffic": traffic,
             "peak_source": peaks["source"] + ": dense bf16 burst; fp16 has the same nominal rate",
             "flops_per_window": fpw, "windows_per_launch": n_cal_local,
             "launch_ms_avg": launch_ms, "launches_timed": reps,
-            "in_step_score_ms": float(np.mean(score_ms)),
-            "share_of_step": (sum(score_ms) / sum(step_ms))}
+            "in_step_score_ms": (stage_ms.get("score_calibration", 0.0) + stage_ms.get("detect", 0.0)) or None,
+            "share_of_step": ((stage_ms["score_calibration"] + stage_ms["detect"]) / ms_per_step
+                              if stage_ms else None)}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        flags_h = torch.empty((N, T - tcal), dtype=torch.int8).pin_memory()
-        Xe = torch.empty_like(X)
+        # the same step through the public API with the trace in pinned HOST memory:
+        # H2D copy of the whole trace, the step, D2H of the flags, every step
+        flags_h = torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory()
+
+        def e2e_step():
+            X.copy_(X_pinned, non_blocking=True)
+            run_step()
+            flags_h.copy_(pipe.flags, non_blocking=True)
+
         for _ in range(2):
-            Xe.copy_(X_pinned, non_blocking=True)
-            step(Xe)
-            flags_h.copy_(flags, non_blocking=True)
+            e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = ev(), ev()
         e0.record(stream)
         for _ in range(args.steps):
-            Xe.copy_(X_pinned, non_blocking=True)
-            step(Xe)
-            flags_h.copy_(flags, non_blocking=True)
+            e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
@@ -345,6 +361,7 @@ def main():
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
+        pipe.result()
         e2e = {"value": wins_local * world * args.steps / (e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(Xh.nbytes), "d2h_bytes_per_step": int(flags_h.numel()),
                "ms_per_step": e_ms / args.steps}
@@ -371,9 +388,8 @@ def main():
                 "l2": "flushed between steps (256 MiB zero-fill, untimed); inputs 164 MB/GPU > L2",
                 "precision": "fp16 operands (x, weights), fp32 accumulate, h/mu hi+lo fp16",
             },
-            "stage_ms": {"score_both_launches": float(np.mean(score_ms)),
-                         "fit_threshold": float(np.mean(fit_ms)),
-                         "other": ms_per_step - float(np.mean(score_ms)) - float(np.mean(fit_ms))},
+            "stage_ms": stage_ms,
+            "step_mode": "CUDA graph replay (1 graph launch/step)" if use_graph else "eager",
             "threshold": {"z_q": thr["z_q"], "t": thr["t"], "gamma": thr["gamma"],
                           "n_peaks": thr["n_peaks"]},
             "roofline": roof,

@@ -22,6 +22,9 @@
  *    score/detect/stats/ring_push are stream-ordered and asynchronous;
  *    enova_compute_stats synchronises only to return n_degenerate;
  *    enova_fit_threshold is synchronous and returns with *out filled.
+ *    The *_async variants (stats, single-GPU threshold, detect) never
+ *    synchronise: their status and results stay in device memory, so a whole
+ *    pipeline step can be enqueued back to back or captured in a CUDA graph.
  *  - Argument and shape errors are detected before any launch; outputs are
  *    then untouched.  Sticky CUDA / NCCL errors surface as ENOVA_ERR_CUDA /
  *    ENOVA_ERR_NCCL; enova_last_error() returns a thread-local detail string.
@@ -115,15 +118,24 @@ enova_status enova_prepare_detector(const enova_detector *det, void *det_ws,
 /* ---------------------------------------------------------------- a-1 ----
  * Per-(instance, metric) mean and population std over samples [0, t_cal_end)
  * ("input metrics are normalized prior"; R-4), accumulated in
- * fp64 and rounded to fp32; std floored at 1e-6.  mean/std: device fp32 [N][M].
+ * fp64 (one pass of shifted sums, time chunks combined in a fixed order) and
+ * rounded to fp32; std floored at 1e-6.  mean/std: device fp32 [N][M].
  * *n_degenerate (host, may be NULL): series whose std was floored.
  * Reads series->metrics / n_instances / n_steps / ld_instance / n_metrics only.
+ * ws: device scratch of enova_stats_workspace_bytes(N, M) bytes, 256-aligned.
  * Returns ENOVA_ERR_NONFINITE if any sample in the horizon is NaN/Inf (R-18);
  * synchronises the stream. */
 size_t enova_stats_workspace_bytes(int64_t n_instances, int32_t n_metrics);
 enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, float *mean, float *std,
                                  int64_t *n_degenerate, void *ws, size_t ws_bytes,
                                  void *stream);
+/* Stream-ordered variant (no synchronisation).  diag_dev (device int64[2], may
+ * be NULL): [0] = series whose std was floored, [1] > 0 iff a sample in the
+ * horizon is NaN/Inf (what enova_compute_stats reports as
+ * ENOVA_ERR_NONFINITE).  Argument errors are still returned synchronously. */
+enova_status enova_compute_stats_async(const enova_series *series, int64_t t_cal_end, float *mean,
+                                       float *std, int64_t *diag_dev, void *ws, size_t ws_bytes,
+                                       void *stream);
 
 /* ------------------------------------------------------------ a-2..a-5 ----
  * KL score (R-6) and MD (R-8) of every window in
@@ -146,6 +158,16 @@ enova_status enova_fit_threshold(const float *scores, int64_t n_local, int64_t n
                                  double init_quantile, double risk_q, enova_comm_t comm,
                                  enova_threshold *out, void *ws, size_t ws_bytes,
                                  void *stream);
+/* Single-GPU, stream-ordered variant (one cooperative kernel, no host sync).
+ * out_dev: DEVICE enova_threshold written by the kernel; out_dev->reserved holds
+ * the enova_status of the fit (ENOVA_OK, ENOVA_ERR_TOO_FEW_EXCEEDANCES,
+ * ENOVA_ERR_WORKSPACE, ENOVA_ERR_UNSUPPORTED) and z_q is NaN unless it is
+ * ENOVA_OK, so enova_detect_async flags nothing from a failed fit.  Argument
+ * errors are returned synchronously. */
+enova_status enova_fit_threshold_async(const float *scores, int64_t n, int64_t n_global_max,
+                                       double init_quantile, double risk_q,
+                                       enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                                       void *stream);
 
 /* ------------------------------------------------------------ a-2..a-6 ----
  * Score every window of the series range and flag it ("An anomaly is
@@ -158,6 +180,13 @@ enova_status enova_detect(const enova_series *series, const enova_detector *det,
                           const void *det_ws, size_t det_ws_bytes,
                           const enova_threshold *thr, int8_t *flags,
                           float *scores_opt, float *md_opt, void *stream);
+/* As enova_detect with the threshold in DEVICE memory (e.g. the out_dev of
+ * enova_fit_threshold_async); z_q is read by the kernel.  A NaN z_q (failed
+ * fit) flags nothing. */
+enova_status enova_detect_async(const enova_series *series, const enova_detector *det,
+                                const void *det_ws, size_t det_ws_bytes,
+                                const enova_threshold *thr_dev, int8_t *flags,
+                                float *scores_opt, float *md_opt, void *stream);
 
 /* ----------------------------------------------------------------- a-10 ----
  * Streaming ("executed in streaming computing framework"): a mirror

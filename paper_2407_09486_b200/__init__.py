@@ -2,12 +2,15 @@
 
 Public API (thin binding over libenova.so, include/enova.h):
   PreparedDetector, compute_stats, score_windows, fit_threshold, detect,
-  ring_push, ring_view, Comm, ThresholdWorkspace, run_pipeline.
+  ring_push, ring_view, Comm, ThresholdWorkspace, run_pipeline; stream-ordered
+  variants compute_stats_async, fit_threshold_async, detect_async,
+  threshold_from_device, and Pipeline (preallocated step, CUDA-graph capture).
 Seeded synthetic inputs live in ``paper_2407_09486_b200.synth``.
 """
 __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold", "detect",
            "ring_push", "ring_view", "Comm", "ThresholdWorkspace", "run_pipeline",
-           "EnovaError"]
+           "EnovaError", "compute_stats_async", "fit_threshold_async", "detect_async",
+           "threshold_from_device", "check_stats_diag", "Pipeline", "StatsWorkspace"]
 
 
 def __getattr__(name):

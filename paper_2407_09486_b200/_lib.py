@@ -25,7 +25,8 @@ EXPORTS = (
     "enova_compute_stats", "enova_score_windows", "enova_threshold_workspace_bytes",
     "enova_fit_threshold", "enova_detect", "enova_ring_push", "enova_comm_unique_id",
     "enova_comm_create", "enova_comm_destroy", "enova_status_string", "enova_last_error",
-    "enova_abi_version", "enova_kernel_launches",
+    "enova_abi_version", "enova_kernel_launches", "enova_compute_stats_async",
+    "enova_fit_threshold_async", "enova_detect_async",
 )
 
 
@@ -86,6 +87,9 @@ def lib() -> C.CDLL:
             "enova_prepare_detector": (C.c_int, [P(Detector), vp, sz, vp]),
             "enova_stats_workspace_bytes": (sz, [i64, i32]),
             "enova_compute_stats": (C.c_int, [P(Series), i64, vp, vp, P(i64), vp, sz, vp]),
+            "enova_compute_stats_async": (C.c_int, [P(Series), i64, vp, vp, vp, vp, sz, vp]),
+            "enova_fit_threshold_async": (C.c_int, [vp, i64, i64, dbl, dbl, vp, vp, sz, vp]),
+            "enova_detect_async": (C.c_int, [P(Series), P(Detector), vp, sz, vp, vp, vp, vp, vp]),
             "enova_score_windows": (C.c_int, [P(Series), P(Detector), vp, sz, vp, vp, vp]),
             "enova_threshold_workspace_bytes": (sz, [i64, dbl]),
             "enova_fit_threshold": (C.c_int, [vp, i64, i64, dbl, dbl, vp, P(Threshold), vp, sz, vp]),

@@ -77,13 +77,49 @@ def compute_stats(metrics: torch.Tensor, t_cal_end: int, *, out=None, stream=Non
         std = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
     else:
         mean, std = out
-    nb = int(lib().enova_stats_workspace_bytes(N, M))
-    ws = torch.empty(nb, dtype=torch.uint8, device=metrics.device)
+    ws = StatsWorkspace(N, M, metrics.device)
     ndeg = C.c_int64(0)
     check(lib().enova_compute_stats(C.byref(s), int(t_cal_end), C.c_void_p(mean.data_ptr()),
                                     C.c_void_p(std.data_ptr()), C.byref(ndeg),
-                                    C.c_void_p(ws.data_ptr()), nb, _stream_ptr(stream)))
+                                    C.c_void_p(ws.buf.data_ptr()), ws.nbytes, _stream_ptr(stream)))
     return mean, std, int(ndeg.value)
+
+
+class StatsWorkspace:
+    """Scratch for enova_compute_stats / _async (sized by enova_stats_workspace_bytes)."""
+
+    def __init__(self, n_instances: int, n_metrics: int, device=None):
+        self.nbytes = int(lib().enova_stats_workspace_bytes(int(n_instances), int(n_metrics)))
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device or "cuda")
+
+
+def compute_stats_async(metrics: torch.Tensor, t_cal_end: int, *, out=None, diag=None,
+                        workspace: StatsWorkspace | None = None, stream=None):
+    """a-1, stream-ordered (no host sync).  diag: device int64[2] = (degenerate
+    series, non-finite flag) -- read it later (e.g. check_stats_diag)."""
+    N, T, M = metrics.shape
+    s = _series(metrics)
+    if out is None:
+        mean = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+        std = torch.empty((N, M), dtype=torch.float32, device=metrics.device)
+    else:
+        mean, std = out
+    if workspace is None:
+        workspace = StatsWorkspace(N, M, metrics.device)
+    check(lib().enova_compute_stats_async(
+        C.byref(s), int(t_cal_end), C.c_void_p(mean.data_ptr()), C.c_void_p(std.data_ptr()),
+        C.c_void_p(diag.data_ptr() if diag is not None else None),
+        C.c_void_p(workspace.buf.data_ptr()), workspace.nbytes, _stream_ptr(stream)))
+    return mean, std
+
+
+def check_stats_diag(diag: torch.Tensor) -> int:
+    """Host check of the diag of compute_stats_async: raises ENOVA_ERR_NONFINITE,
+    returns the number of degenerate series."""
+    d = diag.cpu().tolist()
+    if d[1]:
+        raise _lib.EnovaError(5, "non-finite metric value in the calibration horizon")
+    return int(d[0])
 
 
 def score_windows(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tensor,
@@ -138,6 +174,62 @@ def fit_threshold(scores: torch.Tensor, init_quantile: float = 0.98, risk_q: flo
                                     C.byref(out), C.c_void_p(workspace.buf.data_ptr()),
                                     workspace.nbytes, _stream_ptr(stream)))
     return out.as_dict()
+
+
+THRESHOLD_BYTES = C.sizeof(Threshold)
+
+
+def fit_threshold_async(scores: torch.Tensor, init_quantile: float = 0.98, risk_q: float = 1e-3,
+                        *, workspace: ThresholdWorkspace | None = None, out=None,
+                        stream=None) -> torch.Tensor:
+    """a-7..a-8 on one GPU, stream-ordered: returns the DEVICE enova_threshold
+    (uint8 tensor) written by the kernel; read it with threshold_from_device."""
+    _require_cuda(scores, "scores")
+    flat = scores.reshape(-1)
+    if not flat.is_contiguous():
+        flat = flat.contiguous()
+    n = flat.numel()
+    if workspace is None:
+        workspace = ThresholdWorkspace(n, init_quantile, scores.device)
+    thr = out if out is not None else torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8,
+                                                  device=scores.device)
+    check(lib().enova_fit_threshold_async(
+        C.c_void_p(flat.data_ptr()), n, workspace.n_global_max, float(init_quantile),
+        float(risk_q), C.c_void_p(thr.data_ptr()), C.c_void_p(workspace.buf.data_ptr()),
+        workspace.nbytes, _stream_ptr(stream)))
+    return thr
+
+
+def threshold_from_device(thr_dev: torch.Tensor) -> dict:
+    """Read a device enova_threshold (synchronises); raises on a failed fit."""
+    raw = bytes(thr_dev.cpu().numpy().tobytes())
+    t = Threshold.from_buffer_copy(raw)
+    if t.reserved != 0:
+        raise _lib.EnovaError(int(t.reserved), "device threshold fit failed")
+    return t.as_dict()
+
+
+def detect_async(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tensor,
+                 std: torch.Tensor, thr_dev: torch.Tensor, t_begin: int | None = None,
+                 t_end: int | None = None, *, out=None, stream=None):
+    """a-2..a-6 with the threshold read from device memory (no host sync)."""
+    N, T, M = metrics.shape
+    tb = det.window - 1 if t_begin is None else int(t_begin)
+    te = T if t_end is None else int(t_end)
+    s = _series(metrics, mean, std, tb, te)
+    nw = max(te - tb, 0)
+    if out is None:
+        flags = torch.empty((N, nw), dtype=torch.int8, device=metrics.device)
+        sc = md = None
+    else:
+        flags, sc, md = out
+    check(lib().enova_detect_async(C.byref(s), C.byref(det.struct), C.c_void_p(det.ws.data_ptr()),
+                                   det.ws_bytes, C.c_void_p(thr_dev.data_ptr()),
+                                   C.c_void_p(flags.data_ptr()),
+                                   C.c_void_p(sc.data_ptr() if sc is not None else None),
+                                   C.c_void_p(md.data_ptr() if md is not None else None),
+                                   _stream_ptr(stream)))
+    return flags, sc, md
 
 
 def _thr_struct(thr: dict) -> Threshold:
@@ -253,3 +345,85 @@ def run_pipeline(metrics: torch.Tensor, det: PreparedDetector, t_cal_end: int,
     else:
         flags, sc, md = res, None, None
     return PipelineResult(mean, std, nd, cal, thr, flags, sc, md)
+
+
+class Pipeline:
+    """The whole hot path for a fixed fleet shape, preallocated and stream-ordered:
+    stats over [0, t_cal_end) -> calibration scores -> single-GPU POT threshold
+    (device-resident) -> flags / scores / MD of the windows ending in
+    [t_cal_end, T).  `enqueue` issues the step with no host synchronisation;
+    `capture` records it into a CUDA graph that `replay` relaunches (one graph
+    launch per step); `result` synchronises and checks the device statuses.
+    With a communicator (fleet sharded over ranks) the threshold is the
+    collective enova_fit_threshold, which synchronises: such a step is enqueued
+    eagerly and cannot be captured."""
+
+    def __init__(self, det: PreparedDetector, n_instances: int, n_steps: int, t_cal_end: int,
+                 init_quantile: float = 0.98, risk_q: float = 1e-3, return_scores: bool = True,
+                 device=None, comm: "Comm | None" = None):
+        dev = torch.device(device or "cuda")
+        W, M = det.window, det.n_metrics
+        self.det, self.N, self.T, self.M, self.tcal = det, int(n_instances), int(n_steps), M, int(t_cal_end)
+        self.q0, self.q = float(init_quantile), float(risk_q)
+        N, T, tcal = self.N, self.T, self.tcal
+        self.mean = torch.empty((N, M), dtype=torch.float32, device=dev)
+        self.std = torch.empty((N, M), dtype=torch.float32, device=dev)
+        self.diag = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.cal = torch.empty((N, max(tcal - (W - 1), 0)), dtype=torch.float32, device=dev)
+        self.thr = torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8, device=dev)
+        self.flags = torch.empty((N, T - tcal), dtype=torch.int8, device=dev)
+        self.scores = torch.empty((N, T - tcal), dtype=torch.float32, device=dev) if return_scores else None
+        self.md = torch.empty((N, T - tcal), dtype=torch.float32, device=dev) if return_scores else None
+        self.stats_ws = StatsWorkspace(N, M, dev)
+        self.comm = comm
+        world = comm.world if comm is not None else 1
+        self.thr_ws = ThresholdWorkspace(max(self.cal.numel(), 1) * world, self.q0, dev)
+        self.thr_host = None
+        self.graph = None
+        self._graph_input = None
+
+    def enqueue(self, metrics: torch.Tensor, stream=None):
+        if tuple(metrics.shape) != (self.N, self.T, self.M):
+            raise ValueError(f"metrics must be [{self.N}, {self.T}, {self.M}]")
+        W = self.det.window
+        compute_stats_async(metrics, self.tcal, out=(self.mean, self.std), diag=self.diag,
+                            workspace=self.stats_ws, stream=stream)
+        score_windows(metrics, self.det, self.mean, self.std, W - 1, self.tcal, with_md=False,
+                      out=(self.cal, None), stream=stream)
+        if self.comm is not None:
+            self.thr_host = fit_threshold(self.cal, self.q0, self.q, comm=self.comm,
+                                          workspace=self.thr_ws, stream=stream)
+            detect(metrics, self.det, self.mean, self.std, self.thr_host, self.tcal, self.T,
+                   return_scores=self.scores is not None,
+                   out=(self.flags, self.scores, self.md), stream=stream)
+            return
+        fit_threshold_async(self.cal, self.q0, self.q, workspace=self.thr_ws, out=self.thr,
+                            stream=stream)
+        detect_async(metrics, self.det, self.mean, self.std, self.thr, self.tcal, self.T,
+                     out=(self.flags, self.scores, self.md), stream=stream)
+
+    def capture(self, metrics: torch.Tensor):
+        """Record one step on `metrics` (a fixed device buffer) into a CUDA graph."""
+        if self.comm is not None:
+            raise RuntimeError("a step with a communicator synchronises; it cannot be captured")
+        side = torch.cuda.Stream(device=metrics.device)
+        side.wait_stream(torch.cuda.current_stream(metrics.device))
+        with torch.cuda.stream(side):
+            self.enqueue(metrics)            # warm-up outside capture (one-time attributes)
+        torch.cuda.current_stream(metrics.device).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.enqueue(metrics)
+        self.graph, self._graph_input = g, metrics
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            raise RuntimeError("capture() first")
+        self.graph.replay()
+
+    def result(self) -> PipelineResult:
+        nd = check_stats_diag(self.diag)
+        thr = self.thr_host if self.comm is not None else threshold_from_device(self.thr)
+        return PipelineResult(self.mean, self.std, nd, self.cal, thr, self.flags, self.scores,
+                              self.md)

@@ -26,12 +26,20 @@ enova_status cuda_status(cudaError_t e, const char *what) {
 enova_status prepare_detector(const enova_detector *det, const DetLayout &L, void *ws,
                               cudaStream_t st);
 enova_status compute_stats(const enova_series *s, int64_t t_cal_end, float *mean, float *stdv,
-                           int64_t *n_degenerate, void *ws, cudaStream_t st);
+                           int64_t *n_degenerate, void *ws, size_t ws_bytes, cudaStream_t st);
+enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float *mean,
+                                 float *stdv, unsigned long long *diag_dev, void *ws,
+                                 size_t ws_bytes, cudaStream_t st);
+size_t stats_workspace_bytes(int64_t n, int m);
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
-                          float *scores, float *md, int8_t *flags, double z_q, cudaStream_t st);
+                          float *scores, float *md, int8_t *flags, double z_q, const double *z_q_dev,
+                          cudaStream_t st);
 enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
                            enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
                            int64_t n_global_max, cudaStream_t st);
+enova_status fit_threshold_async(const float *scores, int64_t n, double q0, double q,
+                                 enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                                 int64_t n_global_max, cudaStream_t st);
 size_t threshold_workspace_bytes(int64_t n_max, double q0);
 void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
@@ -169,14 +177,13 @@ enova_status enova_prepare_detector(const enova_detector *det, void *det_ws, siz
 }
 
 size_t enova_stats_workspace_bytes(int64_t n_instances, int32_t n_metrics) {
-  (void)n_instances;
-  (void)n_metrics;
-  return 256;
+  if (n_metrics < 1) n_metrics = 1;
+  return stats_workspace_bytes(n_instances, n_metrics);
 }
 
-enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, float *mean,
-                                 float *std, int64_t *n_degenerate, void *ws, size_t ws_bytes,
-                                 void *stream) {
+static enova_status check_stats_args(const enova_series *series, int64_t t_cal_end,
+                                     const float *mean, const float *std, const void *ws,
+                                     size_t ws_bytes) {
   enova_status r = check_series_base(series);
   if (r) return r;
   if (series->n_metrics > 256) {
@@ -191,17 +198,43 @@ enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, 
     set_error("mean / std outputs are NULL");
     return ENOVA_ERR_INVALID_ARGUMENT;
   }
-  if (!ws || ws_bytes < 256 || !aligned(ws, 256)) {
+  if (!ws || !aligned(ws, 256) ||
+      ws_bytes < stats_workspace_bytes(series->n_instances, series->n_metrics)) {
     set_error("stats workspace missing, too small or misaligned");
     return ENOVA_ERR_WORKSPACE;
   }
-  if ((r = sticky())) return r;
+  return sticky();
+}
+
+enova_status enova_compute_stats(const enova_series *series, int64_t t_cal_end, float *mean,
+                                 float *std, int64_t *n_degenerate, void *ws, size_t ws_bytes,
+                                 void *stream) {
+  enova_status r = check_stats_args(series, t_cal_end, mean, std, ws, ws_bytes);
+  if (r) return r;
   if (series->n_instances == 0) {
     if (n_degenerate) *n_degenerate = 0;
     return ENOVA_OK;
   }
-  return compute_stats(series, t_cal_end, mean, std, n_degenerate, ws,
+  return compute_stats(series, t_cal_end, mean, std, n_degenerate, ws, ws_bytes,
                        static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_compute_stats_async(const enova_series *series, int64_t t_cal_end, float *mean,
+                                       float *std, int64_t *diag_dev, void *ws, size_t ws_bytes,
+                                       void *stream) {
+  enova_status r = check_stats_args(series, t_cal_end, mean, std, ws, ws_bytes);
+  if (r) return r;
+  if (diag_dev && !aligned(diag_dev, 8)) {
+    set_error("diag_dev must be 8-byte aligned");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (series->n_instances == 0) {
+    if (diag_dev) ENOVA_CUDA_TRY(cudaMemsetAsync(diag_dev, 0, 16, st));
+    return ENOVA_OK;
+  }
+  return compute_stats_async(series, t_cal_end, mean, std,
+                             reinterpret_cast<unsigned long long *>(diag_dev), ws, ws_bytes, st);
 }
 
 enova_status enova_score_windows(const enova_series *series, const enova_detector *det,
@@ -222,7 +255,7 @@ enova_status enova_score_windows(const enova_series *series, const enova_detecto
   }
   if ((r = sticky())) return r;
   if (empty) return ENOVA_OK;
-  return launch_score(series, L, det_ws, scores, md, nullptr, 0.0,
+  return launch_score(series, L, det_ws, scores, md, nullptr, 0.0, nullptr,
                       static_cast<cudaStream_t>(stream));
 }
 
@@ -253,6 +286,29 @@ enova_status enova_fit_threshold(const float *scores, int64_t n_local, int64_t n
                        n_global_max, static_cast<cudaStream_t>(stream));
 }
 
+enova_status enova_fit_threshold_async(const float *scores, int64_t n, int64_t n_global_max,
+                                       double init_quantile, double risk_q,
+                                       enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                                       void *stream) {
+  if (!out_dev || n < 1 || !scores || !aligned(out_dev, 8)) {
+    set_error("bad fit_threshold_async arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!(init_quantile >= 0.0 && init_quantile < 1.0) || !(risk_q > 0.0 && risk_q < 1.0)) {
+    set_error("init_quantile must be in [0,1) and risk_q in (0,1)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (n_global_max < n) n_global_max = n;
+  if (!ws || !aligned(ws, 256)) {
+    set_error("threshold workspace missing or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return fit_threshold_async(scores, n, init_quantile, risk_q, out_dev, ws, ws_bytes,
+                             n_global_max, static_cast<cudaStream_t>(stream));
+}
+
 enova_status enova_detect(const enova_series *series, const enova_detector *det,
                           const void *det_ws, size_t det_ws_bytes, const enova_threshold *thr,
                           int8_t *flags, float *scores_opt, float *md_opt, void *stream) {
@@ -275,7 +331,34 @@ enova_status enova_detect(const enova_series *series, const enova_detector *det,
   }
   if ((r = sticky())) return r;
   if (empty) return ENOVA_OK;
-  return launch_score(series, L, det_ws, scores_opt, md_opt, flags, thr->z_q,
+  return launch_score(series, L, det_ws, scores_opt, md_opt, flags, thr->z_q, nullptr,
+                      static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_detect_async(const enova_series *series, const enova_detector *det,
+                                const void *det_ws, size_t det_ws_bytes,
+                                const enova_threshold *thr_dev, int8_t *flags, float *scores_opt,
+                                float *md_opt, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if ((r = check_series_windows(series, L))) return r;
+  if (!thr_dev || !aligned(thr_dev, 8)) {
+    set_error("device threshold missing or misaligned");
+    return ENOVA_ERR_UNCALIBRATED;
+  }
+  const bool empty = series->n_instances == 0 || series->t_end == series->t_begin;
+  if (!flags && !empty) {
+    set_error("flags output is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  if (empty) return ENOVA_OK;
+  return launch_score(series, L, det_ws, scores_opt, md_opt, flags, 0.0, &thr_dev->z_q,
                       static_cast<cudaStream_t>(stream));
 }
 

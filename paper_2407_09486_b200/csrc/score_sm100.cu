@@ -43,6 +43,7 @@ struct ScoreParams {
   float *scores, *md;
   int8_t *flags;
   double z_q;
+  const double *z_q_dev;   // device threshold (enova_detect_async); overrides z_q
 };
 
 constexpr int kRows = 128;       // windows per tile (UMMA M)
@@ -374,7 +375,10 @@ __global__ void __launch_bounds__(128, 2) k_score(const ScoreParams p) {
     const int64_t o = inst * p.nw + r0 + tid;
     if (p.scores) p.scores[o] = score;
     if (p.md) p.md[o] = mdv;
-    if (p.flags) p.flags[o] = ((double)score > p.z_q) ? (mdv >= 0.f ? 1 : -1) : 0;
+    if (p.flags) {
+      const double zq = p.z_q_dev ? __ldg(p.z_q_dev) : p.z_q;
+      p.flags[o] = ((double)score > zq) ? (mdv >= 0.f ? 1 : -1) : 0;
+    }
   }
 
   tc_fence_before();
@@ -402,7 +406,7 @@ static enova_status launch_score_t(const ScoreParams &p, cudaStream_t st) {
 bool pair_path_ok(const DetLayout &L);
 enova_status launch_score_pair(const enova_series *s, const DetLayout &L, const void *det_ws,
                                float *scores, float *md, int8_t *flags, double z_q,
-                               cudaStream_t st);
+                               const double *z_q_dev, cudaStream_t st);
 
 // Kernel choice by shape: the weight-stationary CTA-pair kernel whenever half of
 // W1 fits in shared memory (all BASELINE configs), else the W1-streaming kernel.
@@ -417,9 +421,10 @@ static bool force_stream() {
 }
 
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
-                          float *scores, float *md, int8_t *flags, double z_q, cudaStream_t st) {
+                          float *scores, float *md, int8_t *flags, double z_q, const double *z_q_dev,
+                          cudaStream_t st) {
   if (!force_stream() && pair_path_ok(L))
-    return launch_score_pair(s, L, det_ws, scores, md, flags, z_q, st);
+    return launch_score_pair(s, L, det_ws, scores, md, flags, z_q, z_q_dev, st);
   ScoreParams p{};
   const uint8_t *b = static_cast<const uint8_t *>(det_ws);
   p.X = s->metrics;
@@ -449,6 +454,7 @@ enova_status launch_score(const enova_series *s, const DetLayout &L, const void 
   p.md = md;
   p.flags = flags;
   p.z_q = z_q;
+  p.z_q_dev = z_q_dev;
   if (p.nw <= 0) return ENOVA_OK;
   switch (L.H * 100 + L.ZP) {
     case 3208: return launch_score_t<32, 8>(p, st);

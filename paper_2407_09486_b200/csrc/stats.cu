@@ -3,106 +3,154 @@
 // "The input metrics are normalized prior to being fed into the VAE"
 // (PAPER.md:282); per-dimension z-score with stats from the training horizon
 // reused at inference, std floored at 1e-6 (R-4).
-// One CTA per instance streams its [T_cal][M] block with coalesced 128-bit
-// loads, twice (mean, then centred second moment), accumulating in fp64 with
-// a fixed reduction order; results are rounded to fp32.
+//
+// One HBM pass: the calibration horizon of each instance is split into
+// `nchunk` contiguous time chunks, one CTA each, streamed with coalesced
+// 128-bit loads (4 in flight per thread).  Each thread accumulates the SHIFTED
+// sums S1 = sum(x - K), S2 = sum((x - K)^2) in fp64, with K = the series' first
+// sample (the same shift in every chunk, so chunk sums simply add); the CTA
+// reduces them in a fixed order and the last CTA of the instance (ticket)
+// combines the chunks in chunk order: mean = K + S1/n, var = S2/n - (S1/n)^2.
+// With fp32 data and K inside the series' range this equals the two-pass fp64
+// result to ~1e-16 relative, far below the fp32 rounding that follows.
 #include "common.cuh"
 
 namespace enova {
 
-__global__ void __launch_bounds__(1024) k_series_stats(const float *__restrict__ X, int64_t ld, int M, int64_t T_cal,
-                               float *__restrict__ mean_out, float *__restrict__ std_out,
-                               unsigned long long *__restrict__ counters) {
-  extern __shared__ double red[];  // [nslots][M]
-  __shared__ double mean_s[256];
+constexpr int kStatsThreads = 512;
+constexpr int kStatsMaxChunks = 16;
+
+// workspace: [0, 256) diag counters | tickets u32[N] | partial sums f64[N][nchunk][2][M]
+static inline int stats_max_chunks(int64_t n) {
+  if (n <= 0) return 1;
+  int64_t c = (1024 + n - 1) / n;
+  return (int)(c < 1 ? 1 : c > kStatsMaxChunks ? kStatsMaxChunks : c);
+}
+
+size_t stats_workspace_bytes(int64_t n, int m) {
+  if (n < 0) n = 0;
+  return 256 + align_up((size_t)n * 4, 256) +
+         align_up((size_t)n * stats_max_chunks(n) * 2 * m * sizeof(double), 256);
+}
+
+__global__ void __launch_bounds__(kStatsThreads) k_series_stats(
+    const float *__restrict__ X, int64_t ld, int M, int64_t T_cal, int nchunk,
+    float *__restrict__ mean_out, float *__restrict__ std_out, unsigned long long *diag,
+    unsigned int *ticket, double *part) {
+  extern __shared__ double red[];  // [nslots][2][M]
+  __shared__ bool last;
   const int G = M / 4;
   const int g = threadIdx.x % G;
   const int slot = threadIdx.x / G;
   const int nslots = blockDim.x / G;
-  const int64_t inst = blockIdx.x;
+  const int64_t inst = blockIdx.x / nchunk;
+  const int chunk = blockIdx.x % nchunk;
   const float4 *base = reinterpret_cast<const float4 *>(X + inst * ld);
+  const int64_t t0 = T_cal * chunk / nchunk, t1 = T_cal * (chunk + 1) / nchunk;
+  const float4 K = __ldg(base + g);   // shift: the series' first sample
 
-  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
   int bad = 0;
-  int64_t t = slot;
-  for (; t + 3 * nslots < T_cal; t += 4 * nslots) {   // 4 independent 128-bit loads in flight
-    float4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(base + (t + u * nslots) * G + g);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      bad |= !(isfinite(v[u].x) && isfinite(v[u].y) && isfinite(v[u].z) && isfinite(v[u].w));
-      s0 += v[u].x; s1 += v[u].y; s2 += v[u].z; s3 += v[u].w;
-    }
-  }
-  for (; t < T_cal; t += nslots) {
-    float4 v = __ldg(base + t * G + g);
+  auto acc = [&](const float4 v) {
     bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-    s0 += v.x; s1 += v.y; s2 += v.z; s3 += v.w;
-  }
-  red[slot * M + 4 * g + 0] = s0;
-  red[slot * M + 4 * g + 1] = s1;
-  red[slot * M + 4 * g + 2] = s2;
-  red[slot * M + 4 * g + 3] = s3;
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x < M) {
-    double s = 0;
-    for (int k = 0; k < nslots; ++k) s += red[k * M + threadIdx.x];
-    mean_s[threadIdx.x] = s / (double)T_cal;
-  }
-  __syncthreads();
-  const double m0 = mean_s[4 * g], m1 = mean_s[4 * g + 1], m2 = mean_s[4 * g + 2],
-               m3 = mean_s[4 * g + 3];
-  s0 = s1 = s2 = s3 = 0;
-  for (t = slot; t + 3 * nslots < T_cal; t += 4 * nslots) {
+    const double d0 = (double)v.x - K.x, d1 = (double)v.y - K.y, d2 = (double)v.z - K.z,
+                 d3 = (double)v.w - K.w;
+    a0 += d0; a1 += d1; a2 += d2; a3 += d3;
+    q0 = fma(d0, d0, q0); q1 = fma(d1, d1, q1); q2 = fma(d2, d2, q2); q3 = fma(d3, d3, q3);
+  };
+  int64_t t = t0 + slot;
+  for (; t + 3 * nslots < t1; t += 4 * nslots) {
     float4 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = __ldg(base + (t + u * nslots) * G + g);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double d0 = v[u].x - m0, d1 = v[u].y - m1, d2 = v[u].z - m2, d3 = v[u].w - m3;
-      s0 += d0 * d0; s1 += d1 * d1; s2 += d2 * d2; s3 += d3 * d3;
-    }
+    for (int u = 0; u < 4; ++u) acc(v[u]);
   }
-  for (; t < T_cal; t += nslots) {
-    float4 v = __ldg(base + t * G + g);
-    double d0 = v.x - m0, d1 = v.y - m1, d2 = v.z - m2, d3 = v.w - m3;
-    s0 += d0 * d0; s1 += d1 * d1; s2 += d2 * d2; s3 += d3 * d3;
-  }
-  __syncthreads();
-  red[slot * M + 4 * g + 0] = s0;
-  red[slot * M + 4 * g + 1] = s1;
-  red[slot * M + 4 * g + 2] = s2;
-  red[slot * M + 4 * g + 3] = s3;
-  __syncthreads();
-  if (threadIdx.x < M) {
+  for (; t < t1; t += nslots) acc(__ldg(base + t * G + g));
+  double *r = red + (size_t)slot * 2 * M;
+  r[4 * g + 0] = a0; r[4 * g + 1] = a1; r[4 * g + 2] = a2; r[4 * g + 3] = a3;
+  r[M + 4 * g + 0] = q0; r[M + 4 * g + 1] = q1; r[M + 4 * g + 2] = q2; r[M + 4 * g + 3] = q3;
+  bad = __syncthreads_or(bad);
+  double *pc = part + ((size_t)inst * nchunk + chunk) * 2 * M;
+  if (threadIdx.x < 2 * M) {   // fixed-order sum over slots
     double s = 0;
-    for (int k = 0; k < nslots; ++k) s += red[k * M + threadIdx.x];
-    double sd = sqrt(s / (double)T_cal);
+    for (int k = 0; k < nslots; ++k) s += red[(size_t)k * 2 * M + threadIdx.x];
+    pc[threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0 && bad) atomicAdd(diag + 1, 1ull);   // chunks with a non-finite sample
+  // last CTA of this instance combines the chunks in chunk order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket + inst, 1u) == (unsigned)nchunk - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < M) {
+    const int j = threadIdx.x;
+    const double *p0 = part + (size_t)inst * nchunk * 2 * M;
+    double s1 = 0, s2 = 0;
+    for (int c = 0; c < nchunk; ++c) {
+      s1 += *(volatile const double *)(p0 + (size_t)c * 2 * M + j);
+      s2 += *(volatile const double *)(p0 + (size_t)c * 2 * M + M + j);
+    }
+    const double n = (double)T_cal;
+    const double kj = (double)__ldg(X + inst * ld + j);
+    const double m1 = s1 / n;
+    double var = s2 / n - m1 * m1;
+    if (var < 0) var = 0;
+    double sd = sqrt(var);
     if (sd < 1e-6) {
-      atomicAdd(counters + 0, 1ull);
+      atomicAdd(diag + 0, 1ull);
       sd = 1e-6;
     }
-    mean_out[inst * M + threadIdx.x] = (float)mean_s[threadIdx.x];
-    std_out[inst * M + threadIdx.x] = (float)sd;
+    mean_out[inst * M + j] = (float)(kj + m1);
+    std_out[inst * M + j] = (float)sd;
   }
-  if (threadIdx.x == 0 && bad) atomicAdd(counters + 1, 1ull);
+}
+
+// diag[0] = series whose std was floored, diag[1] = (instance, chunk) blocks
+// holding a non-finite sample (> 0 <=> ENOVA_ERR_NONFINITE).
+enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float *mean,
+                                 float *stdv, unsigned long long *diag_dev, void *ws,
+                                 size_t ws_bytes, cudaStream_t st) {
+  const int64_t N = s->n_instances;
+  const int M = s->n_metrics;
+  if (ws_bytes < stats_workspace_bytes(N, M)) {
+    set_error("stats workspace too small (size it with enova_stats_workspace_bytes)");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  char *b = static_cast<char *>(ws);
+  unsigned long long *diag = diag_dev ? diag_dev : reinterpret_cast<unsigned long long *>(b);
+  unsigned int *ticket = reinterpret_cast<unsigned int *>(b + 256);
+  double *part = reinterpret_cast<double *>(b + 256 + align_up((size_t)N * 4, 256));
+  int dev = 0, sms = 148;
+  ENOVA_CUDA_TRY(cudaGetDevice(&dev));
+  ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int64_t nchunk = (4 * (int64_t)sms + N - 1) / N;
+  if (nchunk > stats_max_chunks(N)) nchunk = stats_max_chunks(N);
+  if (nchunk > t_cal_end / 64) nchunk = t_cal_end / 64;
+  if (nchunk < 1) nchunk = 1;
+  const int G = M / 4;
+  const int nthreads = G * (kStatsThreads / G);
+  const int nslots = nthreads / G;
+  if (diag_dev) ENOVA_CUDA_TRY(cudaMemsetAsync(diag_dev, 0, 2 * sizeof(unsigned long long), st));
+  ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, 256 + (size_t)N * 4, st));   // diag (own) + tickets
+  const size_t smem = (size_t)nslots * 2 * M * sizeof(double);
+  if (smem > 48 * 1024)
+    ENOVA_CUDA_TRY(cudaFuncSetAttribute(k_series_stats,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ENOVA_LAUNCH(k_series_stats, (unsigned)(N * nchunk), nthreads, smem, st, s->metrics,
+               s->ld_instance, M, t_cal_end, (int)nchunk, mean, stdv, diag, ticket, part);
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
 }
 
 enova_status compute_stats(const enova_series *s, int64_t t_cal_end, float *mean, float *stdv,
-                           int64_t *n_degenerate, void *ws, cudaStream_t st) {
-  const int M = s->n_metrics;
-  const int G = M / 4;
-  const int nthreads = G * (1024 / G);
-  const int nslots = nthreads / G;
-  unsigned long long *counters = static_cast<unsigned long long *>(ws);
-  ENOVA_CUDA_TRY(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
-  size_t smem = (size_t)nslots * M * sizeof(double);
-  k_series_stats<<<(unsigned)s->n_instances, nthreads, smem, st>>>(
-      s->metrics, s->ld_instance, M, t_cal_end, mean, stdv, counters);
-  ENOVA_CUDA_TRY(cudaGetLastError());
+                           int64_t *n_degenerate, void *ws, size_t ws_bytes, cudaStream_t st) {
+  enova_status r = compute_stats_async(s, t_cal_end, mean, stdv, nullptr, ws, ws_bytes, st);
+  if (r) return r;
   unsigned long long h[2];
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, st));
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
   if (n_degenerate) *n_degenerate = (int64_t)h[0];
   if (h[1]) {

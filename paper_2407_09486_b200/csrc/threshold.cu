@@ -11,16 +11,25 @@
 //   GPD = maximum likelihood by Grimshaw's reduction: the roots of
 //         w(x) = u(x) v(x) - 1 (u = mean 1/(1+xY), v = 1 + mean log1p(xY)) are
 //         bracketed on the fixed 64-point grids of both intervals and refined by
-//         k-section (bisection when S = 1) to a 2^-60 bracket; every root gives
+//         safeguarded Newton to |step| <= 1e-13 |x|; every root gives
 //         gamma = v - 1, sigma = gamma / x, log-likelihood -N (ln sigma + gamma + 1);
 //         the exponential candidate (gamma = 0, sigma = Ybar) is always present;
 //   z_q = t + sigma/gamma * expm1(-gamma ln(q n / N_t))  (t - sigma ln(.) at gamma = 0).
-// All reductions use a fixed block partition and a fixed combine order, so the
-// result is deterministic and identical on every rank.
+//
+// v3 design: the whole single-GPU threshold is ONE cooperative launch
+// (k_pot, one 512-thread CTA per SM) that walks a phase program with grid-wide
+// barriers -- histogram pass 0, select + histogram 1, select + histogram 2,
+// select + stable compaction, then the fit (Y statistics, grid scan, Newton
+// passes, final pass) -- with no host round trip.  With a communicator the same
+// kernel runs the phases in four launches separated by the NCCL exchanges
+// (histogram all-reduce, tail all-gather).  Every CTA keeps an identical copy of
+// the select and fit state and reduces the per-CTA partials itself, in a fixed
+// order, after each barrier: the result is deterministic and, because the fit
+// partition depends only on N_t and the grid size, identical on every rank and
+// for every world size.
 #include <math.h>
 
 #include <vector>
-
 
 #include "comm.h"
 #include "common.cuh"
@@ -28,42 +37,47 @@
 namespace enova {
 
 constexpr int kBins = 2048;
-constexpr int kSelThreads = 1024;
-constexpr int kCompactBlocks = 1184;  // 8 per SM
-constexpr int kCompactThreads = 256;
-constexpr int kFitBlocks = 592;   // 4 per SM; blocks beyond ceil(N_t/256) only join the ticket
-constexpr int kFitThreads = 256;
+constexpr int kPotThreads = 512;
+constexpr int kPotWarps = kPotThreads / 32;
+constexpr int kMaxCtas = 256;
 constexpr int kMaxPts = 128;
 constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
+constexpr int kMaxRefinePasses = 60;
 
 enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
+// phase program of k_pot
+enum { P_HIST0 = 0, P_HIST1 = 1, P_HIST2 = 2, P_COMPACT = 3, P_FIT = 4 };
 
-struct SelState {
-  unsigned int prefix, mask;
+// Device-global state of one fit_threshold call.  The first kHeaderBytes of the
+// workspace (this struct and histogram 0) are zeroed by one memset per call;
+// everything else is initialised by the kernel itself.
+struct PotGlobal {
+  unsigned int bar_count, bar_gen;   // grid barrier
+  int status;                        // enova_status of the device phases
+  int pad0;
+  unsigned int prefix, mask;         // radix-select state after the last select
   unsigned long long k_rem;
   float t;
-  int pad;
+  int pad1;
+  long long nt_local, nt_fit;        // peaks of this rank / of the fit (all ranks)
+  double gamma, sigma, z_q;
+  int method, nroots, converged, overflow;
 };
 
 struct FitState {
   int64_t nt, n;
   double t, q, ybar, ymin, ymax;
-  int phase, npts, nslots, S, iters, overflow;
-  unsigned int counter, pad;
+  int phase, npts, nslots, iters, overflow, converged, nrefine, method, nroots;
   double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts];
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
-  int converged;
   int exact[kMaxSlots];
-  int refine_idx[kMaxSlots];   // slot of the k-th refined bracket
-  int nrefine;
-  // result
+  int refine_idx[kMaxSlots];
   double gamma, sigma, z_q;
-  int method, nroots;
 };
 
 struct ThrLayout {
-  size_t hist, sel, fit, partials, counts, counts_all, nbuf, ylocal, yall, total;
+  size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yall, header, total;
   int64_t cap;
 };
 
@@ -76,18 +90,36 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.cap = (int64_t)ceil(tail) + 16;
   if (L.cap > n_max) L.cap = n_max;
   if (L.cap < 16) L.cap = 16;
-  L.hist = take(kBins * 8);
-  L.sel = take(sizeof(SelState));
-  L.fit = take(sizeof(FitState));
-  L.partials = take((size_t)kFitBlocks * (8 * kMaxPts + 4) * 8);
-  L.counts = take((kCompactBlocks + 1) * 8);
-  L.counts_all = take(1024 * 8);
+  L.glob = take(sizeof(PotGlobal));
+  L.hist = take(3 * kBins * 8);
+  L.header = L.hist + kBins * 8;                    // PotGlobal + histogram 0
+  L.counts = take(kMaxCtas * 8);
+  L.part = take((size_t)2 * 4 * kMaxPts * kMaxCtas * 8);
   L.nbuf = take(16);
+  L.counts_all = take(1024 * 8);
   L.ylocal = take((size_t)L.cap * 8);
   L.yall = take((size_t)L.cap * 8);
   L.total = o;
   return L;
 }
+
+struct PotArgs {
+  const float *scores;
+  int64_t n_local;          // scores on this rank
+  int64_t n;                // scores over all ranks
+  unsigned long long k;     // rank of t in the global ascending order
+  double q;                 // risk
+  PotGlobal *g;
+  unsigned long long *hist; // [3][kBins]
+  long long *counts;        // [gridDim.x]
+  double *part;             // [2][4][kMaxPts][kMaxCtas]
+  double *ydst;             // compaction target (this rank's tail)
+  const double *yfit;       // tail the fit runs on (all ranks, rank order)
+  int64_t cap;
+  int first, last;          // phase range of this launch
+  enova_threshold *out_dev; // optional device copy of the result
+  double q0;
+};
 
 __device__ __forceinline__ unsigned int f2key(float f) {
   unsigned int b = __float_as_uint(f);
@@ -97,233 +129,209 @@ __device__ __forceinline__ float key2f(unsigned int k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// ---------------------------------------------------------------- K3 ----
-__global__ void k_sel_init(SelState *s, unsigned long long k) {
-  s->prefix = 0;
-  s->mask = 0;
-  s->k_rem = k;
-  s->t = 0.f;
-}
-
-__global__ void k_hist(const float *__restrict__ x, int64_t n, const SelState *__restrict__ sel,
-                       unsigned long long *__restrict__ hist, int shift, int nbins) {
-  __shared__ unsigned int h[kBins];
-  for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
+// grid-wide barrier for a cooperative launch (all CTAs co-resident): one arrival
+// per CTA on a global ticket; the last arrival resets the ticket and bumps the
+// generation word the others wait on.  Self-resetting across barriers and
+// launches (the ticket is back at 0 after every barrier).
+__device__ __forceinline__ void grid_sync(PotGlobal *g) {
   __syncthreads();
-  const unsigned int prefix = sel->prefix, mask = sel->mask;
-  const int64_t n4 = n / 4;
-  const float4 *x4 = reinterpret_cast<const float4 *>(x);
-  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  auto add = [&](float f) {
-    unsigned int k = f2key(f);
-    if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & (nbins - 1)], 1u);
-  };
-  if (aligned) {
-    for (int64_t i = i0; i < n4; i += stride) {
-      float4 v = __ldg(x4 + i);
-      add(v.x); add(v.y); add(v.z); add(v.w);
+  if (threadIdx.x == 0) {
+    volatile unsigned int *vgen = &g->bar_gen;
+    const unsigned int gen = *vgen;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&g->bar_count, 1u);
+    if (ticket == gridDim.x - 1) {
+      *(volatile unsigned int *)&g->bar_count = 0;
+      __threadfence();
+      atomicAdd(&g->bar_gen, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(32);
     }
-    for (int64_t i = 4 * n4 + i0; i < n; i += stride) add(__ldg(x + i));
-  } else {
-    for (int64_t i = i0; i < n; i += stride) add(__ldg(x + i));
+    __threadfence();
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nbins; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, (unsigned long long)h[i]);
 }
 
-// one block of 1024 threads, 2 bins per thread: find the digit holding rank k_rem
-__global__ void k_select(unsigned long long *__restrict__ hist, SelState *__restrict__ sel,
-                         int shift, int nbins) {
-  __shared__ unsigned long long warp_tot[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  unsigned long long c0 = 0, c1 = 0;
-  if (2 * tid < nbins) c0 = hist[2 * tid];
-  if (2 * tid + 1 < nbins) c1 = hist[2 * tid + 1];
-  unsigned long long v = c0 + c1, incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long wv = warp_tot[lane], wi = wv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
-    }
-    warp_tot[lane] = wi - wv;  // exclusive warp offsets
-  }
-  __syncthreads();
-  const unsigned long long before = warp_tot[warp] + incl - v;  // exclusive prefix of bin 2*tid
-  const unsigned long long k = sel->k_rem;
-  __syncthreads();
-  int digit = -1;
-  unsigned long long below = 0;
-  if (c0 && k >= before && k < before + c0) {
-    digit = 2 * tid;
-    below = before;
-  } else if (c1 && k >= before + c0 && k < before + c0 + c1) {
-    digit = 2 * tid + 1;
-    below = before + c0;
-  }
-  if (digit >= 0) {
-    sel->prefix |= (unsigned int)digit << shift;
-    sel->mask |= (unsigned int)(nbins - 1) << shift;
-    sel->k_rem = k - below;
-    if (shift == 0) sel->t = key2f(sel->prefix);
-  }
-  __syncthreads();
-  if (2 * tid < nbins) hist[2 * tid] = 0;
-  if (2 * tid + 1 < nbins) hist[2 * tid + 1] = 0;
-}
-
-// ---------------------------------------------------------------- K4 ----
-__device__ __forceinline__ void chunk_of(int64_t n, int64_t *b0, int64_t *b1) {
+// contiguous chunk of [0, n) owned by this CTA (multiple of 4 for float4 loads)
+__device__ __forceinline__ void score_chunk(int64_t n, int64_t *b0, int64_t *b1) {
   int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  chunk = (chunk + 255) / 256 * 256;
+  chunk = (chunk + 3) / 4 * 4;
   *b0 = min(n, (int64_t)blockIdx.x * chunk);
   *b1 = min(n, *b0 + chunk);
 }
 
-__global__ void k_count_peaks(const float *__restrict__ x, int64_t n,
-                              const SelState *__restrict__ sel,
-                              long long *__restrict__ counts) {
-  __shared__ int wsum[32];
+struct SelS {
+  unsigned int prefix, mask;
+  unsigned long long k_rem;
+  float t;
+};
+
+// ---------------------------------------------------------------- K3 ----
+// Histogram of the digit at `shift` of every key of this CTA's chunk that
+// matches the selected prefix; warp-aggregated shared atomics (keys of nearby
+// scores share bins), flushed to the global uint64 histogram.
+__device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned int *h) {
+  const int shift = (pass == 0) ? 21 : (pass == 1) ? 10 : 0;
+  const int nbins = (pass == 2) ? 1024 : 2048;
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
   int64_t b0, b1;
-  chunk_of(n, &b0, &b1);
-  const double t = (double)sel->t;
+  score_chunk(a.n_local, &b0, &b1);
+  const unsigned int prefix = sel.prefix, mask = sel.mask;
+  auto add = [&](float f, bool valid) {
+    const unsigned int k = f2key(f);
+    const bool hit = valid && ((k & mask) == prefix);
+    const unsigned int act = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const unsigned int bin = (k >> shift) & (nbins - 1);
+      const unsigned int peers = __match_any_sync(act, bin);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
+    }
+  };
+  const bool al = (reinterpret_cast<uintptr_t>(a.scores + b0) & 15) == 0;
+  if (al) {
+    const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
+    const int64_t n4 = (b1 - b0) / 4;
+    for (int64_t i0 = 0; i0 < n4; i0 += blockDim.x) {   // warp-uniform trip count
+      const int64_t i = i0 + threadIdx.x;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      const bool ok = i < n4;
+      if (ok) v = __ldg(x4 + i);
+      add(v.x, ok); add(v.y, ok); add(v.z, ok); add(v.w, ok);
+    }
+    for (int64_t i0 = b0 + 4 * n4; i0 < b1; i0 += blockDim.x) {
+      const int64_t i = i0 + threadIdx.x;
+      add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
+    }
+  } else {
+    for (int64_t i0 = b0; i0 < b1; i0 += blockDim.x) {
+      const int64_t i = i0 + threadIdx.x;
+      add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
+    }
+  }
+  __syncthreads();
+  unsigned long long *gh = a.hist + (size_t)pass * kBins;
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+    if (h[i]) atomicAdd(gh + i, (unsigned long long)h[i]);
+}
+
+// Every CTA reads the (complete) histogram of `pass` and finds the digit that
+// holds rank k_rem: 512 threads x 4 bins, block exclusive scan.
+__device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned long long *wtot,
+                             int *found) {
+  const int shift = (pass == 0) ? 21 : (pass == 1) ? 10 : 0;
+  const int nbins = (pass == 2) ? 1024 : 2048;
+  const unsigned long long *gh = a.hist + (size_t)pass * kBins;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long c[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int b = 4 * tid + u;
+    c[u] = (b < nbins) ? *(volatile const unsigned long long *)(gh + b) : 0ull;
+  }
+  const unsigned long long v = c[0] + c[1] + c[2] + c[3];
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long wv = (lane < kPotWarps) ? wtot[lane] : 0ull;
+    unsigned long long wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kPotWarps) wtot[lane] = wi - wv;
+  }
+  __syncthreads();
+  const unsigned long long k = sel.k_rem;
+  unsigned long long before = wtot[warp] + incl - v;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (c[u] && k >= before && k < before + c[u]) {
+      found[0] = 4 * tid + u;
+      reinterpret_cast<unsigned long long *>(found)[1] = before;
+    }
+    before += c[u];
+  }
+  __syncthreads();
+  const unsigned int digit = (unsigned int)found[0];
+  const unsigned long long below = reinterpret_cast<unsigned long long *>(found)[1];
+  sel.prefix |= digit << shift;
+  sel.mask |= (unsigned int)(nbins - 1) << shift;
+  sel.k_rem = k - below;
+  if (pass == 2) sel.t = key2f(sel.prefix);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- K4 ----
+// Stable compaction of the peaks Y = s - t (s > t) of this rank in index order.
+__device__ void compact(const PotArgs &a, const SelS &sel, int *wcnt, long long *cta_base) {
+  int64_t b0, b1;
+  score_chunk(a.n_local, &b0, &b1);
+  const float t = sel.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c = 0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += ((double)__ldg(x + i) > t);
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += (__ldg(a.scores + i) > t);
+#pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  if (lane == 0) wcnt[warp] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
     long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wsum[w];
-    counts[blockIdx.x] = s;
+    for (int w = 0; w < kPotWarps; ++w) s += wcnt[w];
+    a.counts[blockIdx.x] = s;
   }
-}
-
-// exclusive scan of nblk (<= 2048) counts in place; total at counts[nblk].
-// One block of 1024 threads, two counts per thread (warp shuffles + warp totals).
-__global__ void k_scan_counts(long long *counts, int nblk) {
-  __shared__ long long warp_tot[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  long long c0 = (2 * tid < nblk) ? counts[2 * tid] : 0;
-  long long c1 = (2 * tid + 1 < nblk) ? counts[2 * tid + 1] : 0;
-  long long v = c0 + c1, incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    long long y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    long long wv = warp_tot[lane], wi = wv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      long long y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
+  grid_sync(a.g);
+  if (warp == 0) {   // exclusive prefix of this CTA and the total, fixed order
+    long long before = 0, tot = 0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      const long long v = *(volatile long long *)(a.counts + b);
+      tot += v;
+      if (b < (int)blockIdx.x) before += v;
     }
-    warp_tot[lane] = wi - wv;
-    if (lane == 31) counts[nblk] = wi;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (lane == 0) {
+      cta_base[0] = before;
+      cta_base[1] = tot;
+    }
   }
   __syncthreads();
-  const long long before = warp_tot[warp] + incl - v;
-  if (2 * tid < nblk) counts[2 * tid] = before;
-  if (2 * tid + 1 < nblk) counts[2 * tid + 1] = before + c0;
-}
-
-__global__ void k_scatter_peaks(const float *__restrict__ x, int64_t n,
-                                const SelState *__restrict__ sel,
-                                const long long *__restrict__ offsets, double *__restrict__ Y,
-                                int64_t cap) {
-  __shared__ int woff[kCompactThreads / 32 + 1];
-  int64_t b0, b1;
-  chunk_of(n, &b0, &b1);
-  const double t = (double)sel->t;
-  long long base = offsets[blockIdx.x];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long base = cta_base[0];
+  const double td = (double)t;
   for (int64_t i0 = b0; i0 < b1; i0 += blockDim.x) {
-    int64_t i = i0 + threadIdx.x;
-    double s = (i < b1) ? (double)__ldg(x + i) : 0.0;
-    bool f = (i < b1) && (s > t);
-    unsigned int bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) woff[warp] = __popc(bal);
+    const int64_t i = i0 + threadIdx.x;
+    const float s = (i < b1) ? __ldg(a.scores + i) : 0.f;
+    const bool f = (i < b1) && (s > t);
+    const unsigned int bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wcnt[warp] = __popc(bal);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0;
-      for (int w = 0; w < nw; ++w) {
-        int c = woff[w];
-        woff[w] = run;
-        run += c;
-      }
-      woff[nw] = run;
+    int off = 0, all = 0;
+    for (int w = 0; w < kPotWarps; ++w) {
+      const int v = wcnt[w];
+      off += (w < warp) ? v : 0;
+      all += v;
     }
-    __syncthreads();
     if (f) {
-      const long long o = base + woff[warp] + __popc(bal & ((1u << lane) - 1u));
-      if (o < cap) Y[o] = s - t;
+      const long long o = base + off + __popc(bal & ((1u << lane) - 1u));
+      if (o < a.cap) a.ydst[o] = (double)s - td;
     }
-    base += woff[nw];
+    base += all;
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- K5 ----
-__device__ bool last_block_done(unsigned int *counter) {
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int ticket = atomicAdd(counter, 1u);
-    last = (ticket == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) __threadfence();
-  return last;
-}
-
-template <typename T, typename Op>
-__device__ T block_reduce(T v, Op op, T *scratch) {
-  // fixed-order tree: warp xor-shuffle, then warp totals in order
-  for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) scratch[warp] = v;
-  __syncthreads();
-  T r = scratch[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = op(r, scratch[w]);
-  return r;
-}
-
-__device__ void setup_grid(FitState *f) {
-  // the fixed scan grids of R-13 (same formulas as the oracle)
-  const double ymax = f->ymax, ymin = f->ymin, ybar = f->ybar;
-  for (int k = 0; k < kGrid; ++k) {
-    double th = 1e-8 + k * ((1.0 - 2e-8) / (kGrid - 1));
-    f->xs[k] = (-1.0 / ymax) * (1.0 - th);
-  }
-  double a = 1e-12 / ybar;
-  double b = 2.0 * (ybar - ymin) / (ymin * ymin);
-  int np = kGrid;
-  if (b > a) {
-    double la = log(a), lb = log(b);
-    for (int k = 0; k < kGrid; ++k) f->xs[kGrid + k] = exp(la + k * ((lb - la) / (kGrid - 1)));
-    np = 2 * kGrid;
-  }
-  f->npts = np;
-  f->phase = PH_GRID;
-}
-
-// Phase machine run by the last block of each evaluation launch.
+// Phase machine (identical in every CTA, run by thread 0 after each pass):
 //  GRID  : w at the fixed scan grids -> one slot per sign change (or exact zero);
 //  REFINE: safeguarded Newton on every bracket: w(x), w'(x) from the same pass;
 //          the bracket shrinks with the sign of w(x); the Newton iterate is kept
@@ -404,13 +412,14 @@ __device__ void controller(FitState *f) {
       if (!(fabs(xn - x) <= 1e-13 * fabs(x))) all_conv = false;
       f->xs[r] = xn;
     }
-    if (all_conv) {
+    ++f->iters;
+    if (all_conv || f->iters >= kMaxRefinePasses) {
       // every slot's root estimate is final (exact grid zeros keep lo)
       for (int r = 0; r < f->nrefine; ++r) f->lo[f->refine_idx[r]] = f->xs[r];
       for (int s = 0; s < f->nslots; ++s) f->xs[s] = f->lo[s];
       f->npts = f->nslots;
       f->phase = PH_FINAL;
-      f->converged = 1;
+      f->converged = all_conv ? 1 : 0;
     }
     return;
   }
@@ -444,87 +453,93 @@ __device__ void controller(FitState *f) {
   }
 }
 
-// K5 as ONE cooperative launch (one CTA per SM, grid-wide barriers): every CTA
-// keeps an identical copy of the fit state in shared memory and, after each
-// grid barrier, reduces the per-CTA partial sums itself in a fixed order and
-// runs the same controller -- so no host round trips, no extra broadcast
-// barrier, and a deterministic result.
-//   phase 0: Ybar, Ymin, Ymax -> scan grids;  then per pass: evaluate
-//   P = mean(-xY/(1+xY)), L = mean(log1p(xY)) (+ dP = mean(-Y/(1+xY)^2),
-//   dL = mean(Y/(1+xY)) for Newton) at the state's points; controller.
-constexpr int kCoopThreads = 256;
-
-// grid-wide barrier for a cooperative launch (all CTAs co-resident): one arrival
-// per CTA on a global ticket, the last one bumps the generation word.
-__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen,
-                                             unsigned int nb) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int g = *(volatile unsigned int *)gen;
-    __threadfence();
-    const unsigned int ticket = atomicAdd(count, 1u);
-    if (ticket == nb - 1) {
-      *(volatile unsigned int *)count = 0;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (*(volatile unsigned int *)gen == g) __nanosleep(20);
-    }
-    __threadfence();
+// the fixed scan grids of R-13 (same formulas as the oracle), one point per thread
+__device__ void setup_grid(FitState *f) {
+  const double ymax = f->ymax, ymin = f->ymin, ybar = f->ybar;
+  const double a = 1e-12 / ybar;
+  const double b = 2.0 * (ybar - ymin) / (ymin * ymin);
+  const int k = threadIdx.x;
+  if (k < kGrid) {
+    const double th = 1e-8 + k * ((1.0 - 2e-8) / (kGrid - 1));
+    f->xs[k] = (-1.0 / ymax) * (1.0 - th);
+  } else if (k < 2 * kGrid && b > a) {
+    const double la = log(a), lb = log(b);
+    f->xs[k] = exp(la + (k - kGrid) * ((lb - la) / (kGrid - 1)));
   }
-  __syncthreads();
-}
-constexpr int kMaxRefinePasses = 60;
-
-__device__ __forceinline__ void coop_reduce_points(FitState &f, const double *part, int nb,
-                                                   int npts, bool deriv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double N = (double)f.nt;
-  const int nk = deriv ? 4 : 2;
-  for (int pt = warp; pt < npts; pt += kCoopThreads / 32) {
-    double a[4] = {0, 0, 0, 0};
-    for (int b = lane; b < nb; b += 32)
-      for (int k = 0; k < nk; ++k) a[k] += part[((size_t)k * kMaxPts + pt) * kFitBlocks + b];
-#pragma unroll
-    for (int o = 16; o; o >>= 1)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-    if (lane == 0) {
-      const double Pm = a[0] / N, Lm = a[1] / N, dPm = a[2] / N, dLm = a[3] / N;
-      f.w[pt] = Pm + Lm + Pm * Lm;
-      f.L[pt] = Lm;
-      f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
-    }
+  if (k == 0) {
+    f->npts = (b > a) ? 2 * kGrid : kGrid;
+    f->phase = PH_GRID;
   }
 }
 
-__global__ void __launch_bounds__(kCoopThreads, 1)
-    k_fit_coop(const double *__restrict__ Y, FitState *gf, double *__restrict__ part,
-               const long long *nt_dev, int64_t n, const SelState *sel, double q) {
-  __shared__ FitState f;
-  unsigned int *bar_count = &gf->counter, *bar_gen = &gf->pad;
-  __shared__ double wS[4][kCoopThreads / 32][kMaxPts];
+// Sums over this CTA's slice of Y of P = -xY/(1+xY), L = log1p(xY) and, for
+// Newton, dP = -Y/(1+xY)^2, dL = Y/(1+xY), for up to 4 points x per warp item.
+template <bool kDeriv>
+__device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t s1,
+                                            const double (&x)[4], int nu, double (&acc)[4][4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[u][k] = 0.0;
+  for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
+    const double y = Y[i];   // written by this kernel's compaction: coherent load, not .nc
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u < nu) {
+        const double xy = x[u] * y;
+        const double r = 1.0 / (1.0 + xy);
+        acc[u][0] -= xy * r;
+        acc[u][1] += log1p(xy);
+        if (kDeriv) {
+          const double yr = y * r;
+          acc[u][2] -= yr * r;
+          acc[u][3] += yr;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
+}
+
+struct FitShared {
+  FitState f;
+  double sred[kMaxPts][4];   // per warp item partial sums [item][k]
+  double red[4][kMaxPts];    // grid totals after the barrier
+};
+
+__device__ void fit(const PotArgs &a, FitShared &S) {
+  FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
+  const int64_t nt = *(volatile long long *)&a.g->nt_fit;
+  if (nt < 10 || nt > a.cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      a.g->status = (nt < 10) ? ENOVA_ERR_TOO_FEW_EXCEEDANCES : ENOVA_ERR_WORKSPACE;
+    return;   // uniform over the grid
+  }
   if (threadIdx.x == 0) {
-    f.nt = *nt_dev;
-    f.n = n;
-    f.t = (double)sel->t;
-    f.q = q;
+    f.nt = nt;
+    f.n = a.n;
+    f.t = (double)*(volatile float *)&a.g->t;
+    f.q = a.q;
     f.overflow = 0;
     f.converged = 0;
     f.iters = 0;
     f.phase = PH_GRID;
   }
-  __syncthreads();
-  const int64_t nt = f.nt;
   const int64_t chunk = (nt + nb - 1) / nb;
-  const int64_t b0 = min(nt, (int64_t)blockIdx.x * chunk), b1 = min(nt, b0 + chunk);
+  const int64_t c0 = min(nt, (int64_t)blockIdx.x * chunk), c1 = min(nt, c0 + chunk);
+  const double *Y = a.yfit;
 
-  // ---- Ybar, Ymin, Ymax ----
+  // ---- Ybar, Ymin, Ymax (pass 0, partial buffer 0) ----
   {
     double s = 0.0, mn = INFINITY, mx = -INFINITY;
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
       const double y = Y[i];
       s += y;
       mn = fmin(mn, y);
@@ -537,29 +552,29 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
     if (lane == 0) {
-      wS[0][warp][0] = s;
-      wS[1][warp][0] = mn;
-      wS[2][warp][0] = mx;
+      S.sred[warp][0] = s;
+      S.sred[warp][1] = mn;
+      S.sred[warp][2] = mx;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
-      for (int w = 0; w < kCoopThreads / 32; ++w) {
-        ts += wS[0][w][0];
-        tmn = fmin(tmn, wS[1][w][0]);
-        tmx = fmax(tmx, wS[2][w][0]);
+      for (int w = 0; w < kPotWarps; ++w) {
+        ts += S.sred[w][0];
+        tmn = fmin(tmn, S.sred[w][1]);
+        tmx = fmax(tmx, S.sred[w][2]);
       }
-      part[blockIdx.x] = ts;
-      part[kFitBlocks + blockIdx.x] = tmn;
-      part[2 * kFitBlocks + blockIdx.x] = tmx;
+      a.part[0 * kMaxCtas + blockIdx.x] = ts;
+      a.part[1 * kMaxCtas + blockIdx.x] = tmn;
+      a.part[2 * kMaxCtas + blockIdx.x] = tmx;
     }
-    grid_barrier(bar_count, bar_gen, nb);
+    grid_sync(a.g);
     if (warp == 0) {
       double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
       for (int b = lane; b < nb; b += 32) {
-        ts += part[b];
-        tmn = fmin(tmn, part[kFitBlocks + b]);
-        tmx = fmax(tmx, part[2 * kFitBlocks + b]);
+        ts += *(volatile double *)(a.part + b);
+        tmn = fmin(tmn, *(volatile double *)(a.part + kMaxCtas + b));
+        tmx = fmax(tmx, *(volatile double *)(a.part + 2 * kMaxCtas + b));
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -571,111 +586,248 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         f.ybar = ts / (double)nt;
         f.ymin = tmn;
         f.ymax = tmx;
-        setup_grid(&f);
       }
     }
+    __syncthreads();
+    setup_grid(&f);
     __syncthreads();
   }
 
   // ---- evaluation passes (partials double-buffered: one barrier per pass) ----
-  for (int pass = 0; pass < kMaxRefinePasses + 3; ++pass) {
-    double *pw = part + 4 * kFitBlocks + (size_t)(pass & 1) * 4 * kMaxPts * kFitBlocks;
+  for (int pass = 1;; ++pass) {
     const int phase = f.phase;
     if (phase == PH_DONE) break;
+    double *pw = a.part + (size_t)(pass & 1) * 4 * kMaxPts * kMaxCtas;
     const int npts = f.npts;
     const bool deriv = (phase == PH_REFINE);
-    if (npts > 0) {
-      for (int q0 = 0; q0 < npts; q0 += 4) {
-        double P[4] = {0, 0, 0, 0}, L[4] = {0, 0, 0, 0}, dP[4] = {0, 0, 0, 0},
-               dL[4] = {0, 0, 0, 0};
-        double x[4];
-        int nu = min(4, npts - q0);
+    const int nk = deriv ? 4 : 2;
+    const int nbund = (npts + 3) / 4;
+    const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
+    const int items = nbund * slices;
+    for (int it = warp; it < items; it += kPotWarps) {
+      const int bnd = it % nbund, sl = it / nbund;
+      const int64_t len = c1 - c0;
+      const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
+      double x[4];
+      const int nu = min(4, npts - 4 * bnd);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[q0 + u] : 0.0;
-        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-          const double y = Y[i];
+      for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[4 * bnd + u] : 0.0;
+      double acc[4][4];
+      if (deriv)
+        eval_bundle<true>(Y, s0, s1, x, nu, acc);
+      else
+        eval_bundle<false>(Y, s0, s1, x, nu, acc);
+      if (lane == 0) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (u < nu) {
-              const double xy = x[u] * y;
-              const double r = 1.0 / (1.0 + xy);
-              P[u] -= xy * r;
-              L[u] += log1p(xy);
-              if (deriv) {
-                const double yr = y * r;
-                dL[u] += yr;
-                dP[u] -= yr * r;
-              }
-            }
-          }
-        }
+        for (int u = 0; u < 4; ++u)
+          if (u < nu)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            P[u] += __shfl_xor_sync(0xffffffffu, P[u], o);
-            L[u] += __shfl_xor_sync(0xffffffffu, L[u], o);
-            dP[u] += __shfl_xor_sync(0xffffffffu, dP[u], o);
-            dL[u] += __shfl_xor_sync(0xffffffffu, dL[u], o);
-          }
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (u < nu) {
-              wS[0][warp][q0 + u] = P[u];
-              wS[1][warp][q0 + u] = L[u];
-              wS[2][warp][q0 + u] = dP[u];
-              wS[3][warp][q0 + u] = dL[u];
-            }
-        }
-      }
-      __syncthreads();
-      const int nk = deriv ? 4 : 2;
-      for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
-        const int k = i / npts, pt = i % npts;
-        double sum = 0.0;
-        for (int w = 0; w < kCoopThreads / 32; ++w) sum += wS[k][w][pt];
-        pw[((size_t)k * kMaxPts + pt) * kFitBlocks + blockIdx.x] = sum;
+            for (int k = 0; k < 4; ++k) S.sred[sl * npts + 4 * bnd + u][k] = acc[u][k];
       }
     }
-    grid_barrier(bar_count, bar_gen, nb);
-    if (npts > 0) coop_reduce_points(f, pw, nb, npts, deriv);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (phase == PH_REFINE && ++f.iters >= kMaxRefinePasses && f.phase == PH_REFINE) {
-        // not converged: keep the current iterates, mark, and finish
-        for (int r = 0; r < f.nrefine; ++r) f.lo[f.refine_idx[r]] = f.xs[r];
-        controller(&f);
-        if (f.phase == PH_REFINE) {
-          for (int s2 = 0; s2 < f.nslots; ++s2) f.xs[s2] = f.lo[s2];
-          f.npts = f.nslots;
-          f.phase = PH_FINAL;
-        }
-      } else {
-        controller(&f);
+    // CTA partial per (k, point): slices summed in order
+    for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
+      const int k = i / npts, pt = i % npts;
+      double s = 0.0;
+      for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
+      pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
+    }
+    grid_sync(a.g);
+    // grid totals, fixed order: one warp per (k, point)
+    for (int i = warp; i < nk * npts; i += kPotWarps) {
+      const int k = i / npts, pt = i % npts;
+      const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
+      double v[(kMaxCtas + 31) / 32];
+#pragma unroll
+      for (int j = 0; j < (kMaxCtas + 31) / 32; ++j) {
+        const int b = lane + 32 * j;
+        v[j] = (b < nb) ? *(volatile const double *)(src + b) : 0.0;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < (kMaxCtas + 31) / 32; ++j) s += v[j];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) S.red[k][pt] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < npts) {
+      const int pt = threadIdx.x;
+      const double N = (double)nt;
+      const double Pm = S.red[0][pt] / N, Lm = S.red[1][pt] / N;
+      f.w[pt] = Pm + Lm + Pm * Lm;
+      f.L[pt] = Lm;
+      if (deriv) {
+        const double dPm = S.red[2][pt] / N, dLm = S.red[3][pt] / N;
+        f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) controller(&f);
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    gf->nt = f.nt;
-    gf->gamma = f.gamma;
-    gf->sigma = f.sigma;
-    gf->z_q = f.z_q;
-    gf->method = f.method;
-    gf->nroots = f.nroots;
-    gf->overflow = f.overflow;
-    gf->converged = f.converged;
-    gf->phase = f.phase;
+    PotGlobal *g = a.g;
+    g->gamma = f.gamma;
+    g->sigma = f.sigma;
+    g->z_q = f.z_q;
+    g->method = f.method;
+    g->nroots = f.nroots;
+    g->overflow = f.overflow;
+    g->converged = f.converged;
+    int st = ENOVA_OK;
+    if (f.overflow) st = ENOVA_ERR_UNSUPPORTED;
+    else if (!f.converged) st = ENOVA_ERR_UNSUPPORTED;
+    g->status = st;
   }
 }
 
+union PotShared {
+  unsigned int h[kBins];
+  FitShared fit;
+};
+
+__global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
+  __shared__ PotShared sh;
+  __shared__ SelS sel;
+  __shared__ unsigned long long wtot[kPotWarps];
+  __shared__ long long found[2];
+  __shared__ long long cta_base[2];
+  __shared__ int wcnt[kPotWarps];
+  PotGlobal *g = a.g;
+  if (threadIdx.x == 0) {
+    if (a.first == P_HIST0) {
+      sel.prefix = 0;
+      sel.mask = 0;
+      sel.k_rem = a.k;
+      sel.t = 0.f;
+    } else {
+      sel.prefix = g->prefix;
+      sel.mask = g->mask;
+      sel.k_rem = g->k_rem;
+      sel.t = g->t;
+    }
+  }
+  __syncthreads();
+  for (int ph = a.first; ph <= a.last; ++ph) {
+    if (ph > a.first) grid_sync(g);
+    if (ph == P_HIST0) {
+      // zero what is not covered by the per-call header memset (first used
+      // after the next barrier)
+      unsigned long long *h12 = a.hist + kBins;
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kBins;
+           i += gridDim.x * blockDim.x)
+        h12[i] = 0ull;
+      hist_pass(a, sel, 0, sh.h);
+    } else if (ph == P_HIST1 || ph == P_HIST2) {
+      select_digit(a, sel, ph - 1, wtot, reinterpret_cast<int *>(found));
+      hist_pass(a, sel, ph, sh.h);
+    } else if (ph == P_COMPACT) {
+      select_digit(a, sel, 2, wtot, reinterpret_cast<int *>(found));
+      compact(a, sel, wcnt, cta_base);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g->t = sel.t;
+        g->nt_local = cta_base[1];
+        g->nt_fit = cta_base[1];
+        if (cta_base[1] > a.cap) g->status = ENOVA_ERR_WORKSPACE;
+      }
+    } else if (ph == P_FIT) {
+      fit(a, sh.fit);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.last < P_COMPACT) {
+      g->prefix = sel.prefix;
+      g->mask = sel.mask;
+      g->k_rem = sel.k_rem;
+    }
+    if (a.last == P_FIT && a.out_dev) {
+      enova_threshold *o = a.out_dev;
+      const int st = g->status;
+      o->init_quantile = a.q0;
+      o->risk_q = a.q;
+      o->t = (double)g->t;
+      o->gamma = g->gamma;
+      o->sigma = g->sigma;
+      o->z_q = (st == ENOVA_OK) ? g->z_q : __longlong_as_double(0x7ff8000000000000ll);
+      o->n = a.n;
+      o->n_peaks = g->nt_fit;
+      o->method = g->method;
+      o->reserved = st;
+    }
+  }
+}
 
 // ------------------------------------------------------------- driver ----
-// Host syncs: single GPU 2 (after the grid scan: N_t, iteration count; at the
-// end: the result).  With a communicator 2 more (global n; tail counts for the
-// rank-ordered allgatherv).
+static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st) {
+  PotArgs c = a;
+  void *args[] = {(void *)&c};
+  count_launch();
+  ENOVA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_pot, dim3(nb), dim3(kPotThreads),
+                                             args, 0, st));
+  return ENOVA_OK;
+}
+
+static int pot_grid() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms < kMaxCtas ? sms : kMaxCtas;
+}
+
+static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double q0, double q,
+                         char *b, const ThrLayout &L, bool comm) {
+  PotArgs a;
+  a.scores = scores;
+  a.n_local = n_local;
+  a.n = n;
+  a.k = (unsigned long long)floor(q0 * (double)n);
+  a.q = q;
+  a.q0 = q0;
+  a.g = reinterpret_cast<PotGlobal *>(b + L.glob);
+  a.hist = reinterpret_cast<unsigned long long *>(b + L.hist);
+  a.counts = reinterpret_cast<long long *>(b + L.counts);
+  a.part = reinterpret_cast<double *>(b + L.part);
+  a.ydst = reinterpret_cast<double *>(b + (comm ? L.ylocal : L.yall));
+  a.yfit = reinterpret_cast<const double *>(b + L.yall);
+  a.cap = L.cap;
+  a.first = P_HIST0;
+  a.last = P_FIT;
+  a.out_dev = nullptr;
+  return a;
+}
+
+static enova_status check_k(int64_t n, double q0) {
+  if (n <= 0) {
+    set_error("no scores");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  const int64_t k = (int64_t)floor(q0 * (double)n);
+  if (k < 0 || k >= n) {
+    set_error("init_quantile out of range");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  return ENOVA_OK;
+}
+
+static enova_status status_error(int st) {
+  switch (st) {
+    case ENOVA_OK: return ENOVA_OK;
+    case ENOVA_ERR_TOO_FEW_EXCEEDANCES:
+      set_error("fewer than 10 exceedances above the initial threshold");
+      break;
+    case ENOVA_ERR_WORKSPACE: set_error("peak count exceeds workspace capacity"); break;
+    case ENOVA_ERR_UNSUPPORTED:
+      set_error("GPD fit: more than 64 Grimshaw roots or root refinement did not converge");
+      break;
+    default: set_error("threshold fit failed"); break;
+  }
+  return (enova_status)st;
+}
+
+// Host syncs: single GPU one (the result).  With a communicator two more
+// (global n; tail counts for the rank-ordered allgatherv).
 enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
                            enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
                            int64_t n_global_max, cudaStream_t st) {
@@ -686,17 +838,8 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     return ENOVA_ERR_WORKSPACE;
   }
   unsigned long long *nbuf = reinterpret_cast<unsigned long long *>(b + L.nbuf);
-  unsigned long long *hist = reinterpret_cast<unsigned long long *>(b + L.hist);
-  SelState *sel = reinterpret_cast<SelState *>(b + L.sel);
-  FitState *fit = reinterpret_cast<FitState *>(b + L.fit);
-  double *partials = reinterpret_cast<double *>(b + L.partials);
-  long long *counts = reinterpret_cast<long long *>(b + L.counts);
   long long *counts_all = reinterpret_cast<long long *>(b + L.counts_all);
-  double *ylocal = reinterpret_cast<double *>(b + L.ylocal);
-  double *yall = reinterpret_cast<double *>(b + L.yall);
-  long long *nt_dev = counts + kCompactBlocks;  // total written by k_scan_counts
 
-  // global n
   int64_t n = n_local;
   if (comm) {
     unsigned long long hn = (unsigned long long)n_local;
@@ -707,148 +850,93 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
     n = (int64_t)hn;
   }
-  if (n <= 0) {
-    set_error("no scores");
-    return ENOVA_ERR_INVALID_ARGUMENT;
-  }
+  enova_status r = check_k(n, q0);
+  if (r) return r;
   if (n > n_global_max) {
     set_error("total score count exceeds n_global_max used to size the workspace");
     return ENOVA_ERR_WORKSPACE;
   }
-  const int64_t k = (int64_t)floor(q0 * (double)n);
-  if (k < 0 || k >= n) {
-    set_error("init_quantile out of range");
-    return ENOVA_ERR_INVALID_ARGUMENT;
-  }
-
-  // K3: radix select of the k-th smallest key (3 digit passes, exact)
-  ENOVA_CUDA_TRY(cudaMemsetAsync(hist, 0, kBins * 8, st));
-  ENOVA_LAUNCH(k_sel_init, 1, 1, 0, st, sel, (unsigned long long)k);
-  const int shifts[3] = {21, 10, 0};
-  const int nbins[3] = {2048, 2048, 1024};
-  int hblocks = (int)((n_local + 4095) / 4096);   // ~8 keys per thread
-  if (hblocks < 1) hblocks = 1;
-  if (hblocks > 148 * 4) hblocks = 148 * 4;
-  for (int pass = 0; pass < 3; ++pass) {
-    if (n_local > 0)
-      ENOVA_LAUNCH(k_hist, hblocks, 512, 0, st, scores, n_local, sel, hist, shifts[pass],
-                   nbins[pass]);
-    if (comm) {
-      enova_status s = comm_allreduce_u64_sum(comm, hist, hist, (size_t)nbins[pass], st);
-      if (s) return s;
-    }
-    ENOVA_LAUNCH(k_select, 1, kSelThreads, 0, st, hist, sel, shifts[pass], nbins[pass]);
-  }
-
-  // K4: stable compaction of the peaks (bounded by the workspace capacity)
-  double *ydst = comm ? ylocal : yall;
-  if (n_local > 0) {
-    ENOVA_LAUNCH(k_count_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel,
-                 counts);
-    ENOVA_LAUNCH(k_scan_counts, 1, 1024, 0, st, counts, kCompactBlocks);
-    ENOVA_LAUNCH(k_scatter_peaks, kCompactBlocks, kCompactThreads, 0, st, scores, n_local, sel,
-                 counts, ydst, L.cap);
+  PotArgs a = make_args(scores, n_local, n, q0, q, b, L, comm != nullptr);
+  const int nb = pot_grid();
+  ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, L.header, st));
+  if (!comm) {
+    if ((r = launch_pot(a, nb, st))) return r;
   } else {
-    ENOVA_CUDA_TRY(cudaMemsetAsync(nt_dev, 0, 8, st));
-  }
-  ENOVA_CUDA_TRY(cudaGetLastError());
-  if (comm) {
-    enova_status s = comm_allgather_i64(comm, nt_dev, counts_all, st);
-    if (s) return s;
+    for (int p = P_HIST0; p <= P_HIST2; ++p) {
+      a.first = a.last = p;
+      if ((r = launch_pot(a, nb, st))) return r;
+      r = comm_allreduce_u64_sum(comm, a.hist + (size_t)p * kBins, a.hist + (size_t)p * kBins,
+                                 (size_t)kBins, st);
+      if (r) return r;
+    }
+    a.first = a.last = P_COMPACT;
+    if ((r = launch_pot(a, nb, st))) return r;
+    r = comm_allgather_i64(comm, &a.g->nt_local, counts_all, st);
+    if (r) return r;
     std::vector<int64_t> hc(comm->world), off(comm->world);
     ENOVA_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts_all, 8 * comm->world,
                                    cudaMemcpyDeviceToHost, st));
     ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
     int64_t tot = 0;
-    for (int r = 0; r < comm->world; ++r) {
-      off[r] = tot;
-      if (hc[r] > L.cap) {
+    for (int rk = 0; rk < comm->world; ++rk) {
+      off[rk] = tot;
+      if (hc[rk] > L.cap) {
         set_error("peak count exceeds workspace capacity");
         return ENOVA_ERR_WORKSPACE;
       }
-      tot += hc[r];
+      tot += hc[rk];
     }
     if (tot > L.cap) {
       set_error("peak count exceeds workspace capacity");
       return ENOVA_ERR_WORKSPACE;
     }
-    s = comm_allgatherv_f64(comm, ylocal, yall, hc.data(), off.data(), st);
-    if (s) return s;
+    r = comm_allgatherv_f64(comm, a.ydst, const_cast<double *>(a.yfit), hc.data(), off.data(),
+                            st);
+    if (r) return r;
     long long tl = tot;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(nbuf + 1, &tl, 8, cudaMemcpyHostToDevice, st));
-    nt_dev = reinterpret_cast<long long *>(nbuf + 1);
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(&a.g->nt_fit, &tl, 8, cudaMemcpyHostToDevice, st));
+    ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->status, 0, sizeof(int), st));
+    a.first = a.last = P_FIT;
+    if ((r = launch_pot(a, nb, st))) return r;
   }
-
-  // K5: GPD fit (replicated, deterministic).  N_t is read back once so every fit
-  // launch is sized to the tail (few blocks -> cheap last-block tickets).
-  int64_t nt_h = 0;
-  {
-    long long v = 0;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(&v, nt_dev, 8, cudaMemcpyDeviceToHost, st));
-    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-    nt_h = v;
-  }
-  if (nt_h > L.cap) {
-    set_error("peak count exceeds workspace capacity");
-    return ENOVA_ERR_WORKSPACE;
-  }
-  if (nt_h < 10) {
-    set_error("fewer than 10 exceedances above the initial threshold");
-    return ENOVA_ERR_TOO_FEW_EXCEEDANCES;
-  }
-  {
-    int dev = 0, sms = 148;
-    ENOVA_CUDA_TRY(cudaGetDevice(&dev));
-    ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int nb = sms < kFitBlocks ? sms : kFitBlocks;
-    const int64_t need = (nt_h + 63) / 64;   // >= 64 peaks per CTA
-    if (need < nb) nb = (int)(need < 1 ? 1 : need);
-    const double *Yc = yall;
-    FitState *fc = fit;
-    double *pc = partials;
-    const long long *ntc = nt_dev;
-    int64_t nc = n;
-    const SelState *sc = sel;
-    double qc = q;
-    void *args[] = {(void *)&Yc, (void *)&fc, (void *)&pc, (void *)&ntc,
-                    (void *)&nc, (void *)&sc, (void *)&qc};
-    ENOVA_CUDA_TRY(cudaMemsetAsync(&fit->counter, 0, sizeof(unsigned int), st));
-    count_launch();
-    ENOVA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_fit_coop, dim3(nb),
-                                               dim3(kCoopThreads), args, 0, st));
-  }
-  struct {
-    int overflow, converged;
-  } hh;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&hh.overflow, &fit->overflow, 4, cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&hh.converged, &fit->converged, 4, cudaMemcpyDeviceToHost, st));
-  struct {
-    double gamma, sigma, z_q;
-    int method, nroots;
-  } res;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&res, &fit->gamma, sizeof(res), cudaMemcpyDeviceToHost, st));
-  float t = 0.f;
-  ENOVA_CUDA_TRY(cudaMemcpyAsync(&t, &sel->t, 4, cudaMemcpyDeviceToHost, st));
+  PotGlobal hg;
+  ENOVA_CUDA_TRY(cudaMemcpyAsync(&hg, a.g, sizeof(hg), cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-  if (hh.overflow) {
-    set_error("more than 64 Grimshaw roots");
-    return ENOVA_ERR_UNSUPPORTED;
-  }
-  if (!hh.converged) {
-    set_error("GPD root refinement did not converge");
-    return ENOVA_ERR_UNSUPPORTED;
-  }
+  if ((r = status_error(hg.status))) return r;
   out->init_quantile = q0;
   out->risk_q = q;
-  out->t = (double)t;
-  out->gamma = res.gamma;
-  out->sigma = res.sigma;
-  out->z_q = res.z_q;
+  out->t = (double)hg.t;
+  out->gamma = hg.gamma;
+  out->sigma = hg.sigma;
+  out->z_q = hg.z_q;
   out->n = n;
-  out->n_peaks = nt_h;
-  out->method = res.method;
+  out->n_peaks = hg.nt_fit;
+  out->method = hg.method;
   out->reserved = 0;
   return ENOVA_OK;
+}
+
+// Stream-ordered single-GPU variant: no host synchronisation; the result (and
+// its status in out_dev->reserved) is written to device memory by the kernel.
+enova_status fit_threshold_async(const float *scores, int64_t n, double q0, double q,
+                                 enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                                 int64_t n_global_max, cudaStream_t st) {
+  char *b = static_cast<char *>(ws);
+  const ThrLayout L = thr_layout(n_global_max, q0);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = check_k(n, q0);
+  if (r) return r;
+  if (n > n_global_max) {
+    set_error("score count exceeds n_global_max used to size the workspace");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  PotArgs a = make_args(scores, n, n, q0, q, b, L, false);
+  a.out_dev = out_dev;
+  ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, L.header, st));
+  return launch_pot(a, pot_grid(), st);
 }
 
 size_t threshold_workspace_bytes(int64_t n_max, double q0) { return thr_layout(n_max, q0).total; }

@@ -356,3 +356,72 @@ def test_streaming_ring_matches_batch(E):
             f, s, m = E.detect(view, det, mean, std, thr, W - 1, W, return_scores=True)
             assert torch.equal(s[:, 0], sb[:, k - W + 1])
             assert torch.equal(f[:, 0], fb[:, k - W + 1])
+
+
+# ------------------------------------------- stream-ordered / graph path ----
+def test_async_pipeline_matches_sync_and_oracle(E):
+    """Pipeline (stats_async -> scores -> fit_threshold_async -> detect_async) gives
+    bitwise the same result as the synchronous calls, eagerly and as a CUDA graph."""
+    W, M, H, Z = 64, 16, 128, 16
+    N, T = 12, 3000
+    X = synth.metric_trace(N, T, M, seed=51)
+    wts = synth.detector_weights(W, M, H, Z, seed=51)
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    ref = E.run_pipeline(Xc, det, T // 2)
+    pipe = E.Pipeline(det, N, T, T // 2)
+    pipe.enqueue(Xc)
+    res = pipe.result()
+    assert res.threshold == ref.threshold
+    assert torch.equal(res.mean, ref.mean) and torch.equal(res.std, ref.std)
+    assert torch.equal(res.cal_scores, ref.cal_scores)
+    assert torch.equal(res.flags, ref.flags) and torch.equal(res.scores, ref.scores)
+    assert torch.equal(res.md, ref.md)
+    pipe.flags.zero_()
+    pipe.capture(Xc)
+    for _ in range(2):
+        pipe.replay()
+    res2 = pipe.result()
+    assert res2.threshold == ref.threshold and torch.equal(res2.flags, ref.flags)
+    o = O.pot_threshold(ref.cal_scores.cpu().numpy(), 0.98, 1e-3)
+    assert abs(res2.threshold["z_q"] - o["z_q"]) <= 1e-9 * o["z_q"]
+
+
+def test_async_failures_are_reported_on_device(E):
+    s = np.random.default_rng(1).exponential(1.0, 400).astype(np.float32)
+    thr = E.fit_threshold_async(cuda(s), 0.98, 1e-3)
+    with pytest.raises(E.EnovaError) as ei:
+        E.threshold_from_device(thr)
+    assert ei.value.name == "ENOVA_ERR_TOO_FEW_EXCEEDANCES"
+    from paper_2407_09486_b200 import _lib
+    t = _lib.Threshold.from_buffer_copy(bytes(thr.cpu().numpy().tobytes()))
+    assert math.isnan(t.z_q)
+    # a failed fit flags nothing
+    W, M, H, Z = 32, 8, 32, 4
+    X = synth.metric_trace(2, 400, M, seed=52)
+    det = E.PreparedDetector(synth.detector_weights(W, M, H, Z, seed=52))
+    Xc = cuda(X)
+    mean, std, _ = E.compute_stats(Xc, 200)
+    f, _, _ = E.detect_async(Xc, det, mean, std, thr)
+    assert int((f != 0).sum()) == 0
+    # non-finite calibration data is reported through diag
+    X[1, 10, 3] = np.inf
+    diag = torch.zeros(2, dtype=torch.int64, device="cuda")
+    E.compute_stats_async(cuda(X), 200, diag=diag)
+    with pytest.raises(E.EnovaError) as ei:
+        E.check_stats_diag(diag)
+    assert ei.value.name == "ENOVA_ERR_NONFINITE"
+
+
+def test_stats_chunked_one_pass_matches_oracle(E):
+    """One-pass shifted sums over time chunks: many instances (1 chunk each) and
+    few long ones (up to 16 chunks), incl. a degenerate and an offset series."""
+    for N, T, M in ((1, 20000, 8), (3, 9000, 32), (700, 300, 16)):
+        X = synth.metric_trace(N, T, M, seed=53 + N)
+        X[0, :, 1] = 7.25                                    # constant -> floored
+        X[-1, :, 0] += 1e4                                   # large offset vs spread
+        mean, std, nd = E.compute_stats(cuda(X), T // 2 + 3)
+        om, os_, ond = O.series_stats(X, T // 2 + 3)
+        assert nd == ond
+        assert np.max(np.abs(mean.cpu().numpy().view(np.int32) - om.view(np.int32))) <= 1
+        assert np.max(np.abs(std.cpu().numpy().view(np.int32) - os_.view(np.int32))) <= 1
