@@ -290,20 +290,19 @@ class Comm:
         self.handle, self.rank, self.world = handle, rank, world
 
     @staticmethod
-    def create(rank: int, world: int, device: int, group=None) -> "Comm":
-        import torch.distributed as dist
-        buf = (C.c_uint8 * 128)()
+    def unique_id(rank: int, world: int, group=None) -> bytes:
+        """Rank 0 draws the NCCL id (enova_comm_unique_id); every rank returns it."""
+        from .fleet import broadcast_unique_id
+        raw = None
         if rank == 0:
+            buf = (C.c_uint8 * 128)()
             check(lib().enova_comm_unique_id(buf))
-        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        if dist.is_initialized() and world > 1:
-            if dist.get_backend(group) == "nccl":
-                t = t.cuda(device)
-                dist.broadcast(t, 0, group=group)
-                t = t.cpu()
-            else:
-                dist.broadcast(t, 0, group=group)
-        raw = (C.c_uint8 * 128)(*t.tolist())
+            raw = bytes(buf)
+        return broadcast_unique_id(raw, rank, world, group)
+
+    @staticmethod
+    def create(rank: int, world: int, device: int, group=None) -> "Comm":
+        raw = (C.c_uint8 * 128)(*Comm.unique_id(rank, world, group))
         h = C.c_void_p()
         check(lib().enova_comm_create(C.byref(h), rank, world, raw, device))
         return Comm(h.value, rank, world)
