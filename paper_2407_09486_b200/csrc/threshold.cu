@@ -44,6 +44,7 @@ constexpr int kMaxPts = 128;
 constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
 constexpr int kMaxRefinePasses = 60;
+constexpr int kMaxStamps = 96;
 
 enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
 // phase program of k_pot
@@ -53,7 +54,7 @@ enum { P_HIST0 = 0, P_HIST1 = 1, P_HIST2 = 2, P_COMPACT = 3, P_FIT = 4 };
 // workspace (this struct and histogram 0) are zeroed by one memset per call;
 // everything else is initialised by the kernel itself.
 struct PotGlobal {
-  unsigned int bar_count, bar_gen;   // grid barrier
+  unsigned int bar_count, bar_gen;   // grid barrier arrivals (bar_gen unused)
   int status;                        // enova_status of the device phases
   int pad0;
   unsigned int prefix, mask;         // radix-select state after the last select
@@ -63,6 +64,9 @@ struct PotGlobal {
   long long nt_local, nt_fit;        // peaks of this rank / of the fit (all ranks)
   double gamma, sigma, z_q;
   int method, nroots, converged, overflow;
+  int n_stamps, fit_passes;
+  unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
+  unsigned long long t_first_start, t_last_end;   // over all CTAs (diagnostic)
 };
 
 struct FitState {
@@ -119,6 +123,7 @@ struct PotArgs {
   int first, last;          // phase range of this launch
   enova_threshold *out_dev; // optional device copy of the result
   double q0;
+  int ycache_cap;           // Y values per CTA held in dynamic shared memory
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -129,27 +134,40 @@ __device__ __forceinline__ float key2f(unsigned int k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// grid-wide barrier for a cooperative launch (all CTAs co-resident): one arrival
-// per CTA on a global ticket; the last arrival resets the ticket and bumps the
-// generation word the others wait on.  Self-resetting across barriers and
-// launches (the ticket is back at 0 after every barrier).
-__device__ __forceinline__ void grid_sync(PotGlobal *g) {
+// grid-wide barrier for a cooperative launch (all CTAs co-resident): a
+// monotonically increasing arrival counter (zeroed by the per-call header
+// memset, or before each launch of the communicator path).  Barrier number b
+// (1-based, counted per CTA in `epoch`) completes when the counter reaches
+// b * gridDim.x: one release-add per CTA, then acquire-polls of the same word
+// -- no fences, no second hop through a generation flag.
+__device__ __forceinline__ void grid_sync(PotGlobal *g, unsigned int &epoch) {
   __syncthreads();
+  ++epoch;
   if (threadIdx.x == 0) {
-    volatile unsigned int *vgen = &g->bar_gen;
-    const unsigned int gen = *vgen;
-    __threadfence();
-    const unsigned int ticket = atomicAdd(&g->bar_count, 1u);
-    if (ticket == gridDim.x - 1) {
-      *(volatile unsigned int *)&g->bar_count = 0;
-      __threadfence();
-      atomicAdd(&g->bar_gen, 1u);
-    } else {
-      while (*vgen == gen) __nanosleep(32);
+    const unsigned int target = epoch * gridDim.x;
+    unsigned int *p = &g->bar_count;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if (v >= target) break;
+      __nanosleep(16);
     }
-    __threadfence();
   }
   __syncthreads();
+}
+
+// diagnostic timestamps (CTA 0, thread 0): the running index lives in shared
+// memory -- no global read on the critical path; the stores are fire-and-forget
+__shared__ int s_nstamp;
+__device__ __forceinline__ void stamp(PotGlobal *g) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int i = s_nstamp;
+    if (i < kMaxStamps - 1) g->stamps[i] = t;
+    s_nstamp = i + 1;
+  }
 }
 
 // contiguous chunk of [0, n) owned by this CTA (multiple of 4 for float4 loads)
@@ -169,18 +187,26 @@ struct SelS {
 // ---------------------------------------------------------------- K3 ----
 // Histogram of the digit at `shift` of every key of this CTA's chunk that
 // matches the selected prefix; warp-aggregated shared atomics (keys of nearby
-// scores share bins), flushed to the global uint64 histogram.
-__device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned int *h) {
+// scores share bins), flushed to the global uint64 histogram.  Each thread
+// keeps 4 float4 loads in flight.  Pass 2 also counts this CTA's keys above
+// the selected 22-bit bucket (*above), so the peak count of the CTA follows
+// from its own histogram once the last digit is chosen (no counting pass).
+__device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned int *h,
+                          int *above_smem) {
   const int shift = (pass == 0) ? 21 : (pass == 1) ? 10 : 0;
   const int nbins = (pass == 2) ? 1024 : 2048;
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
+  if (threadIdx.x == 0) *above_smem = 0;
   __syncthreads();
   int64_t b0, b1;
   score_chunk(a.n_local, &b0, &b1);
   const unsigned int prefix = sel.prefix, mask = sel.mask;
+  const unsigned int bucket_hi = prefix | ~mask;   // pass 2: largest key of the bucket
+  int above = 0;
   auto add = [&](float f, bool valid) {
     const unsigned int k = f2key(f);
     const bool hit = valid && ((k & mask) == prefix);
+    above += (valid && k > bucket_hi);
     const unsigned int act = __ballot_sync(0xffffffffu, hit);
     if (hit) {
       const unsigned int bin = (k >> shift) & (nbins - 1);
@@ -189,25 +215,37 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
     }
   };
   const bool al = (reinterpret_cast<uintptr_t>(a.scores + b0) & 15) == 0;
+  int64_t tail0 = b0;
   if (al) {
     const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
     const int64_t n4 = (b1 - b0) / 4;
-    for (int64_t i0 = 0; i0 < n4; i0 += blockDim.x) {   // warp-uniform trip count
-      const int64_t i = i0 + threadIdx.x;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      const bool ok = i < n4;
-      if (ok) v = __ldg(x4 + i);
-      add(v.x, ok); add(v.y, ok); add(v.z, ok); add(v.w, ok);
+    for (int64_t i0 = 0; i0 < n4; i0 += 4 * blockDim.x) {   // warp-uniform trip count
+      float4 v[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * blockDim.x + threadIdx.x;
+        ok[u] = i < n4;
+        v[u] = ok[u] ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        add(v[u].x, ok[u]);
+        add(v[u].y, ok[u]);
+        add(v[u].z, ok[u]);
+        add(v[u].w, ok[u]);
+      }
     }
-    for (int64_t i0 = b0 + 4 * n4; i0 < b1; i0 += blockDim.x) {
-      const int64_t i = i0 + threadIdx.x;
-      add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
-    }
-  } else {
-    for (int64_t i0 = b0; i0 < b1; i0 += blockDim.x) {
-      const int64_t i = i0 + threadIdx.x;
-      add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
-    }
+    tail0 = b0 + 4 * n4;
+  }
+  for (int64_t i0 = tail0; i0 < b1; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
+  }
+  if (pass == 2) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+    if ((threadIdx.x & 31) == 0 && above) atomicAdd(above_smem, above);
   }
   __syncthreads();
   unsigned long long *gh = a.hist + (size_t)pass * kBins;
@@ -271,23 +309,45 @@ __device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned lon
 
 // ---------------------------------------------------------------- K4 ----
 // Stable compaction of the peaks Y = s - t (s > t) of this rank in index order.
-__device__ void compact(const PotArgs &a, const SelS &sel, int *wcnt, long long *cta_base) {
+// The CTA's peak count is known without reading the scores: keys above the
+// 22-bit bucket (counted in pass 2) plus its own pass-2 histogram bins above
+// the selected digit (h, still in shared memory).  One barrier publishes the
+// per-CTA counts; the scatter then keeps 4 float4 loads in flight per thread
+// and orders the output by (load slot, thread, element) = index order.
+__device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h, int above,
+                        bool have_hist, int *wcnt, long long *cta_base, unsigned int &epoch) {
   int64_t b0, b1;
   score_chunk(a.n_local, &b0, &b1);
   const float t = sel.t;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c = 0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += (__ldg(a.scores + i) > t);
+  if (have_hist) {
+    const unsigned int digit = f2key(t) & 1023u;
+    for (int i = (int)digit + 1 + threadIdx.x; i < 1024; i += blockDim.x) c += (int)h[i];
+  } else {   // separate launch (communicator path): count by reading the chunk
+    above = 0;
+    for (int64_t i0 = b0; i0 < b1; i0 += 4 * blockDim.x) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * blockDim.x + threadIdx.x;
+        v[u] = (i < b1) ? __ldg(a.scores + i) : -INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c += (v[u] > t);
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) wcnt[warp] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long s = 0;
+    long long s = above;
     for (int w = 0; w < kPotWarps; ++w) s += wcnt[w];
     a.counts[blockIdx.x] = s;
   }
-  grid_sync(a.g);
+  grid_sync(a.g, epoch);
+  stamp(a.g);
   if (warp == 0) {   // exclusive prefix of this CTA and the total, fixed order
     long long before = 0, tot = 0;
     for (int b = lane; b < (int)gridDim.x; b += 32) {
@@ -308,148 +368,256 @@ __device__ void compact(const PotArgs &a, const SelS &sel, int *wcnt, long long 
   __syncthreads();
   long long base = cta_base[0];
   const double td = (double)t;
-  for (int64_t i0 = b0; i0 < b1; i0 += blockDim.x) {
-    const int64_t i = i0 + threadIdx.x;
-    const float s = (i < b1) ? __ldg(a.scores + i) : 0.f;
-    const bool f = (i < b1) && (s > t);
-    const unsigned int bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) wcnt[warp] = __popc(bal);
-    __syncthreads();
-    int off = 0, all = 0;
-    for (int w = 0; w < kPotWarps; ++w) {
-      const int v = wcnt[w];
-      off += (w < warp) ? v : 0;
-      all += v;
+  const bool al = (reinterpret_cast<uintptr_t>(a.scores + b0) & 15) == 0;
+  int *wc = wcnt;   // [4][kPotWarps]
+  auto scatter4 = [&](const float (&v)[4][4], const bool (&ok)[4][4]) {
+    int cnt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      cnt[u] = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cnt[u] += (ok[u][e] && v[u][e] > t);
     }
-    if (f) {
-      const long long o = base + off + __popc(bal & ((1u << lane) - 1u));
-      if (o < a.cap) a.ydst[o] = (double)s - td;
+    int incl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      incl[u] = cnt[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl[u], o);
+        if (lane >= o) incl[u] += y;
+      }
+      if (lane == 31) wc[u * kPotWarps + warp] = incl[u];
     }
-    base += all;
     __syncthreads();
+    long long off_u = base;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int before_w = 0, all = 0;
+      for (int w = 0; w < kPotWarps; ++w) {
+        const int vv = wc[u * kPotWarps + w];
+        before_w += (w < warp) ? vv : 0;
+        all += vv;
+      }
+      long long o = off_u + before_w + incl[u] - cnt[u];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (ok[u][e] && v[u][e] > t) {
+          if (o < a.cap) a.ydst[o] = (double)v[u][e] - td;
+          ++o;
+        }
+      off_u += all;
+    }
+    base = off_u;
+    __syncthreads();
+  };
+  int64_t tail0 = b0;
+  if (al) {
+    const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
+    const int64_t n4 = (b1 - b0) / 4;
+    for (int64_t i0 = 0; i0 < n4; i0 += 4 * blockDim.x) {
+      float v[4][4];
+      bool ok[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * blockDim.x + threadIdx.x;
+        const bool g = i < n4;
+        const float4 q = g ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ok[u][e] = g;
+      }
+      scatter4(v, ok);
+    }
+    tail0 = b0 + 4 * n4;
+  }
+  for (int64_t i0 = tail0; i0 < b1; i0 += 16 * blockDim.x) {   // ragged tail / unaligned
+    float v[4][4];
+    bool ok[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + (int64_t)u * 4 * blockDim.x + 4 * threadIdx.x + e;
+        ok[u][e] = i < b1;
+        v[u][e] = ok[u][e] ? __ldg(a.scores + i) : 0.f;
+      }
+    scatter4(v, ok);
   }
 }
 
 // ---------------------------------------------------------------- K5 ----
-// Phase machine (identical in every CTA, run by thread 0 after each pass):
-//  GRID  : w at the fixed scan grids -> one slot per sign change (or exact zero);
-//  REFINE: safeguarded Newton on every bracket: w(x), w'(x) from the same pass;
-//          the bracket shrinks with the sign of w(x); the Newton iterate is kept
-//          if it falls strictly inside the bracket, else the bracket midpoint is
-//          used; converged when every step is <= 1e-13 |x| (the oracle bisects
-//          to a 2^-60 bracket: both land on the same root of the fp64 w);
-//  FINAL : L(x) at the roots -> gamma, sigma, log-likelihood; pick; z_q.
-__device__ void controller(FitState *f) {
-  if (f->phase == PH_GRID) {
-    int ns = 0;
-    auto push = [&](double lo, double hi, double wlo, double whi, int exact) {
-      if (ns >= kMaxSlots) {
-        f->overflow = 1;
-        return;
+// Phase machine, run by the whole CTA after each pass (identical in every CTA):
+//  GRID  : w at the fixed scan grids -> one slot per sign change (or exact zero),
+//          slots in grid order (block prefix count over the points);
+//  REFINE: safeguarded Newton on every bracket, one thread per root: w(x), w'(x)
+//          from the same pass; the bracket shrinks with the sign of w(x); the
+//          Newton iterate is kept if it falls strictly inside the bracket, else
+//          the bracket midpoint is used; converged when every step is
+//          <= 1e-13 |x| (the oracle bisects to a 2^-60 bracket: both land on the
+//          same root of the fp64 w);
+//  FINAL : L(x) at the roots -> gamma, sigma, log-likelihood (one thread per
+//          root); pick the best; z_q.
+__device__ void controller(FitState *f, int *scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int phase = f->phase;   // read by all threads before any write below
+  __syncthreads();
+  if (phase == PH_GRID) {
+    const int npts = f->npts;
+    bool ex = false, br = false;
+    double xk = 0.0, xk1 = 0.0, wk = 0.0, wk1 = 0.0;
+    if (tid < npts) {
+      const int j = tid % kGrid;
+      xk = f->xs[tid];
+      wk = f->w[tid];
+      ex = (wk == 0.0);
+      if (!ex && j < kGrid - 1) {
+        xk1 = f->xs[tid + 1];
+        wk1 = f->w[tid + 1];
+        br = (wk * wk1 < 0.0);
       }
-      f->lo[ns] = lo;
-      f->hi[ns] = hi;
-      f->wlo[ns] = wlo;
-      f->whi[ns] = whi;
-      f->exact[ns] = exact;
-      ++ns;
-    };
-    for (int g = 0; g * kGrid < f->npts; ++g) {
-      const double *x = f->xs + g * kGrid;
-      const double *w = f->w + g * kGrid;
-      for (int k = 0; k < kGrid - 1; ++k) {
-        if (w[k] == 0.0)
-          push(x[k], x[k], 0.0, 0.0, 1);
-        else if (w[k] * w[k + 1] < 0.0)
-          push(x[k], x[k + 1], w[k], w[k + 1], 0);
-      }
-      if (w[kGrid - 1] == 0.0) push(x[kGrid - 1], x[kGrid - 1], 0.0, 0.0, 1);
     }
-    f->nslots = ns;
+    const bool has = ex || br;
+    const unsigned int bh = __ballot_sync(0xffffffffu, has), bb = __ballot_sync(0xffffffffu, br);
+    if (lane == 0 && warp < kMaxPts / 32) {
+      scratch[warp] = __popc(bh);
+      scratch[8 + warp] = __popc(bb);
+    }
+    __syncthreads();   // all reads of xs / w done
+    int tot_h = 0, tot_b = 0, off_h = 0, off_b = 0;
+    for (int w = 0; w < kMaxPts / 32; ++w) {
+      tot_h += scratch[w];
+      tot_b += scratch[8 + w];
+      if (w < warp) {
+        off_h += scratch[w];
+        off_b += scratch[8 + w];
+      }
+    }
+    const unsigned int lt = (1u << lane) - 1u;
+    off_h += __popc(bh & lt);
+    off_b += __popc(bb & lt);
+    const int ns = min(tot_h, kMaxSlots);
+    if (has && off_h < kMaxSlots) {
+      f->lo[off_h] = xk;
+      f->hi[off_h] = ex ? xk : xk1;
+      f->wlo[off_h] = ex ? 0.0 : wk;
+      f->whi[off_h] = ex ? 0.0 : wk1;
+      f->exact[off_h] = ex ? 1 : 0;
+    }
+    // refine slots: the bracket slots that fit, in slot order
     int nr = 0;
-    for (int s = 0; s < ns; ++s)
-      if (!f->exact[s]) f->refine_idx[nr++] = s;
-    f->nrefine = nr;
-    f->converged = 0;
-    if (nr > 0) {
-      for (int r = 0; r < nr; ++r) {   // first iterate: secant (regula falsi) point
-        const int s = f->refine_idx[r];
-        const double lo = f->lo[s], hi = f->hi[s];
-        double x0 = lo - f->wlo[s] * (hi - lo) / (f->whi[s] - f->wlo[s]);
-        if (!(x0 > fmin(lo, hi) && x0 < fmax(lo, hi))) x0 = 0.5 * (lo + hi);
-        f->xs[r] = x0;
-      }
-      f->npts = nr;
-      f->phase = PH_REFINE;
-    } else {
-      f->phase = PH_FINAL;
-      f->converged = 1;
-      for (int s = 0; s < ns; ++s) f->xs[s] = f->lo[s];
-      f->npts = ns;
+    {
+      // brackets among the first kMaxSlots slots: count those with off_h < kMaxSlots
+      const unsigned int bbf = __ballot_sync(0xffffffffu, br && off_h < kMaxSlots);
+      if (lane == 0 && warp < kMaxPts / 32) scratch[16 + warp] = __popc(bbf);
+      __syncthreads();
+      for (int w = 0; w < kMaxPts / 32; ++w) nr += scratch[16 + w];
     }
+    if (br && off_h < kMaxSlots) {
+      f->refine_idx[off_b] = off_h;
+      double x0 = xk - wk * (xk1 - xk) / (wk1 - wk);   // first iterate: secant point
+      if (!(x0 > fmin(xk, xk1) && x0 < fmax(xk, xk1))) x0 = 0.5 * (xk + xk1);
+      f->xs[off_b] = x0;
+    }
+    __syncthreads();
+    if (nr == 0 && tid < ns) f->xs[tid] = f->lo[tid];
+    if (tid == 0) {
+      f->nslots = ns;
+      f->overflow = (tot_h > kMaxSlots) ? 1 : f->overflow;
+      f->nrefine = nr;
+      f->converged = (nr == 0) ? 1 : 0;
+      f->npts = (nr > 0) ? nr : ns;
+      f->phase = (nr > 0) ? PH_REFINE : PH_FINAL;
+    }
+    __syncthreads();
     return;
   }
-  if (f->phase == PH_REFINE) {
-    bool all_conv = true;
-    for (int r = 0; r < f->nrefine; ++r) {
-      const int s = f->refine_idx[r];
-      const double x = f->xs[r], w = f->w[r], dw = f->dw[r];
-      double lo = f->lo[s], hi = f->hi[s];
+  if (phase == PH_REFINE) {
+    const int nr = f->nrefine, iters = f->iters;
+    bool conv = true;
+    double xn = 0.0;
+    int sidx = 0;
+    if (tid < nr) {
+      sidx = f->refine_idx[tid];
+      const double x = f->xs[tid], w = f->w[tid], dw = f->dw[tid];
+      double lo = f->lo[sidx], hi = f->hi[sidx];
       if (w == 0.0) {
         lo = hi = x;
-      } else if ((w > 0) == (f->wlo[s] > 0)) {
+      } else if ((w > 0) == (f->wlo[sidx] > 0)) {
         lo = x;
-        f->wlo[s] = w;
+        f->wlo[sidx] = w;
       } else {
         hi = x;
       }
-      f->lo[s] = lo;
-      f->hi[s] = hi;
-      double xn = (dw != 0.0) ? x - w / dw : 0.5 * (lo + hi);
+      f->lo[sidx] = lo;
+      f->hi[sidx] = hi;
+      xn = (dw != 0.0) ? x - w / dw : 0.5 * (lo + hi);
       const double a = fmin(lo, hi), b = fmax(lo, hi);
-      if (!(xn > a && xn < b) || f->iters > 20) xn = 0.5 * (lo + hi);   // safeguard: bisect
+      if (!(xn > a && xn < b) || iters > 20) xn = 0.5 * (lo + hi);   // safeguard: bisect
       if (lo == hi) xn = lo;
-      if (!(fabs(xn - x) <= 1e-13 * fabs(x))) all_conv = false;
-      f->xs[r] = xn;
+      conv = fabs(xn - x) <= 1e-13 * fabs(x);
+      f->xs[tid] = xn;
     }
-    ++f->iters;
-    if (all_conv || f->iters >= kMaxRefinePasses) {
+    const int all_conv = __syncthreads_and(conv);
+    const bool done = all_conv || iters + 1 >= kMaxRefinePasses;
+    if (done) {
       // every slot's root estimate is final (exact grid zeros keep lo)
-      for (int r = 0; r < f->nrefine; ++r) f->lo[f->refine_idx[r]] = f->xs[r];
-      for (int s = 0; s < f->nslots; ++s) f->xs[s] = f->lo[s];
-      f->npts = f->nslots;
-      f->phase = PH_FINAL;
-      f->converged = all_conv ? 1 : 0;
+      if (tid < nr) f->lo[sidx] = xn;
+      __syncthreads();
+      if (tid < f->nslots) f->xs[tid] = f->lo[tid];
     }
-    return;
-  }
-  if (f->phase == PH_FINAL) {
-    const double N = (double)f->nt;
-    double bg = 0.0, bs = f->ybar, bll = -N * (log(f->ybar) + 1.0);
-    int method = 1, nroots = 0;
-    for (int s = 0; s < f->nslots; ++s) {
-      const double x = f->xs[s];
-      const double g = f->L[s];
-      if (x == 0.0 || g == 0.0) continue;
-      const double sg = g / x;
-      if (!(sg > 0.0)) continue;
-      ++nroots;
-      const double ll = -N * (log(sg) + g + 1.0);
-      if (ll > bll || (ll == bll && fabs(g) < fabs(bg))) {
-        bll = ll;
-        bg = g;
-        bs = sg;
-        method = 0;
+    if (tid == 0) {
+      f->iters = iters + 1;
+      if (done) {
+        f->npts = f->nslots;
+        f->phase = PH_FINAL;
+        f->converged = all_conv ? 1 : 0;
       }
     }
-    const double r = f->q * (double)f->n / N;
-    const double lr = log(r);
-    f->gamma = bg;
-    f->sigma = bs;
-    f->method = method;
-    f->nroots = nroots;
-    f->z_q = (bg == 0.0) ? f->t - bs * lr : f->t + (bs / bg) * expm1(-bg * lr);
-    f->phase = PH_DONE;
+    __syncthreads();
+    return;
+  }
+  if (phase == PH_FINAL) {
+    const double N = (double)f->nt;
+    const int ns = f->nslots;
+    // candidate log-likelihoods, one thread per root (kept in dw / w)
+    if (tid < ns) {
+      const double x = f->xs[tid];
+      const double g = f->L[tid];
+      double ll = -INFINITY, sg = 0.0;
+      if (x != 0.0 && g != 0.0) {
+        sg = g / x;
+        if (sg > 0.0) ll = -N * (log(sg) + g + 1.0);
+      }
+      f->dw[tid] = ll;
+      f->w[tid] = sg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bg = 0.0, bs = f->ybar, bll = -N * (log(f->ybar) + 1.0);
+      int method = 1, nroots = 0;
+      for (int s2 = 0; s2 < ns; ++s2) {
+        const double ll = f->dw[s2];
+        if (!(f->w[s2] > 0.0) || f->xs[s2] == 0.0 || f->L[s2] == 0.0) continue;
+        ++nroots;
+        const double g = f->L[s2];
+        if (ll > bll || (ll == bll && fabs(g) < fabs(bg))) {
+          bll = ll;
+          bg = g;
+          bs = f->w[s2];
+          method = 0;
+        }
+      }
+      const double r = f->q * (double)f->n / N;
+      const double lr = log(r);
+      f->gamma = bg;
+      f->sigma = bs;
+      f->method = method;
+      f->nroots = nroots;
+      f->z_q = (bg == 0.0) ? f->t - bs * lr : f->t + (bs / bg) * expm1(-bg * lr);
+      f->phase = PH_DONE;
+    }
+    __syncthreads();
   }
 }
 
@@ -472,24 +640,86 @@ __device__ void setup_grid(FitState *f) {
   }
 }
 
+// ---- fp64 kernels of the w(x) sums: reciprocal and log1p ----------------
+// 1/v: MUFU seed (rcp.approx.ftz.f64) + two Newton steps (rounding-limited).
+__device__ __forceinline__ double rcp_nr(double v) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  double e = fma(-v, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-v, r, 1.0);
+  return fma(r, e, r);
+}
+
+constexpr int kLogTab = 130;      // nodes c_i = 1 + (i - kLogOne)/181, i = 0..128 (+1 pad)
+constexpr int kLogOne = 53;       // c_53 = 1 exactly: log(c) = 0, no cancellation near v = 1
+constexpr double kLogStep = 181.0;
+struct LogTab {
+  double inv_c[kLogTab], tlog[kLogTab];   // 1/c_i and -log(1/c_i)
+};
+__device__ void fill_logtab(LogTab &T) {
+  for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) {
+    const double c = 1.0 + (double)(i - kLogOne) / kLogStep;
+    const double ic = 1.0 / c;
+    T.inv_c[i] = ic;
+    T.tlog[i] = (i == kLogOne) ? 0.0 : -log(ic);
+  }
+}
+
+// log1p(u) for u > -1, given v = fl(1 + u) and iv = 1/v:
+//   log1p(u) = log(v) + c/v, c = u - (v - 1) the rounding error of v (exact);
+//   log(v) = e ln2 + log(c_i) + log1p(r), v = 2^e m, m in [sqrt(1/2), sqrt(2)),
+//   c_i the nearest of the nodes 1 + k/181 and r = m/c_i - 1 (|r| < 2^-8,
+//   degree-7 alternating series).  Near v = 1 the node is 1 itself, so r = v - 1
+//   exactly and the result keeps full relative accuracy for tiny |u|.  One
+//   branch-free path (about 2 ulp measured against long-double log1p).
+__device__ __forceinline__ double log1p_fast(double u, double v, double iv, const LogTab &T) {
+  const double c = u - (v - 1.0);
+  int hi = __double2hiint(v);
+  const int lo = __double2loint(v);
+  int e = (hi >> 20) - 1023;
+  hi = (hi & 0x000fffff) | 0x3ff00000;
+  if (hi > 0x3ff6a09e) {   // m > sqrt(2): halve
+    hi -= 0x00100000;
+    ++e;
+  }
+  const double m = __hiloint2double(hi, lo);
+  int idx = __double2int_rd(fma(m - 1.0, kLogStep, kLogOne + 0.5));
+  idx = min(max(idx, 0), kLogTab - 2);
+  const double r = fma(m, T.inv_c[idx], -1.0);
+  double p = -0.125;
+  p = fma(p, r, 1.0 / 7.0);
+  p = fma(p, r, -1.0 / 6.0);
+  p = fma(p, r, 0.2);
+  p = fma(p, r, -0.25);
+  p = fma(p, r, 1.0 / 3.0);
+  p = fma(p, r, -0.5);
+  p = fma(p, r, 1.0);
+  constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+  const double ed = (double)e;
+  return fma(ed, kLn2Hi, T.tlog[idx]) + fma(ed, kLn2Lo, fma(p, r, c * iv));
+}
+
 // Sums over this CTA's slice of Y of P = -xY/(1+xY), L = log1p(xY) and, for
 // Newton, dP = -Y/(1+xY)^2, dL = Y/(1+xY), for up to 4 points x per warp item.
 template <bool kDeriv>
 __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t s1,
-                                            const double (&x)[4], int nu, double (&acc)[4][4]) {
+                                            const double (&x)[4], int nu, double (&acc)[4][4],
+                                            const LogTab &T) {
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[u][k] = 0.0;
   for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
-    const double y = Y[i];   // written by this kernel's compaction: coherent load, not .nc
+    const double y = Y[i];   // shared-memory copy (or global: coherent load, not .nc)
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (u < nu) {
         const double xy = x[u] * y;
-        const double r = 1.0 / (1.0 + xy);
+        const double v = 1.0 + xy;
+        const double r = rcp_nr(v);
         acc[u][0] -= xy * r;
-        acc[u][1] += log1p(xy);
+        acc[u][1] += log1p_fast(xy, v, r, T);
         if (kDeriv) {
           const double yr = y * r;
           acc[u][2] -= yr * r;
@@ -508,11 +738,13 @@ __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t
 
 struct FitShared {
   FitState f;
+  LogTab tab;
+  int scratch[32];
   double sred[kMaxPts][4];   // per warp item partial sums [item][k]
   double red[4][kMaxPts];    // grid totals after the barrier
 };
 
-__device__ void fit(const PotArgs &a, FitShared &S) {
+__device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
   FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
@@ -534,13 +766,19 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
   }
   const int64_t chunk = (nt + nb - 1) / nb;
   const int64_t c0 = min(nt, (int64_t)blockIdx.x * chunk), c1 = min(nt, c0 + chunk);
-  const double *Y = a.yfit;
+  // this CTA's slice of Y is staged in shared memory by the Y-statistics pass
+  // (every later pass reads it from there); global reads if it does not fit
+  extern __shared__ double ycache[];
+  const bool cached = (c1 - c0) <= (int64_t)a.ycache_cap;
+  const double *Y = cached ? (const double *)ycache - c0 : a.yfit;
+  fill_logtab(S.tab);   // first read after the next barrier
 
   // ---- Ybar, Ymin, Ymax (pass 0, partial buffer 0) ----
   {
     double s = 0.0, mn = INFINITY, mx = -INFINITY;
     for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const double y = Y[i];
+      const double y = a.yfit[i];   // written by this kernel's compaction: coherent load
+      if (cached) ycache[i - c0] = y;
       s += y;
       mn = fmin(mn, y);
       mx = fmax(mx, y);
@@ -568,7 +806,8 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
       a.part[1 * kMaxCtas + blockIdx.x] = tmn;
       a.part[2 * kMaxCtas + blockIdx.x] = tmx;
     }
-    grid_sync(a.g);
+    grid_sync(a.g, epoch);
+    stamp(a.g);
     if (warp == 0) {
       double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
       for (int b = lane; b < nb; b += 32) {
@@ -614,9 +853,9 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
       for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[4 * bnd + u] : 0.0;
       double acc[4][4];
       if (deriv)
-        eval_bundle<true>(Y, s0, s1, x, nu, acc);
+        eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
       else
-        eval_bundle<false>(Y, s0, s1, x, nu, acc);
+        eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
       if (lane == 0) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -633,23 +872,37 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
       for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
       pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
     }
-    grid_sync(a.g);
-    // grid totals, fixed order: one warp per (k, point)
-    for (int i = warp; i < nk * npts; i += kPotWarps) {
-      const int k = i / npts, pt = i % npts;
-      const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
-      double v[(kMaxCtas + 31) / 32];
+    stamp(a.g);
+    grid_sync(a.g, epoch);
+    stamp(a.g);
+    // grid totals, fixed order: one warp per (k, point), 4 items in flight per warp
+    {
+      constexpr int kJ = (kMaxCtas + 31) / 32;
+      const int nitems = nk * npts;
+      for (int i0 = 4 * warp; i0 < nitems; i0 += 4 * kPotWarps) {
+        double v[4][kJ];
 #pragma unroll
-      for (int j = 0; j < (kMaxCtas + 31) / 32; ++j) {
-        const int b = lane + 32 * j;
-        v[j] = (b < nb) ? *(volatile const double *)(src + b) : 0.0;
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + q;
+          const int k = i / npts, pt = i % npts;
+          const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
+#pragma unroll
+          for (int j = 0; j < kJ; ++j) {
+            const int b = lane + 32 * j;
+            v[q][j] = (i < nitems && b < nb) ? *(volatile const double *)(src + b) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double sum = 0.0;
+#pragma unroll
+          for (int j = 0; j < kJ; ++j) sum += v[q][j];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          const int i = i0 + q;
+          if (lane == 0 && i < nitems) S.red[i / npts][i % npts] = sum;
+        }
       }
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < (kMaxCtas + 31) / 32; ++j) s += v[j];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) S.red[k][pt] = s;
     }
     __syncthreads();
     if (threadIdx.x < npts) {
@@ -664,8 +917,8 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) controller(&f);
-    __syncthreads();
+    stamp(a.g);
+    controller(&f, S.scratch);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     PotGlobal *g = a.g;
@@ -676,6 +929,7 @@ __device__ void fit(const PotArgs &a, FitShared &S) {
     g->nroots = f.nroots;
     g->overflow = f.overflow;
     g->converged = f.converged;
+    g->fit_passes = f.iters;
     int st = ENOVA_OK;
     if (f.overflow) st = ENOVA_ERR_UNSUPPORTED;
     else if (!f.converged) st = ENOVA_ERR_UNSUPPORTED;
@@ -694,8 +948,19 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   __shared__ unsigned long long wtot[kPotWarps];
   __shared__ long long found[2];
   __shared__ long long cta_base[2];
-  __shared__ int wcnt[kPotWarps];
+  __shared__ int wcnt[4 * kPotWarps];
+  __shared__ int above;
   PotGlobal *g = a.g;
+  unsigned int epoch = 0;   // grid barriers passed in this launch
+  if (threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (blockIdx.x == 0) {
+      g->stamps[kMaxStamps - 1] = t0;
+      s_nstamp = g->n_stamps;
+    }
+    atomicMax(&g->t_first_start, ~t0);   // stored complemented: max(~t) = ~min(t)
+  }
   if (threadIdx.x == 0) {
     if (a.first == P_HIST0) {
       sel.prefix = 0;
@@ -711,7 +976,8 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   }
   __syncthreads();
   for (int ph = a.first; ph <= a.last; ++ph) {
-    if (ph > a.first) grid_sync(g);
+    if (ph > a.first) grid_sync(g, epoch);
+    stamp(g);
     if (ph == P_HIST0) {
       // zero what is not covered by the per-call header memset (first used
       // after the next barrier)
@@ -719,13 +985,13 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kBins;
            i += gridDim.x * blockDim.x)
         h12[i] = 0ull;
-      hist_pass(a, sel, 0, sh.h);
+      hist_pass(a, sel, 0, sh.h, &above);
     } else if (ph == P_HIST1 || ph == P_HIST2) {
       select_digit(a, sel, ph - 1, wtot, reinterpret_cast<int *>(found));
-      hist_pass(a, sel, ph, sh.h);
+      hist_pass(a, sel, ph, sh.h, &above);
     } else if (ph == P_COMPACT) {
       select_digit(a, sel, 2, wtot, reinterpret_cast<int *>(found));
-      compact(a, sel, wcnt, cta_base);
+      compact(a, sel, sh.h, above, a.first < P_COMPACT, wcnt, cta_base, epoch);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         g->t = sel.t;
         g->nt_local = cta_base[1];
@@ -733,10 +999,17 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
         if (cta_base[1] > a.cap) g->status = ENOVA_ERR_WORKSPACE;
       }
     } else if (ph == P_FIT) {
-      fit(a, sh.fit);
+      fit(a, sh.fit, epoch);
     }
   }
+  stamp(g);
+  if (threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicMax(&g->t_last_end, t1);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g->n_stamps = s_nstamp;
     if (a.last < P_COMPACT) {
       g->prefix = sel.prefix;
       g->mask = sel.mask;
@@ -760,12 +1033,30 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
 }
 
 // ------------------------------------------------------------- driver ----
-static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st) {
+constexpr int kMaxYCacheBytes = 160 * 1024;
+
+static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool reset_barrier = false) {
   PotArgs c = a;
+  static bool attr_set[64] = {};   // per device (function attributes are per context)
+  int dev = 0;
+  ENOVA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kMaxYCacheBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  // the fit partitions N_t <= cap peaks into nb contiguous slices
+  const int64_t per_cta = (a.cap + nb - 1) / nb;
+  const int64_t cap_vals = per_cta < kMaxYCacheBytes / 8 ? per_cta : kMaxYCacheBytes / 8;
+  c.ycache_cap = (int)cap_vals;
+  const size_t dyn = (a.first <= P_FIT && a.last >= P_FIT) ? (size_t)cap_vals * 8 : 0;
+  if (dyn == 0) c.ycache_cap = 0;
+  if (reset_barrier) ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->bar_count, 0, sizeof(unsigned int), st));
   void *args[] = {(void *)&c};
   count_launch();
   ENOVA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_pot, dim3(nb), dim3(kPotThreads),
-                                             args, 0, st));
+                                             args, dyn, st));
   return ENOVA_OK;
 }
 
@@ -864,13 +1155,13 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
   } else {
     for (int p = P_HIST0; p <= P_HIST2; ++p) {
       a.first = a.last = p;
-      if ((r = launch_pot(a, nb, st))) return r;
+      if ((r = launch_pot(a, nb, st, p > P_HIST0))) return r;
       r = comm_allreduce_u64_sum(comm, a.hist + (size_t)p * kBins, a.hist + (size_t)p * kBins,
                                  (size_t)kBins, st);
       if (r) return r;
     }
     a.first = a.last = P_COMPACT;
-    if ((r = launch_pot(a, nb, st))) return r;
+    if ((r = launch_pot(a, nb, st, true))) return r;
     r = comm_allgather_i64(comm, &a.g->nt_local, counts_all, st);
     if (r) return r;
     std::vector<int64_t> hc(comm->world), off(comm->world);
@@ -897,7 +1188,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
     ENOVA_CUDA_TRY(cudaMemcpyAsync(&a.g->nt_fit, &tl, 8, cudaMemcpyHostToDevice, st));
     ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->status, 0, sizeof(int), st));
     a.first = a.last = P_FIT;
-    if ((r = launch_pot(a, nb, st))) return r;
+    if ((r = launch_pot(a, nb, st, true))) return r;
   }
   PotGlobal hg;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&hg, a.g, sizeof(hg), cudaMemcpyDeviceToHost, st));
