@@ -200,6 +200,15 @@ def fit_threshold_async(scores: torch.Tensor, init_quantile: float = 0.98, risk_
     return thr
 
 
+def threshold_to_device(thr: dict, device=None) -> torch.Tensor:
+    """A host threshold (fit_threshold's dict) as a DEVICE enova_threshold for
+    detect_async (e.g. a fleet threshold frozen for streaming)."""
+    t = _thr_struct(thr)
+    t.reserved = 0
+    raw = np.frombuffer(bytes(t), dtype=np.uint8).copy()
+    return torch.from_numpy(raw).to(device or "cuda")
+
+
 def threshold_from_device(thr_dev: torch.Tensor) -> dict:
     """Read a device enova_threshold (synchronises); raises on a failed fit."""
     raw = bytes(thr_dev.cpu().numpy().tobytes())
