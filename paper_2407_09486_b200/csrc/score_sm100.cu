@@ -408,22 +408,37 @@ enova_status launch_score_pair(const enova_series *s, const DetLayout &L, const 
                                float *scores, float *md, int8_t *flags, double z_q,
                                const double *z_q_dev, cudaStream_t st);
 
-// Kernel choice by shape: the weight-stationary CTA-pair kernel whenever half of
-// W1 fits in shared memory (all BASELINE configs), else the W1-streaming kernel.
-// ENOVA_SCORE_KERNEL=stream forces the streaming kernel (diagnostic / A-B tests).
-static bool force_stream() {
+bool rows_path_ok(const DetLayout &L);
+enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const void *det_ws,
+                               float *scores, float *md, int8_t *flags, double z_q,
+                               const double *z_q_dev, cudaStream_t st);
+
+// Kernel choice by shape:
+//  * few windows per instance (nw <= kRowModeMaxWindows, e.g. a streaming tick):
+//    the instance-batched row kernel (128 independent windows per tile);
+//  * else the weight-stationary CTA-pair kernel whenever half of W1 fits in
+//    shared memory (all BASELINE configs), else the W1-streaming kernel.
+// ENOVA_SCORE_KERNEL=stream | pair | rows forces a kernel (diagnostic / A-B tests;
+// "rows" only where the row kernel supports the shape).
+constexpr int64_t kRowModeMaxWindows = 16;
+static int forced_kernel() {   // 0 auto, 1 stream, 2 pair, 3 rows
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("ENOVA_SCORE_KERNEL");
-    v = (e && strcmp(e, "stream") == 0) ? 1 : 0;
+    v = !e ? 0 : strcmp(e, "stream") == 0 ? 1 : strcmp(e, "pair") == 0 ? 2
+             : strcmp(e, "rows") == 0 ? 3 : 0;
   }
-  return v == 1;
+  return v;
 }
 
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
                           float *scores, float *md, int8_t *flags, double z_q, const double *z_q_dev,
                           cudaStream_t st) {
-  if (!force_stream() && pair_path_ok(L))
+  const int f = forced_kernel();
+  const int64_t nw = s->t_end - s->t_begin;
+  if (rows_path_ok(L) && (f == 3 || (f == 0 && nw <= kRowModeMaxWindows)))
+    return launch_score_rows(s, L, det_ws, scores, md, flags, z_q, z_q_dev, st);
+  if (f != 1 && pair_path_ok(L))
     return launch_score_pair(s, L, det_ws, scores, md, flags, z_q, z_q_dev, st);
   ScoreParams p{};
   const uint8_t *b = static_cast<const uint8_t *>(det_ws);
