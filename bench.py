@@ -241,18 +241,19 @@ def run_streaming(args, rank, world, local_rank):
     # samples of the streamed ticks, [tick][instance][metric]
     S = X[:, t_hist:].transpose(0, 1).contiguous()
     S_h = torch.from_numpy(np.ascontiguousarray(Xh[:, t_hist:].transpose(1, 0, 2))).pin_memory()
-    ring = torch.zeros((n, 2 * W, M), dtype=torch.float32, device=dev)
+    # the ingest-normalised fp16 ring (enova_stream_*), filled with the W-1
+    # samples before the first streamed tick
+    ring = E.StreamRing(det, mean, std)
     for t in range(t_hist - W + 1, t_hist):
-        E.ring_push(ring, X[:, t].contiguous(), t)
+        ring.push(X[:, t].contiguous(), t)
     stage = torch.empty((n, M), dtype=torch.float32, device=dev)
-    flags = torch.empty((n, 1), dtype=torch.int8, device=dev)
-    scores = torch.empty((n, 1), dtype=torch.float32, device=dev)
-    md = torch.empty((n, 1), dtype=torch.float32, device=dev)
+    flags = torch.empty(n, dtype=torch.int8, device=dev)
+    scores = torch.empty(n, dtype=torch.float32, device=dev)
+    md = torch.empty(n, dtype=torch.float32, device=dev)
 
     def tick_ops(t):
-        E.ring_push(ring, stage, t)
-        E.detect_async(E.ring_view(ring, t), det, mean, std, thr_dev, W - 1, W,
-                       out=(flags, scores, md))
+        ring.push(stage, t)
+        ring.detect(t, thr_dev, out=(flags, scores, md))
 
     l0 = _lib.lib().enova_kernel_launches()
     stage.copy_(S[0])
@@ -266,7 +267,7 @@ def run_streaming(args, rank, world, local_rank):
     for ph in range(W):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
-            tick_ops(ph)
+            tick_ops(ph + W)      # same ring phase, tick >= W-1
         graphs[ph] = g
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
@@ -275,7 +276,7 @@ def run_streaming(args, rank, world, local_rank):
 
     def run(k0, e2e):
         starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
-        flags_h = torch.empty((n, 1), dtype=torch.int8).pin_memory()
+        flags_h = torch.empty(n, dtype=torch.int8).pin_memory()
         for k in range(k0, k0 + ticks):
             i = k - k0 - args.warmup
             if i >= 0:
@@ -302,7 +303,8 @@ def run_streaming(args, rank, world, local_rank):
     t_last = t_hist + ticks - 1
     fb, sb, mb = E.detect(X[:, t_last - W + 1:t_last + 1].contiguous(), det, mean, std, thr,
                           W - 1, W, return_scores=True)
-    assert torch.equal(sb, scores) and torch.equal(fb, flags), "streaming tick != batch scoring"
+    assert torch.equal(sb[:, 0], scores) and torch.equal(fb[:, 0], flags), \
+        "streaming tick != batch scoring"
     tot = max_over_ranks(tot)
     lat_e2e, tot_e2e = run(ticks, True)
     tot_e2e = max_over_ranks(tot_e2e)
@@ -337,8 +339,10 @@ def run_streaming(args, rank, world, local_rank):
                                    f"sample per instance per tick; stats and fleet threshold frozen "
                                    f"from a {t_hist}-step calibration horizon",
                        "instances": n_global, "parallelism": f"instance-sharded x{world}",
-                       "step": "one tick: ring push + scores/MD/flags of every instance's newest window",
-                       "l2": "not flushed: the 82 MB ring is the streaming working set (resident)"},
+                       "step": "one tick: ingest-normalise the new samples into the fp16 ring "
+                               "(enova_stream_push) + scores/MD/flags of every instance's newest "
+                               "window (enova_stream_detect: TMA ring -> tcgen05)",
+                       "l2": "not flushed: the 41 MB fp16 ring is the streaming working set"},
             "tick_latency_us": {"p50": 1e3 * _pct(lat, 50), "p99": 1e3 * _pct(lat, 99),
                                 "max": 1e3 * max(lat)},
             "step_mode": "one CUDA graph replay per tick (graph per ring phase)",

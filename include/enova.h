@@ -199,6 +199,36 @@ enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window,
                              int32_t n_metrics, const float *sample, int64_t tick,
                              void *stream);
 
+/* ------------------------------------------------ a-10, ingest-normalised ----
+ * Streaming fast path: each new sample is normalised ONCE when it
+ * arrives, with the frozen calibration statistics (R-4), into an fp16
+ * mirror ring, so a tick scores every instance's newest window with no
+ * re-normalisation and half the HBM bytes of the fp32 ring; the window's GEMM1
+ * operand is fed to the tensor cores by TMA straight from the ring.  Results
+ * are bit-identical to enova_detect on the same windows (same quantisation x =
+ * fp16_RNE(clamp((X - mean)/std)), same sample-sum association).
+ *
+ * ring: device, 256-byte aligned, enova_stream_ring_bytes(N, W, M) bytes,
+ * caller-owned: fp16 x [N][2W][M] (the sample of tick k at slots k mod W and
+ * (k mod W) + W) followed (at a 256-byte boundary) by fp32 per-sample sums
+ * s = sum_j x_j [N][2W].  M in {8, 16, 32, 64}.
+ * enova_stream_push: sample device fp32 [N][M] (16-byte aligned) for tick
+ * `tick` (>= 0); norm_mean / norm_std device fp32 [N][M] (enova_compute_stats).
+ * enova_stream_detect: after pushes of ticks tick-W+1 .. tick (tick >= W-1),
+ * scores / MD / flags of the window ending at `tick` of every instance:
+ * outputs device [N] (scores_opt, md_opt may be NULL); thr_dev: DEVICE
+ * enova_threshold (e.g. from enova_fit_threshold_async), required when flags
+ * is not NULL; a NaN z_q flags nothing.  Both are stream-ordered and capturable
+ * in CUDA graphs (one graph per ring phase tick mod W). */
+size_t enova_stream_ring_bytes(int64_t n_instances, int32_t window, int32_t n_metrics);
+enova_status enova_stream_push(void *ring, int64_t n_instances, int32_t window, int32_t n_metrics,
+                               const float *sample, const float *norm_mean, const float *norm_std,
+                               int64_t tick, void *stream);
+enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t tick,
+                                 const enova_detector *det, const void *det_ws,
+                                 size_t det_ws_bytes, const enova_threshold *thr_dev,
+                                 int8_t *flags, float *scores_opt, float *md_opt, void *stream);
+
 /* ------------------------------------------------------------ comm (§8e) ----
  * NCCL communicator for the fleet-wide threshold.  Rank 0 creates the 128-byte
  * unique id; the caller broadcasts it (e.g. torch.distributed) and every rank

@@ -26,7 +26,8 @@ EXPORTS = (
     "enova_fit_threshold", "enova_detect", "enova_ring_push", "enova_comm_unique_id",
     "enova_comm_create", "enova_comm_destroy", "enova_status_string", "enova_last_error",
     "enova_abi_version", "enova_kernel_launches", "enova_compute_stats_async",
-    "enova_fit_threshold_async", "enova_detect_async",
+    "enova_fit_threshold_async", "enova_detect_async", "enova_stream_ring_bytes",
+    "enova_stream_push", "enova_stream_detect",
 )
 
 
@@ -95,6 +96,9 @@ def lib() -> C.CDLL:
             "enova_fit_threshold": (C.c_int, [vp, i64, i64, dbl, dbl, vp, P(Threshold), vp, sz, vp]),
             "enova_detect": (C.c_int, [P(Series), P(Detector), vp, sz, P(Threshold), vp, vp, vp, vp]),
             "enova_ring_push": (C.c_int, [vp, i64, i32, i32, vp, i64, vp]),
+            "enova_stream_ring_bytes": (sz, [i64, i32, i32]),
+            "enova_stream_push": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
+            "enova_stream_detect": (C.c_int, [vp, i64, i64, P(Detector), vp, sz, vp, vp, vp, vp, vp]),
             "enova_comm_unique_id": (C.c_int, [vp]),
             "enova_comm_create": (C.c_int, [P(vp), C.c_int, C.c_int, vp, C.c_int]),
             "enova_comm_destroy": (None, [vp]),

@@ -292,6 +292,49 @@ def ring_view(ring: torch.Tensor, tick: int) -> torch.Tensor:
     return ring.as_strided((N, W, M), (W2 * M, M, 1), ring.storage_offset() + off * M)
 
 
+class StreamRing:
+    """a-10 fast path: the ingest-normalised fp16 mirror ring of a fleet
+    (enova_stream_*).  push() normalises one new sample per instance with the
+    frozen calibration statistics; detect() scores the window ending at a tick
+    for every instance (bit-identical to detect() on the same windows)."""
+
+    def __init__(self, det: PreparedDetector, mean: torch.Tensor, std: torch.Tensor, device=None):
+        _require_cuda(mean, "mean")
+        _require_cuda(std, "std")
+        self.det, self.mean, self.std = det, mean.contiguous(), std.contiguous()
+        self.n = int(mean.shape[0])
+        self.W, self.M = det.window, det.n_metrics
+        nbytes = int(lib().enova_stream_ring_bytes(self.n, self.W, self.M))
+        if nbytes == 0:
+            raise _lib.EnovaError(2, "stream ring: unsupported shape")
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device or mean.device)
+
+    def push(self, sample: torch.Tensor, tick: int, stream=None):
+        _require_cuda(sample, "sample")
+        if tuple(sample.shape) != (self.n, self.M) or not sample.is_contiguous():
+            raise ValueError(f"sample must be contiguous [{self.n}, {self.M}]")
+        check(lib().enova_stream_push(C.c_void_p(self.buf.data_ptr()), self.n, self.W, self.M,
+                                      C.c_void_p(sample.data_ptr()), C.c_void_p(self.mean.data_ptr()),
+                                      C.c_void_p(self.std.data_ptr()), int(tick), _stream_ptr(stream)))
+
+    def detect(self, tick: int, thr_dev: torch.Tensor | None = None, *, out=None, stream=None):
+        """(flags, scores, md) of the windows ending at `tick`, each [n]; flags
+        need a device threshold (threshold_to_device / fit_threshold_async)."""
+        dev = self.buf.device
+        if out is None:
+            flags = torch.empty(self.n, dtype=torch.int8, device=dev) if thr_dev is not None else None
+            sc = torch.empty(self.n, dtype=torch.float32, device=dev)
+            md = torch.empty(self.n, dtype=torch.float32, device=dev)
+        else:
+            flags, sc, md = out
+        ptr = lambda t: C.c_void_p(t.data_ptr() if t is not None else None)
+        check(lib().enova_stream_detect(C.c_void_p(self.buf.data_ptr()), self.n, int(tick),
+                                        C.byref(self.det.struct), C.c_void_p(self.det.ws.data_ptr()),
+                                        self.det.ws_bytes, ptr(thr_dev), ptr(flags), ptr(sc), ptr(md),
+                                        _stream_ptr(stream)))
+        return flags, sc, md
+
+
 class Comm:
     """NCCL communicator for the fleet-wide threshold (one per rank)."""
 

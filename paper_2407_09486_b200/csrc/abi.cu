@@ -44,6 +44,12 @@ size_t threshold_workspace_bytes(int64_t n_max, double q0);
 void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
+size_t stream_ring_bytes(int64_t n, int W, int M);
+enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sample,
+                         const float *mean, const float *stdv, int64_t tick, cudaStream_t st);
+enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
+                           const void *det_ws, const double *z_q_dev, int8_t *flags, float *scores,
+                           float *md, cudaStream_t st);
 
 static inline bool aligned(const void *p, size_t a) {
   return (reinterpret_cast<uintptr_t>(p) % a) == 0;
@@ -373,6 +379,67 @@ enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window, i
   if (r) return r;
   return ring_push(ring, n_instances, window, n_metrics, sample, tick,
                    static_cast<cudaStream_t>(stream));
+}
+
+size_t enova_stream_ring_bytes(int64_t n_instances, int32_t window, int32_t n_metrics) {
+  if (n_instances < 0 || window < 2 || window > 256 || (window % 2) != 0 ||
+      !(n_metrics == 8 || n_metrics == 16 || n_metrics == 32 || n_metrics == 64))
+    return 0;
+  return stream_ring_bytes(n_instances, window, n_metrics);
+}
+
+enova_status enova_stream_push(void *ring, int64_t n_instances, int32_t window, int32_t n_metrics,
+                               const float *sample, const float *norm_mean, const float *norm_std,
+                               int64_t tick, void *stream) {
+  if (enova_stream_ring_bytes(n_instances, window, n_metrics) == 0) {
+    set_error("stream ring: bad shape (W even 2..256, M in {8,16,32,64})");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (!ring || !sample || !norm_mean || !norm_std || tick < 0 || !aligned(ring, 256) ||
+      !aligned(sample, 16) || !aligned(norm_mean, 16) || !aligned(norm_std, 16)) {
+    set_error("bad stream_push arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return stream_push(ring, n_instances, window, n_metrics, sample, norm_mean, norm_std, tick,
+                     static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t tick,
+                                 const enova_detector *det, const void *det_ws,
+                                 size_t det_ws_bytes, const enova_threshold *thr_dev,
+                                 int8_t *flags, float *scores_opt, float *md_opt, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if (enova_stream_ring_bytes(n_instances, L.W, L.M) == 0) {
+    set_error("stream ring: bad shape (M in {8,16,32,64})");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (!ring || !aligned(ring, 256) || n_instances < 0) {
+    set_error("stream ring missing or misaligned");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (tick < L.W - 1) {
+    set_error("stream_detect needs W pushed ticks (tick >= W-1)");
+    return ENOVA_ERR_INSUFFICIENT_HISTORY;
+  }
+  if (flags && (!thr_dev || !aligned(thr_dev, 8))) {
+    set_error("device threshold missing or misaligned");
+    return ENOVA_ERR_UNCALIBRATED;
+  }
+  if (!flags && !scores_opt && !md_opt && n_instances > 0) {
+    set_error("no output requested");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  return stream_detect(ring, n_instances, tick, L, det_ws, thr_dev ? &thr_dev->z_q : nullptr,
+                       flags, scores_opt, md_opt, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -26,6 +26,9 @@
 //             window scored in a batch.
 //
 // Envelope: M in {8, 16} (a K-step holds whole samples), H in {32, 64, 128}.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "layout.h"
@@ -48,8 +51,8 @@ struct RowParams {
 
 constexpr int kRR = 128;                 // rows per tile (UMMA M)
 constexpr int kRWStageSteps = 4;         // W1 ring: K-steps per stage
-constexpr int kRWStages = 8;             // W1 ring depth
-constexpr int kRAStages = 8;             // A ring depth (one K-step each)
+constexpr int kRWStages = 4;             // W1 ring depth
+constexpr int kRAStages = 16;            // A ring depth (one K-step each)
 constexpr uint32_t kRAStepBytes = kRR * 16 * 2;   // 4 KB
 constexpr int kRowThreads = 128;         // thread = row
 constexpr int kRThreads = kRowThreads + 64;       // + MMA issuer warp + W1 producer warp
@@ -66,7 +69,8 @@ struct RowLayoutSm {
   uint32_t region, astage, heads, w3, mubuf, vec, bars, total, w_stage_bytes, tmem_cols;
 };
 
-__host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP) {
+__host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
+                                                       uint32_t a_ring_bytes = kRAStages * kRAStepBytes) {
   RowLayoutSm L;
   uint32_t o = 0;
   auto take = [&](uint32_t b, uint32_t a) {
@@ -78,7 +82,7 @@ __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP) {
   L.w_stage_bytes = (uint32_t)kRWStageSteps * 32 * H;
   const uint32_t ring = kRWStages * L.w_stage_bytes, hb = 2u * kRR * H * 2;
   L.region = take(ring > hb ? ring : hb, 1024);      // W1 ring, then h hi | lo
-  L.astage = take(kRAStages * kRAStepBytes, 1024);
+  L.astage = take(a_ring_bytes, 1024);
   L.heads = take((uint32_t)2 * ZP * H * 2, 128);
   L.w3 = take((uint32_t)H * 16 * 2, 128);
   L.mubuf = take(2u * kRR * 16 * 2, 128);
@@ -122,6 +126,147 @@ struct WinSum {
     }
   }
 };
+
+// E1 (encoder tanh -> h hi/lo; GEMM1 columns re-armed with b3), E2 (KL score,
+// mu hi/lo), E3 (MD by the column-sum identity, flag) for one row of a row
+// tile -- the CTA-pair kernel's element-wise arithmetic (epilogue.cuh) in the
+// same association.  Row threads of warps 0-3; GEMM2/GEMM3 are issued by the
+// MMA warp between the h_full / mu_full arrivals and the g2_done / g3_done
+// commits of RowBars.
+template <int H, int ZP, class Bars>
+__device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane, int r, int64_t row,
+                                              bool valid, float sx, uint8_t *region,
+                                              uint8_t *mubuf, const float *b3s, const float *wbs,
+                                              const float *bmls, Bars &B, int Z, int D,
+                                              const double *bbar, float *scores, float *md_out,
+                                              int8_t *flags, double z_q, const double *z_q_dev,
+                                              unsigned long long *tr = nullptr) {
+  auto stamp = [&](int slot) {
+    if (tr && r == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[slot] = t;
+    }
+  };
+    // ---- E1: h = tanh(acc) -> hi/lo fp16 A images; re-arm acc with b3 ----
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    mbar_wait_sleep(&B.g1_done, 0);
+    stamp(6);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c16 = 0; c16 < H; c16 += 16) {
+      float v[16];
+      tmem_ld16(lane_addr + c16, v);
+      tmem_wait_ld();
+      tmem_fill_cols<16>(lane_addr + c16, b3s + c16);
+#pragma unroll
+      for (int e8 = 0; e8 < 16; e8 += 8) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const float h0 = tanh_2mufu(v[e8 + k]);
+          const float h1 = tanh_2mufu(v[e8 + k + 1]);
+          float a0, r0, a1, r1;
+          split_unit(h0, a0, r0);
+          split_unit(h1, a1, r1);
+          hi[k >> 1] = cvt_pack_f16x2(a0, a1);
+          lo[k >> 1] = cvt_pack_f16x2(r0, r1);
+        }
+        const size_t off = kmajor_step_offset(r, c16 + e8, kRR);
+        *reinterpret_cast<uint4 *>(region + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4 *>(region + kRR * H * 2 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+    }
+    tmem_wait_st();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.h_full);
+    stamp(7);
+
+    // ---- E2: KL score; mu -> hi/lo fp16 ----
+    mbar_wait_sleep(&B.g2_done, 0, 64);
+    stamp(8);
+    tc_fence_after();
+    float score;
+    {
+      const uint32_t hacc = lane_addr + H;
+      float vm[ZP], vl[ZP];
+      if constexpr (ZP == 16) {
+        tmem_ld16(hacc, vm);
+        tmem_ld16(hacc + ZP, vl);
+      } else {
+        tmem_ld8(hacc, vm);
+        tmem_ld8(hacc + ZP, vl);
+      }
+      tmem_wait_ld();
+      float kl = 0.f;
+      uint32_t hi[8], lo[8];
+#pragma unroll
+      for (int z = 0; z < ZP; z += 2) {
+        float m2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float m = 0.f;
+          if (z + u < Z) {
+            m = vm[z + u] + bmls[z + u];
+            kl += kl_term2(m, vl[z + u] + bmls[ZP + z + u]);
+          }
+          m2[u] = m;
+        }
+        const uint32_t hp = cvt_pack_f16x2(m2[0], m2[1]);
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
+        hi[z >> 1] = hp;
+        lo[z >> 1] = cvt_pack_f16x2(m2[0] - hf.x, m2[1] - hf.y);
+      }
+      const size_t off0 = kmajor_step_offset(r, 0, kRR);
+      *reinterpret_cast<uint4 *>(mubuf + off0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if constexpr (ZP == 16) {
+        const size_t off1 = kmajor_step_offset(r, 8, kRR);
+        *reinterpret_cast<uint4 *>(mubuf + off1) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+        *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off1) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+      }
+      score = fmaxf(0.5f * kl, 0.f);
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.mu_full);
+    stamp(9);
+
+    // ---- E3: MD by the column-sum identity; flag ----
+    mbar_wait_sleep(&B.g3_done, 0, 64);
+    stamp(10);
+    tc_fence_after();
+    float d4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int c32 = 0; c32 < H; c32 += 32) {
+      float v[32];
+      tmem_ld16(lane_addr + c32, *reinterpret_cast<float(*)[16]>(&v[0]));
+      tmem_ld16(lane_addr + c32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        const float4 ww = *reinterpret_cast<const float4 *>(wbs + c32 + k);
+        d4[0] = fmaf(ww.x, tanh_mufu(v[k]), d4[0]);
+        d4[1] = fmaf(ww.y, tanh_mufu(v[k + 1]), d4[1]);
+        d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2]), d4[2]);
+        d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3]), d4[3]);
+      }
+    }
+    const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+    const float mdv = (sx - dot - (float)(*bbar)) / (float)D;
+    if (valid) {
+      if (scores) scores[row] = score;
+      if (md_out) md_out[row] = mdv;
+      if (flags) {
+        const double zq = z_q_dev ? __ldg(z_q_dev) : z_q;
+        flags[row] = ((double)score > zq) ? (mdv >= 0.f ? 1 : -1) : 0;
+      }
+    }
+    stamp(11);
+}
 
 template <int H, int ZP, int M>
 __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) {
@@ -209,16 +354,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
       mbar_wait(&B.a_full[a], (q / kRAStages) & 1);
       if (q % kRWStageSteps == 0) mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint64_t ad = make_sdesc(aa + a * kRAStepBytes, kRR * 16, 128);
-        const uint64_t bd = make_sdesc(
-            ra + st * SL.w_stage_bytes + (q % kRWStageSteps) * 32 * H, 16 * H, 128);
-        mma_f16_ss(tmem, ad, bd, idesc1, 1u);
-        mma_commit(&B.a_empty[a]);
-        if (q % kRWStageSteps == kRWStageSteps - 1 || q == p.nsteps - 1) mma_commit(&B.w_empty[st]);
-        if (q == p.nsteps - 1) mma_commit(&B.g1_done);
-      }
-      __syncwarp();
+      const uint64_t ad = make_sdesc(aa + a * kRAStepBytes, kRR * 16, 128);
+      const uint64_t bd = make_sdesc(
+          ra + st * SL.w_stage_bytes + (q % kRWStageSteps) * 32 * H, 16 * H, 128);
+      mma_f16_warp(tmem, ad, bd, idesc1, 1u);
+      mma_commit_warp(&B.a_empty[a]);
+      if (q % kRWStageSteps == kRWStageSteps - 1 || q == p.nsteps - 1) mma_commit_warp(&B.w_empty[st]);
+      if (q == p.nsteps - 1) mma_commit_warp(&B.g1_done);
     }
     // heads GEMM2: [mu | lv] = (h_hi + h_lo) [Wmu | Wlv]^T, accumulator at column H
     mbar_wait(&B.wimg, 0);
@@ -333,118 +475,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     }
     const float sx = ws.acc0 + ws.acc1;
 
-    // ---- E1: h = tanh(acc) -> hi/lo fp16 A images; re-arm acc with b3 ----
-    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-    mbar_wait(&B.g1_done, 0);
-    tc_fence_after();
-#pragma unroll 1
-    for (int c16 = 0; c16 < H; c16 += 16) {
-      float v[16];
-      tmem_ld16(lane_addr + c16, v);
-      tmem_wait_ld();
-      tmem_fill_cols<16>(lane_addr + c16, b3s + c16);
-#pragma unroll
-      for (int e8 = 0; e8 < 16; e8 += 8) {
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          const float h0 = tanh_2mufu(v[e8 + k]);
-          const float h1 = tanh_2mufu(v[e8 + k + 1]);
-          float a0, r0, a1, r1;
-          split_unit(h0, a0, r0);
-          split_unit(h1, a1, r1);
-          hi[k >> 1] = cvt_pack_f16x2(a0, a1);
-          lo[k >> 1] = cvt_pack_f16x2(r0, r1);
-        }
-        const size_t off = kmajor_step_offset(r, c16 + e8, kRR);
-        *reinterpret_cast<uint4 *>(region + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4 *>(region + kRR * H * 2 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-    }
-    tmem_wait_st();
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&B.h_full);
-
-    // ---- E2: KL score; mu -> hi/lo fp16 ----
-    mbar_wait(&B.g2_done, 0);
-    tc_fence_after();
-    float score;
-    {
-      const uint32_t hacc = lane_addr + H;
-      float vm[ZP], vl[ZP];
-      if constexpr (ZP == 16) {
-        tmem_ld16(hacc, vm);
-        tmem_ld16(hacc + ZP, vl);
-      } else {
-        tmem_ld8(hacc, vm);
-        tmem_ld8(hacc + ZP, vl);
-      }
-      tmem_wait_ld();
-      float kl = 0.f;
-      uint32_t hi[8], lo[8];
-#pragma unroll
-      for (int z = 0; z < ZP; z += 2) {
-        float m2[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          float m = 0.f;
-          if (z + u < p.Z) {
-            m = vm[z + u] + bmls[z + u];
-            kl += kl_term2(m, vl[z + u] + bmls[ZP + z + u]);
-          }
-          m2[u] = m;
-        }
-        const uint32_t hp = cvt_pack_f16x2(m2[0], m2[1]);
-        const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
-        hi[z >> 1] = hp;
-        lo[z >> 1] = cvt_pack_f16x2(m2[0] - hf.x, m2[1] - hf.y);
-      }
-      const size_t off0 = kmajor_step_offset(r, 0, kRR);
-      *reinterpret_cast<uint4 *>(mubuf + off0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if constexpr (ZP == 16) {
-        const size_t off1 = kmajor_step_offset(r, 8, kRR);
-        *reinterpret_cast<uint4 *>(mubuf + off1) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-        *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off1) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-      }
-      score = fmaxf(0.5f * kl, 0.f);
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&B.mu_full);
-
-    // ---- E3: MD by the column-sum identity; flag ----
-    mbar_wait(&B.g3_done, 0);
-    tc_fence_after();
-    float d4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int c32 = 0; c32 < H; c32 += 32) {
-      float v[32];
-      tmem_ld16(lane_addr + c32, *reinterpret_cast<float(*)[16]>(&v[0]));
-      tmem_ld16(lane_addr + c32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const float4 ww = *reinterpret_cast<const float4 *>(wbs + c32 + k);
-        d4[0] = fmaf(ww.x, tanh_mufu(v[k]), d4[0]);
-        d4[1] = fmaf(ww.y, tanh_mufu(v[k + 1]), d4[1]);
-        d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2]), d4[2]);
-        d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3]), d4[3]);
-      }
-    }
-    const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
-    const float mdv = (sx - dot - (float)(*p.bbar)) / (float)p.D;
-    if (valid) {
-      if (p.scores) p.scores[row] = score;
-      if (p.md) p.md[row] = mdv;
-      if (p.flags) {
-        const double zq = p.z_q_dev ? __ldg(p.z_q_dev) : p.z_q;
-        p.flags[row] = ((double)score > zq) ? (mdv >= 0.f ? 1 : -1) : 0;
-      }
-    }
+    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx, region, mubuf, b3s, wbs, bmls, B,
+                         p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev);
   }
   tc_fence_before();
   __syncthreads();
@@ -523,6 +555,414 @@ enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const 
     case 172816: return launch_rows_t<128, 16, 16>(p, st);
   }
   set_error("unsupported (M, H, Z) for the row kernel");
+  return ENOVA_ERR_UNSUPPORTED;
+}
+
+// =====================================================================
+// Ingest-normalised streaming ring (a-10 fast path; include/enova.h
+// enova_stream_*).  Each new sample is normalised ONCE on ingest with the frozen
+// calibration statistics (R-4) -- exactly the windowed kernels'
+// arithmetic: x = fp16_RN(clamp(RN((X - mean) / std), +-1e4)) -- and kept as
+// fp16 in a mirror ring [N][2W][M] (the W samples of the window ending at tick
+// k are contiguous: slots (k+1) mod W ..) next to its fp32 sample sum
+// s = sum_j x_j (the windowed kernels' association) in [N][2W].  A tick needs
+// no normalisation: the GEMM1 A operand of 4 K-steps for 128 instances is ONE
+// 2-D TMA box (64 fp16 = 128 B per instance x 128 instances, SWIZZLE_128B,
+// 16 KB) consumed by K-major SWIZZLE_128B UMMA descriptors (+32 B per K-step),
+// so the kernel is a TMA -> tcgen05 pipeline plus the shared epilogue.
+// =====================================================================
+
+size_t stream_sums_offset(int64_t n, int W, int M) {
+  return align_up((size_t)2 * W * n * M * 2, 256);
+}
+size_t stream_ring_bytes(int64_t n, int W, int M) {
+  return stream_sums_offset(n, W, M) + (size_t)2 * W * n * 4;
+}
+
+template <int G>
+__global__ void k_stream_push(__half *__restrict__ ring16, float *__restrict__ sums, int64_t n,
+                              int W, const float *__restrict__ sample,
+                              const float *__restrict__ mean, const float *__restrict__ stdv,
+                              int64_t tick) {
+  constexpr int M = 4 * G;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int slot = (int)(tick % W);
+  const float4 *xs = reinterpret_cast<const float4 *>(sample + i * M);
+  const float4 *ms = reinterpret_cast<const float4 *>(mean + i * M);
+  const float4 *ss = reinterpret_cast<const float4 *>(stdv + i * M);
+  __half *r0 = ring16 + ((size_t)i * 2 * W + slot) * M;   // [N][2W][M]
+  __half *r1 = r0 + (size_t)W * M;
+  float pg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float4 v = __ldg(xs + g), mu = __ldg(ms + g), sd = __ldg(ss + g);
+    const float z0 = fminf(fmaxf(div_rn(__fsub_rn(v.x, mu.x), sd.x, __frcp_rn(sd.x)), -1e4f), 1e4f);
+    const float z1 = fminf(fmaxf(div_rn(__fsub_rn(v.y, mu.y), sd.y, __frcp_rn(sd.y)), -1e4f), 1e4f);
+    const float z2 = fminf(fmaxf(div_rn(__fsub_rn(v.z, mu.z), sd.z, __frcp_rn(sd.z)), -1e4f), 1e4f);
+    const float z3 = fminf(fmaxf(div_rn(__fsub_rn(v.w, mu.w), sd.w, __frcp_rn(sd.w)), -1e4f), 1e4f);
+    uint2 pk;
+    pk.x = cvt_pack_f16x2(z0, z1);
+    pk.y = cvt_pack_f16x2(z2, z3);
+    *reinterpret_cast<uint2 *>(r0 + 4 * g) = pk;
+    *reinterpret_cast<uint2 *>(r1 + 4 * g) = pk;
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.y));
+    pg[g] = (f01.x + f01.y) + (f23.x + f23.y);
+  }
+  // balanced tree over the G groups (= the windowed kernels' lane xor tree)
+#pragma unroll
+  for (int w = 1; w < G; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < G; k += 2 * w) pg[k] = pg[k] + pg[k + w];
+  sums[(size_t)i * 2 * W + slot] = pg[0];
+  sums[(size_t)i * 2 * W + slot + W] = pg[0];
+}
+
+enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sample,
+                         const float *mean, const float *stdv, int64_t tick, cudaStream_t st) {
+  if (n == 0) return ENOVA_OK;
+  __half *r16 = static_cast<__half *>(ring);
+  float *sums = reinterpret_cast<float *>(static_cast<uint8_t *>(ring) + stream_sums_offset(n, W, M));
+  const int threads = 128;
+  const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+  switch (M) {
+    case 8: ENOVA_LAUNCH(k_stream_push<2>, blocks, threads, 0, st, r16, sums, n, W, sample, mean, stdv, tick); break;
+    case 16: ENOVA_LAUNCH(k_stream_push<4>, blocks, threads, 0, st, r16, sums, n, W, sample, mean, stdv, tick); break;
+    case 32: ENOVA_LAUNCH(k_stream_push<8>, blocks, threads, 0, st, r16, sums, n, W, sample, mean, stdv, tick); break;
+    case 64: ENOVA_LAUNCH(k_stream_push<16>, blocks, threads, 0, st, r16, sums, n, W, sample, mean, stdv, tick); break;
+    default: set_error("stream ring: M must be 8, 16, 32 or 64"); return ENOVA_ERR_UNSUPPORTED;
+  }
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1,
+                                            int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// A ring of the stream kernel: stages of kSAK K-steps = one TMA box of
+// 64 fp16 (128 B, the SWIZZLE_128B atom width) x 128 instances = 16 KB.
+constexpr int kSAK = 4;
+constexpr int kSAStages = 8;
+constexpr int kSAWarp = 6;                        // A (TMA) producer warp
+constexpr int kSThreads = kRThreads + 32;
+constexpr uint32_t kSAStageBytes = kRR * 128;
+
+// K-major SWIZZLE_128B smem descriptor (TMA CU_TENSOR_MAP_SWIZZLE_128B layout):
+// 8-row x 128-B swizzle atoms, SBO = 1024 B between 8-row groups, LBO unused;
+// the K=16 step j of an atom starts at +32 j bytes.
+__device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                    // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+struct StreamParams {
+  const float *sums;        // [N][2W] fp32 sample sums
+  int64_t n, tick;
+  int W, M, D, Z, nsteps;
+  const uint8_t *w1img, *headsimg, *w3img;
+  const float *b1, *bml, *b3, *wbar;
+  const double *bbar;
+  float *scores, *md;
+  int8_t *flags;
+  const double *z_q_dev;
+  unsigned long long *trace;   // diagnostic timeline of CTA 0 (NULL normally)
+};
+
+template <int H, int ZP>
+__global__ void __launch_bounds__(kSThreads, 1)
+    k_stream_rows(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  constexpr int N2 = 2 * ZP;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
+  uint8_t *region = smem + SL.region;
+  uint8_t *astage = smem + SL.astage;
+  uint8_t *heads = smem + SL.heads;
+  uint8_t *w3s = smem + SL.w3;
+  uint8_t *mubuf = smem + SL.mubuf;
+  RowBars &B = *reinterpret_cast<RowBars *>(smem + SL.bars);
+  float *b1s = reinterpret_cast<float *>(smem + SL.vec);
+  float *b3s = b1s + H;
+  float *wbs = b3s + H;
+  float *bmls = wbs + H;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * kRR;
+  const int W = p.W;
+  const int woff = (int)((p.tick + 1) % W);   // oldest sample's slot of the window ending at tick
+  unsigned long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;
+  auto stamp = [&](int slot) {
+    if (tr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[slot] = t;
+    }
+  };
+  if (tid == 0) stamp(0);
+
+  if (tid == 0) {
+    for (int i = 0; i < kRWStages; ++i) {
+      mbar_init(&B.w_full[i], 1);
+      mbar_init(&B.w_empty[i], 1);
+    }
+    for (int i = 0; i < kRAStages; ++i) {
+      mbar_init(&B.a_full[i], 1);   // producer's expect_tx; TMA completes the bytes
+      mbar_init(&B.a_empty[i], 1);
+    }
+    mbar_init(&B.wimg, 1);
+    mbar_init(&B.g1_done, 1);
+    mbar_init(&B.h_full, kRowThreads / 32);
+    mbar_init(&B.g2_done, 1);
+    mbar_init(&B.mu_full, kRowThreads / 32);
+    mbar_init(&B.g3_done, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < H; i += blockDim.x) {
+    b1s[i] = p.b1[i];
+    b3s[i] = p.b3[i];
+    wbs[i] = p.wbar[i];
+  }
+  for (int i = tid; i < N2; i += blockDim.x) bmls[i] = p.bml[i];
+  for (int i = tid; i < (int)(2 * kRR * 16 * 2 / 16); i += blockDim.x)
+    reinterpret_cast<uint4 *>(mubuf)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 0) tmem_alloc(&B.tmem_slot, SL.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_slot;
+  if (warp < 4) {
+    tmem_fill_cols<H>(tmem + ((uint32_t)(warp * 32) << 16), b1s);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == kRProdWarp) {
+    // ---------------- producer: W1 ring (bulk) + A ring (TMA from the fp16 ring) ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const uint32_t hb = (uint32_t)N2 * H * 2, w3b = (uint32_t)H * 16 * 2;
+      mbar_arrive_expect_tx(&B.wimg, hb + w3b);
+      bulk_g2s(heads, p.headsimg, hb, &B.wimg);
+      bulk_g2s(w3s, p.w3img, w3b, &B.wimg);
+      // W1 ring: one stage (kRWStageSteps = kSAK K-steps) per group
+      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+      for (int g = 0; g < n_groups; ++g) {
+        const int st = g % kRWStages;
+        if (g >= kRWStages) mbar_wait_sleep(&B.w_empty[st], ((g / kRWStages) - 1) & 1, 64);
+        const int steps = min(kSAK, p.nsteps - g * kSAK);
+        const uint32_t bytes = (uint32_t)steps * 32 * H;
+        mbar_arrive_expect_tx(&B.w_full[st], bytes);
+        bulk_g2s(region + st * SL.w_stage_bytes, p.w1img + (size_t)g * SL.w_stage_bytes, bytes,
+                 &B.w_full[st]);
+      }
+    }
+  } else if (warp == kSAWarp) {
+    // ---------------- A producer: one TMA box (kSAK K-steps x 128 instances) per group ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+      for (int g = 0; g < n_groups; ++g) {
+        const int a = g % kSAStages;
+        if (g >= kSAStages) mbar_wait_sleep(&B.a_empty[a], ((g / kSAStages) - 1) & 1, 64);
+        mbar_arrive_expect_tx(&B.a_full[a], kSAStageBytes);
+        tma_load_2d(astage + a * kSAStageBytes, &tmap, woff * p.M + 16 * kSAK * g, (int)row0,
+                    &B.a_full[a]);
+        if (g < 20) stamp(16 + g);
+        if (g == 0) stamp(1);
+        if (g == n_groups - 1) stamp(2);
+      }
+    }
+  } else if (warp == kRMmaWarp) {
+    // ---------------- MMA issuer (as k_score_rows) ----------------
+    const uint32_t idesc1 = make_idesc_f16(128, H);
+    const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
+    for (int q = 0; q < p.nsteps; ++q) {
+      const int g = q / kSAK, j = q % kSAK, a = g % kSAStages, st = g % kRWStages;
+      if (j == 0) {
+        mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
+        if (lane == 0 && g < 20) stamp(36 + g);
+        mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
+        tc_fence_after();
+      }
+      const uint64_t ad = make_sdesc_sw128(aa + a * kSAStageBytes + j * 32);
+      const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
+      mma_f16_warp(tmem, ad, bd, idesc1, 1u);
+      if (lane == 0 && q == 0) stamp(3);
+      if (lane == 0 && q == p.nsteps - 1) stamp(4);
+      if (j == kSAK - 1 || q == p.nsteps - 1) {
+        mma_commit_warp(&B.a_empty[a]);
+        mma_commit_warp(&B.w_empty[st]);
+      }
+      if (q == p.nsteps - 1) mma_commit_warp(&B.g1_done);
+    }
+    mbar_wait(&B.wimg, 0);
+    mbar_wait(&B.h_full, 0);
+    tc_fence_after();
+    if (lane == 0) {
+      const uint32_t idesc2 = make_idesc_f16(128, N2);
+      const uint32_t hb = smem_u32(heads);
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const uint32_t ab = smem_u32(region) + (uint32_t)pass * (kRR * H * 2);
+        for (int s = 0; s < H / 16; ++s) {
+          const uint64_t ad = make_sdesc(ab + s * (32 * kRR), 16 * kRR, 128);
+          const uint64_t bd = make_sdesc(hb + s * (32 * N2), 16 * N2, 128);
+          mma_f16_ss(tmem + H, ad, bd, idesc2, (pass | s) ? 1u : 0u);
+        }
+      }
+      mma_commit(&B.g2_done);
+    }
+    __syncwarp();
+    mbar_wait(&B.mu_full, 0);
+    tc_fence_after();
+    if (lane == 0) {
+      const uint32_t idesc3 = make_idesc_f16(128, H);
+      const uint64_t bd = make_sdesc(smem_u32(w3s), 16 * H, 128);
+      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 1u);
+      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf) + kRR * 16 * 2, 16 * kRR, 128), bd, idesc3, 1u);
+      mma_commit(&B.g3_done);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- row threads: window sums while GEMM1 runs, then the epilogues ----------------
+    const int r = tid;
+    const int64_t row = row0 + r;
+    const bool valid = row < p.n;
+    const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
+    WinSum ws;
+    ws.init();
+    if (valid) {
+      const float *sp = p.sums + (size_t)row * 2 * W + woff;
+      for (int t0 = 0; t0 < W; t0 += 64) {   // 64 loads in flight per thread
+        float v[64];
+#pragma unroll
+        for (int k = 0; k < 64; ++k) v[k] = (t0 + k < W) ? __ldg(sp + t0 + k) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 64; ++k)
+          if (t0 + k < W) ws.push(t0 + k, v[k], W8, nb2);
+      }
+    }
+    const float sx = ws.acc0 + ws.acc1;
+    if (r == 0) stamp(5);
+    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx, region, mubuf, b3s, wbs, bmls, B,
+                         p.Z, p.D, p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, SL.tmem_cols);
+}
+
+unsigned long long *pair_trace();
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+template <int H, int ZP>
+static enova_status launch_stream_t(const CUtensorMap &tm, const StreamParams &p, cudaStream_t st) {
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
+  auto kern = k_stream_rows<H, ZP>;
+  static thread_local int cached_dev = -1;
+  int dev = 0;
+  ENOVA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != cached_dev) {
+    ENOVA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SL.total));
+    cached_dev = dev;
+  }
+  const int64_t tiles = (p.n + kRR - 1) / kRR;
+  if (tiles > 0x7fffffffLL) {
+    set_error("too many instances for one launch");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  ENOVA_LAUNCH(kern, (unsigned)tiles, kSThreads, SL.total, st, tm, p);
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
+}
+
+enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
+                           const void *det_ws, const double *z_q_dev, int8_t *flags, float *scores,
+                           float *md, cudaStream_t st) {
+  if (n == 0) return ENOVA_OK;
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return ENOVA_ERR_CUDA;
+  }
+  const int W = L.W, M = L.M;
+  CUtensorMap tm;   // [instance N][2W*M] fp16; box = 64 K-elements (128 B) x 128 instances
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * W * M), (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)(2 * W * M * 2)};
+  const cuuint32_t box[2] = {16 * kSAK, (cuuint32_t)kRR};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ring), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed for the stream ring");
+    return ENOVA_ERR_CUDA;
+  }
+  StreamParams p{};
+  const uint8_t *b = static_cast<const uint8_t *>(det_ws);
+  p.sums = reinterpret_cast<const float *>(static_cast<const uint8_t *>(ring) +
+                                           stream_sums_offset(n, W, M));
+  p.n = n;
+  p.tick = tick;
+  p.W = W;
+  p.M = M;
+  p.D = L.D;
+  p.Z = L.Z;
+  p.nsteps = L.D / 16;
+  p.w1img = b + L.off_w1;
+  p.headsimg = b + L.off_heads;
+  p.w3img = b + L.off_w3;
+  p.b1 = reinterpret_cast<const float *>(b + L.off_b1);
+  p.bml = reinterpret_cast<const float *>(b + L.off_bml);
+  p.b3 = reinterpret_cast<const float *>(b + L.off_b3);
+  p.wbar = reinterpret_cast<const float *>(b + L.off_wbar);
+  p.bbar = reinterpret_cast<const double *>(b + L.off_bbar);
+  p.scores = scores;
+  p.md = md;
+  p.flags = flags;
+  p.z_q_dev = z_q_dev;
+  p.trace = pair_trace();
+  switch (L.H * 100 + L.ZP) {
+    case 3208: return launch_stream_t<32, 8>(tm, p, st);
+    case 3216: return launch_stream_t<32, 16>(tm, p, st);
+    case 6408: return launch_stream_t<64, 8>(tm, p, st);
+    case 6416: return launch_stream_t<64, 16>(tm, p, st);
+    case 12808: return launch_stream_t<128, 8>(tm, p, st);
+    case 12816: return launch_stream_t<128, 16>(tm, p, st);
+  }
+  set_error("unsupported (H, Z)");
   return ENOVA_ERR_UNSUPPORTED;
 }
 

@@ -410,6 +410,38 @@ def test_streaming_ring_matches_batch(E):
             assert torch.equal(f[:, 0], fb[:, k - W + 1])
 
 
+@pytest.mark.parametrize("W,M,H,Z,N", [(64, 16, 128, 16, 300), (32, 8, 32, 4, 130), (16, 32, 64, 8, 70)],
+                         ids=lambda v: str(v))
+def test_stream_ring_matches_batch_and_oracle(E, W, M, H, Z, N):
+    """a-10 fast path: ingest-normalised fp16 ring + TMA-fed row kernel.  Every
+    tick's scores / MD / flags equal the batch detect() of the same windows bit
+    for bit (M <= 16: same epilogue and association as the CTA-pair kernel) and
+    match the oracle within the parity tolerances."""
+    T = W + 40
+    X = synth.metric_trace(N, T, M, seed=W + M + N)
+    wts = synth.detector_weights(W, M, H, Z, seed=W + M + N)
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    mean, std, _ = E.compute_stats(Xc, T)
+    thr = {"z_q": 1.5, "t": 1.0, "gamma": 0.0, "sigma": 1.0, "n": 1, "n_peaks": 10,
+           "init_quantile": 0.98, "risk_q": 1e-3, "method": 1}
+    thr_dev = E.threshold_to_device(thr)
+    fb, sb, mb = E.detect(Xc, det, mean, std, thr, return_scores=True)
+    rs, rmd = O.score_windows(X, wts, mean.cpu().numpy(), std.cpu().numpy(), W - 1, T)
+    ring = E.StreamRing(det, mean, std)
+    for k in range(T):
+        ring.push(Xc[:, k, :].contiguous(), k)
+        if k >= W - 1:
+            f, s_, m_ = ring.detect(k, thr_dev)
+            j = k - W + 1
+            assert_scores(s_.cpu().numpy(), rs[:, j], "stream scores")
+            assert_md(m_.cpu().numpy(), rmd[:, j])
+            if M <= 16:
+                assert torch.equal(s_, sb[:, j]), f"tick {k}: stream scores != batch"
+                assert torch.equal(m_, mb[:, j]), f"tick {k}: stream md != batch"
+                assert torch.equal(f, fb[:, j])
+
+
 # ------------------------------------------- stream-ordered / graph path ----
 def test_async_pipeline_matches_sync_and_oracle(E):
     """Pipeline (stats_async -> scores -> fit_threshold_async -> detect_async) gives
