@@ -6,7 +6,7 @@
 //
 // One HBM pass: the calibration horizon of each instance is split into
 // `nchunk` contiguous time chunks, one CTA each, streamed with coalesced
-// 128-bit loads (4 in flight per thread).  Each thread accumulates the SHIFTED
+// 128-bit loads (4 in flight per thread, ragged tail predicated; 2 CTAs per SM).  Each thread accumulates the SHIFTED
 // sums S1 = sum(x - K), S2 = sum((x - K)^2) in fp64, with K = the series' first
 // sample (the same shift in every chunk, so chunk sums simply add); the CTA
 // reduces them in a fixed order and the last CTA of the instance (ticket)
@@ -33,11 +33,11 @@ size_t stats_workspace_bytes(int64_t n, int m) {
          align_up((size_t)n * stats_max_chunks(n) * 2 * m * sizeof(double), 256);
 }
 
-__global__ void __launch_bounds__(kStatsThreads) k_series_stats(
+__global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
     const float *__restrict__ X, int64_t ld, int M, int64_t T_cal, int nchunk,
     float *__restrict__ mean_out, float *__restrict__ std_out, unsigned long long *diag,
     unsigned int *ticket, double *part) {
-  extern __shared__ double red[];  // [nslots][2][M]
+  extern __shared__ double red[];  // [nwarps][2][M]
   __shared__ bool last;
   const int G = M / 4;
   const int g = threadIdx.x % G;
@@ -58,23 +58,32 @@ __global__ void __launch_bounds__(kStatsThreads) k_series_stats(
     a0 += d0; a1 += d1; a2 += d2; a3 += d3;
     q0 = fma(d0, d0, q0); q1 = fma(d1, d1, q1); q2 = fma(d2, d2, q2); q3 = fma(d3, d3, q3);
   };
-  int64_t t = t0 + slot;
-  for (; t + 3 * nslots < t1; t += 4 * nslots) {
+  for (int64_t t = t0 + slot; t < t1; t += 4 * nslots) {   // 4 x 128-bit loads in flight
     float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(base + (t + u * nslots) * G + g);
+    for (int u = 0; u < 4; ++u)
+      if (t + u * nslots < t1) v[u] = __ldg(base + (t + u * nslots) * G + g);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc(v[u]);
+    for (int u = 0; u < 4; ++u)
+      if (t + u * nslots < t1) acc(v[u]);
   }
-  for (; t < t1; t += nslots) acc(__ldg(base + t * G + g));
-  double *r = red + (size_t)slot * 2 * M;
-  r[4 * g + 0] = a0; r[4 * g + 1] = a1; r[4 * g + 2] = a2; r[4 * g + 3] = a3;
-  r[M + 4 * g + 0] = q0; r[M + 4 * g + 1] = q1; r[M + 4 * g + 2] = q2; r[M + 4 * g + 3] = q3;
+  // fixed-order tree over the slots of a warp (lanes with the same g), then a
+  // fixed-order sum over the warps
+  double v8[8] = {a0, a1, a2, a3, q0, q1, q2, q3};
+  for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v8[k] += __shfl_xor_sync(0xffffffffu, v8[k], o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (lane < G) {
+    double *r = red + (size_t)warp * 2 * M;
+    r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
+    r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
+  }
   bad = __syncthreads_or(bad);
   double *pc = part + ((size_t)inst * nchunk + chunk) * 2 * M;
-  if (threadIdx.x < 2 * M) {   // fixed-order sum over slots
+  if (threadIdx.x < 2 * M) {   // fixed-order sum over warps
     double s = 0;
-    for (int k = 0; k < nslots; ++k) s += red[(size_t)k * 2 * M + threadIdx.x];
+    for (int k = 0; k < nwarps; ++k) s += red[(size_t)k * 2 * M + threadIdx.x];
     pc[threadIdx.x] = s;
   }
   if (threadIdx.x == 0 && bad) atomicAdd(diag + 1, 1ull);   // chunks with a non-finite sample
@@ -126,7 +135,7 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   int dev = 0, sms = 148;
   ENOVA_CUDA_TRY(cudaGetDevice(&dev));
   ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int64_t nchunk = (4 * (int64_t)sms + N - 1) / N;
+  int64_t nchunk = (2 * (int64_t)sms + N - 1) / N;   // ~one wave of 2 CTAs per SM
   if (nchunk > stats_max_chunks(N)) nchunk = stats_max_chunks(N);
   if (nchunk > t_cal_end / 64) nchunk = t_cal_end / 64;
   if (nchunk < 1) nchunk = 1;
@@ -135,7 +144,8 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   const int nslots = nthreads / G;
   if (diag_dev) ENOVA_CUDA_TRY(cudaMemsetAsync(diag_dev, 0, 2 * sizeof(unsigned long long), st));
   ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, 256 + (size_t)N * 4, st));   // diag (own) + tickets
-  const size_t smem = (size_t)nslots * 2 * M * sizeof(double);
+  const size_t smem = (size_t)(nthreads / 32) * 2 * M * sizeof(double);
+  (void)nslots;
   if (smem > 48 * 1024)
     ENOVA_CUDA_TRY(cudaFuncSetAttribute(k_series_stats,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
