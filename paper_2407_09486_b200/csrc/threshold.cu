@@ -45,6 +45,8 @@ constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
 constexpr int kMaxRefinePasses = 60;
 constexpr int kMaxStamps = 96;
+constexpr int kSums = 6;              // P, L, dP, dL, d2P, d2L per evaluation point
+constexpr double kCertRel = 5e-14;    // certification half-width (relative)
 
 enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
 // phase program of k_pot
@@ -73,7 +75,9 @@ struct FitState {
   int64_t nt, n;
   double t, q, ybar, ymin, ymax;
   int phase, npts, nslots, iters, overflow, converged, nrefine, method, nroots;
-  double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts];
+  double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts], ddw[kMaxPts];
+  int triple;                 // REFINE evaluates (x, x(1-d), x(1+d)) per root (certifying)
+  int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
   int exact[kMaxSlots];
   int refine_idx[kMaxSlots];
@@ -98,7 +102,7 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.hist = take(3 * kBins * 8);
   L.header = L.hist + kBins * 8;                    // PotGlobal + histogram 0
   L.counts = take(kMaxCtas * 8);
-  L.part = take((size_t)2 * 4 * kMaxPts * kMaxCtas * 8);
+  L.part = take((size_t)2 * kSums * kMaxPts * kMaxCtas * 8);
   L.nbuf = take(16);
   L.counts_all = take(1024 * 8);
   L.ylocal = take((size_t)L.cap * 8);
@@ -116,7 +120,7 @@ struct PotArgs {
   PotGlobal *g;
   unsigned long long *hist; // [3][kBins]
   long long *counts;        // [gridDim.x]
-  double *part;             // [2][4][kMaxPts][kMaxCtas]
+  double *part;             // [2][kSums][kMaxPts][kMaxCtas]
   double *ydst;             // compaction target (this rank's tail)
   const double *yfit;       // tail the fit runs on (all ranks, rank order)
   int64_t cap;
@@ -513,11 +517,19 @@ __device__ void controller(FitState *f, int *scratch) {
       __syncthreads();
       for (int w = 0; w < kMaxPts / 32; ++w) nr += scratch[16 + w];
     }
+    const bool triple = 3 * nr <= kMaxPts;
     if (br && off_h < kMaxSlots) {
       f->refine_idx[off_b] = off_h;
+      f->rdone[off_b] = 0;
       double x0 = xk - wk * (xk1 - xk) / (wk1 - wk);   // first iterate: secant point
       if (!(x0 > fmin(xk, xk1) && x0 < fmax(xk, xk1))) x0 = 0.5 * (xk + xk1);
-      f->xs[off_b] = x0;
+      if (triple) {
+        f->xs[3 * off_b] = x0;
+        f->xs[3 * off_b + 1] = x0 * (1.0 - kCertRel);
+        f->xs[3 * off_b + 2] = x0 * (1.0 + kCertRel);
+      } else {
+        f->xs[off_b] = x0;
+      }
     }
     __syncthreads();
     if (nr == 0 && tid < ns) f->xs[tid] = f->lo[tid];
@@ -525,9 +537,89 @@ __device__ void controller(FitState *f, int *scratch) {
       f->nslots = ns;
       f->overflow = (tot_h > kMaxSlots) ? 1 : f->overflow;
       f->nrefine = nr;
+      f->triple = triple ? 1 : 0;
       f->converged = (nr == 0) ? 1 : 0;
-      f->npts = (nr > 0) ? nr : ns;
+      f->npts = (nr > 0) ? (triple ? 3 * nr : nr) : ns;
       f->phase = (nr > 0) ? PH_REFINE : PH_FINAL;
+    }
+    __syncthreads();
+    return;
+  }
+  if (phase == PH_REFINE && f->triple) {
+    // Halley from the centre point, bracket shrunk with all three points, and
+    // certification: opposite signs of w at x(1 -+ d) put the root within
+    // 2 d |x| = 1e-13 |x| of x in the SAME pass that found it.
+    const int nr = f->nrefine, iters = f->iters;
+    bool conv = true;
+    int sidx = 0;
+    double xfin = 0.0;
+    if (tid < nr) {
+      sidx = f->refine_idx[tid];
+      const double x = f->xs[3 * tid];
+      xfin = x;
+      if (!f->rdone[tid]) {
+        const double w = f->w[3 * tid], dw = f->dw[3 * tid], ddw = f->ddw[3 * tid];
+        const double xm = f->xs[3 * tid + 1], wm = f->w[3 * tid + 1];
+        const double xp = f->xs[3 * tid + 2], wp = f->w[3 * tid + 2];
+        double lo = f->lo[sidx], hi = f->hi[sidx], wlo = f->wlo[sidx];
+        bool done = false;
+        auto absorb = [&](double xq, double wq) {   // shrink the bracket with an interior point
+          if (!(xq > fmin(lo, hi) && xq < fmax(lo, hi))) return;
+          if (wq == 0.0) {
+            lo = hi = xq;
+            xfin = xq;
+            done = true;
+          } else if ((wq > 0) == (wlo > 0)) {
+            lo = xq;
+            wlo = wq;
+          } else {
+            hi = xq;
+          }
+        };
+        absorb(xm, wm);
+        absorb(x, w);
+        absorb(xp, wp);
+        if (!done && (w == 0.0 || wm == 0.0 || wp == 0.0 || ((wm > 0) != (wp > 0)))) {
+          done = true;   // certified: a sign change inside [x(1-d), x(1+d)]
+          xfin = (w == 0.0) ? x : (wm == 0.0) ? xm : (wp == 0.0) ? xp : x;
+        }
+        if (!done && lo == hi) {
+          done = true;
+          xfin = lo;
+        }
+        f->lo[sidx] = lo;
+        f->hi[sidx] = hi;
+        f->wlo[sidx] = wlo;
+        if (done) {
+          f->rdone[tid] = 1;
+          f->xs[3 * tid] = xfin;
+        } else {
+          const double den = 2.0 * dw * dw - w * ddw;
+          double xn = (den != 0.0 && isfinite(den)) ? x - 2.0 * w * dw / den
+                      : (dw != 0.0 ? x - w / dw : 0.5 * (lo + hi));
+          const double a = fmin(lo, hi), b = fmax(lo, hi);
+          if (!(xn > a && xn < b) || iters > 20) xn = 0.5 * (lo + hi);   // safeguard: bisect
+          f->xs[3 * tid] = xn;
+          f->xs[3 * tid + 1] = xn * (1.0 - kCertRel);
+          f->xs[3 * tid + 2] = xn * (1.0 + kCertRel);
+          conv = false;
+        }
+      }
+    }
+    const int all_conv = __syncthreads_and(conv);
+    const bool done = all_conv || iters + 1 >= kMaxRefinePasses;
+    if (done) {
+      if (tid < nr) f->lo[sidx] = f->xs[3 * tid];
+      __syncthreads();
+      if (tid < f->nslots) f->xs[tid] = f->lo[tid];
+    }
+    if (tid == 0) {
+      f->iters = iters + 1;
+      if (done) {
+        f->npts = f->nslots;
+        f->phase = PH_FINAL;
+        f->converged = all_conv ? 1 : 0;
+      }
     }
     __syncthreads();
     return;
@@ -701,15 +793,16 @@ __device__ __forceinline__ double log1p_fast(double u, double v, double iv, cons
 }
 
 // Sums over this CTA's slice of Y of P = -xY/(1+xY), L = log1p(xY) and, for
-// Newton, dP = -Y/(1+xY)^2, dL = Y/(1+xY), for up to 4 points x per warp item.
+// the REFINE passes, their x-derivatives dP = -Y r^2, dL = Y r, d2P = 2 Y^2 r^3,
+// d2L = -Y^2 r^2 (r = 1/(1+xY)), for up to 4 points x per warp item.
 template <bool kDeriv>
 __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t s1,
-                                            const double (&x)[4], int nu, double (&acc)[4][4],
-                                            const LogTab &T) {
+                                            const double (&x)[4], int nu,
+                                            double (&acc)[4][kSums], const LogTab &T) {
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[u][k] = 0.0;
+    for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
   for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
     const double y = Y[i];   // shared-memory copy (or global: coherent load, not .nc)
 #pragma unroll
@@ -722,16 +815,20 @@ __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t
         acc[u][1] += log1p_fast(xy, v, r, T);
         if (kDeriv) {
           const double yr = y * r;
+          const double yr2 = yr * yr;
           acc[u][2] -= yr * r;
           acc[u][3] += yr;
+          acc[u][4] = fma(2.0 * yr2, r, acc[u][4]);
+          acc[u][5] -= yr2;
         }
       }
     }
   }
+  constexpr int nk = kDeriv ? kSums : 2;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < nk; ++k)
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
 }
@@ -740,8 +837,8 @@ struct FitShared {
   FitState f;
   LogTab tab;
   int scratch[32];
-  double sred[kMaxPts][4];   // per warp item partial sums [item][k]
-  double red[4][kMaxPts];    // grid totals after the barrier
+  double sred[kMaxPts][kSums];   // per warp item partial sums [item][k]
+  double red[kSums][kMaxPts];    // grid totals after the barrier
 };
 
 __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
@@ -836,10 +933,10 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
   for (int pass = 1;; ++pass) {
     const int phase = f.phase;
     if (phase == PH_DONE) break;
-    double *pw = a.part + (size_t)(pass & 1) * 4 * kMaxPts * kMaxCtas;
+    double *pw = a.part + (size_t)(pass & 1) * kSums * kMaxPts * kMaxCtas;
     const int npts = f.npts;
     const bool deriv = (phase == PH_REFINE);
-    const int nk = deriv ? 4 : 2;
+    const int nk = deriv ? kSums : 2;
     const int nbund = (npts + 3) / 4;
     const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
     const int items = nbund * slices;
@@ -851,7 +948,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
       const int nu = min(4, npts - 4 * bnd);
 #pragma unroll
       for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[4 * bnd + u] : 0.0;
-      double acc[4][4];
+      double acc[4][kSums];
       if (deriv)
         eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
       else
@@ -861,7 +958,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
         for (int u = 0; u < 4; ++u)
           if (u < nu)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) S.sred[sl * npts + 4 * bnd + u][k] = acc[u][k];
+            for (int k = 0; k < kSums; ++k) S.sred[sl * npts + 4 * bnd + u][k] = acc[u][k];
       }
     }
     __syncthreads();
@@ -913,7 +1010,9 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
       f.L[pt] = Lm;
       if (deriv) {
         const double dPm = S.red[2][pt] / N, dLm = S.red[3][pt] / N;
+        const double d2Pm = S.red[4][pt] / N, d2Lm = S.red[5][pt] / N;
         f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
+        f.ddw[pt] = d2Pm + d2Lm + d2Pm * Lm + 2.0 * dPm * dLm + Pm * d2Lm;
       }
     }
     __syncthreads();
