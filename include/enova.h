@@ -229,6 +229,23 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
                                  size_t det_ws_bytes, const enova_threshold *thr_dev,
                                  int8_t *flags, float *scores_opt, float *md_opt, void *stream);
 
+/* ----------------------------------------------------- NEXT-4, evaluation ----
+ * Point-adjusted detection counts ("we adopt a point-adjusted
+ * approach"; the rule as SPEC.md:530-533 states it, R-21): for each
+ * contiguous true-anomaly segment containing at least one predicted point,
+ * every point of the segment counts as predicted; then pointwise counts.
+ * Points are the window end times t in [t_begin, t_begin + n_windows) of every
+ * instance: prediction = flags[i][t - t_begin] != 0 (device int8 [N][n_windows],
+ * the enova_detect output), truth = labels[i*ld_labels + t] != 0 (device int8,
+ * ld_labels >= t_begin + n_windows).  Segments are clipped to the range and
+ * never cross instances.  counts_dev: device uint64[4] = {TP, FP, FN, TN}
+ * (overwritten), so precision = TP/(TP+FP), recall = TP/(TP+FN); exact integers,
+ * summable across ranks.  Stream-ordered. */
+enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels,
+                                         const int8_t *flags, int64_t n_instances,
+                                         int64_t t_begin, int64_t n_windows,
+                                         uint64_t *counts_dev, void *stream);
+
 /* ------------------------------------------------------------ comm (§8e) ----
  * NCCL communicator for the fleet-wide threshold.  Rank 0 creates the 128-byte
  * unique id; the caller broadcasts it (e.g. torch.distributed) and every rank

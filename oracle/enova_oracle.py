@@ -32,6 +32,9 @@ numbers ``S:n``; readings ``R-n`` are listed in DESIGN.md):
 8. ``flags``          0 if score <= z_q, else +1 (scale up) if MD >= 0 else -1
    (P:297 "exceeds this threshold", "scale up or down"; S:484, S:521-529;
    R-9, R-10).
+9. ``point_adjusted_counts``  NEXT-4 evaluation: point-adjusted TP/FP/FN/TN of
+   the flags against anomaly labels ("we adopt a point-adjusted
+   approach"; the rule as S:530-533 states it; R-21).
 
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``): SPEC worked examples
 (tests/golden/spec_examples.json), KL closed forms and a quadrature check of
@@ -402,3 +405,54 @@ def detect_pipeline(X: np.ndarray, weights: dict, t_cal_end: int,
     sc, md = score_windows(X, weights, mean32, std32, t_cal_end, T, mode)
     return dict(mean=mean32, std=std32, n_degenerate=n_deg, cal_scores=cal, threshold=thr,
                 scores=sc, md=md, flags=flags(sc, md, thr["z_q"]))
+
+
+# ----------------------------------------------------------------------------
+# 9. point-adjusted evaluation (NEXT-4, R-21)
+# ----------------------------------------------------------------------------
+
+def point_adjusted_counts(labels, preds):
+    """One sequence: (TP, FP, FN, TN) after point adjustment.  S:532-533: "for
+    each contiguous true-anomaly segment containing >= 1 predicted point, all
+    points of that segment count as correctly predicted; then pointwise"."""
+    labels = [bool(v) for v in labels]
+    preds = [bool(v) for v in preds]
+    if len(labels) != len(preds):
+        raise ValueError("length mismatch")
+    adjusted = list(preds)
+    i, n = 0, len(labels)
+    while i < n:
+        if labels[i]:
+            j = i
+            while j < n and labels[j]:
+                j += 1
+            if any(preds[i:j]):                                  # segment detected
+                for k in range(i, j):
+                    adjusted[k] = True
+            i = j
+        else:
+            i += 1
+    tp = sum(1 for a, p in zip(labels, adjusted) if a and p)
+    fp = sum(1 for a, p in zip(labels, adjusted) if not a and p)
+    fn = sum(1 for a, p in zip(labels, adjusted) if a and not p)
+    tn = sum(1 for a, p in zip(labels, adjusted) if not a and not p)
+    return tp, fp, fn, tn
+
+
+def precision_recall_f1(tp, fp, fn):
+    prec = tp / (tp + fp) if tp + fp else 0.0
+    rec = tp / (tp + fn) if tp + fn else 0.0
+    f1 = 2 * prec * rec / (prec + rec) if prec + rec else 0.0
+    return prec, rec, f1
+
+
+def fleet_point_adjusted_counts(labels: np.ndarray, flags: np.ndarray, t_begin: int):
+    """labels [N][T] (!= 0 = anomaly), flags [N][nw] of the windows ending at
+    t_begin .. t_begin + nw - 1: counts summed over instances (segments are
+    per instance and clipped to the evaluated range)."""
+    nw = flags.shape[1]
+    tot = [0, 0, 0, 0]
+    for i in range(flags.shape[0]):
+        c = point_adjusted_counts(labels[i, t_begin:t_begin + nw], flags[i])
+        tot = [a + b for a, b in zip(tot, c)]
+    return tuple(tot)

@@ -11,7 +11,7 @@ __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold"
            "ring_push", "ring_view", "Comm", "ThresholdWorkspace", "run_pipeline",
            "EnovaError", "compute_stats_async", "fit_threshold_async", "detect_async",
            "threshold_from_device", "threshold_to_device", "check_stats_diag", "Pipeline",
-           "StatsWorkspace", "StreamRing"]
+           "StatsWorkspace", "StreamRing", "point_adjusted_counts", "point_adjusted_f1"]
 
 
 def __getattr__(name):

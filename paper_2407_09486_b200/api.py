@@ -335,6 +335,40 @@ class StreamRing:
         return flags, sc, md
 
 
+def point_adjusted_counts(labels: torch.Tensor, flags: torch.Tensor, t_begin: int, *,
+                          out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """NEXT-4: device uint64[4] (as int64) = {TP, FP, FN, TN} of the point-adjusted
+    evaluation of `flags` [N, nw] against `labels` [N, T] (int8, != 0 = anomaly)
+    at the window end times t_begin .. t_begin + nw - 1."""
+    _require_cuda(labels, "labels", torch.int8)
+    _require_cuda(flags, "flags", torch.int8)
+    if labels.dim() != 2 or flags.dim() != 2 or labels.shape[0] != flags.shape[0]:
+        raise ValueError("labels [N, T] and flags [N, nw] expected")
+    if labels.stride(1) != 1 or not flags.is_contiguous():
+        raise ValueError("labels rows and flags must be contiguous")
+    N, nw = flags.shape
+    ld = labels.stride(0) if N > 1 else labels.shape[1]
+    counts = out if out is not None else torch.empty(4, dtype=torch.int64, device=flags.device)
+    check(lib().enova_point_adjusted_counts(C.c_void_p(labels.data_ptr()), ld,
+                                            C.c_void_p(flags.data_ptr()), N, int(t_begin), nw,
+                                            C.c_void_p(counts.data_ptr()), _stream_ptr(stream)))
+    return counts
+
+
+def point_adjusted_f1(labels: torch.Tensor, flags: torch.Tensor, t_begin: int, comm=None) -> dict:
+    """Precision / recall / F1 (point-adjusted) of the flags; with a torch.distributed
+    process group the integer counts are summed over ranks first (exact)."""
+    c = point_adjusted_counts(labels, flags, t_begin)
+    if comm is not None:
+        import torch.distributed as dist
+        dist.all_reduce(c, group=comm)
+    tp, fp, fn, tn = (int(v) for v in c.cpu().tolist())
+    prec = tp / (tp + fp) if tp + fp else 0.0
+    rec = tp / (tp + fn) if tp + fn else 0.0
+    f1 = 2 * prec * rec / (prec + rec) if prec + rec else 0.0
+    return dict(tp=tp, fp=fp, fn=fn, tn=tn, precision=prec, recall=rec, f1=f1)
+
+
 class Comm:
     """NCCL communicator for the fleet-wide threshold (one per rank)."""
 

@@ -45,6 +45,9 @@ void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
 size_t stream_ring_bytes(int64_t n, int W, int M);
+enova_status point_adjust_counts(const int8_t *labels, int64_t ld_labels, const int8_t *flags,
+                                 int64_t n_inst, int64_t t_begin, int64_t nw,
+                                 unsigned long long *counts_dev, cudaStream_t st);
 enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sample,
                          const float *mean, const float *stdv, int64_t tick, cudaStream_t st);
 enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
@@ -440,6 +443,22 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
   if ((r = sticky())) return r;
   return stream_detect(ring, n_instances, tick, L, det_ws, thr_dev ? &thr_dev->z_q : nullptr,
                        flags, scores_opt, md_opt, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels,
+                                         const int8_t *flags, int64_t n_instances,
+                                         int64_t t_begin, int64_t n_windows,
+                                         uint64_t *counts_dev, void *stream) {
+  if (!counts_dev || !aligned(counts_dev, 8) || n_instances < 0 || n_windows < 0 || t_begin < 0 ||
+      ld_labels < t_begin + n_windows || (n_instances > 0 && n_windows > 0 && (!labels || !flags))) {
+    set_error("bad point_adjusted_counts arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return point_adjust_counts(labels, ld_labels, flags, n_instances, t_begin, n_windows,
+                             reinterpret_cast<unsigned long long *>(counts_dev),
+                             static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -174,13 +174,14 @@ def detector_weights(window: int, n_metrics: int, hidden: int, latent: int,
 # u99 = 0.5 * chi2_16 99th percentile = 0.5 * 31.99993 (scipy.stats.chi2.ppf).
 C5_TAIL_WEIGHT = 1e-3
 def _trace_block(args):
-    n, T, M, seed, off = args
-    return metric_trace(n, T, M, seed=seed, instance_offset=off)
+    n, T, M, seed, off, labels = args
+    return metric_trace(n, T, M, seed=seed, instance_offset=off, return_labels=labels)
 
 
 def metric_trace_parallel(n_instances: int, n_steps: int, n_metrics: int = 16,
                           seed: int = DEFAULT_SEED, instance_offset: int = 0,
-                          workers: int | None = None, block: int = 32) -> np.ndarray:
+                          workers: int | None = None, block: int = 32,
+                          return_labels: bool = False):
     """``metric_trace`` generated over a process pool in instance blocks; equal
     to the serial call bit for bit (every instance has its own Philox stream)."""
     import os
@@ -192,16 +193,21 @@ def metric_trace_parallel(n_instances: int, n_steps: int, n_metrics: int = 16,
         except AttributeError:
             workers = os.cpu_count() or 1
     if workers <= 1 or N <= block:
-        return metric_trace(N, n_steps, n_metrics, seed=seed, instance_offset=instance_offset)
-    jobs = [(min(block, N - a), n_steps, n_metrics, seed, instance_offset + a)
+        return metric_trace(N, n_steps, n_metrics, seed=seed, instance_offset=instance_offset,
+                            return_labels=return_labels)
+    jobs = [(min(block, N - a), n_steps, n_metrics, seed, instance_offset + a, return_labels)
             for a in range(0, N, block)]
     out = np.empty((N, int(n_steps), int(n_metrics)), dtype=np.float32)
+    lab = np.empty((N, int(n_steps)), dtype=np.int8) if return_labels else None
     with ProcessPoolExecutor(max_workers=workers) as ex:
         a = 0
         for blk in ex.map(_trace_block, jobs):
+            if return_labels:
+                blk, lb = blk
+                lab[a:a + blk.shape[0]] = lb
             out[a:a + blk.shape[0]] = blk
             a += blk.shape[0]
-    return out
+    return (out, lab) if return_labels else out
 
 
 C5_U99 = 0.5 * 31.999926908815176

@@ -509,3 +509,40 @@ def test_stats_chunked_one_pass_matches_oracle(E):
         assert nd == ond
         assert np.max(np.abs(mean.cpu().numpy().view(np.int32) - om.view(np.int32))) <= 1
         assert np.max(np.abs(std.cpu().numpy().view(np.int32) - os_.view(np.int32))) <= 1
+
+
+# ------------------------------------------------------------------ NEXT-4 ----
+def test_point_adjusted_counts_match_oracle(E):
+    """Point-adjusted TP/FP/FN/TN on the GPU (one warp per instance, 32-point
+    ballots with segments carried across chunks) equal the oracle's exactly:
+    random segment structures incl. segments crossing and filling 32-point
+    chunks and the range ends, several t_begin, plus a real detect run against
+    the synthetic injected-event labels."""
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        N, T = int(rng.integers(1, 40)), int(rng.integers(33, 400))
+        tb = int(rng.integers(0, T // 3))
+        nw = T - tb - int(rng.integers(0, 5))
+        lab = np.zeros((N, T), np.int8)
+        for i in range(N):
+            for _ in range(int(rng.integers(0, 6))):
+                a = int(rng.integers(0, T))
+                lab[i, a:a + int(rng.integers(1, 80))] = rng.choice([-1, 1])
+        if trial == 0:
+            lab[:, :] = 1                       # one segment over everything
+        fl = ((rng.random((N, nw)) < rng.uniform(0, 0.3)) * rng.choice([-1, 1])).astype(np.int8)
+        got = E.point_adjusted_counts(cuda(lab), cuda(fl), tb).cpu().tolist()
+        ref = O.fleet_point_adjusted_counts(lab, fl, tb)
+        assert tuple(got) == ref, (trial, got, ref)
+    # a detect run against the generator's labels (c1-shaped detector)
+    X, labels = synth.metric_trace(6, 3000, 8, seed=17, return_labels=True)
+    d = detectors.mean_detector(32, 8, 32, 4, alpha=4.0, beta=2.0) if hasattr(detectors, "mean_detector") \
+        else synth.detector_weights(32, 8, 32, 4, seed=17)
+    det = E.PreparedDetector(d)
+    res = E.run_pipeline(cuda(X), det, 1500)
+    fl = res.flags
+    got = E.point_adjusted_counts(cuda(labels), fl, 1500).cpu().tolist()
+    ref = O.fleet_point_adjusted_counts(labels, fl.cpu().numpy(), 1500)
+    assert tuple(got) == ref
+    m = E.point_adjusted_f1(cuda(labels), fl, 1500)
+    assert 0.0 <= m["precision"] <= 1.0 and 0.0 <= m["recall"] <= 1.0
