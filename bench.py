@@ -515,7 +515,8 @@ def run_windows(args, rank, world, local_rank):
     N = INST_PER_GPU if args.workload == "c2" else cfg["n_instances"] // 8
     D = W * M
     tcal = T // 2
-    Xh = synth.metric_trace_parallel(N, T, M, seed=synth.DEFAULT_SEED + 2, instance_offset=rank * N)
+    Xh, labels_h = synth.metric_trace_parallel(N, T, M, seed=synth.DEFAULT_SEED + 2,
+                                               instance_offset=rank * N, return_labels=True)
     wts = synth.detector_weights(W, M, H, Z, seed=synth.DEFAULT_SEED + 2)
     X_pinned = torch.from_numpy(Xh).pin_memory()
     X = X_pinned.to(dev)
@@ -631,6 +632,45 @@ def run_windows(args, rank, world, local_rank):
             "share_of_step": ((stage_ms["score_calibration"] + stage_ms["detect"]) / ms_per_step
                               if stage_ms else None)}
 
+    # ---- NEXT-1 / NEXT-4 on this step's detection flags (not part of the step) ----
+    extras = None
+    if world == 1:
+        labels = torch.from_numpy(labels_h).to(dev)
+        reps = 10
+        t0e, t1e = ev(), ev()
+        t0e.record(stream)
+        for _ in range(reps):
+            cnt = E.point_adjusted_counts(labels, pipe.flags, tcal)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        pa_ms = t0e.elapsed_time(t1e) / reps
+        pa = E.point_adjusted_f1(labels, pipe.flags, tcal)
+        ids = E.select_flagged(pipe.flags)
+        # explain at least 10 000 windows: the flagged ones, padded with a fixed stride
+        if ids.numel() < 10000:
+            pad = torch.arange(0, pipe.flags.numel(), max(1, pipe.flags.numel() // 10000),
+                               device=dev)[:10000 - ids.numel()]
+            sel = torch.cat([ids, pad]).sort().values
+        else:
+            sel = ids
+        E.explain_windows(X, det, mean, std, sel, tcal, T)
+        t0e.record(stream)
+        for _ in range(reps):
+            E.explain_windows(X, det, mean, std, sel, tcal, T)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        ex_ms = t0e.elapsed_time(t1e) / reps
+        extras = {
+            "point_adjusted_eval": {"us": 1e3 * pa_ms, "points": int(pipe.flags.numel()),
+                                    "precision": pa["precision"], "recall": pa["recall"],
+                                    "f1": pa["f1"],
+                                    "note": "random-init detector: the P/R/F1 values carry no "
+                                            "semantic meaning; the kernel time is the measurement"},
+            "explain_windows": {"windows": int(sel.numel()), "flagged": int(ids.numel()),
+                                "us": 1e3 * ex_ms,
+                                "windows_per_s": sel.numel() / (ex_ms * 1e-3)},
+        }
+
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -687,6 +727,7 @@ def run_windows(args, rank, world, local_rank):
                 "precision": "fp16 operands (x, weights), fp32 accumulate, h/mu hi+lo fp16",
             },
             "stage_ms": stage_ms,
+            "next_rows": extras,
             "step_mode": "CUDA graph replay (1 graph launch/step)" if use_graph else "eager",
             "threshold": {"z_q": thr["z_q"], "t": thr["t"], "gamma": thr["gamma"],
                           "n_peaks": thr["n_peaks"]},

@@ -229,6 +229,32 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
                                  size_t det_ws_bytes, const enova_threshold *thr_dev,
                                  int8_t *flags, float *scores_opt, float *md_opt, void *stream);
 
+/* ----------------------------------------------------- NEXT-1, explanation ----
+ * Per-metric root cause of flagged windows ("the root cause could
+ * be localized to the lack of GPU memory for KV cache"): for each
+ * listed window, the per-metric mean difference
+ *   MD_j = (1/W) sum_tau (x_{tau,j} - m'_{tau,j}),  j = 0..M-1
+ * between the normalised input x and the decoder reconstruction m' (P:297's MD
+ * resolved per metric; MD = mean_j MD_j), computed by the column-sum identity per
+ * metric (w_bar_j = sum_tau W_dec2[tau*M + j, :], exact algebra, R-8) on the
+ * tensor-core row kernel.
+ * enova_select_flagged: ids_out (device int64, capacity n) receives the
+ * indices i of flags[i] != 0 in ascending order (flags device int8 [n], e.g.
+ * the [N][nw] output of enova_detect flattened); *count_dev (device int64) the
+ * number.  scratch: device, enova_select_flagged_scratch_bytes(n) bytes.
+ * enova_explain_windows: ids_dev (device int64 [n_ids]) are window ids
+ * g = instance * nw + (t - t_begin) of the series range (nw = t_end - t_begin);
+ * md_metric: device fp32 [n_ids][M]; scores_opt / md_opt: device fp32 [n_ids]
+ * (bit-identical to the batch kernels' score / MD of the same window).
+ * M in {8, 16}.  Both stream-ordered. */
+size_t enova_select_flagged_scratch_bytes(int64_t n);
+enova_status enova_select_flagged(const int8_t *flags, int64_t n, int64_t *ids_out,
+                                  int64_t *count_dev, void *scratch, void *stream);
+enova_status enova_explain_windows(const enova_series *series, const enova_detector *det,
+                                   const void *det_ws, size_t det_ws_bytes, const int64_t *ids_dev,
+                                   int64_t n_ids, float *md_metric, float *scores_opt,
+                                   float *md_opt, void *stream);
+
 /* ----------------------------------------------------- NEXT-4, evaluation ----
  * Point-adjusted detection counts ("we adopt a point-adjusted
  * approach"; the rule as SPEC.md:530-533 states it, R-21): for each

@@ -32,6 +32,9 @@ numbers ``S:n``; readings ``R-n`` are listed in DESIGN.md):
 8. ``flags``          0 if score <= z_q, else +1 (scale up) if MD >= 0 else -1
    (P:297 "exceeds this threshold", "scale up or down"; S:484, S:521-529;
    R-9, R-10).
+9b. ``per_metric_mean_difference``  NEXT-1 explanation: MD_j = (1/W) sum_tau
+   (x_{tau,j} - m'_{tau,j}) per metric with the explicit D-wide decoder (P:297's
+   MD resolved per metric, the root-cause reading of P:512; MD = mean_j MD_j).
 9. ``point_adjusted_counts``  NEXT-4 evaluation: point-adjusted TP/FP/FN/TN of
    the flags against anomaly labels ("we adopt a point-adjusted
    approach"; the rule as S:530-533 states it; R-21).
@@ -223,6 +226,26 @@ def score_windows(X: np.ndarray, weights: dict, mean32: np.ndarray, std32: np.nd
         scores[i] = kl_score(mu, lv)
         md[i] = mean_difference(xw, decoder(det, mu, round_mu=(mode == "fp16h")))
     return scores, md
+
+
+def per_metric_mean_difference(X: np.ndarray, weights: dict, mean32: np.ndarray,
+                               std32: np.ndarray, t_begin: int, t_end: int,
+                               mode: str = "x16") -> np.ndarray:
+    """NEXT-1: per-metric MD of every window ending in [t_begin, t_end):
+    MD_j = mean over the window's W samples of (x_{tau,j} - m'_{tau,j}), with
+    m' the explicit D-wide reconstruction.  [N, n, M] fp64."""
+    det = weights if isinstance(weights, Detector) else Detector.from_weights(weights)
+    X = np.asarray(X)
+    N, T, M = X.shape
+    x = normalise_exact(X, mean32, std32) if mode == "exact" else normalise_x16(X, mean32, std32)
+    n = t_end - t_begin
+    out = np.empty((N, n, M))
+    for i in range(N):
+        xw = window_matrix(x[i:i + 1], det.W, t_begin, t_end)[0]         # [n, W*M]
+        mu, _ = encoder(det, xw)
+        resid = xw - decoder(det, mu)                                   # [n, W*M], k = tau*M + j
+        out[i] = resid.reshape(n, det.W, M).mean(axis=1)
+    return out
 
 
 def flags(score: np.ndarray, md: np.ndarray, z_q: float) -> np.ndarray:

@@ -28,6 +28,7 @@ EXPORTS = (
     "enova_abi_version", "enova_kernel_launches", "enova_compute_stats_async",
     "enova_fit_threshold_async", "enova_detect_async", "enova_stream_ring_bytes",
     "enova_stream_push", "enova_stream_detect", "enova_point_adjusted_counts",
+    "enova_select_flagged_scratch_bytes", "enova_select_flagged", "enova_explain_windows",
 )
 
 
@@ -98,6 +99,9 @@ def lib() -> C.CDLL:
             "enova_ring_push": (C.c_int, [vp, i64, i32, i32, vp, i64, vp]),
             "enova_stream_ring_bytes": (sz, [i64, i32, i32]),
             "enova_point_adjusted_counts": (C.c_int, [vp, i64, vp, i64, i64, i64, vp, vp]),
+            "enova_select_flagged_scratch_bytes": (sz, [i64]),
+            "enova_select_flagged": (C.c_int, [vp, i64, vp, vp, vp, vp]),
+            "enova_explain_windows": (C.c_int, [P(Series), P(Detector), vp, sz, vp, i64, vp, vp, vp, vp]),
             "enova_stream_push": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, i64, vp]),
             "enova_stream_detect": (C.c_int, [vp, i64, i64, P(Detector), vp, sz, vp, vp, vp, vp, vp]),
             "enova_comm_unique_id": (C.c_int, [vp]),

@@ -335,6 +335,43 @@ class StreamRing:
         return flags, sc, md
 
 
+def select_flagged(flags: torch.Tensor, stream=None) -> torch.Tensor:
+    """NEXT-1 helper: ascending flat indices of the nonzero flags (device int64;
+    synchronises once to read the count)."""
+    _require_cuda(flags, "flags", torch.int8)
+    f = flags.reshape(-1)
+    n = f.numel()
+    ids = torch.empty(max(n, 1), dtype=torch.int64, device=flags.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=flags.device)
+    scratch = torch.empty(max(int(lib().enova_select_flagged_scratch_bytes(n)), 1),
+                          dtype=torch.uint8, device=flags.device)
+    check(lib().enova_select_flagged(C.c_void_p(f.data_ptr()), n, C.c_void_p(ids.data_ptr()),
+                                     C.c_void_p(cnt.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                     _stream_ptr(stream)))
+    return ids[:int(cnt.item())]
+
+
+def explain_windows(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tensor,
+                    std: torch.Tensor, ids: torch.Tensor, t_begin: int | None = None,
+                    t_end: int | None = None, *, stream=None):
+    """NEXT-1: per-metric mean difference [n_ids, M] (+ score, MD) of the windows
+    with ids g = instance * nw + (t - t_begin) of the range [t_begin, t_end)."""
+    N, T, M = metrics.shape
+    tb = det.window - 1 if t_begin is None else int(t_begin)
+    te = T if t_end is None else int(t_end)
+    s = _series(metrics, mean, std, tb, te)
+    ids = ids.to(dtype=torch.int64).contiguous()
+    n = ids.numel()
+    mdm = torch.empty((n, M), dtype=torch.float32, device=metrics.device)
+    sc = torch.empty(n, dtype=torch.float32, device=metrics.device)
+    md = torch.empty(n, dtype=torch.float32, device=metrics.device)
+    check(lib().enova_explain_windows(C.byref(s), C.byref(det.struct), C.c_void_p(det.ws.data_ptr()),
+                                      det.ws_bytes, C.c_void_p(ids.data_ptr() if n else None), n,
+                                      C.c_void_p(mdm.data_ptr()), C.c_void_p(sc.data_ptr()),
+                                      C.c_void_p(md.data_ptr()), _stream_ptr(stream)))
+    return mdm, sc, md
+
+
 def point_adjusted_counts(labels: torch.Tensor, flags: torch.Tensor, t_begin: int, *,
                           out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """NEXT-4: device uint64[4] (as int64) = {TP, FP, FN, TN} of the point-adjusted

@@ -45,6 +45,13 @@ void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
 size_t stream_ring_bytes(int64_t n, int W, int M);
+enova_status select_flagged(const int8_t *flags, int64_t n, int64_t *ids, long long *count_dev,
+                            void *scratch, cudaStream_t st);
+size_t select_flagged_scratch_bytes(int64_t n);
+enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, const void *det_ws,
+                                 const int64_t *rows_dev, int64_t n_rows, float *md_metric,
+                                 float *scores, float *md, cudaStream_t st);
+bool rows_path_ok(const DetLayout &L);
 enova_status point_adjust_counts(const int8_t *labels, int64_t ld_labels, const int8_t *flags,
                                  int64_t n_inst, int64_t t_begin, int64_t nw,
                                  unsigned long long *counts_dev, cudaStream_t st);
@@ -443,6 +450,48 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
   if ((r = sticky())) return r;
   return stream_detect(ring, n_instances, tick, L, det_ws, thr_dev ? &thr_dev->z_q : nullptr,
                        flags, scores_opt, md_opt, static_cast<cudaStream_t>(stream));
+}
+
+size_t enova_select_flagged_scratch_bytes(int64_t n) {
+  return n < 0 ? 0 : select_flagged_scratch_bytes(n);
+}
+
+enova_status enova_select_flagged(const int8_t *flags, int64_t n, int64_t *ids_out,
+                                  int64_t *count_dev, void *scratch, void *stream) {
+  if (n < 0 || !count_dev || !aligned(count_dev, 8) ||
+      (n > 0 && (!flags || !ids_out || !scratch || !aligned(ids_out, 8)))) {
+    set_error("bad select_flagged arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return select_flagged(flags, n, ids_out, reinterpret_cast<long long *>(count_dev), scratch,
+                        static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_explain_windows(const enova_series *series, const enova_detector *det,
+                                   const void *det_ws, size_t det_ws_bytes, const int64_t *ids_dev,
+                                   int64_t n_ids, float *md_metric, float *scores_opt,
+                                   float *md_opt, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if ((r = check_series_windows(series, L))) return r;
+  if (!rows_path_ok(L)) {
+    set_error("explain_windows supports M in {8, 16}");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (n_ids < 0 || (n_ids > 0 && (!ids_dev || !md_metric))) {
+    set_error("bad explain_windows arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  return launch_explain_rows(series, L, det_ws, ids_dev, n_ids, md_metric, scores_opt, md_opt,
+                             static_cast<cudaStream_t>(stream));
 }
 
 enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels,

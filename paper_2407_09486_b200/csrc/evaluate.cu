@@ -105,4 +105,67 @@ enova_status point_adjust_counts(const int8_t *labels, int64_t ld_labels, const 
   return ENOVA_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-1 ----
+// Stable compaction of the flagged window ids (flags != 0), index order: blocks
+// of 1024 flags count, then each block adds up the counts before it (fixed
+// order) and scatters with warp ballots.  Feeds enova_explain_windows.
+constexpr int kSelBlock = 1024;
+
+__global__ void k_flag_count(const int8_t *__restrict__ flags, int64_t n,
+                             unsigned int *__restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)kSelBlock + threadIdx.x;
+  const int c = __syncthreads_count(i < n && flags[i] != 0);
+  if (threadIdx.x == 0) counts[blockIdx.x] = (unsigned int)c;
+}
+
+__global__ void k_flag_scatter(const int8_t *__restrict__ flags, int64_t n,
+                               const unsigned int *__restrict__ counts, int nblocks,
+                               int64_t *__restrict__ ids, long long *__restrict__ total) {
+  __shared__ unsigned long long base;
+  __shared__ int wsum[kSelBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {   // exclusive prefix of this block (fixed order)
+    unsigned long long s = 0, all = 0;
+    for (int b = lane; b < nblocks; b += 32) {
+      const unsigned long long v = counts[b];
+      all += v;
+      if (b < (int)blockIdx.x) s += v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) {
+      base = s;
+      if (blockIdx.x == 0) *total = (long long)all;
+    }
+  }
+  const int64_t i = blockIdx.x * (int64_t)kSelBlock + threadIdx.x;
+  const bool f = i < n && flags[i] != 0;
+  const unsigned int bal = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += wsum[w];
+  if (f) ids[base + before + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
+enova_status select_flagged(const int8_t *flags, int64_t n, int64_t *ids, long long *count_dev,
+                            void *scratch, cudaStream_t st) {
+  ENOVA_CUDA_TRY(cudaMemsetAsync(count_dev, 0, sizeof(long long), st));
+  if (n == 0) return ENOVA_OK;
+  const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
+  unsigned int *counts = static_cast<unsigned int *>(scratch);
+  ENOVA_LAUNCH(k_flag_count, (unsigned)nb, kSelBlock, 0, st, flags, n, counts);
+  ENOVA_LAUNCH(k_flag_scatter, (unsigned)nb, kSelBlock, 0, st, flags, n, counts, (int)nb, ids,
+               count_dev);
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
+}
+
+size_t select_flagged_scratch_bytes(int64_t n) {
+  return align_up((size_t)((n + kSelBlock - 1) / kSelBlock) * 4, 256);
+}
+
 }  // namespace enova

@@ -17,6 +17,7 @@ struct DetLayout {
   size_t off_w1, off_heads, off_w3;        // fp16 canonical UMMA B images
   size_t off_b1, off_bml, off_b3, off_wbar; // fp32 vectors
   size_t off_bbar;                           // fp64 scalar
+  size_t off_wbarm, off_bbarm;               // NEXT-1: per-metric column sums [M][H] fp32, [M] fp32
   // CTA-pair (cta_group::2) images: rank r holds B rows [r*N/2, (r+1)*N/2)
   size_t off_w1p, off_headsp, off_w3p;
   bool pair_ok;                              // W1 half fits in shared memory
@@ -44,6 +45,8 @@ static inline bool det_layout(int W, int M, int H, int Z, DetLayout *L) {
   L->off_b3 = take((size_t)H * 4);
   L->off_wbar = take((size_t)H * 4);
   L->off_bbar = take(8);
+  L->off_wbarm = take((size_t)M * H * 4);
+  L->off_bbarm = take((size_t)M * 4);
   L->off_w1p = take((size_t)H * L->D * 2);
   L->off_headsp = take((size_t)L->N2 * H * 2);
   L->off_w3p = take((size_t)H * 16 * 2);

@@ -90,6 +90,32 @@ __global__ void k_colsum(const float *__restrict__ w2, const float *__restrict__
   }
 }
 
+// NEXT-1 (per-metric MD): block (j, h): w_bar_m[j][h] = sum_tau W_dec2[tau*M + j][h]
+// (h < H) or b_bar_m[j] = sum_tau b_dec2[tau*M + j] (h == H); fp64 fixed-order tree.
+__global__ void k_colsum_metric(const float *__restrict__ w2, const float *__restrict__ b2,
+                                float *__restrict__ wbarm, float *__restrict__ bbarm, int H,
+                                int W, int M) {
+  __shared__ double red[256];
+  const int j = blockIdx.x / (H + 1), h = blockIdx.x % (H + 1);
+  double s = 0.0;
+  for (int tau = threadIdx.x; tau < W; tau += blockDim.x) {
+    const size_t k = (size_t)tau * M + j;
+    s += (h < H) ? (double)w2[k * H + h] : (double)b2[k];
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (h < H)
+      wbarm[j * H + h] = (float)red[0];
+    else
+      bbarm[j] = (float)red[0];
+  }
+}
+
 // CTA-pair images (pair_offset): W1 [H][D], heads [N2][H] (mu rows | lv rows),
 // W3 [H][16] (z >= Z zero padded)
 __global__ void k_pack_pair(const float *__restrict__ w1, const float *__restrict__ wmu,
@@ -138,6 +164,9 @@ enova_status prepare_detector(const enova_detector *det, const DetLayout &L, voi
   ENOVA_LAUNCH(k_colsum, L.H + 1, 256, 0, st, det->dec_w2, det->dec_b2,
                                     reinterpret_cast<float *>(base + L.off_wbar),
                                     reinterpret_cast<double *>(base + L.off_bbar), L.H, L.D);
+  ENOVA_LAUNCH(k_colsum_metric, L.M * (L.H + 1), 256, 0, st, det->dec_w2, det->dec_b2,
+               reinterpret_cast<float *>(base + L.off_wbarm),
+               reinterpret_cast<float *>(base + L.off_bbarm), L.H, L.W, L.M);
   ENOVA_LAUNCH(k_pack_pair, 296, 256, 0, st, det->enc_w1, det->enc_wmu, det->enc_wlv, det->dec_w1,
                reinterpret_cast<__half *>(base + L.off_w1p),
                reinterpret_cast<__half *>(base + L.off_headsp),

@@ -47,6 +47,10 @@ struct RowParams {
   int8_t *flags;
   double z_q;
   const double *z_q_dev;
+  // NEXT-1 explain mode: rows are gathered window ids, outputs per metric
+  const int64_t *rows;          // [n_rows] window ids g = instance * nw + (t - t_begin)
+  const float *wbarm, *bbarm;   // [M][H], [M] per-metric column sums of W_dec2, b_dec2
+  float *md_metric;             // [n_rows][M]
 };
 
 constexpr int kRR = 128;                 // rows per tile (UMMA M)
@@ -66,7 +70,7 @@ struct RowBars {
 };
 
 struct RowLayoutSm {
-  uint32_t region, astage, heads, w3, mubuf, vec, bars, total, w_stage_bytes, tmem_cols;
+  uint32_t region, astage, heads, w3, mubuf, vec, wbarm, bars, total, w_stage_bytes, tmem_cols;
 };
 
 __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
@@ -87,6 +91,7 @@ __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
   L.w3 = take((uint32_t)H * 16 * 2, 128);
   L.mubuf = take(2u * kRR * 16 * 2, 128);
   L.vec = take((3u * H + 2u * ZP) * 4, 16);           // b1 | b3 | w_bar | [bmu | blv]
+  L.wbarm = take(16u * H * 4, 16);                     // explain mode: per-metric w_bar [M<=16][H]
   L.bars = take(sizeof(RowBars), 16);
   L.total = o;
   const uint32_t cols = (uint32_t)(H + 2 * ZP);
@@ -140,7 +145,11 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
                                               const float *bmls, Bars &B, int Z, int D,
                                               const double *bbar, float *scores, float *md_out,
                                               int8_t *flags, double z_q, const double *z_q_dev,
-                                              unsigned long long *tr = nullptr) {
+                                              unsigned long long *tr = nullptr,
+                                              const float *wbarm_s = nullptr,
+                                              const float *xsum = nullptr,
+                                              const float *bbarm = nullptr, float *md_metric = nullptr,
+                                              int M = 0, int W = 0) {
   auto stamp = [&](int slot) {
     if (tr && r == 0) {
       unsigned long long t;
@@ -248,6 +257,32 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     }
     const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
     const float mdv = (sx - dot - (float)(*bbar)) / (float)D;
+    if (wbarm_s) {
+      // NEXT-1: per-metric mean difference MD_j = (sum_tau x_{tau,j} - w_bar_j . a3 -
+      // b_bar_j) / W with w_bar_j = sum_tau W_dec2[tau M + j, :] (the column-sum
+      // identity per metric; MD = mean_j MD_j).  Accurate tanh here (explain path).
+      float dm[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dm[j] = 0.f;
+#pragma unroll 1
+      for (int c16 = 0; c16 < H; c16 += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + c16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float a3 = tanh_2mufu(v[k]);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < M) dm[j] = fmaf(wbarm_s[j * H + c16 + k], a3, dm[j]);
+        }
+      }
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < M) md_metric[row * M + j] = (xsum[j] - dm[j] - __ldg(bbarm + j)) / (float)W;
+      }
+    }
     if (valid) {
       if (scores) scores[row] = score;
       if (md_out) md_out[row] = mdv;
@@ -259,11 +294,14 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     stamp(11);
 }
 
-template <int H, int ZP, int M>
+template <int H, int ZP, int M, bool kExplain>
 __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) {
   constexpr int N2 = 2 * ZP;
   extern __shared__ __align__(1024) uint8_t smem[];
   const RowLayoutSm SL = row_smem_layout(H, ZP);
+  float *wbarm_s = reinterpret_cast<float *>(smem + SL.wbarm);
+  if (kExplain)
+    for (int i = threadIdx.x; i < M * H; i += blockDim.x) wbarm_s[i] = p.wbarm[i];
   uint8_t *region = smem + SL.region;
   uint8_t *astage = smem + SL.astage;
   uint8_t *heads = smem + SL.heads;
@@ -388,8 +426,12 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     const int r = tid;
     const int64_t row = row0 + r;
     const bool valid = row < p.n_rows;
-    const int64_t inst = valid ? row / p.nw : 0;
-    const int64_t wi = valid ? row - inst * p.nw : 0;
+    const int64_t gid = kExplain ? (valid ? __ldg(p.rows + row) : 0) : row;   // window id
+    const int64_t inst = valid ? gid / p.nw : 0;
+    const int64_t wi = valid ? gid - inst * p.nw : 0;
+    float xsum[kExplain ? M : 1];
+#pragma unroll
+    for (int j = 0; j < (kExplain ? M : 1); ++j) xsum[j] = 0.f;
     float mu[M], sd[M], rc[M];
 #pragma unroll
     for (int j = 0; j < M; j += 4) {
@@ -442,6 +484,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
             const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&h2));
             xr[e] = f.x;
             xr[e + 1] = f.y;
+            if constexpr (kExplain) {   // per-metric window sums, tau ascending
+              xsum[j0] += f.x;
+              xsum[j1] += f.y;
+            }
           }
           const int a = q % kRAStages;
           if (q >= kRAStages) mbar_wait(&B.a_empty[a], ((q / kRAStages) - 1) & 1);
@@ -467,17 +513,19 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     const float sx = ws.acc0 + ws.acc1;
 
     rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx, region, mubuf, b3s, wbs, bmls, B,
-                         p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev);
+                         p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev, nullptr,
+                         kExplain ? wbarm_s : nullptr, kExplain ? xsum : nullptr, p.bbarm,
+                         p.md_metric, M, p.W);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, SL.tmem_cols);
 }
 
-template <int H, int ZP, int M>
+template <int H, int ZP, int M, bool kExplain>
 static enova_status launch_rows_t(const RowParams &p, cudaStream_t st) {
   const RowLayoutSm SL = row_smem_layout(H, ZP);
-  auto kern = k_score_rows<H, ZP, M>;
+  auto kern = k_score_rows<H, ZP, M, kExplain>;
   static thread_local int cached_dev = -1;
   int dev = 0;
   ENOVA_CUDA_TRY(cudaGetDevice(&dev));
@@ -500,9 +548,27 @@ bool rows_path_ok(const DetLayout &L) {
   return (L.M == 8 || L.M == 16) && row_smem_layout(L.H, L.ZP).total <= 227 * 1024;
 }
 
-enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const void *det_ws,
-                               float *scores, float *md, int8_t *flags, double z_q,
-                               const double *z_q_dev, cudaStream_t st) {
+template <bool kExplain>
+static enova_status dispatch_rows(const DetLayout &L, const RowParams &p, cudaStream_t st) {
+  switch (L.M * 10000 + L.H * 100 + L.ZP) {
+    case 83208: return launch_rows_t<32, 8, 8, kExplain>(p, st);
+    case 83216: return launch_rows_t<32, 16, 8, kExplain>(p, st);
+    case 86408: return launch_rows_t<64, 8, 8, kExplain>(p, st);
+    case 86416: return launch_rows_t<64, 16, 8, kExplain>(p, st);
+    case 92808: return launch_rows_t<128, 8, 8, kExplain>(p, st);
+    case 92816: return launch_rows_t<128, 16, 8, kExplain>(p, st);
+    case 163208: return launch_rows_t<32, 8, 16, kExplain>(p, st);
+    case 163216: return launch_rows_t<32, 16, 16, kExplain>(p, st);
+    case 166408: return launch_rows_t<64, 8, 16, kExplain>(p, st);
+    case 166416: return launch_rows_t<64, 16, 16, kExplain>(p, st);
+    case 172808: return launch_rows_t<128, 8, 16, kExplain>(p, st);
+    case 172816: return launch_rows_t<128, 16, 16, kExplain>(p, st);
+  }
+  set_error("unsupported (M, H, Z) for the row kernel");
+  return ENOVA_ERR_UNSUPPORTED;
+}
+
+static RowParams row_params(const enova_series *s, const DetLayout &L, const void *det_ws) {
   RowParams p{};
   const uint8_t *b = static_cast<const uint8_t *>(det_ws);
   p.X = s->metrics;
@@ -525,28 +591,38 @@ enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const 
   p.b3 = reinterpret_cast<const float *>(b + L.off_b3);
   p.wbar = reinterpret_cast<const float *>(b + L.off_wbar);
   p.bbar = reinterpret_cast<const double *>(b + L.off_bbar);
+  p.wbarm = reinterpret_cast<const float *>(b + L.off_wbarm);
+  p.bbarm = reinterpret_cast<const float *>(b + L.off_bbarm);
+  return p;
+}
+
+enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const void *det_ws,
+                               float *scores, float *md, int8_t *flags, double z_q,
+                               const double *z_q_dev, cudaStream_t st) {
+  RowParams p = row_params(s, L, det_ws);
   p.scores = scores;
   p.md = md;
   p.flags = flags;
   p.z_q = z_q;
   p.z_q_dev = z_q_dev;
   if (p.nw <= 0 || p.n_rows == 0) return ENOVA_OK;
-  switch (L.M * 10000 + L.H * 100 + L.ZP) {
-    case 83208: return launch_rows_t<32, 8, 8>(p, st);
-    case 83216: return launch_rows_t<32, 16, 8>(p, st);
-    case 86408: return launch_rows_t<64, 8, 8>(p, st);
-    case 86416: return launch_rows_t<64, 16, 8>(p, st);
-    case 92808: return launch_rows_t<128, 8, 8>(p, st);
-    case 92816: return launch_rows_t<128, 16, 8>(p, st);
-    case 163208: return launch_rows_t<32, 8, 16>(p, st);
-    case 163216: return launch_rows_t<32, 16, 16>(p, st);
-    case 166408: return launch_rows_t<64, 8, 16>(p, st);
-    case 166416: return launch_rows_t<64, 16, 16>(p, st);
-    case 172808: return launch_rows_t<128, 8, 16>(p, st);
-    case 172816: return launch_rows_t<128, 16, 16>(p, st);
-  }
-  set_error("unsupported (M, H, Z) for the row kernel");
-  return ENOVA_ERR_UNSUPPORTED;
+  return dispatch_rows<false>(L, p, st);
+}
+
+// NEXT-1: explain the windows whose ids are listed in rows_dev (g = instance *
+// nw + (t - t_begin) within the series range): per-metric MD plus the window's
+// score and MD (bit-identical to the batch kernels), one row each.
+enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, const void *det_ws,
+                                 const int64_t *rows_dev, int64_t n_rows, float *md_metric,
+                                 float *scores, float *md, cudaStream_t st) {
+  RowParams p = row_params(s, L, det_ws);
+  p.n_rows = n_rows;
+  p.rows = rows_dev;
+  p.md_metric = md_metric;
+  p.scores = scores;
+  p.md = md;
+  if (n_rows == 0) return ENOVA_OK;
+  return dispatch_rows<true>(L, p, st);
 }
 
 // =====================================================================

@@ -546,3 +546,33 @@ def test_point_adjusted_counts_match_oracle(E):
     assert tuple(got) == ref
     m = E.point_adjusted_f1(cuda(labels), fl, 1500)
     assert 0.0 <= m["precision"] <= 1.0 and 0.0 <= m["recall"] <= 1.0
+
+
+# ------------------------------------------------------------------ NEXT-1 ----
+@pytest.mark.parametrize("W,M,H,Z", [(64, 16, 128, 16), (32, 8, 32, 4), (24, 8, 64, 9)],
+                         ids=lambda v: str(v))
+def test_explain_windows_match_oracle(E, W, M, H, Z):
+    """select_flagged = np.flatnonzero; explain_windows gives per-metric MD within
+    the MD tolerance of the oracle's explicit D-wide decoder, and scores / MD
+    bit-identical to the batch detect of the same windows."""
+    N, T = 7, 260 + W
+    X = synth.metric_trace(N, T, M, seed=W + H)
+    wts = synth.detector_weights(W, M, H, Z, seed=W + H)
+    mean, std, _ = O.series_stats(X, T // 2)
+    det = E.PreparedDetector(wts)
+    tb, te = W - 1 + 5, T - 3
+    thr = {"z_q": 1.0}
+    fl, sc, md = E.detect(cuda(X), det, cuda(mean), cuda(std), thr, tb, te, return_scores=True)
+    ids = E.select_flagged(fl)
+    assert np.array_equal(ids.cpu().numpy(), np.flatnonzero(fl.cpu().numpy().reshape(-1)))
+    rng = np.random.default_rng(W)
+    extra = rng.choice(N * (te - tb), size=300, replace=False)
+    for sel in (ids, torch.from_numpy(np.sort(extra)).cuda()):
+        if sel.numel() == 0:
+            continue
+        mdm, s2, m2 = E.explain_windows(cuda(X), det, cuda(mean), cuda(std), sel, tb, te)
+        g = sel.cpu().numpy()
+        assert torch.equal(s2, sc.reshape(-1)[sel]) and torch.equal(m2, md.reshape(-1)[sel])
+        ref = O.per_metric_mean_difference(X, wts, mean, std, tb, te).reshape(-1, M)[g]
+        err = np.abs(mdm.cpu().numpy() - ref)
+        assert np.all(err <= 1e-4 + 1e-3 * np.abs(ref)), err.max()

@@ -247,3 +247,52 @@ def test_surge_and_drop_flags():
     for zq in np.linspace(out["threshold"]["z_q"], out["threshold"]["z_q"] * 3, 5):
         f2 = O.flags(out["scores"], out["md"], zq)
         assert np.all((f2 != 0) <= (out["flags"] != 0))
+
+
+# ------------------------------------------------------------- NEXT-1 pins ----
+def _mdm_setup(seed=4):
+    from paper_2407_09486_b200 import synth as S
+    X = S.metric_trace(2, 300, 8, seed=seed)
+    w = S.detector_weights(16, 8, 32, 4, seed=seed)
+    mean, std, _ = O.series_stats(X, 150)
+    return X, w, mean, std
+
+
+def test_per_metric_md_averages_to_md():
+    """MD = mean_j MD_j (the definitions of P:297's MD and its per-metric split)."""
+    X, w, mean, std = _mdm_setup()
+    mdm = O.per_metric_mean_difference(X, w, mean, std, 15, 300)
+    _, md = O.score_windows(X, w, mean, std, 15, 300)
+    assert np.max(np.abs(mdm.mean(axis=-1) - md)) < 1e-12
+
+
+def test_per_metric_md_closed_form_constant_decoder():
+    """Zero decoder weights, b_dec2[tau*M + j] = c_j: m'_{tau,j} = c_j, so
+    MD_j = mean_tau x_{tau,j} - c_j -- pins the (tau, j) orientation of the
+    time-major flattening."""
+    X, w, mean, std = _mdm_setup(5)
+    W, M = 16, 8
+    c = np.array([0.5, -0.25, 1.0, 0.0, 2.0, -1.5, 0.125, 0.75], np.float32)
+    w = dict(w)
+    w["dec_w2"] = np.zeros_like(w["dec_w2"])
+    w["dec_b2"] = np.tile(c, W).astype(np.float32)
+    mdm = O.per_metric_mean_difference(X, w, mean, std, W - 1, 300)
+    x = O.normalise_x16(X, mean, std)
+    for i in range(2):
+        for r, t in enumerate(range(W - 1, 300)):
+            ref = x[i, t - W + 1:t + 1, :].mean(axis=0) - c
+            assert np.allclose(mdm[i, r], ref, atol=1e-12)
+
+
+def test_per_metric_md_localises_a_single_metric_surge():
+    """A +8 sigma surge on metric j* only (zero decoder) makes MD_{j*} the
+    largest per-metric deviation of the windows covering it (P:512 root cause)."""
+    X, w, mean, std = _mdm_setup(6)
+    w = dict(w)
+    w["dec_w2"] = np.zeros_like(w["dec_w2"])
+    w["dec_b2"] = np.zeros_like(w["dec_b2"])
+    js = 5
+    X = X.copy()
+    X[0, 200:216, js] = mean[0, js] + 8 * std[0, js]
+    mdm = O.per_metric_mean_difference(X, w, mean, std, 215, 216)
+    assert int(np.argmax(mdm[0, 0])) == js
