@@ -306,6 +306,51 @@ def run_streaming(args, rank, world, local_rank):
     assert torch.equal(sb[:, 0], scores) and torch.equal(fb[:, 0], flags), \
         "streaming tick != batch scoring"
     tot = max_over_ranks(tot)
+
+    # ---- NEXT-2: the same ticks with online SPOT (single GPU) ----
+    spot_line = None
+    if world == 1:
+        spot_line = {}
+        for every in (10, 1):
+            # fresh SPOT state per run, calibrated on the same calibration scores;
+            # capacity for every streamed score to be a peak (no overflow)
+            spot = E.Spot(cal.numel() + 50 * n * ticks, device=dev)
+            spot.calibrate(cal.reshape(-1))
+            sgraphs = {}
+            side.wait_stream(torch.cuda.current_stream())
+            for ph in range(W):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    ring.push(stage, ph + W)
+                    ring.detect(ph + W, spot.thr, out=(flags, scores, md))
+                    spot.update(scores, flags)
+                sgraphs[ph] = g
+            gref = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gref, stream=side):
+                spot.refit()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            for t in range(t_hist - W + 1, t_hist):    # restore the ring to the stream start
+                ring.push(X[:, t].contiguous(), t)
+            st_, en_ = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+            for k in range(ticks):
+                i = k - args.warmup
+                if i >= 0:
+                    st_[i].record(stream)
+                stage.copy_(S[k])
+                sgraphs[(t_hist + k) % W].replay()
+                if (k + 1) % every == 0:
+                    gref.replay()
+                if i >= 0:
+                    en_[i].record(stream)
+            torch.cuda.synchronize()
+            lat_s = [a_.elapsed_time(b_) for a_, b_ in zip(st_, en_)]
+            tot_s = st_[0].elapsed_time(en_[-1])
+            thr_s = spot.threshold()
+            spot_line[f"refit_every_{every}"] = {
+                "windows_per_s": n * args.steps / (tot_s * 1e-3),
+                "tick_latency_us": {"p50": 1e3 * _pct(lat_s, 50), "p99": 1e3 * _pct(lat_s, 99)},
+                "n_peaks_end": thr_s["n_peaks"], "n_end": thr_s["n"], "z_q_end": thr_s["z_q"]}
     lat_e2e, tot_e2e = run(ticks, True)
     tot_e2e = max_over_ranks(tot_e2e)
     value = n_global * args.steps / (tot * 1e-3)
@@ -347,6 +392,7 @@ def run_streaming(args, rank, world, local_rank):
                                 "max": 1e3 * max(lat)},
             "step_mode": "one CUDA graph replay per tick (graph per ring phase)",
             "threshold": {"z_q": thr["z_q"], "n_peaks": thr["n_peaks"]},
+            "next_rows": {"online_spot": spot_line},
             "cpu_baseline": cpu,
             "e2e": {"value": n_global * args.steps / (tot_e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(n * M * 4), "d2h_bytes_per_step": int(n),

@@ -229,6 +229,28 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
                                  size_t det_ws_bytes, const enova_threshold *thr_dev,
                                  int8_t *flags, float *scores_opt, float *md_opt, void *stream);
 
+/* ------------------------------------------------------ NEXT-2, online SPOT ----
+ * Streaming threshold updates (SPOT, Siffer et al. 2017 -- the method PAPER.md:297
+ * cites for the POT threshold; R-23, tick-synchronous): the SPOT state
+ * is the single-GPU threshold workspace left by enova_fit_threshold_async on the
+ * calibration scores (peaks Y, N_t, t, and the observation count n), sized with
+ * an n_global_max large enough for the calibration plus the streamed scores.
+ * Per tick: flag the tick's scores against the current threshold
+ * (enova_stream_detect / enova_detect_async with thr_dev), then
+ * enova_spot_update(scores, flags) appends every NON-anomalous score above t to
+ * Y in index order (anomalies never update the model) and adds the number of
+ * non-anomalous scores to n; enova_spot_refit re-fits the GPD on the grown Y and
+ * writes the new device threshold (same as enova_fit_threshold_async's out_dev)
+ * -- call it every tick (exact SPOT semantics per tick) or periodically.  Peaks
+ * beyond the workspace capacity are dropped and reported by the next refit as
+ * ENOVA_ERR_WORKSPACE in out_dev->reserved.  Both stream-ordered and
+ * capturable; single GPU. */
+enova_status enova_spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,
+                               size_t ws_bytes, int64_t n_global_max, double init_quantile,
+                               void *stream);
+enova_status enova_spot_refit(double risk_q, enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                              int64_t n_global_max, double init_quantile, void *stream);
+
 /* ----------------------------------------------------- NEXT-1, explanation ----
  * Per-metric root cause of flagged windows ("the root cause could
  * be localized to the lack of GPU memory for KV cache"): for each

@@ -32,6 +32,9 @@ numbers ``S:n``; readings ``R-n`` are listed in DESIGN.md):
 8. ``flags``          0 if score <= z_q, else +1 (scale up) if MD >= 0 else -1
    (P:297 "exceeds this threshold", "scale up or down"; S:484, S:521-529;
    R-9, R-10).
+7b. ``spot_classic`` / ``spot_ticks``  NEXT-2 online threshold: SPOT (Siffer
+   et al. 2017, Algorithm 1, the method P:297 cites), per observation; and its
+   tick-synchronous form (R-23) that the GPU implements.
 9b. ``per_metric_mean_difference``  NEXT-1 explanation: MD_j = (1/W) sum_tau
    (x_{tau,j} - m'_{tau,j}) per metric with the explicit D-wide decoder (P:297's
    MD resolved per metric, the root-cause reading of P:512; MD = mean_j MD_j).
@@ -410,6 +413,73 @@ def pot_threshold(scores: np.ndarray, init_quantile: float = 0.98, risk_q: float
     z_q = pot_quantile(t, gamma, sigma, n, Y.size, risk_q)
     return dict(init_quantile=float(init_quantile), risk_q=float(risk_q), t=t, gamma=gamma,
                 sigma=sigma, z_q=z_q, n=n, n_peaks=int(Y.size), method=method)
+
+
+# ----------------------------------------------------------------------------
+# 7b. online SPOT (NEXT-2; P:297 citing Siffer et al. 2017; R-23)
+# ----------------------------------------------------------------------------
+
+def spot_classic(init_scores, stream, init_quantile=0.98, risk_q=1e-3):
+    """SPOT, Algorithm 1 of the cited paper, one observation at a time:
+    calibrate (t, GPD, z_q) on the initial batch with k = n observations; then
+    for each x: x > z_q -> anomaly (no update); elif x > t -> add the peak
+    x - t, k += 1, refit, recompute z_q; else k += 1.  Returns (flags, z_q
+    after every observation)."""
+    init = np.asarray(init_scores, dtype=np.float32).ravel()
+    thr = pot_threshold(init, init_quantile, risk_q)
+    t, z = thr["t"], thr["z_q"]
+    Y = list(peaks(init, t))
+    k = init.size
+    out_f, out_z = [], []
+    for x in np.asarray(stream, dtype=np.float32).ravel():
+        xd = float(x)
+        if xd > z:
+            out_f.append(True)
+        else:
+            out_f.append(False)
+            if xd > t:
+                Y.append(xd - t)
+                k += 1
+                g, s_, _ = gpd_grimshaw(np.asarray(Y))
+                z = pot_quantile(t, g, s_, k, len(Y), risk_q)
+            else:
+                k += 1
+        out_z.append(z)
+    return np.array(out_f), np.array(out_z)
+
+
+def spot_ticks(init_scores, ticks, init_quantile=0.98, risk_q=1e-3, refit_every=1):
+    """Tick-synchronous SPOT (R-23): every score of a tick is flagged against
+    the threshold current at the tick's start; then the tick's non-anomalous
+    scores above t are added to Y in index order and k grows by the number of
+    non-anomalous scores; every `refit_every` ticks the GPD is refitted if a
+    peak arrived since the last fit.
+    Returns a list of (flags, threshold dict after the tick)."""
+    init = np.asarray(init_scores, dtype=np.float32).ravel()
+    thr = pot_threshold(init, init_quantile, risk_q)
+    t, z = thr["t"], thr["z_q"]
+    Y = list(peaks(init, t))
+    k = init.size
+    res = []
+    cur = dict(thr)
+    added = 0
+    for it, tick in enumerate(ticks):
+        x = np.asarray(tick, dtype=np.float32).ravel().astype(np.float64)
+        fl = x > z
+        normal = x[~fl]
+        new = normal[normal > t] - t
+        Y.extend(list(new))
+        added += int(new.size)
+        k += int(normal.size)
+        # scheduled refit, only if a peak arrived since the last fit (Algorithm 1
+        # refits exactly when a peak is added)
+        if (it + 1) % refit_every == 0 and added > 0:
+            added = 0
+            g, s_, m = gpd_grimshaw(np.asarray(Y))
+            z = pot_quantile(t, g, s_, k, len(Y), risk_q)
+            cur = dict(t=t, gamma=g, sigma=s_, z_q=z, n=k, n_peaks=len(Y), method=m)
+        res.append((fl, dict(cur)))
+    return res
 
 
 # ----------------------------------------------------------------------------

@@ -12,7 +12,7 @@ __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold"
            "EnovaError", "compute_stats_async", "fit_threshold_async", "detect_async",
            "threshold_from_device", "threshold_to_device", "check_stats_diag", "Pipeline",
            "StatsWorkspace", "StreamRing", "point_adjusted_counts", "point_adjusted_f1", "select_flagged",
-           "explain_windows"]
+           "explain_windows", "Spot"]
 
 
 def __getattr__(name):

@@ -335,6 +335,40 @@ class StreamRing:
         return flags, sc, md
 
 
+class Spot:
+    """NEXT-2 online SPOT state on one GPU: calibrate() fits the initial POT
+    threshold (device-resident, `thr` usable by detect_async / StreamRing.detect);
+    update(scores, flags) adds a tick's non-anomalous peaks; refit() re-fits."""
+
+    def __init__(self, n_max: int, init_quantile: float = 0.98, risk_q: float = 1e-3, device=None):
+        self.q0, self.q = float(init_quantile), float(risk_q)
+        self.ws = ThresholdWorkspace(n_max, self.q0, device)
+        self.thr = torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8, device=device or "cuda")
+
+    def calibrate(self, scores: torch.Tensor, stream=None):
+        fit_threshold_async(scores, self.q0, self.q, workspace=self.ws, out=self.thr, stream=stream)
+        return self.thr
+
+    def update(self, scores: torch.Tensor, flags: torch.Tensor, stream=None):
+        _require_cuda(scores, "scores")
+        _require_cuda(flags, "flags", torch.int8)
+        s, f = scores.reshape(-1), flags.reshape(-1)
+        if s.numel() != f.numel() or not s.is_contiguous() or not f.is_contiguous():
+            raise ValueError("scores and flags: contiguous, same length")
+        check(lib().enova_spot_update(C.c_void_p(s.data_ptr()), C.c_void_p(f.data_ptr()), s.numel(),
+                                      C.c_void_p(self.ws.buf.data_ptr()), self.ws.nbytes,
+                                      self.ws.n_global_max, self.q0, _stream_ptr(stream)))
+
+    def refit(self, stream=None):
+        check(lib().enova_spot_refit(self.q, C.c_void_p(self.thr.data_ptr()),
+                                     C.c_void_p(self.ws.buf.data_ptr()), self.ws.nbytes,
+                                     self.ws.n_global_max, self.q0, _stream_ptr(stream)))
+        return self.thr
+
+    def threshold(self) -> dict:
+        return threshold_from_device(self.thr)
+
+
 def select_flagged(flags: torch.Tensor, stream=None) -> torch.Tensor:
     """NEXT-1 helper: ascending flat indices of the nonzero flags (device int64;
     synchronises once to read the count)."""

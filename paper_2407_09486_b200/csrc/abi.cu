@@ -45,6 +45,10 @@ void set_pair_trace(void *t);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
 size_t stream_ring_bytes(int64_t n, int W, int M);
+enova_status spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,
+                         size_t ws_bytes, int64_t n_global_max, double q0, cudaStream_t st);
+enova_status spot_refit(double q, enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                        int64_t n_global_max, double q0, cudaStream_t st);
 enova_status select_flagged(const int8_t *flags, int64_t n, int64_t *ids, long long *count_dev,
                             void *scratch, cudaStream_t st);
 size_t select_flagged_scratch_bytes(int64_t n);
@@ -450,6 +454,33 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
   if ((r = sticky())) return r;
   return stream_detect(ring, n_instances, tick, L, det_ws, thr_dev ? &thr_dev->z_q : nullptr,
                        flags, scores_opt, md_opt, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,
+                               size_t ws_bytes, int64_t n_global_max, double init_quantile,
+                               void *stream) {
+  if (n < 0 || !ws || !aligned(ws, 256) || n_global_max <= 0 || !(init_quantile > 0.0) ||
+      !(init_quantile < 1.0) || (n > 0 && (!scores || !flags))) {
+    set_error("bad spot_update arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return spot_update(scores, flags, n, ws, ws_bytes, n_global_max, init_quantile,
+                     static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_spot_refit(double risk_q, enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                              int64_t n_global_max, double init_quantile, void *stream) {
+  if (!out_dev || !aligned(out_dev, 8) || !ws || !aligned(ws, 256) || n_global_max <= 0 ||
+      !(risk_q > 0.0) || !(risk_q < 1.0) || !(init_quantile > 0.0) || !(init_quantile < 1.0)) {
+    set_error("bad spot_refit arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return spot_refit(risk_q, out_dev, ws, ws_bytes, n_global_max, init_quantile,
+                    static_cast<cudaStream_t>(stream));
 }
 
 size_t enova_select_flagged_scratch_bytes(int64_t n) {

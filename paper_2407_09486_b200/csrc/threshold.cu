@@ -66,6 +66,8 @@ struct PotGlobal {
   long long nt_local, nt_fit;        // peaks of this rank / of the fit (all ranks)
   double gamma, sigma, z_q;
   int method, nroots, converged, overflow;
+  long long n_spot;                  // NEXT-2: observations counted by the online SPOT state
+  long long nt_refit;                // NEXT-2: N_t at the last (re)fit
   int n_stamps, fit_passes;
   unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
   unsigned long long t_first_start, t_last_end;   // over all CTAs (diagnostic)
@@ -128,6 +130,7 @@ struct PotArgs {
   enova_threshold *out_dev; // optional device copy of the result
   double q0;
   int ycache_cap;           // Y values per CTA held in dynamic shared memory
+  const long long *n_dev;   // NEXT-2 refit: n read from device (g->n_spot), else a.n
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -853,7 +856,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
   }
   if (threadIdx.x == 0) {
     f.nt = nt;
-    f.n = a.n;
+    f.n = a.n_dev ? *(volatile const long long *)a.n_dev : a.n;
     f.t = (double)*(volatile float *)&a.g->t;
     f.q = a.q;
     f.overflow = 0;
@@ -1051,6 +1054,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   __shared__ int above;
   PotGlobal *g = a.g;
   unsigned int epoch = 0;   // grid barriers passed in this launch
+  bool spot_skip = false;
   if (threadIdx.x == 0) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1098,7 +1102,10 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
         if (cta_base[1] > a.cap) g->status = ENOVA_ERR_WORKSPACE;
       }
     } else if (ph == P_FIT) {
-      fit(a, sh.fit, epoch);
+      // SPOT refit with no peak added since the last fit: the model is unchanged
+      // (the cited Algorithm 1 refits only when a peak arrives) -- keep the threshold
+      spot_skip = a.n_dev && *(volatile long long *)&g->nt_fit == *(volatile long long *)&g->nt_refit;
+      if (!spot_skip) fit(a, sh.fit, epoch);
     }
   }
   stamp(g);
@@ -1114,7 +1121,9 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       g->mask = sel.mask;
       g->k_rem = sel.k_rem;
     }
-    if (a.last == P_FIT && a.out_dev) {
+    if (a.last == P_FIT && !a.n_dev) g->n_spot = a.n;   // SPOT state starts at the calibration
+    if (a.last == P_FIT && !spot_skip) g->nt_refit = g->nt_fit;
+    if (a.last == P_FIT && a.out_dev && !spot_skip) {
       enova_threshold *o = a.out_dev;
       const int st = g->status;
       o->init_quantile = a.q0;
@@ -1123,7 +1132,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       o->gamma = g->gamma;
       o->sigma = g->sigma;
       o->z_q = (st == ENOVA_OK) ? g->z_q : __longlong_as_double(0x7ff8000000000000ll);
-      o->n = a.n;
+      o->n = a.n_dev ? *(volatile const long long *)a.n_dev : a.n;
       o->n_peaks = g->nt_fit;
       o->method = g->method;
       o->reserved = st;
@@ -1185,6 +1194,7 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.first = P_HIST0;
   a.last = P_FIT;
   a.out_dev = nullptr;
+  a.n_dev = nullptr;
   return a;
 }
 
@@ -1330,5 +1340,100 @@ enova_status fit_threshold_async(const float *scores, int64_t n, double q0, doub
 }
 
 size_t threshold_workspace_bytes(int64_t n_max, double q0) { return thr_layout(n_max, q0).total; }
+
+// ---------------------------------------------------------------- NEXT-2 ----
+// Online SPOT (Siffer et al. 2017, cited by PAPER.md:297 for the POT threshold;
+// DESIGN.md R-23) on the single-GPU threshold workspace left by a calibration
+// fit: Y (the peaks) stays at L.yall, N_t in g->nt_fit, t in g->t, the count of
+// non-anomalous observations in g->n_spot.  A tick's scores are flagged against
+// the current z_q (enova_detect*), then k_spot_append adds every NON-anomalous
+// score above t to Y in index order (anomalies are never used to update the
+// model) and counts the non-anomalous observations; a refit re-runs the fit
+// phase of k_pot on the grown Y with n read from the device.
+__global__ void __launch_bounds__(1024) k_spot_append(const float *__restrict__ scores,
+                                                      const int8_t *__restrict__ flags, int64_t n,
+                                                      PotGlobal *g, double *__restrict__ Y,
+                                                      int64_t cap) {
+  // one CTA; thread i owns the contiguous span [i*per, (i+1)*per): count its
+  // peaks, block-exclusive scan (fixed order), then write them in index order
+  __shared__ long long wpk[32], wna[32];
+  __shared__ long long base_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = min(n, (int64_t)threadIdx.x * per), b1 = min(n, b0 + per);
+  const float t = *(volatile float *)&g->t;
+  const double td = (double)t;
+  long long pk = 0, na = 0;
+  for (int64_t i = b0; i < b1; ++i) {
+    const bool normal = flags[i] == 0;
+    na += normal;
+    pk += normal && scores[i] > t;
+  }
+  long long incl = pk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  long long nas = na;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nas += __shfl_xor_sync(0xffffffffu, nas, o);
+  if (lane == 31) wpk[warp] = incl;
+  if (lane == 0) wna[warp] = nas;
+  if (threadIdx.x == 0) base_s = *(volatile long long *)&g->nt_fit;
+  __syncthreads();
+  long long before = incl - pk;
+  for (int w = 0; w < warp; ++w) before += wpk[w];
+  long long idx = base_s + before;
+  for (int64_t i = b0; i < b1 && idx < cap; ++i) {
+    const float sv = scores[i];
+    if (flags[i] == 0 && sv > t) Y[idx++] = (double)sv - td;
+  }
+  if (threadIdx.x == 0) {
+    long long tp = 0, tn = 0;
+    for (int w = 0; w < nw; ++w) {
+      tp += wpk[w];
+      tn += wna[w];
+    }
+    g->n_spot += tn;
+    long long nt = base_s + tp;
+    if (nt > cap) {
+      g->overflow = 1;
+      nt = cap;
+    }
+    g->nt_fit = nt;
+  }
+}
+
+enova_status spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,
+                         size_t ws_bytes, int64_t n_global_max, double q0, cudaStream_t st) {
+  const ThrLayout L = thr_layout(n_global_max, q0);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  char *b = static_cast<char *>(ws);
+  if (n == 0) return ENOVA_OK;
+  ENOVA_LAUNCH(k_spot_append, 1, 1024, 0, st, scores, flags, n,
+               reinterpret_cast<PotGlobal *>(b + L.glob), reinterpret_cast<double *>(b + L.yall),
+               L.cap);
+  ENOVA_CUDA_TRY(cudaGetLastError());
+  return ENOVA_OK;
+}
+
+enova_status spot_refit(double q, enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                        int64_t n_global_max, double q0, cudaStream_t st) {
+  const ThrLayout L = thr_layout(n_global_max, q0);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  char *b = static_cast<char *>(ws);
+  PotArgs a = make_args(nullptr, 0, 0, q0, q, b, L, false);
+  a.first = a.last = P_FIT;
+  a.out_dev = out_dev;
+  a.n_dev = &a.g->n_spot;
+  return launch_pot(a, pot_grid(), st, true);
+}
 
 }  // namespace enova

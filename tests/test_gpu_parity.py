@@ -576,3 +576,33 @@ def test_explain_windows_match_oracle(E, W, M, H, Z):
         ref = O.per_metric_mean_difference(X, wts, mean, std, tb, te).reshape(-1, M)[g]
         err = np.abs(mdm.cpu().numpy() - ref)
         assert np.all(err <= 1e-4 + 1e-3 * np.abs(ref)), err.max()
+
+
+# ------------------------------------------------------------------ NEXT-2 ----
+@pytest.mark.parametrize("refit_every", [1, 3])
+def test_spot_ticks_match_oracle(E, refit_every):
+    """Online SPOT on the device state (calibration fit -> per-tick appends of the
+    non-anomalous peaks -> refits) tracks the oracle's tick-synchronous SPOT:
+    identical flags, t, n and N_t, z_q within 1e-9 relative, after every tick."""
+    init = synth.score_mixture(200_000, seed=21)
+    ticks = [synth.score_mixture(2000, seed=22, offset=2000 * k) for k in range(10)]
+    ticks[4][[7, 900]] = 80.0                        # anomalies never enter the model
+    ref = O.spot_ticks(init, ticks, refit_every=refit_every)
+    spot = E.Spot(2_000_000)
+    spot.calibrate(cuda(init))
+    z0 = spot.threshold()
+    r0 = O.pot_threshold(init)
+    assert z0["n_peaks"] == r0["n_peaks"] and abs(z0["z_q"] - r0["z_q"]) <= 1e-9 * r0["z_q"]
+    for k, tick in enumerate(ticks):
+        sc = cuda(tick)
+        z = spot.threshold()["z_q"]
+        fl = (sc.double() > z).to(torch.int8)
+        spot.update(sc, fl)
+        if (k + 1) % refit_every == 0:
+            spot.refit()
+        got = spot.threshold()
+        rfl, rthr = ref[k]
+        assert np.array_equal(fl.cpu().numpy().astype(bool), rfl), k
+        assert got["n"] == rthr["n"] and got["n_peaks"] == rthr["n_peaks"], (k, got, rthr)
+        assert got["t"] == rthr["t"]
+        assert abs(got["z_q"] - rthr["z_q"]) <= 1e-9 * rthr["z_q"], (k, got["z_q"], rthr["z_q"])

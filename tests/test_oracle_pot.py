@@ -121,3 +121,33 @@ def test_quantile_formula_closed_forms():
     z = O.pot_quantile(2.0, g, sg, 10_000, 200, 1e-3)
     # P(S > z) = (N_t/n) * (1 + g (z - t)/sg)^(-1/g) must equal q
     assert (200 / 10_000) * (1 + g * (z - 2.0) / sg) ** (-1 / g) == pytest.approx(1e-3, rel=1e-12)
+
+
+# ------------------------------------------------------------- NEXT-2 pins ----
+def test_spot_ticks_of_one_equal_classic_spot():
+    """The tick-synchronous SPOT the GPU implements (R-23) reduces to the cited
+    per-observation SPOT (Algorithm 1) when every tick holds one score."""
+    rng = np.random.default_rng(2)
+    init = rng.exponential(1.0, 5000).astype(np.float32)
+    stream = rng.exponential(1.0, 300).astype(np.float32)
+    stream[[50, 120, 200]] = 40.0                     # anomalies: never update the model
+    f1, z1 = O.spot_classic(init, stream)
+    res = O.spot_ticks(init, [[v] for v in stream])
+    f2 = np.array([r[0][0] for r in res])
+    z2 = np.array([r[1]["z_q"] for r in res])
+    assert np.array_equal(f1, f2) and np.array_equal(z1, z2)
+    assert f1[[50, 120, 200]].all()
+
+
+def test_spot_threshold_stays_calibrated_on_a_stationary_stream():
+    """exp(1) stream: z_q stays within 10% of ln(1/q) (S:238's bar) while the
+    peak set grows, and anomalies (> z_q) are a fraction ~q of the stream."""
+    rng = np.random.default_rng(3)
+    init = rng.exponential(1.0, 20000).astype(np.float32)
+    ticks = [rng.exponential(1.0, 2000).astype(np.float32) for _ in range(10)]
+    res = O.spot_ticks(init, ticks, refit_every=2)
+    for fl, thr in res:
+        assert abs(thr["z_q"] - math.log(1000.0)) < 0.1 * math.log(1000.0)
+    frac = np.mean(np.concatenate([fl for fl, _ in res]))
+    assert frac < 5e-3
+    assert res[-1][1]["n_peaks"] > 400 and res[-1][1]["n"] > 20000
