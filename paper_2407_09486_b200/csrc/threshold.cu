@@ -226,15 +226,18 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
   if (al) {
     const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
     const int64_t n4 = (b1 - b0) / 4;
-    for (int64_t i0 = 0; i0 < n4; i0 += 4 * blockDim.x) {   // warp-uniform trip count
-      float4 v[4];
-      bool ok[4];
+    // two register batches of 4 float4 ping-pong: batch k+1 is in flight while
+    // batch k is binned (8 x 128-bit loads outstanding per thread)
+    const int64_t step = 4 * (int64_t)blockDim.x;
+    auto load = [&](float4 (&v)[4], bool (&ok)[4], int64_t i0) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + u * blockDim.x + threadIdx.x;
         ok[u] = i < n4;
         v[u] = ok[u] ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    };
+    auto bin = [&](const float4 (&v)[4], const bool (&ok)[4]) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         add(v[u].x, ok[u]);
@@ -242,6 +245,15 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
         add(v[u].z, ok[u]);
         add(v[u].w, ok[u]);
       }
+    };
+    float4 va[4], vb[4];
+    bool oka[4], okb[4];
+    load(va, oka, 0);
+    for (int64_t i0 = 0; i0 < n4; i0 += 2 * step) {   // warp-uniform trip count
+      load(vb, okb, i0 + step);
+      bin(va, oka);
+      if (i0 + 2 * step < n4) load(va, oka, i0 + 2 * step);
+      bin(vb, okb);
     }
     tail0 = b0 + 4 * n4;
   }
@@ -422,17 +434,30 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
   if (al) {
     const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
     const int64_t n4 = (b1 - b0) / 4;
-    for (int64_t i0 = 0; i0 < n4; i0 += 4 * blockDim.x) {
+    // the next batch's 4 float4 are loaded before this batch is scattered
+    const int64_t step = 4 * (int64_t)blockDim.x;
+    float4 nq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = u * blockDim.x + threadIdx.x;
+      nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int64_t i0 = 0; i0 < n4; i0 += step) {
       float v[4][4];
       bool ok[4][4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + u * blockDim.x + threadIdx.x;
         const bool g = i < n4;
-        const float4 q = g ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 q = nq[u];
         v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
 #pragma unroll
         for (int e = 0; e < 4; ++e) ok[u][e] = g;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + step + u * blockDim.x + threadIdx.x;
+        nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       scatter4(v, ok);
     }

@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2407_09486_b200 as E  # noqa: E402
 from paper_2407_09486_b200 import synth  # noqa: E402
 
-OFF_NSTAMPS, OFF_STAMPS = 96, 104
+OFF_NSTAMPS, OFF_STAMPS = 112, 120
 
 
 def report(scores, label, reps=5):
