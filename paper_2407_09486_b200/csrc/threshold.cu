@@ -37,7 +37,7 @@
 namespace enova {
 
 constexpr int kBins = 2048;
-constexpr int kPotThreads = 512;
+constexpr int kPotThreads = 512;   // select_digit covers 2048 bins as 512 threads x 4
 constexpr int kPotWarps = kPotThreads / 32;
 constexpr int kMaxCtas = 256;
 constexpr int kMaxPts = 128;
