@@ -252,8 +252,7 @@ def run_streaming(args, rank, world, local_rank):
     md = torch.empty(n, dtype=torch.float32, device=dev)
 
     def tick_ops(t):
-        ring.push(stage, t)
-        ring.detect(t, thr_dev, out=(flags, scores, md))
+        ring.step(stage, t, thr_dev, out=(flags, scores, md))   # one fused launch per tick
 
     l0 = _lib.lib().enova_kernel_launches()
     stage.copy_(S[0])
@@ -321,8 +320,7 @@ def run_streaming(args, rank, world, local_rank):
             for ph in range(W):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=side):
-                    ring.push(stage, ph + W)
-                    ring.detect(ph + W, spot.thr, out=(flags, scores, md))
+                    ring.step(stage, ph + W, spot.thr, out=(flags, scores, md))
                     spot.update(scores, flags)
                 sgraphs[ph] = g
             gref = torch.cuda.CUDAGraph()
@@ -385,8 +383,9 @@ def run_streaming(args, rank, world, local_rank):
                                    f"from a {t_hist}-step calibration horizon",
                        "instances": n_global, "parallelism": f"instance-sharded x{world}",
                        "step": "one tick: ingest-normalise the new samples into the fp16 ring "
-                               "(enova_stream_push) + scores/MD/flags of every instance's newest "
-                               "window (enova_stream_detect: TMA ring -> tcgen05)",
+                               "and score/flag every instance's newest window in ONE launch "
+                               "(enova_stream_step: push fused into the TMA ring -> tcgen05 "
+                               "row kernel)",
                        "l2": "not flushed: the 41 MB fp16 ring is the streaming working set"},
             "tick_latency_us": {"p50": 1e3 * _pct(lat, 50), "p99": 1e3 * _pct(lat, 99),
                                 "max": 1e3 * max(lat)},

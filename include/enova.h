@@ -221,6 +221,15 @@ enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window,
  * is not NULL; a NaN z_q flags nothing.  Both are stream-ordered and capturable
  * in CUDA graphs (one graph per ring phase tick mod W). */
 size_t enova_stream_ring_bytes(int64_t n_instances, int32_t window, int32_t n_metrics);
+/* One launch per tick: enova_stream_push of `sample` (tick `tick`) fused into
+ * enova_stream_detect of the windows ending at `tick` (each CTA ingests its own
+ * instances' samples, then TMA-loads their windows).  Same results as the two
+ * calls; requires the pushes of ticks tick-W+1 .. tick-1 before. */
+enova_status enova_stream_step(void *ring, int64_t n_instances, int64_t tick, const float *sample,
+                               const float *norm_mean, const float *norm_std,
+                               const enova_detector *det, const void *det_ws,
+                               size_t det_ws_bytes, const enova_threshold *thr_dev,
+                               int8_t *flags, float *scores_opt, float *md_opt, void *stream);
 enova_status enova_stream_push(void *ring, int64_t n_instances, int32_t window, int32_t n_metrics,
                                const float *sample, const float *norm_mean, const float *norm_std,
                                int64_t tick, void *stream);

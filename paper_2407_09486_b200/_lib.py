@@ -29,7 +29,7 @@ EXPORTS = (
     "enova_fit_threshold_async", "enova_detect_async", "enova_stream_ring_bytes",
     "enova_stream_push", "enova_stream_detect", "enova_point_adjusted_counts",
     "enova_select_flagged_scratch_bytes", "enova_select_flagged", "enova_explain_windows",
-    "enova_spot_update", "enova_spot_refit",
+    "enova_spot_update", "enova_spot_refit", "enova_stream_step",
 )
 
 
@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
             "enova_point_adjusted_counts": (C.c_int, [vp, i64, vp, i64, i64, i64, vp, vp]),
             "enova_select_flagged_scratch_bytes": (sz, [i64]),
             "enova_spot_update": (C.c_int, [vp, vp, i64, vp, sz, i64, dbl, vp]),
+            "enova_stream_step": (C.c_int, [vp, i64, i64, vp, vp, vp, P(Detector), vp, sz, vp, vp, vp, vp, vp]),
             "enova_spot_refit": (C.c_int, [dbl, vp, vp, sz, i64, dbl, vp]),
             "enova_select_flagged": (C.c_int, [vp, i64, vp, vp, vp, vp]),
             "enova_explain_windows": (C.c_int, [P(Series), P(Detector), vp, sz, vp, i64, vp, vp, vp, vp]),

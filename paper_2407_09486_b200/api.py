@@ -317,6 +317,27 @@ class StreamRing:
                                       C.c_void_p(sample.data_ptr()), C.c_void_p(self.mean.data_ptr()),
                                       C.c_void_p(self.std.data_ptr()), int(tick), _stream_ptr(stream)))
 
+    def step(self, sample: torch.Tensor, tick: int, thr_dev: torch.Tensor | None = None, *,
+             out=None, stream=None):
+        """push(sample, tick) + detect(tick) in ONE launch (enova_stream_step)."""
+        _require_cuda(sample, "sample")
+        if tuple(sample.shape) != (self.n, self.M) or not sample.is_contiguous():
+            raise ValueError(f"sample must be contiguous [{self.n}, {self.M}]")
+        dev = self.buf.device
+        if out is None:
+            flags = torch.empty(self.n, dtype=torch.int8, device=dev) if thr_dev is not None else None
+            sc = torch.empty(self.n, dtype=torch.float32, device=dev)
+            md = torch.empty(self.n, dtype=torch.float32, device=dev)
+        else:
+            flags, sc, md = out
+        ptr = lambda t: C.c_void_p(t.data_ptr() if t is not None else None)
+        check(lib().enova_stream_step(C.c_void_p(self.buf.data_ptr()), self.n, int(tick),
+                                      ptr(sample), ptr(self.mean), ptr(self.std),
+                                      C.byref(self.det.struct), C.c_void_p(self.det.ws.data_ptr()),
+                                      self.det.ws_bytes, ptr(thr_dev), ptr(flags), ptr(sc), ptr(md),
+                                      _stream_ptr(stream)))
+        return flags, sc, md
+
     def detect(self, tick: int, thr_dev: torch.Tensor | None = None, *, out=None, stream=None):
         """(flags, scores, md) of the windows ending at `tick`, each [n]; flags
         need a device threshold (threshold_to_device / fit_threshold_async)."""

@@ -56,6 +56,10 @@ enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, cons
                                  const int64_t *rows_dev, int64_t n_rows, float *md_metric,
                                  float *scores, float *md, cudaStream_t st);
 bool rows_path_ok(const DetLayout &L);
+enova_status stream_step(void *ring, int64_t n, int64_t tick, const DetLayout &L,
+                         const void *det_ws, const float *sample, const float *mean,
+                         const float *stdv, const double *z_q_dev, int8_t *flags, float *scores,
+                         float *md, cudaStream_t st);
 enova_status point_adjust_counts(const int8_t *labels, int64_t ld_labels, const int8_t *flags,
                                  int64_t n_inst, int64_t t_begin, int64_t nw,
                                  unsigned long long *counts_dev, cudaStream_t st);
@@ -63,7 +67,8 @@ enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sampl
                          const float *mean, const float *stdv, int64_t tick, cudaStream_t st);
 enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
                            const void *det_ws, const double *z_q_dev, int8_t *flags, float *scores,
-                           float *md, cudaStream_t st);
+                           float *md, cudaStream_t st, const float *sample = nullptr,
+                           const float *mean = nullptr, const float *stdv = nullptr);
 
 static inline bool aligned(const void *p, size_t a) {
   return (reinterpret_cast<uintptr_t>(p) % a) == 0;
@@ -454,6 +459,46 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
   if ((r = sticky())) return r;
   return stream_detect(ring, n_instances, tick, L, det_ws, thr_dev ? &thr_dev->z_q : nullptr,
                        flags, scores_opt, md_opt, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_stream_step(void *ring, int64_t n_instances, int64_t tick, const float *sample,
+                               const float *norm_mean, const float *norm_std,
+                               const enova_detector *det, const void *det_ws,
+                               size_t det_ws_bytes, const enova_threshold *thr_dev,
+                               int8_t *flags, float *scores_opt, float *md_opt, void *stream) {
+  DetLayout L;
+  enova_status r = check_detector(det, &L);
+  if (r) return r;
+  if (enova_stream_ring_bytes(n_instances, L.W, L.M) == 0) {
+    set_error("stream ring: bad shape (M in {8,16,32,64})");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  if (!ring || !aligned(ring, 256) || n_instances < 0 ||
+      (n_instances > 0 && (!sample || !norm_mean || !norm_std || !aligned(sample, 16) ||
+                           !aligned(norm_mean, 16) || !aligned(norm_std, 16)))) {
+    set_error("bad stream_step arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (tick < L.W - 1) {
+    set_error("stream_step needs W-1 earlier pushed ticks (tick >= W-1)");
+    return ENOVA_ERR_INSUFFICIENT_HISTORY;
+  }
+  if (flags && (!thr_dev || !aligned(thr_dev, 8))) {
+    set_error("device threshold missing or misaligned");
+    return ENOVA_ERR_UNCALIBRATED;
+  }
+  if (!flags && !scores_opt && !md_opt && n_instances > 0) {
+    set_error("no output requested");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!det_ws || det_ws_bytes < L.total || !aligned(det_ws, 256)) {
+    set_error("prepared-detector workspace missing, too small or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  if ((r = sticky())) return r;
+  return stream_step(ring, n_instances, tick, L, det_ws, sample, norm_mean, norm_std,
+                     thr_dev ? &thr_dev->z_q : nullptr, flags, scores_opt, md_opt,
+                     static_cast<cudaStream_t>(stream));
 }
 
 enova_status enova_spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,

@@ -753,7 +753,47 @@ struct StreamParams {
   int8_t *flags;
   const double *z_q_dev;
   unsigned long long *trace;   // diagnostic timeline of CTA 0 (NULL normally)
+  // fused ingest (enova_stream_step): push sample [N][M] of `tick` before scoring
+  const float *sample, *mean, *stdv;
+  __half *ring16;
+  float *sums_w;
 };
+
+// ingest of one instance's new sample (k_stream_push's arithmetic, G float4 groups)
+template <int G>
+__device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i) {
+  constexpr int M = 4 * G;
+  const int W = p.W;
+  const int slot = (int)(p.tick % W);
+  const float4 *xs = reinterpret_cast<const float4 *>(p.sample + i * M);
+  const float4 *ms = reinterpret_cast<const float4 *>(p.mean + i * M);
+  const float4 *ss = reinterpret_cast<const float4 *>(p.stdv + i * M);
+  __half *r0 = p.ring16 + ((size_t)i * 2 * W + slot) * M;
+  __half *r1 = r0 + (size_t)W * M;
+  float pg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float4 v = __ldg(xs + g), mu = __ldg(ms + g), sd = __ldg(ss + g);
+    const float z0 = fminf(fmaxf(div_rn(__fsub_rn(v.x, mu.x), sd.x, __frcp_rn(sd.x)), -1e4f), 1e4f);
+    const float z1 = fminf(fmaxf(div_rn(__fsub_rn(v.y, mu.y), sd.y, __frcp_rn(sd.y)), -1e4f), 1e4f);
+    const float z2 = fminf(fmaxf(div_rn(__fsub_rn(v.z, mu.z), sd.z, __frcp_rn(sd.z)), -1e4f), 1e4f);
+    const float z3 = fminf(fmaxf(div_rn(__fsub_rn(v.w, mu.w), sd.w, __frcp_rn(sd.w)), -1e4f), 1e4f);
+    uint2 pk;
+    pk.x = cvt_pack_f16x2(z0, z1);
+    pk.y = cvt_pack_f16x2(z2, z3);
+    *reinterpret_cast<uint2 *>(r0 + 4 * g) = pk;
+    *reinterpret_cast<uint2 *>(r1 + 4 * g) = pk;
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.y));
+    pg[g] = (f01.x + f01.y) + (f23.x + f23.y);
+  }
+#pragma unroll
+  for (int w = 1; w < G; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < G; k += 2 * w) pg[k] = pg[k] + pg[k + w];
+  p.sums_w[(size_t)i * 2 * W + slot] = pg[0];
+  p.sums_w[(size_t)i * 2 * W + slot + W] = pg[0];
+}
 
 template <int H, int ZP>
 __global__ void __launch_bounds__(kSThreads, 1)
@@ -845,6 +885,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     }
   } else if (warp == kSAWarp) {
     // ---------------- A producer: one TMA box (kSAK K-steps x 128 instances) per group ----------------
+    if (p.sample) named_bar_sync(5, kRowThreads + 32);   // fused ingest: wait for the pushes
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
@@ -915,6 +956,18 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const int r = tid;
     const int64_t row = row0 + r;
     const bool valid = row < p.n;
+    if (p.sample) {   // fused ingest of this tick's sample, visible to the TMA (async proxy)
+      if (valid) {
+        switch (p.M) {
+          case 8: stream_push_one<2>(p, row); break;
+          case 16: stream_push_one<4>(p, row); break;
+          case 32: stream_push_one<8>(p, row); break;
+          default: stream_push_one<16>(p, row); break;
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      named_bar_sync(5, kRowThreads + 32);
+    }
     const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
     WinSum ws;
     ws.init();
@@ -940,6 +993,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 unsigned long long *pair_trace();
+enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
+                           const void *det_ws, const double *z_q_dev, int8_t *flags, float *scores,
+                           float *md, cudaStream_t st, const float *sample = nullptr,
+                           const float *mean = nullptr, const float *stdv = nullptr);
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -977,7 +1034,8 @@ static enova_status launch_stream_t(const CUtensorMap &tm, const StreamParams &p
 
 enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetLayout &L,
                            const void *det_ws, const double *z_q_dev, int8_t *flags, float *scores,
-                           float *md, cudaStream_t st) {
+                           float *md, cudaStream_t st, const float *sample,
+                           const float *mean, const float *stdv) {
   if (n == 0) return ENOVA_OK;
   auto enc = tensor_map_encoder();
   if (!enc) {
@@ -1021,6 +1079,11 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
   p.flags = flags;
   p.z_q_dev = z_q_dev;
   p.trace = pair_trace();
+  p.sample = sample;
+  p.mean = mean;
+  p.stdv = stdv;
+  p.ring16 = const_cast<__half *>(static_cast<const __half *>(ring));
+  p.sums_w = const_cast<float *>(p.sums);
   switch (L.H * 100 + L.ZP) {
     case 3208: return launch_stream_t<32, 8>(tm, p, st);
     case 3216: return launch_stream_t<32, 16>(tm, p, st);
@@ -1031,6 +1094,13 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
   }
   set_error("unsupported (H, Z)");
   return ENOVA_ERR_UNSUPPORTED;
+}
+
+enova_status stream_step(void *ring, int64_t n, int64_t tick, const DetLayout &L,
+                         const void *det_ws, const float *sample, const float *mean,
+                         const float *stdv, const double *z_q_dev, int8_t *flags, float *scores,
+                         float *md, cudaStream_t st) {
+  return stream_detect(ring, n, tick, L, det_ws, z_q_dev, flags, scores, md, st, sample, mean, stdv);
 }
 
 }  // namespace enova

@@ -429,10 +429,15 @@ def test_stream_ring_matches_batch_and_oracle(E, W, M, H, Z, N):
     fb, sb, mb = E.detect(Xc, det, mean, std, thr, return_scores=True)
     rs, rmd = O.score_windows(X, wts, mean.cpu().numpy(), std.cpu().numpy(), W - 1, T)
     ring = E.StreamRing(det, mean, std)
+    ring2 = E.StreamRing(det, mean, std)           # fused push + detect (enova_stream_step)
     for k in range(T):
         ring.push(Xc[:, k, :].contiguous(), k)
+        if k < W - 1:
+            ring2.push(Xc[:, k, :].contiguous(), k)
         if k >= W - 1:
             f, s_, m_ = ring.detect(k, thr_dev)
+            f2, s2, m2 = ring2.step(Xc[:, k, :].contiguous(), k, thr_dev)
+            assert torch.equal(f, f2) and torch.equal(s_, s2) and torch.equal(m_, m2), k
             j = k - W + 1
             assert_scores(s_.cpu().numpy(), rs[:, j], "stream scores")
             assert_md(m_.cpu().numpy(), rmd[:, j])
