@@ -209,9 +209,11 @@ enova_status enova_ring_push(float *ring, int64_t n_instances, int32_t window,
  * fp16_RNE(clamp((X - mean)/std)), same sample-sum association).
  *
  * ring: device, 256-byte aligned, enova_stream_ring_bytes(N, W, M) bytes,
- * caller-owned: fp16 x [N][2W][M] (the sample of tick k at slots k mod W and
- * (k mod W) + W) followed (at a 256-byte boundary) by fp32 per-sample sums
- * s = sum_j x_j [N][2W].  M in {8, 16, 32, 64}.
+ * caller-owned, opaque to the caller: per instance a row of fp16 x (2W slots
+ * of M metrics, the sample of tick k at slots k mod W and (k mod W) + W, the row
+ * pitch padded off powers of two) followed (at a 256-byte boundary) by the fp32
+ * per-sample sums s = sum_j x_j, 2W per instance (padded pitch).
+ * M in {8, 16, 32, 64}.
  * enova_stream_push: sample device fp32 [N][M] (16-byte aligned) for tick
  * `tick` (>= 0); norm_mean / norm_std device fp32 [N][M] (enova_compute_stats).
  * enova_stream_detect: after pushes of ticks tick-W+1 .. tick (tick >= W-1),

@@ -27,6 +27,7 @@
 //
 // Envelope: M in {8, 16} (a K-step holds whole samples), H in {32, 64, 128}.
 #include <cuda.h>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -138,9 +139,9 @@ struct WinSum {
 // same association.  Row threads of warps 0-3; GEMM2/GEMM3 are issued by the
 // MMA warp between the h_full / mu_full arrivals and the g2_done / g3_done
 // commits of RowBars.
-template <int H, int ZP, class Bars>
+template <int H, int ZP, class Bars, class SxFn>
 __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane, int r, int64_t row,
-                                              bool valid, float sx, uint8_t *region,
+                                              bool valid, SxFn &&sx_fn, uint8_t *region,
                                               uint8_t *mubuf, const float *b3s, const float *wbs,
                                               const float *bmls, Bars &B, int Z, int D,
                                               const double *bbar, float *scores, float *md_out,
@@ -236,6 +237,7 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     stamp(9);
 
     // ---- E3: MD by the column-sum identity; flag ----
+    const float sx = sx_fn();   // window sum (may be computed here, off the E1 path)
     mbar_wait_sleep(&B.g3_done, 0, 64);
     stamp(10);
     tc_fence_after();
@@ -512,7 +514,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     }
     const float sx = ws.acc0 + ws.acc1;
 
-    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx, region, mubuf, b3s, wbs, bmls, B,
+    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, [&]() { return sx; }, region, mubuf,
+                         b3s, wbs, bmls, B,
                          p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev, nullptr,
                          kExplain ? wbarm_s : nullptr, kExplain ? xsum : nullptr, p.bbarm,
                          p.md_metric, M, p.W);
@@ -639,11 +642,17 @@ enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, cons
 // so the kernel is a TMA -> tcgen05 pipeline plus the shared epilogue.
 // =====================================================================
 
+// Row pitches are padded off powers of two: with the natural pitches (2W*M fp16 =
+// 4 KB, 2W fp32 = 512 B at c4) the 128 instances of a tile hit the same DRAM
+// channel and every A group of the stream kernel was serialised (measured ~1 us
+// per 4-K-step group).  +256 B / +32 B spreads consecutive instances.
+__host__ __device__ inline int64_t stream_pitch(int W, int M) { return (int64_t)2 * W * M + 128; }
+__host__ __device__ inline int64_t sums_pitch(int W) { return (int64_t)2 * W + 8; }
 size_t stream_sums_offset(int64_t n, int W, int M) {
-  return align_up((size_t)2 * W * n * M * 2, 256);
+  return align_up((size_t)n * stream_pitch(W, M) * 2, 256);
 }
 size_t stream_ring_bytes(int64_t n, int W, int M) {
-  return stream_sums_offset(n, W, M) + (size_t)2 * W * n * 4;
+  return stream_sums_offset(n, W, M) + (size_t)n * sums_pitch(W) * 4;
 }
 
 template <int G>
@@ -658,7 +667,7 @@ __global__ void k_stream_push(__half *__restrict__ ring16, float *__restrict__ s
   const float4 *xs = reinterpret_cast<const float4 *>(sample + i * M);
   const float4 *ms = reinterpret_cast<const float4 *>(mean + i * M);
   const float4 *ss = reinterpret_cast<const float4 *>(stdv + i * M);
-  __half *r0 = ring16 + ((size_t)i * 2 * W + slot) * M;   // [N][2W][M]
+  __half *r0 = ring16 + (size_t)i * stream_pitch(W, M) + (size_t)slot * M;   // [N][pitch]
   __half *r1 = r0 + (size_t)W * M;
   float pg[G];
 #pragma unroll
@@ -682,8 +691,8 @@ __global__ void k_stream_push(__half *__restrict__ ring16, float *__restrict__ s
   for (int w = 1; w < G; w <<= 1)
 #pragma unroll
     for (int k = 0; k + w < G; k += 2 * w) pg[k] = pg[k] + pg[k + w];
-  sums[(size_t)i * 2 * W + slot] = pg[0];
-  sums[(size_t)i * 2 * W + slot + W] = pg[0];
+  sums[(size_t)i * sums_pitch(W) + slot] = pg[0];
+  sums[(size_t)i * sums_pitch(W) + slot + W] = pg[0];
 }
 
 enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sample,
@@ -725,7 +734,14 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, in
 // 64 fp16 (128 B, the SWIZZLE_128B atom width) x 128 instances = 16 KB.
 constexpr int kSAK = 4;
 constexpr int kSAStages = 8;
-constexpr int kSAWarp = 6;                        // A (TMA) producer warp
+constexpr int kSAWarp = 6;                        // A (TMA) producer warp (kCpAsyncA == false)
+// A operand loading of the stream kernel: true = the row threads copy their own
+// window with cp.async (LDGSTS, 16 B, kSADepth groups in flight per thread, manual
+// 128B swizzle); false = one TMA box per group from a producer warp.  Measured:
+// the TMA path paces the K loop at ~0.7 us per 4-K-step group (few boxes in
+// flight per SM), the cp.async path keeps 4x more bytes in flight.
+constexpr bool kCpAsyncA = false;
+constexpr int kSADepth = 4;
 constexpr int kSThreads = kRThreads + 32;
 constexpr uint32_t kSAStageBytes = kRR * 128;
 
@@ -759,6 +775,43 @@ struct StreamParams {
   float *sums_w;
 };
 
+// Window sum of one row computed by a whole warp with coalesced loads: lane l
+// holds s_{l + 32c}; 8-sample block sums by xor-shuffles (the ((s0+s1)+(s2+s3)) +
+// ((s4+s5)+(s6+s7)) tree), then the WinSum chains (blocks alternately into acc0 /
+// acc1, a leftover block into acc0, leftover samples into acc1) evaluated
+// redundantly by every lane -- the same association as WinSum::push.
+template <int NC>
+__device__ __forceinline__ float warp_window_sum(const float (&v)[NC], int W) {
+  const int lane = threadIdx.x & 31;
+  const int W8 = W & ~7, nb2 = 2 * (W8 / 16), nblk = W8 / 8;
+  float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    float b = v[c];
+    b += __shfl_xor_sync(0xffffffffu, b, 1);
+    b += __shfl_xor_sync(0xffffffffu, b, 2);
+    b += __shfl_xor_sync(0xffffffffu, b, 4);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int blk = 4 * c + q;
+      const float bs = __shfl_sync(0xffffffffu, b, 8 * q);
+      if (blk < nblk) {
+        if (blk < nb2 && (blk & 1)) acc1 += bs;
+        else acc0 += bs;
+      }
+    }
+  }
+  for (int tau = W8; tau < W; ++tau) {   // leftover samples (W % 8), in order
+    float src = v[0];
+#pragma unroll
+    for (int c = 1; c < NC; ++c)
+      if ((tau >> 5) == c) src = v[c];
+    acc1 += __shfl_sync(0xffffffffu, src, tau & 31);
+  }
+  (void)lane;
+  return acc0 + acc1;
+}
+
 // ingest of one instance's new sample (k_stream_push's arithmetic, G float4 groups)
 template <int G>
 __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i) {
@@ -768,7 +821,7 @@ __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i
   const float4 *xs = reinterpret_cast<const float4 *>(p.sample + i * M);
   const float4 *ms = reinterpret_cast<const float4 *>(p.mean + i * M);
   const float4 *ss = reinterpret_cast<const float4 *>(p.stdv + i * M);
-  __half *r0 = p.ring16 + ((size_t)i * 2 * W + slot) * M;
+  __half *r0 = p.ring16 + (size_t)i * stream_pitch(W, M) + (size_t)slot * M;
   __half *r1 = r0 + (size_t)W * M;
   float pg[G];
 #pragma unroll
@@ -791,8 +844,8 @@ __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i
   for (int w = 1; w < G; w <<= 1)
 #pragma unroll
     for (int k = 0; k + w < G; k += 2 * w) pg[k] = pg[k] + pg[k + w];
-  p.sums_w[(size_t)i * 2 * W + slot] = pg[0];
-  p.sums_w[(size_t)i * 2 * W + slot + W] = pg[0];
+  p.sums_w[(size_t)i * sums_pitch(W) + slot] = pg[0];
+  p.sums_w[(size_t)i * sums_pitch(W) + slot + W] = pg[0];
 }
 
 template <int H, int ZP>
@@ -831,7 +884,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
       mbar_init(&B.w_empty[i], 1);
     }
     for (int i = 0; i < kRAStages; ++i) {
-      mbar_init(&B.a_full[i], 1);   // producer's expect_tx; TMA completes the bytes
+      // TMA: the producer's expect_tx (the TMA completes the bytes); cp.async: one
+      // arrival per row warp
+      mbar_init(&B.a_full[i], kCpAsyncA ? kRowThreads / 32 : 1);
       mbar_init(&B.a_empty[i], 1);
     }
     mbar_init(&B.wimg, 1);
@@ -885,8 +940,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
     }
   } else if (warp == kSAWarp) {
     // ---------------- A producer: one TMA box (kSAK K-steps x 128 instances) per group ----------------
-    if (p.sample) named_bar_sync(5, kRowThreads + 32);   // fused ingest: wait for the pushes
-    if (lane == 0) {
+    if (!kCpAsyncA && p.sample) named_bar_sync(5, kRowThreads + 32);   // fused ingest: wait for the pushes
+    if (!kCpAsyncA && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
       for (int g = 0; g < n_groups; ++g) {
@@ -965,26 +1020,101 @@ __global__ void __launch_bounds__(kSThreads, 1)
           default: stream_push_one<16>(p, row); break;
         }
       }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      named_bar_sync(5, kRowThreads + 32);
+      if constexpr (kCpAsyncA) {
+        __threadfence_block();   // own pushed sample before this thread's cp.async reads
+      } else {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        named_bar_sync(5, kRowThreads + 32);
+      }
+    }
+    // cp.async A loading: this row's window, group g = 64 fp16 (128 B) at element
+    // woff*M + 64 g, into stage (g % kSAStages) row r with the 128B swizzle
+    // (16-byte chunk c of row r at c ^ (r & 7); 8-row atoms 1 KB apart)
+    const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+    const __half *asrc = p.ring16 + (size_t)(valid ? row : 0) * stream_pitch(W, p.M) + (size_t)woff * p.M;
+    const uint32_t adst_row = smem_u32(astage) + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
+    auto issue_group = [&](int g) {
+      const int a = g % kSAStages;
+      const uint32_t dst = adst_row + (uint32_t)a * kSAStageBytes;
+      const __half *src = asrc + 64 * g;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t d = dst + (uint32_t)((c ^ (r & 7)) * 16);
+        const int sz = valid ? 16 : 0;   // zero-fill rows past the fleet
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d),
+                     "l"(src + 8 * c), "r"(sz)
+                     : "memory");
+      }
+    };
+    if constexpr (kCpAsyncA) {
+      for (int g = 0; g < kSADepth; ++g) {
+        if (g < n_groups) issue_group(g);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
     }
     const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
     WinSum ws;
     ws.init();
-    if (valid) {
-      const float *sp = p.sums + (size_t)row * 2 * W + woff;
-      for (int t0 = 0; t0 < W; t0 += 64) {   // 64 loads in flight per thread
-        float v[64];
+    // window sums: each thread prefetches its row's W per-sample sums as aligned
+    // float4 (W <= 64: 17 x 16 B covering [woff, woff + W), issued now, in flight
+    // while the A groups stream) and folds them in WinSum order before E3
+    const bool pre = W <= 64;
+    const int wsh = woff & 3;   // uniform over the CTA
+    float4 sv4[17];
+    if (pre) {
+      const float4 *sp4 = reinterpret_cast<const float4 *>(
+          p.sums + (size_t)(valid ? row : 0) * sums_pitch(W) + (woff - wsh));
 #pragma unroll
-        for (int k = 0; k < 64; ++k) v[k] = (t0 + k < W) ? __ldg(sp + t0 + k) : 0.f;
-#pragma unroll
-        for (int k = 0; k < 64; ++k)
-          if (t0 + k < W) ws.push(t0 + k, v[k], W8, nb2);
+      for (int k = 0; k < 17; ++k)
+        sv4[k] = (valid && 4 * k < wsh + W) ? __ldg(sp4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if constexpr (kCpAsyncA) {
+      for (int g = 0; g < n_groups; ++g) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kSADepth - 1) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.a_full[g % kSAStages]);
+        if (r == 0 && g < 20) stamp(16 + g);
+        const int nx = g + kSADepth;
+        if (nx < n_groups) {
+          if (nx >= kSAStages) mbar_wait(&B.a_empty[nx % kSAStages], ((nx / kSAStages) - 1) & 1);
+          issue_group(nx);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
       }
     }
-    const float sx = ws.acc0 + ws.acc1;
+    // (reduced only before E3, where MD needs it: off the E1 / E2 critical path)
+    auto sx_fn = [&]() -> float {
+      float sx = 0.f;
+      if (pre && valid) {
+        auto fold = [&](auto shift_c) {
+          constexpr int sh = decltype(shift_c)::value;
+#pragma unroll
+          for (int tau = 0; tau < 64; ++tau) {
+            if (tau < W) {
+              const int e = tau + sh;
+              const float4 q = sv4[e >> 2];
+              const float v = (e & 3) == 0 ? q.x : (e & 3) == 1 ? q.y : (e & 3) == 2 ? q.z : q.w;
+              ws.push(tau, v, W8, nb2);
+            }
+          }
+        };
+        switch (wsh) {
+          case 0: fold(std::integral_constant<int, 0>{}); break;
+          case 1: fold(std::integral_constant<int, 1>{}); break;
+          case 2: fold(std::integral_constant<int, 2>{}); break;
+          default: fold(std::integral_constant<int, 3>{}); break;
+        }
+        sx = ws.acc0 + ws.acc1;
+      } else if (valid) {   // long windows: per-thread loads (the association of WinSum)
+        const float *sp = p.sums + (size_t)row * sums_pitch(W) + woff;
+        for (int tau = 0; tau < W; ++tau) ws.push(tau, __ldg(sp + tau), W8, nb2);
+        sx = ws.acc0 + ws.acc1;
+      }
+      return sx;
+    };
     if (r == 0) stamp(5);
-    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx, region, mubuf, b3s, wbs, bmls, B,
+    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx_fn, region, mubuf, b3s, wbs, bmls, B,
                          p.Z, p.D, p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr);
   }
   tc_fence_before();
@@ -1044,8 +1174,8 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
   }
   const int W = L.W, M = L.M;
   CUtensorMap tm;   // [instance N][2W*M] fp16; box = 64 K-elements (128 B) x 128 instances
-  const cuuint64_t dims[2] = {(cuuint64_t)(2 * W * M), (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)(2 * W * M * 2)};
+  const cuuint64_t dims[2] = {(cuuint64_t)stream_pitch(W, M), (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)(stream_pitch(W, M) * 2)};
   const cuuint32_t box[2] = {16 * kSAK, (cuuint32_t)kRR};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ring), dims,
