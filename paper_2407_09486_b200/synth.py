@@ -199,7 +199,9 @@ def metric_trace_parallel(n_instances: int, n_steps: int, n_metrics: int = 16,
             for a in range(0, N, block)]
     out = np.empty((N, int(n_steps), int(n_metrics)), dtype=np.float32)
     lab = np.empty((N, int(n_steps)), dtype=np.int8) if return_labels else None
-    with ProcessPoolExecutor(max_workers=workers) as ex:
+    import multiprocessing as mp
+    # forkserver: the caller may be multi-threaded (torch), where fork() can deadlock
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("forkserver")) as ex:
         a = 0
         for blk in ex.map(_trace_block, jobs):
             if return_labels:

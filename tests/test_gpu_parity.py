@@ -611,3 +611,66 @@ def test_spot_ticks_match_oracle(E, refit_every):
         assert got["n"] == rthr["n"] and got["n_peaks"] == rthr["n_peaks"], (k, got, rthr)
         assert got["t"] == rthr["t"]
         assert abs(got["z_q"] - rthr["z_q"]) <= 1e-9 * rthr["z_q"], (k, got["z_q"], rthr["z_q"])
+
+
+# ------------------------------------------------------- full-size configs ----
+def test_c3_shard_full_size_sampled(E):
+    """c3's per-GPU shard at full size (512 instances x T=50 000, 25.5M windows) in
+    the bench's graph-captured Pipeline: sampled windows one by one against the
+    oracle, the fleet threshold against the oracle fit of the same 12.8M
+    calibration scores, and every flag against the rule."""
+    cfg = synth.CONFIGS["c3"]
+    N, T, M = cfg["n_instances"] // 8, cfg["n_steps"], cfg["n_metrics"]
+    W, H, Z = cfg["window"], cfg["hidden"], cfg["latent"]
+    X = synth.metric_trace_parallel(N, T, M, seed=synth.DEFAULT_SEED + 2, instance_offset=3 * N)
+    wts = synth.detector_weights(W, M, H, Z, seed=synth.DEFAULT_SEED + 2)
+    tcal = T // 2
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    pipe = E.Pipeline(det, N, T, tcal)
+    pipe.capture(Xc)
+    pipe.replay()
+    torch.cuda.synchronize()
+    res = pipe.result()
+    r = np.random.default_rng(13)
+    om, os_, _ = O.series_stats(X, tcal)
+    gs, gmd = res.scores.cpu().numpy(), res.md.cpu().numpy()
+    for i in np.unique(r.integers(0, N, 60)):
+        for t in np.sort(r.choice(np.arange(tcal, T), 3, replace=False)):
+            rs, rmd = O.score_windows(X[i:i + 1], wts, om[i:i + 1], os_[i:i + 1], t, t + 1)
+            assert_scores(gs[i, t - tcal:t - tcal + 1], rs[0], f"inst {i} t {t}")
+            assert_md(gmd[i, t - tcal:t - tcal + 1], rmd[0])
+    o = O.pot_threshold(res.cal_scores.cpu().numpy(), 0.98, 1e-3)
+    assert res.threshold["n_peaks"] == o["n_peaks"] and res.threshold["t"] == o["t"]
+    assert abs(res.threshold["z_q"] - o["z_q"]) <= 1e-9 * o["z_q"]
+    assert np.array_equal(res.flags.cpu().numpy(), O.flags(gs, gmd, res.threshold["z_q"]))
+
+
+def test_c4_streaming_full_size(E):
+    """c4 at full size: 10 000 instances, fused stream ticks (enova_stream_step)
+    against the oracle on a sample of instances per tick and against batch
+    detect bit for bit."""
+    cfg = synth.CONFIGS["c4"]
+    n, M, W, H, Z = cfg["n_instances"], cfg["n_metrics"], cfg["window"], cfg["hidden"], cfg["latent"]
+    t_hist, ticks = 256, 4
+    X = synth.metric_trace_parallel(n, t_hist + ticks, M, seed=synth.DEFAULT_SEED + 4)
+    wts = synth.detector_weights(W, M, H, Z, seed=synth.DEFAULT_SEED + 4)
+    det = E.PreparedDetector(wts)
+    Xc = cuda(X)
+    mean, std, _ = E.compute_stats(Xc[:, :t_hist], t_hist)
+    thr = {"z_q": 3.0}
+    thr_dev = E.threshold_to_device(thr)
+    ring = E.StreamRing(det, mean, std)
+    for t in range(t_hist - W + 1, t_hist):
+        ring.push(Xc[:, t].contiguous(), t)
+    m_np, s_np = mean.cpu().numpy(), std.cpu().numpy()
+    r = np.random.default_rng(4)
+    for t in range(t_hist, t_hist + ticks):
+        f, sc, md = ring.step(Xc[:, t].contiguous(), t, thr_dev)
+        fb, sb, mb = E.detect(Xc[:, t - W + 1:t + 1].contiguous(), det, mean, std, thr, W - 1, W,
+                              return_scores=True)
+        assert torch.equal(sc, sb[:, 0]) and torch.equal(md, mb[:, 0]) and torch.equal(f, fb[:, 0])
+        idx = np.sort(r.choice(n, 50, replace=False))
+        rs, rmd = O.score_windows(X[idx][:, t - W + 1:t + 1], wts, m_np[idx], s_np[idx], W - 1, W)
+        assert_scores(sc.cpu().numpy()[idx], rs[:, 0], f"tick {t}")
+        assert_md(md.cpu().numpy()[idx], rmd[:, 0])
