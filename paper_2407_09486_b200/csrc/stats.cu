@@ -135,7 +135,17 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   int dev = 0, sms = 148;
   ENOVA_CUDA_TRY(cudaGetDevice(&dev));
   ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int64_t nchunk = (2 * (int64_t)sms + N - 1) / N;   // ~one wave of 2 CTAs per SM
+  // chunks per instance: the smallest count (>= one wave of 2 CTAs per SM) whose
+  // last wave is at least 85% full, so no SM idles through a ragged tail wave
+  const int64_t slots = 2 * (int64_t)sms;
+  int64_t nchunk = (slots + N - 1) / N;
+  for (int64_t c = nchunk; c <= stats_max_chunks(N); ++c) {
+    const int64_t rem = (N * c) % slots;
+    if (rem == 0 || rem >= (slots * 85) / 100) {
+      nchunk = c;
+      break;
+    }
+  }
   if (nchunk > stats_max_chunks(N)) nchunk = stats_max_chunks(N);
   if (nchunk > t_cal_end / 64) nchunk = t_cal_end / 64;
   if (nchunk < 1) nchunk = 1;
