@@ -463,6 +463,29 @@ def run_threshold_sweep(args, rank, world, local_rank):
     tot = max_over_ranks(float(sum(step_ms)))
     thr = E.threshold_from_device(thr_dev) if world == 1 else holder["thr"]
     value = n_total * args.steps / (tot * 1e-3)
+    # phase split of one k_pot launch from its %globaltimer stamps (CTA 0):
+    # [0] radix pass 0 ... [3] compaction, [5] fit start, [-1] end
+    phases = None
+    if world == 1:
+        import ctypes as C
+        step()
+        torch.cuda.synchronize()
+        no, so = C.c_int64(), C.c_int64()
+        _lib.lib().enova_internal_pot_stamp_offsets(C.byref(no), C.byref(so))
+        head = ws.buf[:so.value + 8 * 96].cpu().numpy()
+        ns = int(head[no.value:no.value + 4].view(np.int32)[0])
+        st = head[so.value:so.value + 8 * min(ns, 95)].view(np.uint64).astype(np.int64)
+        if ns >= 7:
+            sel_us = (st[5] - st[0]) / 1e3
+            fit_us = (st[-1] - st[5]) / 1e3
+            moved = 4 * 4.0 * n + 8.0 * thr["n_peaks"]        # 3 radix reads + scatter read + Y write
+            phases = {"select_compact_us": sel_us, "fit_us": fit_us,
+                      "select_bytes_moved": moved,
+                      "select_achieved_GBps": moved / (sel_us * 1e-6) / 1e9,
+                      "select_hbm_frac": moved / (sel_us * 1e-6) / 1e9 / load_peaks()["hbm"],
+                      "fit_grid_points": 128, "fit_peaks": thr["n_peaks"],
+                      "note": "stamps of CTA 0 (globaltimer); the fit is fp64 compute "
+                              "(Grimshaw grid + certified Halley passes), not HBM-bound"}
     peaks = load_peaks()
     ms = tot / args.steps
     achieved = 4.0 * n / (ms * 1e-3) / 1e9                 # algorithmic: one read of the shard
@@ -500,6 +523,7 @@ def run_threshold_sweep(args, rank, world, local_rank):
                        "parallelism": f"score-sharded x{world}",
                        "l2": "inputs 400 MB > L2 (no flush needed)"},
             "threshold": {k_: thr[k_] for k_ in ("t", "gamma", "sigma", "z_q", "n_peaks")},
+            "phases": phases,
             "roofline": {"kernel": "k_pot", "bound": "hbm", "achieved": achieved,
                          "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"],
                          "traffic": None, "peak_source": peaks["source"],

@@ -42,6 +42,7 @@ enova_status fit_threshold_async(const float *scores, int64_t n, double q0, doub
                                  int64_t n_global_max, cudaStream_t st);
 size_t threshold_workspace_bytes(int64_t n_max, double q0);
 void set_pair_trace(void *t);
+void pot_stamp_offsets(int64_t *n_off, int64_t *st_off);
 enova_status ring_push(float *ring, int64_t n, int W, int M, const float *sample, int64_t tick,
                        cudaStream_t st);
 size_t stream_ring_bytes(int64_t n, int W, int M);
@@ -160,6 +161,11 @@ int enova_abi_version(void) { return ENOVA_ABI_VERSION; }
 // pair 0 of the next CTA-pair score launches into a device buffer of
 // 2 x 512 x 16 uint64 (NULL disables)
 void enova_internal_set_trace(void *dev_buf) { enova::set_pair_trace(dev_buf); }
+// diagnostic (not in enova.h): where k_pot writes its %globaltimer phase stamps
+// in the threshold workspace (PotGlobal is at offset 0)
+void enova_internal_pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
+  enova::pot_stamp_offsets(n_off, st_off);
+}
 
 uint64_t enova_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -28,6 +28,7 @@
 // partition depends only on N_t and the grid size, identical on every rank and
 // for every world size.
 #include <math.h>
+#include <stddef.h>
 
 #include <vector>
 
@@ -1365,6 +1366,12 @@ enova_status fit_threshold_async(const float *scores, int64_t n, double q0, doub
 }
 
 size_t threshold_workspace_bytes(int64_t n_max, double q0) { return thr_layout(n_max, q0).total; }
+
+// diagnostic: byte offsets of PotGlobal.n_stamps / .stamps in the threshold workspace
+void pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
+  *n_off = (int64_t)offsetof(PotGlobal, n_stamps);
+  *st_off = (int64_t)offsetof(PotGlobal, stamps);
+}
 
 // ---------------------------------------------------------------- NEXT-2 ----
 // Online SPOT (Siffer et al. 2017, cited by PAPER.md:297 for the POT threshold;
