@@ -590,7 +590,10 @@ def run_windows(args, rank, world, local_rank):
     X_pinned = torch.from_numpy(Xh).pin_memory()
     X = X_pinned.to(dev)
     det = E.PreparedDetector(wts, device=dev)
-    comm = E.Comm.create(rank, world, local_rank) if world > 1 else None
+    # ENOVA_BENCH_COMM=1 forces the communicator path at world size 1 (measures
+    # the collective threshold's overhead on one GPU; diagnostic only)
+    force_comm = os.environ.get("ENOVA_BENCH_COMM") == "1"
+    comm = E.Comm.create(rank, world, local_rank) if (world > 1 or force_comm) else None
     n_cal_local = N * (tcal - (W - 1))
     n_det_local = N * (T - tcal)
     wins_local = n_cal_local + n_det_local
@@ -601,10 +604,10 @@ def run_windows(args, rank, world, local_rank):
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
     # one step = pipe.enqueue(X): stats_async -> calibration scores -> POT threshold
-    # (device-resident on one GPU; collective + synchronous with a communicator)
-    # -> flags / scores / MD.  On one GPU the step is captured once into a CUDA
-    # graph and replayed (one graph launch per step).
-    use_graph = world == 1
+    # (device-resident; with a communicator the stream-ordered collective fit)
+    # -> flags / scores / MD.  The step is captured once into a CUDA graph and
+    # replayed (one graph launch per step), NCCL collectives included.
+    use_graph = True   # with a communicator too: the NCCL collectives are captured
     l0 = _lib.lib().enova_kernel_launches()
     pipe.enqueue(X)
     torch.cuda.synchronize()
@@ -769,7 +772,7 @@ def run_windows(args, rank, world, local_rank):
             # step-k graph on the compute stream; every step still copies its whole
             # trace in and its flags out
             X2 = X.clone()   # capture warms up on real data
-            pipe2 = E.Pipeline(det, N, T, tcal, device=dev)
+            pipe2 = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
             pipe2.capture(X2)
             bufs = [(X, pipe, torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory()),
                     (X2, pipe2, torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory())]
@@ -797,6 +800,9 @@ def run_windows(args, rank, world, local_rank):
             w0.record(stream)
             e2e_run(2, w0)
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+                torch.cuda.synchronize()
             e0, e1 = ev(), ev()
             e0.record(stream)
             e2e_run(args.steps, e0)

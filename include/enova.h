@@ -150,10 +150,17 @@ enova_status enova_score_windows(const enova_series *series, const enova_detecto
  * [n_local] (this rank's shard).  comm == NULL: single GPU.  With a comm, all
  * ranks call collectively; integer histograms are all-reduced and score tails
  * all-gathered in rank order, so *out is bit-identical on every rank and for
- * every world size.  n_global_max bounds sum(n_local) over ranks and must be
- * the value the workspace was sized with.  out: host.  Synchronous.
+ * every world size.  Argument / workspace errors are detected per rank before
+ * the first collective: give every rank the same n_global_max (a rank that
+ * returns early leaves the others waiting in a collective, as with NCCL).
+ * n_global_max bounds sum(n_local) over ranks and must be
+ * the value the workspace was sized with: enova_threshold_workspace_bytes
+ * without a comm, enova_threshold_comm_workspace_bytes(.., world) with one.
+ * out: host.  Synchronous.
  * ENOVA_ERR_TOO_FEW_EXCEEDANCES if fewer than 10 scores exceed t. */
 size_t enova_threshold_workspace_bytes(int64_t n_global_max, double init_quantile);
+size_t enova_threshold_comm_workspace_bytes(int64_t n_global_max, double init_quantile,
+                                            int32_t world);
 enova_status enova_fit_threshold(const float *scores, int64_t n_local, int64_t n_global_max,
                                  double init_quantile, double risk_q, enova_comm_t comm,
                                  enova_threshold *out, void *ws, size_t ws_bytes,
@@ -168,6 +175,20 @@ enova_status enova_fit_threshold_async(const float *scores, int64_t n, int64_t n
                                        double init_quantile, double risk_q,
                                        enova_threshold *out_dev, void *ws, size_t ws_bytes,
                                        void *stream);
+
+/* Fleet-wide, stream-ordered variant (§8e): no host synchronisation, so the
+ * whole call -- k_pot phase launches and the NCCL collectives between them
+ * (3 histogram allreduces, an allgather of tail counts, an allgather of
+ * fixed-size fp32 tail slots of capacity ~(1 - init_quantile) * n_global_max
+ * per rank) -- can be captured in a CUDA graph.  n_global: sum of n_local over
+ * the ranks, identical on every rank (e.g. from enova_comm_sum_i64 once at
+ * setup).  out_dev / status as enova_fit_threshold_async; bit-identical to the
+ * single-GPU fit of the rank-ordered concatenation of the shards. */
+enova_status enova_fit_threshold_comm_async(const float *scores, int64_t n_local,
+                                            int64_t n_global, int64_t n_global_max,
+                                            double init_quantile, double risk_q,
+                                            enova_comm_t comm, enova_threshold *out_dev,
+                                            void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------ a-2..a-6 ----
  * Score every window of the series range and flag it ("An anomaly is
@@ -313,6 +334,14 @@ enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels
 enova_status enova_comm_unique_id(void *out128);
 enova_status enova_comm_create(enova_comm_t *comm, int rank, int world, const void *id128,
                                int device);
+/* In-process communicator: comms[0..world) are `world` ranks that live in ONE
+ * process on `device`, each driven by its own host thread (collectives
+ * rendezvous on the host and are ordered across the ranks' streams with
+ * events).  Runs the multi-rank threshold path on one GPU; not graph-capturable.
+ * world <= 16.  Destroy every handle with enova_comm_destroy. */
+enova_status enova_comm_create_local(enova_comm_t *comms, int world, int device);
+/* Synchronous sum of one int64 over the ranks (setup-time helper). */
+enova_status enova_comm_sum_i64(enova_comm_t comm, int64_t in, int64_t *out, void *stream);
 void enova_comm_destroy(enova_comm_t comm);
 
 /* ------------------------------------------------------------- misc ---- */

@@ -30,6 +30,8 @@ EXPORTS = (
     "enova_stream_push", "enova_stream_detect", "enova_point_adjusted_counts",
     "enova_select_flagged_scratch_bytes", "enova_select_flagged", "enova_explain_windows",
     "enova_spot_update", "enova_spot_refit", "enova_stream_step",
+    "enova_threshold_comm_workspace_bytes", "enova_fit_threshold_comm_async",
+    "enova_comm_create_local", "enova_comm_sum_i64",
 )
 
 
@@ -111,6 +113,11 @@ def lib() -> C.CDLL:
             "enova_comm_unique_id": (C.c_int, [vp]),
             "enova_comm_create": (C.c_int, [P(vp), C.c_int, C.c_int, vp, C.c_int]),
             "enova_comm_destroy": (None, [vp]),
+            "enova_comm_create_local": (C.c_int, [P(vp), C.c_int, C.c_int]),
+            "enova_comm_sum_i64": (C.c_int, [vp, i64, P(i64), vp]),
+            "enova_threshold_comm_workspace_bytes": (sz, [i64, dbl, i32]),
+            "enova_fit_threshold_comm_async": (C.c_int, [vp, i64, i64, i64, dbl, dbl, vp, vp, vp,
+                                                         sz, vp]),
             "enova_status_string": (C.c_char_p, [C.c_int]),
             "enova_last_error": (C.c_char_p, []),
             "enova_abi_version": (C.c_int, []),

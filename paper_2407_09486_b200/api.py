@@ -144,13 +144,20 @@ def score_windows(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tens
 
 
 class ThresholdWorkspace:
-    """Scratch for enova_fit_threshold, sized for up to n_global_max scores."""
+    """Scratch for enova_fit_threshold*, sized for up to n_global_max scores; with a
+    communicator of `world` ranks it also holds the gathered tail slots."""
 
-    def __init__(self, n_global_max: int, init_quantile: float = 0.98, device=None):
+    def __init__(self, n_global_max: int, init_quantile: float = 0.98, device=None,
+                 world: int = 0):
         self.n_global_max = int(n_global_max)
         self.init_quantile = float(init_quantile)
-        self.nbytes = int(lib().enova_threshold_workspace_bytes(self.n_global_max,
-                                                                self.init_quantile))
+        self.world = int(world)
+        if self.world > 0:
+            self.nbytes = int(lib().enova_threshold_comm_workspace_bytes(
+                self.n_global_max, self.init_quantile, self.world))
+        else:
+            self.nbytes = int(lib().enova_threshold_workspace_bytes(self.n_global_max,
+                                                                    self.init_quantile))
         self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device or "cuda")
 
 
@@ -164,9 +171,14 @@ def fit_threshold(scores: torch.Tensor, init_quantile: float = 0.98, risk_q: flo
         flat = flat.contiguous()
     n_local = flat.numel()
     if workspace is None:
-        nmax = int(n_global_max if n_global_max is not None else
-                   n_local * (comm.world if comm is not None else 1))
-        workspace = ThresholdWorkspace(nmax, init_quantile, scores.device)
+        if n_global_max is not None:
+            nmax = int(n_global_max)
+        elif comm is not None:   # every rank must size for the same total (collective)
+            nmax = comm.sum_i64(n_local, stream=stream)
+        else:
+            nmax = n_local
+        workspace = ThresholdWorkspace(max(nmax, 1), init_quantile, scores.device,
+                                       world=comm.world if comm is not None else 0)
     out = Threshold()
     check(lib().enova_fit_threshold(C.c_void_p(flat.data_ptr()), n_local, workspace.n_global_max,
                                     float(init_quantile), float(risk_q),
@@ -197,6 +209,29 @@ def fit_threshold_async(scores: torch.Tensor, init_quantile: float = 0.98, risk_
         C.c_void_p(flat.data_ptr()), n, workspace.n_global_max, float(init_quantile),
         float(risk_q), C.c_void_p(thr.data_ptr()), C.c_void_p(workspace.buf.data_ptr()),
         workspace.nbytes, _stream_ptr(stream)))
+    return thr
+
+
+def fit_threshold_comm_async(scores: torch.Tensor, n_global: int, comm: "Comm",
+                             init_quantile: float = 0.98, risk_q: float = 1e-3, *,
+                             workspace: ThresholdWorkspace | None = None, out=None,
+                             stream=None) -> torch.Tensor:
+    """a-7..a-9 across the ranks of `comm`, stream-ordered (no host sync; with
+    NCCL it can be captured in a CUDA graph).  n_global: the total score count
+    over all ranks (Comm.sum_i64 once at setup).  Returns the DEVICE
+    enova_threshold (identical on every rank)."""
+    _require_cuda(scores, "scores")
+    flat = scores.reshape(-1)
+    if not flat.is_contiguous():
+        flat = flat.contiguous()
+    if workspace is None:
+        workspace = ThresholdWorkspace(n_global, init_quantile, scores.device, world=comm.world)
+    thr = out if out is not None else torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8,
+                                                  device=scores.device)
+    check(lib().enova_fit_threshold_comm_async(
+        C.c_void_p(flat.data_ptr()), flat.numel(), int(n_global), workspace.n_global_max,
+        float(init_quantile), float(risk_q), C.c_void_p(comm.handle), C.c_void_p(thr.data_ptr()),
+        C.c_void_p(workspace.buf.data_ptr()), workspace.nbytes, _stream_ptr(stream)))
     return thr
 
 
@@ -462,10 +497,25 @@ def point_adjusted_f1(labels: torch.Tensor, flags: torch.Tensor, t_begin: int, c
 
 
 class Comm:
-    """NCCL communicator for the fleet-wide threshold (one per rank)."""
+    """Communicator for the fleet-wide threshold (one per rank): NCCL (one process
+    per GPU, `create`) or in-process (`create_local`: `world` ranks driven by host
+    threads of one process on one GPU -- runs the multi-rank path on one device)."""
 
-    def __init__(self, handle: int, rank: int, world: int):
-        self.handle, self.rank, self.world = handle, rank, world
+    def __init__(self, handle: int, rank: int, world: int, local: bool = False):
+        self.handle, self.rank, self.world, self.local = handle, rank, world, local
+
+    @staticmethod
+    def create_local(world: int, device: int = 0) -> "list[Comm]":
+        hs = (C.c_void_p * world)()
+        check(lib().enova_comm_create_local(hs, int(world), int(device)))
+        return [Comm(hs[r], r, world, local=True) for r in range(world)]
+
+    def sum_i64(self, value: int, stream=None) -> int:
+        """Synchronous sum of one integer over the ranks (collective)."""
+        out = C.c_int64()
+        check(lib().enova_comm_sum_i64(C.c_void_p(self.handle), int(value), C.byref(out),
+                                       _stream_ptr(stream)))
+        return int(out.value)
 
     @staticmethod
     def unique_id(rank: int, world: int, group=None) -> bytes:
@@ -532,8 +582,11 @@ class Pipeline:
     `capture` records it into a CUDA graph that `replay` relaunches (one graph
     launch per step); `result` synchronises and checks the device statuses.
     With a communicator (fleet sharded over ranks) the threshold is the
-    collective enova_fit_threshold, which synchronises: such a step is enqueued
-    eagerly and cannot be captured."""
+    collective, stream-ordered enova_fit_threshold_comm_async: still no host
+    synchronisation, and with NCCL the step (collectives included) is captured
+    into the graph too; an in-process communicator's step is enqueued eagerly
+    (one host thread per rank).  Construction with a communicator is collective
+    (the global calibration score count is summed once)."""
 
     def __init__(self, det: PreparedDetector, n_instances: int, n_steps: int, t_cal_end: int,
                  init_quantile: float = 0.98, risk_q: float = 1e-3, return_scores: bool = True,
@@ -553,9 +606,12 @@ class Pipeline:
         self.md = torch.empty((N, T - tcal), dtype=torch.float32, device=dev) if return_scores else None
         self.stats_ws = StatsWorkspace(N, M, dev)
         self.comm = comm
-        world = comm.world if comm is not None else 1
-        self.thr_ws = ThresholdWorkspace(max(self.cal.numel(), 1) * world, self.q0, dev)
-        self.thr_host = None
+        if comm is not None:
+            self.n_global = comm.sum_i64(self.cal.numel())
+            self.thr_ws = ThresholdWorkspace(max(self.n_global, 1), self.q0, dev, world=comm.world)
+        else:
+            self.n_global = self.cal.numel()
+            self.thr_ws = ThresholdWorkspace(max(self.cal.numel(), 1), self.q0, dev)
         self.graph = None
         self._graph_input = None
 
@@ -568,21 +624,18 @@ class Pipeline:
         score_windows(metrics, self.det, self.mean, self.std, W - 1, self.tcal, with_md=False,
                       out=(self.cal, None), stream=stream)
         if self.comm is not None:
-            self.thr_host = fit_threshold(self.cal, self.q0, self.q, comm=self.comm,
-                                          workspace=self.thr_ws, stream=stream)
-            detect(metrics, self.det, self.mean, self.std, self.thr_host, self.tcal, self.T,
-                   return_scores=self.scores is not None,
-                   out=(self.flags, self.scores, self.md), stream=stream)
-            return
-        fit_threshold_async(self.cal, self.q0, self.q, workspace=self.thr_ws, out=self.thr,
-                            stream=stream)
+            fit_threshold_comm_async(self.cal, self.n_global, self.comm, self.q0, self.q,
+                                     workspace=self.thr_ws, out=self.thr, stream=stream)
+        else:
+            fit_threshold_async(self.cal, self.q0, self.q, workspace=self.thr_ws, out=self.thr,
+                                stream=stream)
         detect_async(metrics, self.det, self.mean, self.std, self.thr, self.tcal, self.T,
                      out=(self.flags, self.scores, self.md), stream=stream)
 
     def capture(self, metrics: torch.Tensor):
         """Record one step on `metrics` (a fixed device buffer) into a CUDA graph."""
-        if self.comm is not None:
-            raise RuntimeError("a step with a communicator synchronises; it cannot be captured")
+        if self.comm is not None and self.comm.local:
+            raise RuntimeError("an in-process communicator's collectives cannot be captured")
         side = torch.cuda.Stream(device=metrics.device)
         side.wait_stream(torch.cuda.current_stream(metrics.device))
         with torch.cuda.stream(side):
@@ -601,6 +654,6 @@ class Pipeline:
 
     def result(self) -> PipelineResult:
         nd = check_stats_diag(self.diag)
-        thr = self.thr_host if self.comm is not None else threshold_from_device(self.thr)
+        thr = threshold_from_device(self.thr)
         return PipelineResult(self.mean, self.std, nd, self.cal, thr, self.flags, self.scores,
                               self.md)

@@ -41,6 +41,7 @@ constexpr int kBins = 2048;
 constexpr int kPotThreads = 512;   // select_digit covers 2048 bins as 512 threads x 4
 constexpr int kPotWarps = kPotThreads / 32;
 constexpr int kMaxCtas = 256;
+constexpr int kMaxWorld = 256;        // ranks of one communicator (fleet threshold)
 constexpr int kMaxPts = 128;
 constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
@@ -88,11 +89,15 @@ struct FitState {
 };
 
 struct ThrLayout {
-  size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yall, header, total;
+  size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yslot, outdev, yall, header, total;
   int64_t cap;
 };
 
-static inline ThrLayout thr_layout(int64_t n_max, double q0) {
+// world == 0: single-GPU layout.  world >= 1 (communicator): this rank's tail as
+// fp32 scores (ylocal, cap), the all-gathered fixed-size slots of every rank
+// (yslot, world x cap fp32: a rank never holds more than the global tail, so the
+// gather needs no host-side counts), and a device copy of the result.
+static inline ThrLayout thr_layout(int64_t n_max, double q0, int world = 0) {
   ThrLayout L;
   size_t o = 0;
   auto take = [&](size_t b) { size_t r = o; o += (b + 255) / 256 * 256; return r; };
@@ -107,8 +112,10 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0) {
   L.counts = take(kMaxCtas * 8);
   L.part = take((size_t)2 * kSums * kMaxPts * kMaxCtas * 8);
   L.nbuf = take(16);
-  L.counts_all = take(1024 * 8);
-  L.ylocal = take((size_t)L.cap * 8);
+  L.counts_all = take(kMaxWorld * 8);
+  L.ylocal = take(world ? (size_t)L.cap * 4 : 0);
+  L.yslot = take((size_t)world * (size_t)L.cap * 4);
+  L.outdev = take(world ? sizeof(enova_threshold) : 0);
   L.yall = take((size_t)L.cap * 8);
   L.total = o;
   return L;
@@ -124,8 +131,12 @@ struct PotArgs {
   unsigned long long *hist; // [3][kBins]
   long long *counts;        // [gridDim.x]
   double *part;             // [2][kSums][kMaxPts][kMaxCtas]
-  double *ydst;             // compaction target (this rank's tail)
+  double *ydst;             // single GPU: compaction target Y = s - t (the fit's tail)
   const double *yfit;       // tail the fit runs on (all ranks, rank order)
+  float *ylocal;            // communicator: compaction target (raw scores > t), else null
+  const float *yslot;       // communicator: gathered [world][cap] slots, else null
+  const long long *counts_all;   // communicator: gathered per-rank tail counts
+  int world;
   int64_t cap;
   int first, last;          // phase range of this launch
   enova_threshold *out_dev; // optional device copy of the result
@@ -423,7 +434,10 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (ok[u][e] && v[u][e] > t) {
-          if (o < a.cap) a.ydst[o] = (double)v[u][e] - td;
+          if (o < a.cap) {
+            if (a.ylocal) a.ylocal[o] = v[u][e];
+            else a.ydst[o] = (double)v[u][e] - td;
+          }
           ++o;
         }
       off_u += all;
@@ -870,11 +884,47 @@ struct FitShared {
   double red[kSums][kMaxPts];    // grid totals after the barrier
 };
 
-__device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch) {
+// Communicator path: the fit's Y is every rank's tail in rank order -- the
+// order a single GPU's stable compaction of the concatenated scores produces,
+// so the threshold is bit-identical for every world size -- built from the
+// gathered fixed-size slots.  Every CTA derives the rank offsets itself and
+// writes exactly the slice [c0, c1) that fit() assigns it: no grid barrier.
+// Returns N_t (> cap if any rank overflowed its slot: ENOVA_ERR_WORKSPACE).
+__device__ int64_t pack_tails(const PotArgs &a, long long *s_off) {
+  if (threadIdx.x == 0) {
+    long long o = 0;
+    bool bad = false;
+    for (int r = 0; r < a.world; ++r) {
+      const long long c = *(volatile const long long *)(a.counts_all + r);
+      s_off[r] = o;
+      bad = bad || c > a.cap || c < 0;
+      o += bad ? 0 : c;
+    }
+    s_off[a.world] = (bad || o > a.cap) ? a.cap + 1 : o;
+  }
+  __syncthreads();
+  const int64_t nt = s_off[a.world];
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.g->nt_fit = nt;
+  if (nt < 10 || nt > a.cap) return nt;
+  const int nb = gridDim.x;
+  const int64_t chunk = (nt + nb - 1) / nb;
+  const int64_t c0 = min(nt, (int64_t)blockIdx.x * chunk), c1 = min(nt, c0 + chunk);
+  const double td = (double)*(volatile float *)&a.g->t;
+  double *Y = const_cast<double *>(a.yfit);
+  for (int r = 0; r < a.world; ++r) {
+    const int64_t lo = max(c0, (int64_t)s_off[r]), hi = min(c1, (int64_t)s_off[r + 1]);
+    const float *src = a.yslot + (size_t)r * (size_t)a.cap;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      Y[i] = (double)src[i - s_off[r]] - td;
+  }
+  __syncthreads();
+  return nt;
+}
+
+__device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const int64_t nt) {
   FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
-  const int64_t nt = *(volatile long long *)&a.g->nt_fit;
   if (nt < 10 || nt > a.cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       a.g->status = (nt < 10) ? ENOVA_ERR_TOO_FEW_EXCEEDANCES : ENOVA_ERR_WORKSPACE;
@@ -1078,6 +1128,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   __shared__ long long cta_base[2];
   __shared__ int wcnt[4 * kPotWarps];
   __shared__ int above;
+  __shared__ long long s_off[kMaxWorld + 1];
   PotGlobal *g = a.g;
   unsigned int epoch = 0;   // grid barriers passed in this launch
   bool spot_skip = false;
@@ -1131,7 +1182,11 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       // SPOT refit with no peak added since the last fit: the model is unchanged
       // (the cited Algorithm 1 refits only when a peak arrives) -- keep the threshold
       spot_skip = a.n_dev && *(volatile long long *)&g->nt_fit == *(volatile long long *)&g->nt_refit;
-      if (!spot_skip) fit(a, sh.fit, epoch);
+      if (!spot_skip) {
+        const int64_t nt = a.yslot ? pack_tails(a, s_off)
+                                   : (int64_t)*(volatile long long *)&g->nt_fit;
+        fit(a, sh.fit, epoch, nt);
+      }
     }
   }
   stamp(g);
@@ -1214,8 +1269,12 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.hist = reinterpret_cast<unsigned long long *>(b + L.hist);
   a.counts = reinterpret_cast<long long *>(b + L.counts);
   a.part = reinterpret_cast<double *>(b + L.part);
-  a.ydst = reinterpret_cast<double *>(b + (comm ? L.ylocal : L.yall));
+  a.ydst = reinterpret_cast<double *>(b + L.yall);
   a.yfit = reinterpret_cast<const double *>(b + L.yall);
+  a.ylocal = comm ? reinterpret_cast<float *>(b + L.ylocal) : nullptr;
+  a.yslot = comm ? reinterpret_cast<const float *>(b + L.yslot) : nullptr;
+  a.counts_all = comm ? reinterpret_cast<const long long *>(b + L.counts_all) : nullptr;
+  a.world = 0;
   a.cap = L.cap;
   a.first = P_HIST0;
   a.last = P_FIT;
@@ -1252,79 +1311,99 @@ static enova_status status_error(int st) {
   return (enova_status)st;
 }
 
-// Host syncs: single GPU one (the result).  With a communicator two more
-// (global n; tail counts for the rank-ordered allgatherv).
+static enova_status launch_pot_comm(const PotArgs &a, int nb, cudaStream_t st, bool reset,
+                                    enova_comm_t comm) {
+  enova_status r = comm_coop_begin(comm, st);
+  if (r) return r;
+  r = launch_pot(a, nb, st, reset);
+  const enova_status r2 = comm_coop_end(comm, st);
+  return r ? r : r2;
+}
+
+// Communicator path, stream-ordered and free of host synchronisation (so it can
+// be captured in a CUDA graph with the NCCL calls): the phases of k_pot run as
+// separate cooperative launches with the collectives between them --
+//   HIST0 | allreduce h0 | HIST1 | allreduce h1 | HIST2 | allreduce h2 | COMPACT |
+//   allgather tail counts + allgather fixed-size tail slots | FIT (pack + fit).
+// n: the global score count (sum of n_local over ranks, same on every rank).
+enova_status fit_threshold_comm_async(const float *scores, int64_t n_local, int64_t n, double q0,
+                                      double q, enova_comm_t comm, enova_threshold *out_dev,
+                                      void *ws, size_t ws_bytes, int64_t n_global_max,
+                                      cudaStream_t st) {
+  char *b = static_cast<char *>(ws);
+  if (comm->world > kMaxWorld) {
+    set_error("communicator larger than 256 ranks");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  const ThrLayout L = thr_layout(n_global_max, q0, comm->world);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small (size it with the communicator's world size)");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = check_k(n, q0);
+  if (r) return r;
+  if (n > n_global_max || n_local > n) {
+    set_error("total score count exceeds n_global_max used to size the workspace");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  PotArgs a = make_args(scores, n_local, n, q0, q, b, L, true);
+  a.world = comm->world;
+  const int nb = pot_grid();
+  ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, L.header, st));
+  for (int p = P_HIST0; p <= P_HIST2; ++p) {
+    a.first = a.last = p;
+    if ((r = launch_pot_comm(a, nb, st, p > P_HIST0, comm))) return r;
+    r = comm_allreduce_u64_sum(comm, a.hist + (size_t)p * kBins, a.hist + (size_t)p * kBins,
+                               (size_t)kBins, st);
+    if (r) return r;
+  }
+  a.first = a.last = P_COMPACT;
+  if ((r = launch_pot_comm(a, nb, st, true, comm))) return r;
+  r = comm_allgather_i64(comm, &a.g->nt_local, b + L.counts_all, st);
+  if (r) return r;
+  r = comm_allgather_f32(comm, a.ylocal, b + L.yslot, (size_t)L.cap, st);
+  if (r) return r;
+  a.first = a.last = P_FIT;
+  a.out_dev = out_dev;
+  return launch_pot_comm(a, nb, st, true, comm);
+}
+
+// Host syncs: single GPU one (the result).  With a communicator one more (the
+// global score count, all-reduced) before the stream-ordered path above.
 enova_status fit_threshold(const float *scores, int64_t n_local, double q0, double q,
                            enova_comm_t comm, enova_threshold *out, void *ws, size_t ws_bytes,
                            int64_t n_global_max, cudaStream_t st) {
   char *b = static_cast<char *>(ws);
-  const ThrLayout L = thr_layout(n_global_max, q0);
+  const ThrLayout L = thr_layout(n_global_max, q0, comm ? comm->world : 0);
   if (ws_bytes < L.total) {
-    set_error("threshold workspace too small");
+    set_error(comm ? "threshold workspace too small (size it with the communicator's world size)"
+                   : "threshold workspace too small");
     return ENOVA_ERR_WORKSPACE;
   }
-  unsigned long long *nbuf = reinterpret_cast<unsigned long long *>(b + L.nbuf);
-  long long *counts_all = reinterpret_cast<long long *>(b + L.counts_all);
-
-  int64_t n = n_local;
+  enova_status r;
   if (comm) {
-    unsigned long long hn = (unsigned long long)n_local;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(nbuf, &hn, 8, cudaMemcpyHostToDevice, st));
-    enova_status s = comm_allreduce_u64_sum(comm, nbuf, nbuf, 1, st);
-    if (s) return s;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(&hn, nbuf, 8, cudaMemcpyDeviceToHost, st));
+    int64_t n = 0;
+    if ((r = comm_sum_i64_sync(comm, n_local, &n, b + L.nbuf, st))) return r;
+    enova_threshold *od = reinterpret_cast<enova_threshold *>(b + L.outdev);
+    if ((r = fit_threshold_comm_async(scores, n_local, n, q0, q, comm, od, ws, ws_bytes,
+                                      n_global_max, st)))
+      return r;
+    ENOVA_CUDA_TRY(cudaMemcpyAsync(out, od, sizeof(*out), cudaMemcpyDeviceToHost, st));
     ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-    n = (int64_t)hn;
+    if ((r = status_error(out->reserved))) return r;
+    out->reserved = 0;
+    return ENOVA_OK;
   }
-  enova_status r = check_k(n, q0);
+  const int64_t n = n_local;
+  r = check_k(n, q0);
   if (r) return r;
   if (n > n_global_max) {
     set_error("total score count exceeds n_global_max used to size the workspace");
     return ENOVA_ERR_WORKSPACE;
   }
-  PotArgs a = make_args(scores, n_local, n, q0, q, b, L, comm != nullptr);
-  const int nb = pot_grid();
+  PotArgs a = make_args(scores, n_local, n, q0, q, b, L, false);
   ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, L.header, st));
-  if (!comm) {
-    if ((r = launch_pot(a, nb, st))) return r;
-  } else {
-    for (int p = P_HIST0; p <= P_HIST2; ++p) {
-      a.first = a.last = p;
-      if ((r = launch_pot(a, nb, st, p > P_HIST0))) return r;
-      r = comm_allreduce_u64_sum(comm, a.hist + (size_t)p * kBins, a.hist + (size_t)p * kBins,
-                                 (size_t)kBins, st);
-      if (r) return r;
-    }
-    a.first = a.last = P_COMPACT;
-    if ((r = launch_pot(a, nb, st, true))) return r;
-    r = comm_allgather_i64(comm, &a.g->nt_local, counts_all, st);
-    if (r) return r;
-    std::vector<int64_t> hc(comm->world), off(comm->world);
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts_all, 8 * comm->world,
-                                   cudaMemcpyDeviceToHost, st));
-    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
-    int64_t tot = 0;
-    for (int rk = 0; rk < comm->world; ++rk) {
-      off[rk] = tot;
-      if (hc[rk] > L.cap) {
-        set_error("peak count exceeds workspace capacity");
-        return ENOVA_ERR_WORKSPACE;
-      }
-      tot += hc[rk];
-    }
-    if (tot > L.cap) {
-      set_error("peak count exceeds workspace capacity");
-      return ENOVA_ERR_WORKSPACE;
-    }
-    r = comm_allgatherv_f64(comm, a.ydst, const_cast<double *>(a.yfit), hc.data(), off.data(),
-                            st);
-    if (r) return r;
-    long long tl = tot;
-    ENOVA_CUDA_TRY(cudaMemcpyAsync(&a.g->nt_fit, &tl, 8, cudaMemcpyHostToDevice, st));
-    ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->status, 0, sizeof(int), st));
-    a.first = a.last = P_FIT;
-    if ((r = launch_pot(a, nb, st, true))) return r;
-  }
+  if ((r = launch_pot(a, pot_grid(), st))) return r;
   PotGlobal hg;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&hg, a.g, sizeof(hg), cudaMemcpyDeviceToHost, st));
   ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1365,7 +1444,9 @@ enova_status fit_threshold_async(const float *scores, int64_t n, double q0, doub
   return launch_pot(a, pot_grid(), st);
 }
 
-size_t threshold_workspace_bytes(int64_t n_max, double q0) { return thr_layout(n_max, q0).total; }
+size_t threshold_workspace_bytes(int64_t n_max, double q0, int world) {
+  return thr_layout(n_max, q0, world).total;
+}
 
 // diagnostic: byte offsets of PotGlobal.n_stamps / .stamps in the threshold workspace
 void pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {

@@ -63,7 +63,10 @@ def test_workspace_sizing_and_envelope(L):
     a = L.enova_threshold_workspace_bytes(10**8, 0.98)
     b = L.enova_threshold_workspace_bytes(10**6, 0.98)
     assert a > b > 0
-    assert a >= 2 * 8 * int(0.02 * 10**8)        # local + gathered fp64 tails
+    assert a >= 8 * int(0.02 * 10**8)            # the fp64 tail the fit runs on
+    for w in (1, 2, 8):                              # + this rank's fp32 tail + w gathered slots
+        c = L.enova_threshold_comm_workspace_bytes(10**8, 0.98, w)
+        assert c >= a + 4 * int(0.02 * 10**8) * (w + 1)
 
 
 def test_validation_before_any_launch(L):
