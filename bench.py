@@ -236,7 +236,7 @@ def run_streaming(args, rank, world, local_rank):
     hist = X[:, :t_hist]
     mean, std, _ = E.compute_stats(hist, t_hist)
     cal, _ = E.score_windows(hist, det, mean, std, W - 1, t_hist, with_md=False)
-    thr = E.fit_threshold(cal, comm=comm, n_global_max=cal.numel() * world)
+    thr = E.fit_threshold(cal, comm=comm)   # workspace sized for the summed count
     thr_dev = E.threshold_to_device(thr, dev)
     # samples of the streamed ticks, [tick][instance][metric]
     S = X[:, t_hist:].transpose(0, 1).contiguous()
@@ -408,7 +408,8 @@ def run_threshold_sweep(args, rank, world, local_rank):
     """c5: the fleet-wide POT threshold of 100M calibration
     scores; strong scaling (rank r holds a contiguous shard).  One GPU: the
     stream-ordered fit (one cooperative kernel) replayed as a CUDA graph; N > 1:
-    the collective fit (histogram all-reduce + rank-ordered tail gather)."""
+    the collective fit (histogram all-reduces + fixed-slot tail gather), also
+    stream-ordered and replayed as a graph."""
     import torch
     import torch.distributed as dist
 
@@ -423,30 +424,29 @@ def run_threshold_sweep(args, rank, world, local_rank):
     sh = synth.score_mixture(n, offset=a)
     sh_pinned = torch.from_numpy(sh).pin_memory()
     scores = sh_pinned.to(dev)
-    comm = E.Comm.create(rank, world, local_rank) if world > 1 else None
-    ws = E.ThresholdWorkspace(n_total, 0.98, dev)
+    force_comm = os.environ.get("ENOVA_BENCH_COMM") == "1"   # diagnostic, as in run_windows
+    comm = E.Comm.create(rank, world, local_rank) if (world > 1 or force_comm) else None
+    ws = E.ThresholdWorkspace(n_total, 0.98, dev, world=world if comm is not None else 0)
     thr_dev = torch.zeros(E.api.THRESHOLD_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
-    l0 = _lib.lib().enova_kernel_launches()
-    if world == 1:
-        E.fit_threshold_async(scores, workspace=ws, out=thr_dev)
-        torch.cuda.synchronize()
-        per = _lib.lib().enova_kernel_launches() - l0
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(stream)
-        with torch.cuda.graph(g, stream=side):
-            E.fit_threshold_async(scores, workspace=ws, out=thr_dev)
-        stream.wait_stream(side)
-        step = g.replay
-    else:
-        holder = {}
 
-        def step():
-            holder["thr"] = E.fit_threshold(scores, comm=comm, n_global_max=n_total, workspace=ws)
-        step()
-        per = _lib.lib().enova_kernel_launches() - l0
+    def enqueue():
+        if comm is None:
+            E.fit_threshold_async(scores, workspace=ws, out=thr_dev)
+        else:   # stream-ordered collective fit: captured with its NCCL calls
+            E.fit_threshold_comm_async(scores, n_total, comm, workspace=ws, out=thr_dev)
+    l0 = _lib.lib().enova_kernel_launches()
+    enqueue()
+    torch.cuda.synchronize()
+    per = _lib.lib().enova_kernel_launches() - l0
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(stream)
+    with torch.cuda.graph(g, stream=side):
+        enqueue()
+    stream.wait_stream(side)
+    step = g.replay
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -461,12 +461,12 @@ def run_threshold_sweep(args, rank, world, local_rank):
         torch.cuda.synchronize()
     step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
     tot = max_over_ranks(float(sum(step_ms)))
-    thr = E.threshold_from_device(thr_dev) if world == 1 else holder["thr"]
+    thr = E.threshold_from_device(thr_dev)
     value = n_total * args.steps / (tot * 1e-3)
     # phase split of one k_pot launch from its %globaltimer stamps (CTA 0):
     # [0] radix pass 0 ... [3] compaction, [5] fit start, [-1] end
     phases = None
-    if world == 1:
+    if comm is None:
         import ctypes as C
         step()
         torch.cuda.synchronize()
