@@ -56,9 +56,3 @@ for it in range(8, 16):
     a = t[0]; r = a[256 + it]
     f = lambda v: f"{(v - t0) / 1e3:6.2f}"
     print(f"  {it:4d} | {f(a[it,0])} {f(a[it,1])} {f(a[it,2])} {f(a[it,3])} {f(a[it,4])} {f(a[it,5])} | {f(r[0])} {f(r[1])} {f(r[2])} | {f(a[it,7])} {f(a[it,8])} | {f(a[it,11])} {f(a[it,12])} | {f(a[it,9])} {f(a[it,10])}")
-print("epilogue detail (CTA0), us rel. to tile-10 MMA start:")
-print("  tile | E2 start(hf) tmem-ld-done stores-done bar2-done | E3 start(df) first-ld-done loop-done done")
-for it in range(8, 16):
-    a = t[0]; r = a[256 + it]
-    f = lambda v: f"{(v - t0) / 1e3:7.2f}"
-    print(f"  {it:4d} | {f(a[it,11])} {f(r[3])} {f(r[4])} {f(r[5])} | {f(a[it,9])} {f(r[6])} {f(r[7])} {f(a[it,10])}")
