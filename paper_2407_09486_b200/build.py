@@ -39,12 +39,18 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
                      + glob.glob(os.path.join(INCLUDE, "*.h")))
+    # extra nvcc flags (diagnostic builds, e.g. -DENOVA_PAIR_TRACE); a change of
+    # them rebuilds every object
+    extra = os.environ.get("ENOVA_NVCC_FLAGS", "").split()
+    stamp = os.path.join(BUILD, "flags.txt")
+    prev = open(stamp).read() if os.path.exists(stamp) else ""
+    force = prev != " ".join(extra)
     objs = []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
-        if _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+        if force or _stale(o, [s] + headers):
+            cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             if verbose:
@@ -54,6 +60,8 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed on {os.path.basename(s)}")
+    with open(stamp, "w") as f:
+        f.write(" ".join(extra))
     if _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)

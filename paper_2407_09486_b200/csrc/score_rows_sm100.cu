@@ -151,12 +151,17 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
                                               const float *xsum = nullptr,
                                               const float *bbarm = nullptr, float *md_metric = nullptr,
                                               int M = 0, int W = 0) {
-  auto stamp = [&](int slot) {
+  auto stamp = [&](int slot) {   // diagnostic; compiled in with -DENOVA_TRACE only
+#ifdef ENOVA_TRACE
     if (tr && r == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       tr[slot] = t;
     }
+#else
+    (void)slot;
+    (void)tr;
+#endif
   };
     // ---- E1: h = tanh(acc) -> hi/lo fp16 A images; re-arm acc with b3 ----
     const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
@@ -869,12 +874,17 @@ __global__ void __launch_bounds__(kSThreads, 1)
   const int W = p.W;
   const int woff = (int)((p.tick + 1) % W);   // oldest sample's slot of the window ending at tick
   unsigned long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;
-  auto stamp = [&](int slot) {
+  auto stamp = [&](int slot) {   // diagnostic; compiled in with -DENOVA_TRACE only
+#ifdef ENOVA_TRACE
     if (tr) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       tr[slot] = t;
     }
+#else
+    (void)slot;
+    (void)tr;
+#endif
   };
   if (tid == 0) stamp(0);
 

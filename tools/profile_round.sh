@@ -21,5 +21,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_st
 ./tools/ubench_mma > gpurun_out/ubench_mma.txt 2>&1 || true
 python tools/pot_phases.py --c5 > gpurun_out/pot_phases.txt 2>&1
 python tools/trace_pair.py > gpurun_out/trace_pair.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" >> gpurun_out/build.log 2>&1   # back to the untraced build
 python tools/trace_stream.py > gpurun_out/trace_stream.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" >> gpurun_out/build.log 2>&1
 cat gpurun_out/bench.jsonl

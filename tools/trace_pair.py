@@ -1,10 +1,14 @@
 """Pipeline timeline of the CTA-pair scorer (CTA pair 0, %globaltimer ns).
-Diagnostic only."""
+Diagnostic only: rebuilds libenova.so with -DENOVA_TRACE (the stamps are
+compiled out of the default build); rebuild without it afterwards."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-import paper_2407_09486_b200 as E
-from paper_2407_09486_b200 import _lib, synth
+os.environ["ENOVA_NVCC_FLAGS"] = "-DENOVA_TRACE"
+from paper_2407_09486_b200 import build as _B  # noqa: E402
+_B.build()
+import paper_2407_09486_b200 as E  # noqa: E402
+from paper_2407_09486_b200 import _lib, synth  # noqa: E402
 cfg = synth.CONFIGS["c2"]
 W, M, H, Z, T, N = cfg["window"], cfg["n_metrics"], cfg["hidden"], cfg["latent"], cfg["n_steps"], cfg["n_instances"]
 X = torch.from_numpy(synth.metric_trace(N, T, M, seed=7)).cuda()

@@ -3,6 +3,9 @@ Diagnostic only (uses enova_internal_set_trace)."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+os.environ["ENOVA_NVCC_FLAGS"] = "-DENOVA_TRACE"   # stamps are compiled out by default
+from paper_2407_09486_b200 import build as _B  # noqa: E402
+_B.build()
 import paper_2407_09486_b200 as E
 from paper_2407_09486_b200 import _lib, synth
 cfg = synth.CONFIGS["c4"]
