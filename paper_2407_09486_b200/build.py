@@ -39,13 +39,13 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
                      + glob.glob(os.path.join(INCLUDE, "*.h")))
-    # extra nvcc flags (diagnostic builds, e.g. -DENOVA_PAIR_TRACE); a change of
+    # extra nvcc flags (diagnostic builds, e.g. -DENOVA_TRACE); a change of
     # them rebuilds every object
     extra = os.environ.get("ENOVA_NVCC_FLAGS", "").split()
     stamp = os.path.join(BUILD, "flags.txt")
     prev = open(stamp).read() if os.path.exists(stamp) else ""
     force = prev != " ".join(extra)
-    objs = []
+    objs, jobs = [], []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
@@ -55,11 +55,20 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0 or verbose or ptxas_v:
-                sys.stderr.write(r.stdout + r.stderr)
-            if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed on {os.path.basename(s)}")
+            jobs.append((s, cmd))
+
+    def run(job):
+        return job[0], subprocess.run(job[1], capture_output=True, text=True)
+
+    # translation units compile concurrently (nvcc is single-threaded per file)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(run, jobs))
+    for s, r in results:
+        if r.returncode != 0 or verbose or ptxas_v:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {os.path.basename(s)}")
     with open(stamp, "w") as f:
         f.write(" ".join(extra))
     if _stale(LIB, objs):
