@@ -193,3 +193,24 @@ def test_nccl_world1_pipeline_graph_matches_single_gpu(E):
     assert res.threshold == r0.threshold
     assert torch.equal(res.flags, r0.flags)
     assert torch.equal(res.scores, r0.scores)
+
+
+def test_local_comm_c2_scale_fleet_threshold(E):
+    # the c2 calibration score vector (256 instances x 4937 windows, the bench's
+    # threshold input size) sharded by instance over 4 ranks: bit-identical
+    cfg = synth.CONFIGS["c2"]
+    n_inst, per = cfg["n_instances"], cfg["n_steps"] // 2 - cfg["window"] + 1
+    s = synth.score_mixture(n_inst * per, seed=21)
+    sd = torch.from_numpy(s).cuda()
+    single = E.fit_threshold(sd, 0.98, 1e-3)
+    world = 4
+    rows = [(r * n_inst // world) * per for r in range(world + 1)]
+    comms = E.Comm.create_local(world, 0)
+    try:
+        res = run_ranks(world, lambda r, st: E.fit_threshold(
+            sd[rows[r]:rows[r + 1]], 0.98, 1e-3, comm=comms[r], stream=st))
+    finally:
+        for c in comms:
+            c.destroy()
+    assert all(x == single for x in res)
+    assert single["n"] == n_inst * per and single["n_peaks"] >= 10
