@@ -11,7 +11,7 @@ from paper_2407_09486_b200 import _lib, synth
 cfg = synth.CONFIGS["c4"]
 W, M, H, Z, N = cfg["window"], cfg["n_metrics"], cfg["hidden"], cfg["latent"], int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else cfg["n_instances"]
 T = 200
-X = torch.from_numpy(synth.metric_trace_parallel(N, T, M, seed=3)).cuda()
+X = torch.from_numpy(synth.metric_trace(N, T, M, seed=3)).cuda()   # serial: no process pool in a script without a main guard
 det = E.PreparedDetector(synth.detector_weights(W, M, H, Z, seed=3))
 mean, std, _ = E.compute_stats(X, T)
 ring = E.StreamRing(det, mean, std)
