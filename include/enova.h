@@ -338,9 +338,12 @@ enova_status enova_comm_create(enova_comm_t *comm, int rank, int world, const vo
  * process on `device`, each driven by its own host thread (collectives
  * rendezvous on the host and are ordered across the ranks' streams with
  * events).  Runs the multi-rank threshold path on one GPU; not graph-capturable.
- * world <= 16.  Destroy every handle with enova_comm_destroy. */
+ * The ranks' grid-synchronising threshold kernels are serialised on the device
+ * (they must never share the SMs).  world <= 16.  Destroy every handle with
+ * enova_comm_destroy. */
 enova_status enova_comm_create_local(enova_comm_t *comms, int world, int device);
-/* Synchronous sum of one int64 over the ranks (setup-time helper). */
+/* Synchronous sum of one int64 over the ranks (collective; setup-time helper:
+ * it allocates and frees 256 B of device scratch, so keep it off the hot path). */
 enova_status enova_comm_sum_i64(enova_comm_t comm, int64_t in, int64_t *out, void *stream);
 void enova_comm_destroy(enova_comm_t comm);
 
