@@ -557,6 +557,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; N > 1 runs under "
+              f"torchrun (one process per GPU) -- measuring world size {world}", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.workload == "c4":
