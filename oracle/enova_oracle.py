@@ -45,7 +45,9 @@ numbers ``S:n``; readings ``R-n`` are listed in DESIGN.md):
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``): SPEC worked examples
 (tests/golden/spec_examples.json), KL closed forms and a quadrature check of
 the Gaussian KL integral, constructed detectors with closed-form outputs
-(zero encoder, mean detector, single-tap selector, perfect-reconstruction MD),
+(zero encoder, mean detector, single-tap selector, perfect-reconstruction MD,
+and a full-path selector detector whose log-variance head Wlv h and decoder
+hidden layer W3 mu are both non-zero),
 window locality, an independent scipy GPD MLE and a brute-force likelihood
 grid for the tail fit, the exp(1) analytic quantile, and order statistics by
 full sort.  Parity unpinned: absolute scores of a *trained* detector (the

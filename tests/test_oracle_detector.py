@@ -198,6 +198,67 @@ def test_md_decoder_column_sum_closed_form():
         assert md[0, r] == pytest.approx(m - math.tanh(0.5) - bm, rel=1e-12, abs=1e-14)
 
 
+def full_path_closed_form(d, xbar, drop_wlv=False, decoder_input="mu"):
+    """Scalar restatement of the full_path_detector's score and MD for a window
+    of mean xbar (written from the selector structure, not from the oracle's
+    matrix code): exercises W1, Wmu, Wlv (lv head) and the decoder's
+    hidden layer W3 fed with mu (R-7)."""
+    Hh, Zz = d["hidden"], d["latent"]
+    D = d["window"] * d["n_metrics"]
+    f = lambda a: float(np.float32(a))
+    h = [math.tanh(f(d["enc_w1"][k, 0]) * D * xbar + f(d["enc_b1"][k])) for k in range(Hh)]
+    mu = [f(d["enc_bmu"][z]) for z in range(Zz)]
+    lv = [f(d["enc_blv"][z]) for z in range(Zz)]
+    mu[0] += 1.5 * h[2]
+    mu[1] += -0.75 * h[5]
+    if not drop_wlv:
+        lv[0] += 0.5 * h[3]
+        lv[2] += -1.25 * h[1]
+    score = 0.5 * sum(mu[z] ** 2 + math.expm1(lv[z]) - lv[z] for z in range(Zz))
+    lat = mu if decoder_input == "mu" else lv
+    a3_4 = math.tanh(0.875 * lat[1] + f(d["dec_b1"][4]))
+    a3_0 = math.tanh(f(d["dec_b1"][0]))
+    bbar = float(np.mean(d["dec_b2"].astype(np.float64)))
+    md = xbar - (0.625 * a3_4 - 0.5 * a3_0) - bbar
+    return score, md
+
+
+@pytest.mark.parametrize("shape", [(32, 8, 32, 4), (16, 16, 64, 8), (8, 8, 128, 16)])
+def test_full_path_detector_closed_form(shape):
+    """Pins the log-variance head (Wlv h, which every other constructed detector
+    zeroes) and the decoder hidden layer W3 fed with mu (not lv, not a sample):
+    dropping Wlv h, swapping mu/lv into the decoder, or transposing a selector
+    changes the closed form."""
+    Wn, Mn, Hn, Zn = shape
+    d = detectors.full_path_detector(Wn, Mn, Hn, Zn)
+    r = np.random.default_rng(21)
+    T = 3 * Wn + 17
+    X = (r.standard_normal((1, T, Mn)) * 0.7).astype(np.float16).astype(np.float32)
+    s, md = O.score_windows(X, d, np.zeros((1, Mn), np.float32), np.ones((1, Mn), np.float32),
+                            Wn - 1, T)
+    for r_, t in enumerate(range(Wn - 1, T)):
+        xbar = float(np.mean(X[0, t - Wn + 1:t + 1, :].astype(np.float64)))
+        es, em = full_path_closed_form(d, xbar)
+        assert s[0, r_] == pytest.approx(es, rel=1e-12, abs=1e-14)
+        assert md[0, r_] == pytest.approx(em, rel=1e-12, abs=1e-14)
+
+
+def test_full_path_detector_distinguishes_plausible_mistakes():
+    """The closed form separates the mistakes the mean/tap/zero detectors cannot:
+    lv = blv (Wlv h dropped) and lv fed to the decoder in place of mu; an oracle
+    without Wlv (run here on the detector with Wlv zeroed) misses the pin."""
+    d = detectors.full_path_detector(32, 8, 32, 4)
+    for xbar in (-1.0, 0.3, 2.0):
+        es, em = full_path_closed_form(d, xbar)
+        assert abs(es - full_path_closed_form(d, xbar, drop_wlv=True)[0]) > 1e-3
+        assert abs(em - full_path_closed_form(d, xbar, decoder_input="lv")[1]) > 1e-3
+    d0 = dict(d)
+    d0["enc_wlv"] = np.zeros_like(d["enc_wlv"])
+    X = np.full((1, 40, 8), 0.5, np.float32)
+    s0, _ = O.score_windows(X, d0, np.zeros((1, 8), np.float32), np.ones((1, 8), np.float32), 31, 40)
+    assert abs(s0[0, 0] - full_path_closed_form(d, 0.5)[0]) > 1e-3
+
+
 def test_window_locality_and_permutation_equivariance():
     wts = synth.detector_weights(W, M, H, Z, seed=1)
     X = synth.metric_trace(3, 200, M, seed=2)
@@ -215,7 +276,7 @@ def test_window_locality_and_permutation_equivariance():
     assert np.array_equal(sp, s0[perm]) and np.array_equal(mp, m0[perm])
 
 
-def test_outlier_scores_above_normals():         # S:513 (10-sigma outlier)
+def test_outlier_scores_above_normals():         # S:514 (10-sigma outlier)
     d = detectors.mean_detector(W, M, H, Z, alpha=1.0, beta=2.0)
     r = np.random.default_rng(10)
     wins = 0
