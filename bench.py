@@ -118,6 +118,57 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+SPEC_F16_TFLOPS = 2250.0    # B200 dense fp16/bf16 spec sheet (B200_PROFILING.md nominal table)
+SPEC_HBM_GBS = 7700.0       # HGX B200 HBM3e spec sheet
+
+
+def measure_traffic(kernel_regex, argv, timeout=240):
+    """DRAM bytes (read + write) of ONE launch of the kernel, measured live with
+    ncu in a subprocess (never timed: the bench numbers come from CUDA events in
+    this process).  Returns (bytes, read, write) or None if ncu is unavailable."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control",
+           "none", "-k", f"regex:{kernel_regex}", "-c", "1", "--csv", sys.executable] + argv
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    except (subprocess.TimeoutExpired, OSError):
+        return None
+    rd = wr = None
+    import csv
+    import io
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    for row in csv.reader(io.StringIO("\n".join(lines))):
+        if len(row) < 3:
+            continue
+        name, unit, val = row[-3], row[-2], row[-1]
+        try:
+            v = float(val.replace(",", ""))
+        except ValueError:
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
+                 "GB": 1e9}.get(unit, 1)
+        if name == "dram__bytes_read.sum":
+            rd = v * scale
+        elif name == "dram__bytes_write.sum":
+            wr = v * scale
+    if rd is None or wr is None:
+        return None
+    return rd + wr, rd, wr
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -183,7 +234,8 @@ def run_reference(args, rank, world):
         "config": {"workload": "c2 sample: 2 instances x T=10000 x M=16, W=64, H=128, Z=16 "
                                "(stats -> calibration scores -> POT -> flags)",
                    "instances": n_inst, "windows_per_step": wins // args.steps},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "cpu_model": cpu_model(),
+                         "kind": "oracle",
                          "sample": f"{n_inst} of 256 c2 instances, full T, whole pipeline"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -313,7 +365,7 @@ def run_streaming(args, rank, world, local_rank):
         for every in (10, 1):
             # fresh SPOT state per run, calibrated on the same calibration scores;
             # capacity for every streamed score to be a peak (no overflow)
-            spot = E.Spot(cal.numel() + 50 * n * ticks, device=dev)
+            spot = E.Spot(cal.numel(), device=dev, stream_peaks=n * ticks)
             spot.calibrate(cal.reshape(-1))
             sgraphs = {}
             side.wait_stream(torch.cuda.current_stream())
@@ -368,10 +420,36 @@ def run_streaming(args, rank, world, local_rank):
             done += n
             k += 1
         el = time.perf_counter() - t0
-        cpu = {"value": done / el, "unit": "windows/s", "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": done / el, "unit": "windows/s", "cores": cpu_cores(),
+               "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{k} ticks x {n} instances ({el:.1f} s)"}
     if comm is not None:
         comm.destroy()
+    # roofline of the one launch per tick (k_stream_rows with the push fused):
+    # algorithmic bytes = the new samples in + score/md/flag out; the kernel also
+    # re-reads every instance's W-sample window from the fp16 ring (2 D B) and
+    # its W sample sums (4 W B) -- reported separately, labelled
+    peaks = load_peaks()
+    tick_s = tot / args.steps * 1e-3
+    algo_b = n * (M * 4 + 4 + 4 + 1)
+    ring_b = n * (2 * W * M + 4 * W)
+    roof = {"kernel": "k_stream_rows (enova_stream_step)", "bound": "hbm",
+            "achieved": algo_b / tick_s / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": algo_b / tick_s / 1e9 / peaks["hbm"], "traffic": None,
+            "algorithmic_bytes_per_launch": algo_b,
+            "with_ring_reread": {"bytes_per_launch": algo_b + ring_b,
+                                 "achieved": (algo_b + ring_b) / tick_s / 1e9,
+                                 "frac": (algo_b + ring_b) / tick_s / 1e9 / peaks["hbm"],
+                                 "frac_spec": (algo_b + ring_b) / tick_s / 1e9 / SPEC_HBM_GBS,
+                                 "note": "the window of every instance re-read from the fp16 "
+                                         "ring (2*D B) plus its W sample sums (4*W B)"},
+            "ring_read_floor_us": 1e6 * (algo_b + ring_b) / (peaks["hbm"] * 1e9),
+            "frac_of_floor": (algo_b + ring_b) / (peaks["hbm"] * 1e9) / tick_s,
+            "peak_spec": SPEC_HBM_GBS, "frac_spec": algo_b / tick_s / 1e9 / SPEC_HBM_GBS,
+            "peak_source": peaks["source"],
+            "launch_ms_avg": tot / args.steps,
+            "note": "latency-bound: one launch per tick; the per-tick bytes are far below "
+                    "what HBM moves in the tick's duration"}
     if rank == 0:
         line = {
             "metric": METRIC + " (c4 streaming tick)", "value": value, "unit": UNIT,
@@ -391,6 +469,7 @@ def run_streaming(args, rank, world, local_rank):
                                 "max": 1e3 * max(lat)},
             "step_mode": "one CUDA graph replay per tick (graph per ring phase)",
             "threshold": {"z_q": thr["z_q"], "n_peaks": thr["n_peaks"]},
+            "roofline": roof,
             "next_rows": {"online_spot": spot_line},
             "cpu_baseline": cpu,
             "e2e": {"value": n_global * args.steps / (tot_e2e * 1e-3), "unit": UNIT,
@@ -507,7 +586,8 @@ def run_threshold_sweep(args, rank, world, local_rank):
         t0 = time.perf_counter()
         O.pot_threshold(sh[:m], 0.98, 1e-3)
         el = time.perf_counter() - t0
-        cpu = {"value": m / el, "unit": "scores/s", "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": m / el, "unit": "scores/s", "cores": cpu_cores(),
+               "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"first {m} of {n_total} c5 scores: full sort + Grimshaw fit ({el:.1f} s)"}
     if comm is not None:
         comm.destroy()
@@ -527,6 +607,7 @@ def run_threshold_sweep(args, rank, world, local_rank):
             "roofline": {"kernel": "k_pot", "bound": "hbm", "achieved": achieved,
                          "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"],
                          "traffic": None, "peak_source": peaks["source"],
+                         "peak_spec": SPEC_HBM_GBS, "frac_spec": achieved / SPEC_HBM_GBS,
                          "bytes_per_launch": 4 * n,
                          "note": "algorithmic bytes = one fp32 read of the scores; the fit's "
                                  "fp64 grid scan over the 2M peaks is compute, not bytes"},
@@ -550,16 +631,29 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the live ncu DRAM-traffic pass of the roofline kernel")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host-side multi-rank plumbing only (gloo, no GPU, no kernels): "
+                         "shards, barrier, max-over-ranks timing and the JSON line")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: re-exec under
+        # torch.distributed.run, one process per GPU (the driver's own launch)
+        return self_launch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and rank == 0:
-        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; N > 1 runs under "
-              f"torchrun (one process per GPU) -- measuring world size {world}", file=sys.stderr)
+    if args.gpus != world:
+        if rank == 0:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per "
+                  f"GPU with --nproc-per-node {args.gpus} (or omit the launcher)", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.workload == "c4":
@@ -567,6 +661,52 @@ def main():
     if args.workload == "c5":
         return run_threshold_sweep(args, rank, world, local_rank)
     return run_windows(args, rank, world, local_rank)
+
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(n):
+    """Re-run this command under torch.distributed.run with n ranks on 127.0.0.1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank host plumbing without a GPU (gloo): each rank's
+    instance shard, a barrier, a per-rank "step time" reduced with max over
+    ranks and the windows summed over ranks, then rank 0's JSON line.  No
+    kernels run; `value` is null.  Used by the CPU tests to check that
+    `--gpus N` really starts N ranks."""
+    import torch.distributed as dist
+
+    from paper_2407_09486_b200 import synth
+    from paper_2407_09486_b200.fleet import max_over_ranks, shard_range, sum_over_ranks
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = synth.CONFIGS[args.workload if args.workload in ("c2", "c3") else "c2"]
+    n_per = INST_PER_GPU if args.workload == "c2" else cfg["n_instances"] // 8
+    a, b = shard_range(n_per * world, world, rank)
+    T, W = cfg["n_steps"], cfg["window"]
+    wins = sum_over_ranks((b - a) * (T - W + 1))
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+                          "ranks_seen_max": t, "windows_per_step": wins,
+                          "config": {"workload": args.workload,
+                                     "parallelism": f"instance-sharded x{world}"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_windows(args, rank, world, local_rank):
@@ -654,20 +794,23 @@ def run_windows(args, rank, world, local_rank):
     value = wins_local * world * args.steps / (tot_ms * 1e-3)
 
     # ---- per-stage device times (eager, stream-ordered, events between stages) ----
-    stage = {"stats": [], "score_calibration": [], "fit_threshold": [], "detect": []}
+    stage = {"stats": [], "score_calibration": [], "fit_threshold": [], "flag_calibration": [],
+             "detect": []}
     if world == 1:
         for _ in range(5):
             flush.zero_()
-            k = [ev() for _ in range(5)]
+            k = [ev() for _ in range(6)]
             k[0].record(stream)
             E.compute_stats_async(X, tcal, out=(mean, std), diag=pipe.diag, workspace=pipe.stats_ws)
             k[1].record(stream)
-            E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+            E.score_windows(X, det, mean, std, W - 1, tcal, out=(cal, pipe.cal_md))
             k[2].record(stream)
             E.fit_threshold_async(cal, 0.98, 1e-3, workspace=pipe.thr_ws, out=pipe.thr)
             k[3].record(stream)
-            E.detect_async(X, det, mean, std, pipe.thr, tcal, T, out=(pipe.flags, pipe.scores, pipe.md))
+            E.flag_scores_async(cal, pipe.cal_md, pipe.thr, out=pipe.cal_flags)
             k[4].record(stream)
+            E.detect_async(X, det, mean, std, pipe.thr, tcal, T, out=(pipe.flags, pipe.scores, pipe.md))
+            k[5].record(stream)
             torch.cuda.synchronize()
             for j, name in enumerate(stage):
                 stage[name].append(k[j].elapsed_time(k[j + 1]))
@@ -682,30 +825,41 @@ def run_windows(args, rank, world, local_rank):
     reps = 10
     flush.zero_()
     k0, k1 = ev(), ev()
-    E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+    E.score_windows(X, det, mean, std, W - 1, tcal, out=(cal, pipe.cal_md))
     k0.record(stream)
     for _ in range(reps):
-        E.score_windows(X, det, mean, std, W - 1, tcal, with_md=False, out=(cal, None))
+        E.score_windows(X, det, mean, std, W - 1, tcal, out=(cal, pipe.cal_md))
     k1.record(stream)
     torch.cuda.synchronize()
     launch_ms = k0.elapsed_time(k1) / reps
     achieved = fpw * n_cal_local / (launch_ms * 1e-3) / 1e12   # TFLOP/s
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "score_traffic.json")
-    if args.workload == "c2" and os.path.exists(tp):   # ncu capture of the c2 calibration launch
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except (ValueError, OSError):
-            traffic = None
+    traffic, traffic_src = None, None
+    if rank == 0 and world == 1 and args.workload == "c2" and not args.no_traffic:
+        # live ncu pass (subprocess, untimed) over the same calibration launch
+        t_ = measure_traffic("k_score_pair", [os.path.join(ROOT, "tools", "profile_run.py"), "1"])
+        if t_ is not None:
+            traffic = t_[0]
+            traffic_src = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of the first "
+                           f"c2 calibration launch, measured in this run "
+                           f"(read {t_[1] / 1e6:.1f} MB, write {t_[2] / 1e6:.1f} MB)")
+    algo_bytes = N * tcal * M * 4 + n_cal_local * 8   # samples read once + score, md written
     roof = {"kernel": "k_score_pair<128,16>", "bound": "tensor", "achieved": achieved,
             "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16"],
-            "traffic": traffic,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": algo_bytes,
+            "peak_spec": SPEC_F16_TFLOPS, "frac_spec": achieved / SPEC_F16_TFLOPS,
+            "peak_sustained": peaks["bf16_sus"], "frac_sustained": achieved / peaks["bf16_sus"],
             "peak_source": peaks["source"] + ": dense bf16 burst; fp16 has the same nominal rate",
             "flops_per_window": fpw, "windows_per_launch": n_cal_local,
             "launch_ms_avg": launch_ms, "launches_timed": reps,
             "in_step_score_ms": (stage_ms.get("score_calibration", 0.0) + stage_ms.get("detect", 0.0)) or None,
             "share_of_step": ((stage_ms["score_calibration"] + stage_ms["detect"]) / ms_per_step
-                              if stage_ms else None)}
+                              if stage_ms else None),
+            "step_level": {"achieved": fpw * wins_local / (ms_per_step * 1e-3) / 1e12,
+                           "frac": fpw * wins_local / (ms_per_step * 1e-3) / 1e12 / peaks["bf16"],
+                           "frac_spec": fpw * wins_local / (ms_per_step * 1e-3) / 1e12 / SPEC_F16_TFLOPS,
+                           "note": "every window's algorithmic tensor FLOPs / the whole step "
+                                   "(stats, threshold and flags included)"}}
 
     # ---- NEXT-1 / NEXT-4 on this step's detection flags (not part of the step) ----
     extras = None
@@ -769,6 +923,8 @@ def run_windows(args, rank, world, local_rank):
         # the same step through the public API with the trace in pinned HOST memory:
         # H2D copy of the whole trace, the step, D2H of the flags, every step
         flags_h = torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory()
+        cflags_h = torch.empty(tuple(pipe.cal_flags.shape), dtype=torch.int8).pin_memory()
+        d2h = flags_h.numel() + cflags_h.numel()
 
         if use_graph:
             # double-buffered: the H2D copy of step k+1 (copy stream) overlaps the
@@ -777,8 +933,9 @@ def run_windows(args, rank, world, local_rank):
             X2 = X.clone()   # capture warms up on real data
             pipe2 = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
             pipe2.capture(X2)
-            bufs = [(X, pipe, torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory()),
-                    (X2, pipe2, torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory())]
+            mk = lambda: (torch.empty(tuple(pipe.cal_flags.shape), dtype=torch.int8).pin_memory(),
+                          torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory())
+            bufs = [(X, pipe, mk()), (X2, pipe2, mk())]
             cs = torch.cuda.Stream(device=dev)
             copied = [torch.cuda.Event(), torch.cuda.Event()]
             freed = [torch.cuda.Event(), torch.cuda.Event()]
@@ -796,7 +953,8 @@ def run_windows(args, rank, world, local_rank):
                         copied[b].record(cs)
                     stream.wait_event(copied[b])
                     pb.replay()
-                    fh.copy_(pb.flags, non_blocking=True)
+                    fh[0].copy_(pb.cal_flags, non_blocking=True)
+                    fh[1].copy_(pb.flags, non_blocking=True)
                     freed[b].record(stream)
 
             w0 = ev()
@@ -813,13 +971,14 @@ def run_windows(args, rank, world, local_rank):
             torch.cuda.synchronize()
             e_ms = e0.elapsed_time(e1)
             pipe2.result()
-            flags_h = bufs[0][2]
+            d2h = bufs[0][2][0].numel() + bufs[0][2][1].numel()
             e2e_mode = "double-buffered: H2D of step k+1 overlaps the step-k graph"
         else:
             def e2e_step():
                 X.copy_(X_pinned, non_blocking=True)
                 run_step()
                 flags_h.copy_(pipe.flags, non_blocking=True)
+                cflags_h.copy_(pipe.cal_flags, non_blocking=True)
 
             for _ in range(2):
                 e2e_step()
@@ -840,13 +999,14 @@ def run_windows(args, rank, world, local_rank):
             e_ms = float(t.item())
         pipe.result()
         e2e = {"value": wins_local * world * args.steps / (e_ms * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(Xh.nbytes), "d2h_bytes_per_step": int(flags_h.numel()),
+               "h2d_bytes_per_step": int(Xh.nbytes), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / args.steps, "mode": e2e_mode}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, wins, ninst, el = oracle_sample(Xh, wts, tcal, budget_s=args.cpu_budget)
-        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "cpu_model": cpu_model(),
+               "kind": "oracle",
                "sample": f"first {ninst} of {N} {args.workload} instances, all {wins} windows, "
                          f"fp64 NumPy forward incl. explicit decoder ({el:.1f} s)"}
 
@@ -864,6 +1024,8 @@ def run_windows(args, rank, world, local_rank):
                 "windows_per_step": wins_local * world, "parallelism": f"instance-sharded x{world}",
                 "l2": f"flushed between steps (256 MiB zero-fill, untimed); inputs {Xh.nbytes / 1e6:.0f} MB/GPU > L2",
                 "precision": "fp16 operands (x, weights), fp32 accumulate, h/mu hi+lo fp16",
+                "outputs": "every window of the trace (calibration and detection) ends the step "
+                           "with a score, an MD and a flag",
             },
             "stage_ms": stage_ms,
             "next_rows": extras,

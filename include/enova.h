@@ -209,6 +209,18 @@ enova_status enova_detect_async(const enova_series *series, const enova_detector
                                 const enova_threshold *thr_dev, int8_t *flags,
                                 float *scores_opt, float *md_opt, void *stream);
 
+/* a-6 on windows scored before the threshold existed (the calibration windows
+ * of a step: scored with MD, then the POT fit runs on their scores): flags[i]
+ * = 0 if scores[i] <= z_q, else +1 if md[i] >= 0, else -1 (PAPER.md:297
+ * "exceeds this threshold", "scale up or down"; R-9, R-10) --
+ * the comparison the score kernels make, with z_q read from the device
+ * threshold (a failed fit has z_q = NaN: nothing is flagged).  scores, md:
+ * device fp32 [n]; flags: device int8 [n]; all caller-owned.  Stream-ordered,
+ * capturable.  ENOVA_ERR_INVALID_ARGUMENT for n < 0 or NULL buffers with
+ * n > 0; ENOVA_ERR_UNCALIBRATED without a (8-byte aligned) thr_dev. */
+enova_status enova_flag_scores_async(const float *scores, const float *md, int64_t n,
+                                     const enova_threshold *thr_dev, int8_t *flags, void *stream);
+
 /* ----------------------------------------------------------------- a-10 ----
  * Streaming ("executed in streaming computing framework"): a mirror
  * ring of 2W samples per instance, device fp32 [N][2W][M].  enova_ring_push
@@ -273,10 +285,13 @@ enova_status enova_stream_detect(const void *ring, int64_t n_instances, int64_t 
  * Y in index order (anomalies never update the model) and adds the number of
  * non-anomalous scores to n; enova_spot_refit re-fits the GPD on the grown Y and
  * writes the new device threshold (same as enova_fit_threshold_async's out_dev)
- * -- call it every tick (exact SPOT semantics per tick) or periodically.  Peaks
- * beyond the workspace capacity are dropped and reported by the next refit as
- * ENOVA_ERR_WORKSPACE in out_dev->reserved.  Both stream-ordered and
- * capturable; single GPU. */
+ * -- call it every tick (exact SPOT semantics per tick) or periodically.  The
+ * peak capacity is ceil((1 - init_quantile) n_global_max) + 16 (calibration
+ * peaks included).  Peaks beyond it are dropped; the next refit -- and every
+ * later one until a new calibration fit -- does not fit the truncated set and
+ * writes ENOVA_ERR_WORKSPACE to out_dev->reserved with z_q = NaN (so no window
+ * is flagged against a biased threshold).  Both stream-ordered and capturable;
+ * single GPU. */
 enova_status enova_spot_update(const float *scores, const int8_t *flags, int64_t n, void *ws,
                                size_t ws_bytes, int64_t n_global_max, double init_quantile,
                                void *stream);
@@ -352,6 +367,12 @@ const char *enova_status_string(enova_status s);
 /* Number of CUDA kernels this library has launched in this process (all
  * devices, monotonically increasing; diagnostic for benchmarks). */
 uint64_t enova_kernel_launches(void);
+/* Diagnostic kernel override for the windowed scoring calls (score_windows,
+ * detect*): 0 = choose by shape (default), 1 = W1-streaming kernel, 2 = CTA-pair
+ * kernel, 3 = instance-batched row kernel (where the shape allows; otherwise
+ * the choice by shape).  Process-wide; used by A/B and parity tests only.
+ * ENOVA_ERR_INVALID_ARGUMENT for any other value. */
+enova_status enova_set_score_kernel(int which);
 const char *enova_last_error(void);
 int enova_abi_version(void);
 

@@ -13,7 +13,8 @@ __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold"
            "detect_async",
            "threshold_from_device", "threshold_to_device", "check_stats_diag", "Pipeline",
            "StatsWorkspace", "StreamRing", "point_adjusted_counts", "point_adjusted_f1", "select_flagged",
-           "explain_windows", "Spot"]
+           "explain_windows", "Spot", "force_score_kernel",
+           "flag_scores_async"]
 
 
 def __getattr__(name):

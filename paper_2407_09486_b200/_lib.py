@@ -31,7 +31,8 @@ EXPORTS = (
     "enova_select_flagged_scratch_bytes", "enova_select_flagged", "enova_explain_windows",
     "enova_spot_update", "enova_spot_refit", "enova_stream_step",
     "enova_threshold_comm_workspace_bytes", "enova_fit_threshold_comm_async",
-    "enova_comm_create_local", "enova_comm_sum_i64",
+    "enova_comm_create_local", "enova_comm_sum_i64", "enova_set_score_kernel",
+    "enova_flag_scores_async",
 )
 
 
@@ -122,6 +123,8 @@ def lib() -> C.CDLL:
             "enova_last_error": (C.c_char_p, []),
             "enova_abi_version": (C.c_int, []),
             "enova_kernel_launches": (C.c_uint64, []),
+            "enova_set_score_kernel": (C.c_int, [C.c_int]),
+            "enova_flag_scores_async": (C.c_int, [vp, vp, i64, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -29,6 +29,24 @@ def _require_cuda(t: torch.Tensor, name: str, dtype=torch.float32):
         raise TypeError(f"{name} must be {dtype}")
 
 
+_KERNELS = {"auto": 0, "stream": 1, "pair": 2, "rows": 3}
+
+
+class force_score_kernel:
+    """Diagnostic context manager: force the windowed scoring kernel ("stream",
+    "pair", "rows" or "auto") for the calls inside (enova_set_score_kernel)."""
+
+    def __init__(self, name: str):
+        self.k = _KERNELS[name]
+
+    def __enter__(self):
+        check(lib().enova_set_score_kernel(self.k))
+        return self
+
+    def __exit__(self, *a):
+        check(lib().enova_set_score_kernel(0))
+
+
 class PreparedDetector:
     """Detector weights on the GPU plus their prepared fp16 operand image (K0)."""
 
@@ -62,6 +80,13 @@ def _series(metrics: torch.Tensor, mean=None, std=None, t_begin=0, t_end=0) -> S
     if metrics.stride(2) != 1 or metrics.stride(1) != M:
         raise ValueError("metrics rows must be contiguous [T][M] per instance")
     ld = metrics.stride(0) if N > 1 else T * M
+    for name, v in (("mean", mean), ("std", std)):
+        if v is not None:
+            _require_cuda(v, name)
+            if v.device != metrics.device:
+                raise ValueError(f"{name} must be on {metrics.device}")
+            if tuple(v.shape) != (N, M) or not v.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous [{N}, {M}] tensor")
     s = Series(metrics.data_ptr(), N, T, ld, int(t_begin), int(t_end),
                mean.data_ptr() if mean is not None else None,
                std.data_ptr() if std is not None else None, M, 0)
@@ -276,6 +301,25 @@ def detect_async(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Tenso
     return flags, sc, md
 
 
+def flag_scores_async(scores: torch.Tensor, md: torch.Tensor, thr_dev: torch.Tensor, *,
+                      out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a-6 on already-scored windows (e.g. the calibration windows, scored before
+    the fit): flags = 0 / +1 / -1 against the DEVICE threshold (no host sync)."""
+    _require_cuda(scores, "scores")
+    _require_cuda(md, "md")
+    if scores.shape != md.shape or not scores.is_contiguous() or not md.is_contiguous():
+        raise ValueError("scores and md: contiguous, same shape")
+    flags = out if out is not None else torch.empty(scores.shape, dtype=torch.int8,
+                                                    device=scores.device)
+    _require_cuda(flags, "flags", torch.int8)
+    if flags.shape != scores.shape or not flags.is_contiguous():
+        raise ValueError("flags: contiguous, same shape as scores")
+    check(lib().enova_flag_scores_async(C.c_void_p(scores.data_ptr()), C.c_void_p(md.data_ptr()),
+                                        scores.numel(), C.c_void_p(thr_dev.data_ptr()),
+                                        C.c_void_p(flags.data_ptr()), _stream_ptr(stream)))
+    return flags
+
+
 def _thr_struct(thr: dict) -> Threshold:
     t = Threshold()
     for k, _ in Threshold._fields_:
@@ -336,6 +380,10 @@ class StreamRing:
     def __init__(self, det: PreparedDetector, mean: torch.Tensor, std: torch.Tensor, device=None):
         _require_cuda(mean, "mean")
         _require_cuda(std, "std")
+        if mean.dim() != 2 or mean.shape[1] != det.n_metrics or tuple(std.shape) != tuple(mean.shape):
+            raise ValueError(f"mean and std must both be [instances, {det.n_metrics}]")
+        if std.device != mean.device:
+            raise ValueError("mean and std must be on the same device")
         self.det, self.mean, self.std = det, mean.contiguous(), std.contiguous()
         self.n = int(mean.shape[0])
         self.W, self.M = det.window, det.n_metrics
@@ -394,10 +442,23 @@ class StreamRing:
 class Spot:
     """NEXT-2 online SPOT state on one GPU: calibrate() fits the initial POT
     threshold (device-resident, `thr` usable by detect_async / StreamRing.detect);
-    update(scores, flags) adds a tick's non-anomalous peaks; refit() re-fits."""
+    update(scores, flags) adds a tick's non-anomalous peaks; refit() re-fits.
 
-    def __init__(self, n_max: int, init_quantile: float = 0.98, risk_q: float = 1e-3, device=None):
+    Capacity: the peak buffer holds the calibration peaks (<= ceil((1-q0) n_cal)
+    + 16) plus `stream_peaks` streamed ones (default: as many again as the
+    calibration).  Peaks beyond it are dropped and every later refit reports
+    ENOVA_ERR_WORKSPACE (threshold() raises) until the next calibrate()."""
+
+    def __init__(self, n_calibration: int, init_quantile: float = 0.98, risk_q: float = 1e-3,
+                 device=None, stream_peaks: int | None = None):
         self.q0, self.q = float(init_quantile), float(risk_q)
+        n_cal = int(n_calibration)
+        if stream_peaks is None:
+            stream_peaks = int(math.ceil((1.0 - self.q0) * n_cal)) + 16
+        self.n_calibration = n_cal
+        self.stream_peaks = int(stream_peaks)
+        # the workspace cap is ceil((1 - q0) n_max) + 16 peaks
+        n_max = n_cal + int(math.ceil(self.stream_peaks / max(1.0 - self.q0, 1e-12)))
         self.ws = ThresholdWorkspace(n_max, self.q0, device)
         self.thr = torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8, device=device or "cuda")
 
@@ -450,7 +511,7 @@ def explain_windows(metrics: torch.Tensor, det: PreparedDetector, mean: torch.Te
     tb = det.window - 1 if t_begin is None else int(t_begin)
     te = T if t_end is None else int(t_end)
     s = _series(metrics, mean, std, tb, te)
-    ids = ids.to(dtype=torch.int64).contiguous()
+    ids = ids.to(device=metrics.device, dtype=torch.int64).contiguous()
     n = ids.numel()
     mdm = torch.empty((n, M), dtype=torch.float32, device=metrics.device)
     sc = torch.empty(n, dtype=torch.float32, device=metrics.device)
@@ -551,34 +612,42 @@ class PipelineResult:
     flags: torch.Tensor
     scores: torch.Tensor | None
     md: torch.Tensor | None
+    cal_md: torch.Tensor | None = None
+    cal_flags: torch.Tensor | None = None
 
 
 def run_pipeline(metrics: torch.Tensor, det: PreparedDetector, t_cal_end: int,
                  init_quantile: float = 0.98, risk_q: float = 1e-3, comm: Comm | None = None,
                  workspace: ThresholdWorkspace | None = None, return_scores: bool = True,
                  stream=None) -> PipelineResult:
-    """One pass of the whole hot path: stats over [0, t_cal_end) -> scores of the
-    calibration windows (ending in [W-1, t_cal_end)) -> fleet-wide POT threshold
-    -> flags (and scores/MD) of the windows ending in [t_cal_end, T)."""
+    """One pass of the whole hot path: stats over [0, t_cal_end) -> scores and MD
+    of the calibration windows (ending in [W-1, t_cal_end)) -> fleet-wide POT
+    threshold -> flags of the calibration windows -> flags (and scores/MD) of
+    the windows ending in [t_cal_end, T)."""
     T = metrics.shape[1]
     mean, std, nd = compute_stats(metrics, t_cal_end, stream=stream)
-    cal, _ = score_windows(metrics, det, mean, std, det.window - 1, t_cal_end, with_md=False,
-                           stream=stream)
+    cal, cal_md = score_windows(metrics, det, mean, std, det.window - 1, t_cal_end,
+                                stream=stream)
     thr = fit_threshold(cal, init_quantile, risk_q, comm=comm, workspace=workspace, stream=stream)
+    thr_d = threshold_to_device(thr, metrics.device)
+    if stream is not None:
+        thr_d.record_stream(stream)
+    cal_flags = flag_scores_async(cal, cal_md, thr_d, stream=stream)
     res = detect(metrics, det, mean, std, thr, t_cal_end, T, return_scores=return_scores,
                  stream=stream)
     if return_scores:
         flags, sc, md = res
     else:
         flags, sc, md = res, None, None
-    return PipelineResult(mean, std, nd, cal, thr, flags, sc, md)
+    return PipelineResult(mean, std, nd, cal, thr, flags, sc, md, cal_md, cal_flags)
 
 
 class Pipeline:
     """The whole hot path for a fixed fleet shape, preallocated and stream-ordered:
-    stats over [0, t_cal_end) -> calibration scores -> single-GPU POT threshold
-    (device-resident) -> flags / scores / MD of the windows ending in
-    [t_cal_end, T).  `enqueue` issues the step with no host synchronisation;
+    stats over [0, t_cal_end) -> calibration scores and MD -> single-GPU POT
+    threshold (device-resident) -> flags of the calibration windows -> flags /
+    scores / MD of the windows ending in [t_cal_end, T): every window of the
+    trace ends the step with a score, an MD and a flag.  `enqueue` issues the step with no host synchronisation;
     `capture` records it into a CUDA graph that `replay` relaunches (one graph
     launch per step); `result` synchronises and checks the device statuses.
     With a communicator (fleet sharded over ranks) the threshold is the
@@ -600,6 +669,8 @@ class Pipeline:
         self.std = torch.empty((N, M), dtype=torch.float32, device=dev)
         self.diag = torch.zeros(2, dtype=torch.int64, device=dev)
         self.cal = torch.empty((N, max(tcal - (W - 1), 0)), dtype=torch.float32, device=dev)
+        self.cal_md = torch.empty_like(self.cal)
+        self.cal_flags = torch.empty(tuple(self.cal.shape), dtype=torch.int8, device=dev)
         self.thr = torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8, device=dev)
         self.flags = torch.empty((N, T - tcal), dtype=torch.int8, device=dev)
         self.scores = torch.empty((N, T - tcal), dtype=torch.float32, device=dev) if return_scores else None
@@ -621,14 +692,15 @@ class Pipeline:
         W = self.det.window
         compute_stats_async(metrics, self.tcal, out=(self.mean, self.std), diag=self.diag,
                             workspace=self.stats_ws, stream=stream)
-        score_windows(metrics, self.det, self.mean, self.std, W - 1, self.tcal, with_md=False,
-                      out=(self.cal, None), stream=stream)
+        score_windows(metrics, self.det, self.mean, self.std, W - 1, self.tcal,
+                      out=(self.cal, self.cal_md), stream=stream)
         if self.comm is not None:
             fit_threshold_comm_async(self.cal, self.n_global, self.comm, self.q0, self.q,
                                      workspace=self.thr_ws, out=self.thr, stream=stream)
         else:
             fit_threshold_async(self.cal, self.q0, self.q, workspace=self.thr_ws, out=self.thr,
                                 stream=stream)
+        flag_scores_async(self.cal, self.cal_md, self.thr, out=self.cal_flags, stream=stream)
         detect_async(metrics, self.det, self.mean, self.std, self.thr, self.tcal, self.T,
                      out=(self.flags, self.scores, self.md), stream=stream)
 
@@ -656,4 +728,4 @@ class Pipeline:
         nd = check_stats_diag(self.diag)
         thr = threshold_from_device(self.thr)
         return PipelineResult(self.mean, self.std, nd, self.cal, thr, self.flags, self.scores,
-                              self.md)
+                              self.md, self.cal_md, self.cal_flags)

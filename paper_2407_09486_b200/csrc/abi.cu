@@ -31,6 +31,9 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
                                  float *stdv, unsigned long long *diag_dev, void *ws,
                                  size_t ws_bytes, cudaStream_t st);
 size_t stats_workspace_bytes(int64_t n, int m);
+void set_forced_kernel(int k);
+enova_status apply_flags(const float *scores, const float *md, int64_t n,
+                         const enova_threshold *thr_dev, int8_t *flags, cudaStream_t st);
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
                           float *scores, float *md, int8_t *flags, double z_q, const double *z_q_dev,
                           cudaStream_t st);
@@ -172,6 +175,34 @@ void enova_internal_pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
 }
 
 uint64_t enova_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+enova_status enova_flag_scores_async(const float *scores, const float *md, int64_t n,
+                                     const enova_threshold *thr_dev, int8_t *flags, void *stream) {
+  if (n < 0) {
+    enova::set_error("n < 0");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (n > 0 && (!scores || !md || !flags)) {
+    enova::set_error("scores / md / flags must be non-NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!thr_dev || !enova::aligned(thr_dev, 8)) {
+    enova::set_error("device threshold missing or misaligned");
+    return ENOVA_ERR_UNCALIBRATED;
+  }
+  enova_status r = enova::sticky();
+  if (r) return r;
+  return enova::apply_flags(scores, md, n, thr_dev, flags, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_set_score_kernel(int which) {
+  if (which < 0 || which > 3) {
+    enova::set_error("enova_set_score_kernel: which must be 0 (auto), 1 (stream), 2 (pair) or 3 (rows)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  enova::set_forced_kernel(which);
+  return ENOVA_OK;
+}
 
 const char *enova_last_error(void) { return g_last_error.c_str(); }
 

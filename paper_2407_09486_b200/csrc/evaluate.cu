@@ -159,8 +159,9 @@ enova_status point_adjust_counts(const int8_t *labels, int64_t ld_labels, const 
 
 // ---------------------------------------------------------------- NEXT-1 ----
 // Stable compaction of the flagged window ids (flags != 0), index order: blocks
-// of 1024 flags count, then each block adds up the counts before it (fixed
-// order) and scatters with warp ballots.  Feeds enova_explain_windows.
+// of 1024 flags count, one small kernel scans the block counts (fixed order,
+// O(n) total), then each block scatters with warp ballots.  Feeds
+// enova_explain_windows.
 constexpr int kSelBlock = 1024;
 
 __global__ void k_flag_count(const int8_t *__restrict__ flags, int64_t n,
@@ -170,29 +171,40 @@ __global__ void k_flag_count(const int8_t *__restrict__ flags, int64_t n,
   if (threadIdx.x == 0) counts[blockIdx.x] = (unsigned int)c;
 }
 
+// exclusive prefix of the block counts (one CTA, fixed order: each thread sums a
+// contiguous span of blocks, then a block-wide scan of the span sums)
+__global__ void __launch_bounds__(1024) k_flag_scan(const unsigned int *__restrict__ counts,
+                                                    int64_t nblocks,
+                                                    unsigned long long *__restrict__ base,
+                                                    long long *__restrict__ total) {
+  __shared__ unsigned long long wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (nblocks + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = min(nblocks, (int64_t)threadIdx.x * per), b1 = min(nblocks, b0 + per);
+  unsigned long long own = 0;
+  for (int64_t b = b0; b < b1; ++b) own += counts[b];
+  unsigned long long incl = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  unsigned long long run = incl - own;
+  for (int w = 0; w < warp; ++w) run += wsum[w];
+  for (int64_t b = b0; b < b1; ++b) {
+    base[b] = run;
+    run += counts[b];
+  }
+  if (threadIdx.x == blockDim.x - 1) *total = (long long)run;
+}
+
 __global__ void k_flag_scatter(const int8_t *__restrict__ flags, int64_t n,
-                               const unsigned int *__restrict__ counts, int nblocks,
-                               int64_t *__restrict__ ids, long long *__restrict__ total) {
-  __shared__ unsigned long long base;
+                               const unsigned long long *__restrict__ base,
+                               int64_t *__restrict__ ids) {
   __shared__ int wsum[kSelBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {   // exclusive prefix of this block (fixed order)
-    unsigned long long s = 0, all = 0;
-    for (int b = lane; b < nblocks; b += 32) {
-      const unsigned long long v = counts[b];
-      all += v;
-      if (b < (int)blockIdx.x) s += v;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      all += __shfl_xor_sync(0xffffffffu, all, o);
-    }
-    if (lane == 0) {
-      base = s;
-      if (blockIdx.x == 0) *total = (long long)all;
-    }
-  }
   const int64_t i = blockIdx.x * (int64_t)kSelBlock + threadIdx.x;
   const bool f = i < n && flags[i] != 0;
   const unsigned int bal = __ballot_sync(0xffffffffu, f);
@@ -200,8 +212,10 @@ __global__ void k_flag_scatter(const int8_t *__restrict__ flags, int64_t n,
   __syncthreads();
   int before = 0;
   for (int w = 0; w < warp; ++w) before += wsum[w];
-  if (f) ids[base + before + __popc(bal & ((1u << lane) - 1u))] = i;
+  if (f) ids[base[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u))] = i;
 }
+
+static inline size_t sel_counts_bytes(int64_t nb) { return align_up((size_t)nb * 4, 256); }
 
 enova_status select_flagged(const int8_t *flags, int64_t n, int64_t *ids, long long *count_dev,
                             void *scratch, cudaStream_t st) {
@@ -209,15 +223,18 @@ enova_status select_flagged(const int8_t *flags, int64_t n, int64_t *ids, long l
   if (n == 0) return ENOVA_OK;
   const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
   unsigned int *counts = static_cast<unsigned int *>(scratch);
+  unsigned long long *base = reinterpret_cast<unsigned long long *>(
+      static_cast<char *>(scratch) + sel_counts_bytes(nb));
   ENOVA_LAUNCH(k_flag_count, (unsigned)nb, kSelBlock, 0, st, flags, n, counts);
-  ENOVA_LAUNCH(k_flag_scatter, (unsigned)nb, kSelBlock, 0, st, flags, n, counts, (int)nb, ids,
-               count_dev);
+  ENOVA_LAUNCH(k_flag_scan, 1, 1024, 0, st, counts, nb, base, count_dev);
+  ENOVA_LAUNCH(k_flag_scatter, (unsigned)nb, kSelBlock, 0, st, flags, n, base, ids);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }
 
 size_t select_flagged_scratch_bytes(int64_t n) {
-  return align_up((size_t)((n + kSelBlock - 1) / kSelBlock) * 4, 256);
+  const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
+  return sel_counts_bytes(nb) + align_up((size_t)nb * 8, 256);
 }
 
 }  // namespace enova

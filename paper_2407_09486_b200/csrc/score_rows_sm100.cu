@@ -50,6 +50,7 @@ struct RowParams {
   const double *z_q_dev;
   // NEXT-1 explain mode: rows are gathered window ids, outputs per metric
   const int64_t *rows;          // [n_rows] window ids g = instance * nw + (t - t_begin)
+  int64_t n_win;                // explain mode: ids outside [0, n_win) are invalid (NaN rows)
   const float *wbarm, *bbarm;   // [M][H], [M] per-metric column sums of W_dec2, b_dec2
   float *md_metric;             // [n_rows][M]
 };
@@ -433,7 +434,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     const int r = tid;
     const int64_t row = row0 + r;
     const bool valid = row < p.n_rows;
-    const int64_t gid = kExplain ? (valid ? __ldg(p.rows + row) : 0) : row;   // window id
+    const int64_t gid_in = kExplain ? (valid ? __ldg(p.rows + row) : 0) : row;   // window id
+    // explain mode: an id outside the series' windows is scored as window 0
+    // (in-bounds loads) and its outputs are overwritten with NaN below
+    const bool id_ok = !kExplain || (gid_in >= 0 && gid_in < p.n_win);
+    const int64_t gid = id_ok ? gid_in : 0;
     const int64_t inst = valid ? gid / p.nw : 0;
     const int64_t wi = valid ? gid - inst * p.nw : 0;
     float xsum[kExplain ? M : 1];
@@ -524,6 +529,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
                          p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev, nullptr,
                          kExplain ? wbarm_s : nullptr, kExplain ? xsum : nullptr, p.bbarm,
                          p.md_metric, M, p.W);
+    if (kExplain && valid && !id_ok) {   // same thread wrote the row: program order
+      const float qnan = __int_as_float(0x7fc00000);
+      if (p.scores) p.scores[row] = qnan;
+      if (p.md) p.md[row] = qnan;
+#pragma unroll
+      for (int j = 0; j < M; ++j) p.md_metric[row * M + j] = qnan;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -626,6 +638,7 @@ enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, cons
   RowParams p = row_params(s, L, det_ws);
   p.n_rows = n_rows;
   p.rows = rows_dev;
+  p.n_win = s->n_instances * p.nw;
   p.md_metric = md_metric;
   p.scores = scores;
   p.md = md;

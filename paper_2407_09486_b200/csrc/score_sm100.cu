@@ -27,6 +27,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "layout.h"
 
@@ -418,18 +420,13 @@ enova_status launch_score_rows(const enova_series *s, const DetLayout &L, const 
 //    the instance-batched row kernel (128 independent windows per tile);
 //  * else the weight-stationary CTA-pair kernel whenever half of W1 fits in
 //    shared memory (all BASELINE configs), else the W1-streaming kernel.
-// ENOVA_SCORE_KERNEL=stream | pair | rows forces a kernel (diagnostic / A-B tests;
-// "rows" only where the row kernel supports the shape).
+// enova_set_score_kernel(1 | 2 | 3) forces the stream / pair / rows kernel
+// (diagnostic, for A/B and parity tests; "rows" only where the row kernel
+// supports the shape); 0 restores the choice by shape.
 constexpr int64_t kRowModeMaxWindows = 16;
-static int forced_kernel() {   // 0 auto, 1 stream, 2 pair, 3 rows
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("ENOVA_SCORE_KERNEL");
-    v = !e ? 0 : strcmp(e, "stream") == 0 ? 1 : strcmp(e, "pair") == 0 ? 2
-             : strcmp(e, "rows") == 0 ? 3 : 0;
-  }
-  return v;
-}
+static std::atomic<int> g_forced_kernel{0};   // 0 auto, 1 stream, 2 pair, 3 rows
+void set_forced_kernel(int k) { g_forced_kernel.store(k, std::memory_order_relaxed); }
+static int forced_kernel() { return g_forced_kernel.load(std::memory_order_relaxed); }
 
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
                           float *scores, float *md, int8_t *flags, double z_q, const double *z_q_dev,

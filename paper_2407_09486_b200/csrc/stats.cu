@@ -33,11 +33,12 @@ size_t stats_workspace_bytes(int64_t n, int m) {
          align_up((size_t)n * stats_max_chunks(n) * 2 * m * sizeof(double), 256);
 }
 
+template <bool kPow2Group>
 __global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
     const float *__restrict__ X, int64_t ld, int M, int64_t T_cal, int nchunk,
     float *__restrict__ mean_out, float *__restrict__ std_out, unsigned long long *diag,
     unsigned int *ticket, double *part) {
-  extern __shared__ double red[];  // [nwarps][2][M]
+  extern __shared__ double red[];  // [nwarps or nslots][2][M]
   __shared__ bool last;
   const int G = M / 4;
   const int g = threadIdx.x % G;
@@ -67,24 +68,46 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
     for (int u = 0; u < 4; ++u)
       if (t + u * nslots < t1) acc(v[u]);
   }
-  // fixed-order tree over the slots of a warp (lanes with the same g), then a
-  // fixed-order sum over the warps
   double v8[8] = {a0, a1, a2, a3, q0, q1, q2, q3};
-  for (int o = G; o < 32; o <<= 1)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int nred;   // partial sums per output left in red[] (summed below in index order)
+  if (kPow2Group) {
+    // G a power of two <= 32 (M in {8, ..., 128}), full warps: fixed-order
+    // shuffle tree over the slots of a warp (lanes with the same g), then one
+    // row of red[] per warp
+    for (int o = G; o < 32; o <<= 1)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v8[k] += __shfl_xor_sync(0xffffffffu, v8[k], o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (lane < G) {
-    double *r = red + (size_t)warp * 2 * M;
+      for (int k = 0; k < 8; ++k) v8[k] += __shfl_xor_sync(0xffffffffu, v8[k], o);
+    if (lane < G) {
+      double *r = red + (size_t)warp * 2 * M;
+      r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
+      r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
+    }
+    nred = blockDim.x >> 5;
+  } else {
+    // any G (M a multiple of 4 up to 256, partial last warp allowed): one row
+    // of red[] per slot, then a fixed-order pairwise tree over the slots in
+    // shared memory (row s += row s + half), so the result does not depend on
+    // warp boundaries
+    double *r = red + (size_t)slot * 2 * M;
     r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
     r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
+    int rows = nslots;
+    while (rows > 1) {
+      const int half = (rows + 1) >> 1;
+      __syncthreads();
+      for (int e = threadIdx.x; e < (rows - half) * 2 * M; e += blockDim.x)
+        red[e] += red[(size_t)half * 2 * M + e];
+      rows = half;
+    }
+    nred = 1;
   }
   bad = __syncthreads_or(bad);
   double *pc = part + ((size_t)inst * nchunk + chunk) * 2 * M;
-  if (threadIdx.x < 2 * M) {   // fixed-order sum over warps
+  for (int e = threadIdx.x; e < 2 * M; e += blockDim.x) {   // fixed-order sum over rows
     double s = 0;
-    for (int k = 0; k < nwarps; ++k) s += red[(size_t)k * 2 * M + threadIdx.x];
-    pc[threadIdx.x] = s;
+    for (int k = 0; k < nred; ++k) s += red[(size_t)k * 2 * M + e];
+    pc[e] = s;
   }
   if (threadIdx.x == 0 && bad) atomicAdd(diag + 1, 1ull);   // chunks with a non-finite sample
   // last CTA of this instance combines the chunks in chunk order
@@ -94,8 +117,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < M) {
-    const int j = threadIdx.x;
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
     const double *p0 = part + (size_t)inst * nchunk * 2 * M;
     double s1 = 0, s2 = 0;
     for (int c = 0; c < nchunk; ++c) {
@@ -154,12 +176,13 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   const int nslots = nthreads / G;
   if (diag_dev) ENOVA_CUDA_TRY(cudaMemsetAsync(diag_dev, 0, 2 * sizeof(unsigned long long), st));
   ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, 256 + (size_t)N * 4, st));   // diag (own) + tickets
-  const size_t smem = (size_t)(nthreads / 32) * 2 * M * sizeof(double);
-  (void)nslots;
+  const bool pow2 = (G & (G - 1)) == 0 && G <= 32;
+  const size_t smem = (size_t)(pow2 ? nthreads / 32 : nslots) * 2 * M * sizeof(double);
+  auto kern = pow2 ? k_series_stats<true> : k_series_stats<false>;
   if (smem > 48 * 1024)
-    ENOVA_CUDA_TRY(cudaFuncSetAttribute(k_series_stats,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ENOVA_LAUNCH(k_series_stats, (unsigned)(N * nchunk), nthreads, smem, st, s->metrics,
+    ENOVA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+  ENOVA_LAUNCH(kern, (unsigned)(N * nchunk), nthreads, smem, st, s->metrics,
                s->ld_instance, M, t_cal_end, (int)nchunk, mean, stdv, diag, ticket, part);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;

@@ -75,6 +75,9 @@ struct PotGlobal {
   int method, nroots, converged, overflow;
   long long n_spot;                  // NEXT-2: observations counted by the online SPOT state
   long long nt_refit;                // NEXT-2: N_t at the last (re)fit
+  int spot_overflow;                 // NEXT-2: a tick's peaks exceeded the Y capacity (sticky
+                                     // until the next calibration fit zeroes the header)
+  int pad2;
   int n_stamps, fit_passes;
   unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
   unsigned long long t_first_start, t_last_end;   // over all CTAs (diagnostic)
@@ -1137,6 +1140,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   PotGlobal *g = a.g;
   unsigned int epoch = 0;   // grid barriers passed in this launch
   bool spot_skip = false;
+  bool spot_full = false;   // SPOT refit on a truncated peak set: report, do not fit
   if (threadIdx.x == 0) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1186,8 +1190,10 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
     } else if (ph == P_FIT) {
       // SPOT refit with no peak added since the last fit: the model is unchanged
       // (the cited Algorithm 1 refits only when a peak arrives) -- keep the threshold
-      spot_skip = a.n_dev && *(volatile long long *)&g->nt_fit == *(volatile long long *)&g->nt_refit;
-      if (!spot_skip) {
+      spot_full = a.n_dev && *(volatile int *)&g->spot_overflow != 0;
+      spot_skip = !spot_full && a.n_dev &&
+                  *(volatile long long *)&g->nt_fit == *(volatile long long *)&g->nt_refit;
+      if (!spot_skip && !spot_full) {
         const int64_t nt = a.yslot ? pack_tails(a, s_off)
                                    : (int64_t)*(volatile long long *)&g->nt_fit;
         fit(a, sh.fit, epoch, nt);
@@ -1208,7 +1214,8 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       g->k_rem = sel.k_rem;
     }
     if (a.last == P_FIT && !a.n_dev) g->n_spot = a.n;   // SPOT state starts at the calibration
-    if (a.last == P_FIT && !spot_skip) g->nt_refit = g->nt_fit;
+    if (a.last == P_FIT && !spot_skip && !spot_full) g->nt_refit = g->nt_fit;
+    if (spot_full) g->status = ENOVA_ERR_WORKSPACE;
     if (a.last == P_FIT && a.out_dev && !spot_skip) {
       enova_threshold *o = a.out_dev;
       const int st = g->status;
@@ -1515,8 +1522,8 @@ __global__ void __launch_bounds__(1024) k_spot_append(const float *__restrict__ 
     }
     g->n_spot += tn;
     long long nt = base_s + tp;
-    if (nt > cap) {
-      g->overflow = 1;
+    if (nt > cap) {   // peaks beyond the capacity are lost: the next refit reports
+      g->spot_overflow = 1;   // ENOVA_ERR_WORKSPACE instead of fitting a truncated Y
       nt = cap;
     }
     g->nt_fit = nt;

@@ -111,32 +111,18 @@ def test_scores_match_oracle_shapes(E, W, M, H, Z):
             assert_md(md.cpu().numpy(), rmd)
 
 
-def test_streaming_kernel_matches_oracle_c2_slice():
-    """The W1-streaming kernel (forced by ENOVA_SCORE_KERNEL=stream) on the
-    benchmark detector, in a fresh process (the switch is read once)."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, sys\n"
-        "sys.path.insert(0, '.')\n"
-        "import paper_2407_09486_b200 as E\n"
-        "from paper_2407_09486_b200 import synth\n"
-        "from oracle import enova_oracle as O\n"
-        "X = synth.metric_trace(4, 800, 16, seed=9)\n"
-        "w = synth.detector_weights(64, 16, 128, 16, seed=9)\n"
-        "m, s, _ = O.series_stats(X, 400)\n"
-        "d = E.PreparedDetector(w)\n"
-        "sc, md = E.score_windows(torch.from_numpy(X).cuda(), d, torch.from_numpy(m).cuda(), torch.from_numpy(s).cuda())\n"
-        "rs, rmd = O.score_windows(X, w, m, s, 63, 800)\n"
-        "e = np.abs(sc.cpu().numpy() - rs) / (np.abs(rs) + 1e-6)\n"
-        "f = np.abs(md.cpu().numpy() - rmd)\n"
-        "assert e.max() < 1e-3 and f.max() < 1e-4, (e.max(), f.max())\n"
-        "print('ok', e.max())\n")
-    import os
-    env = dict(os.environ, ENOVA_SCORE_KERNEL="stream")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
+def test_streaming_kernel_matches_oracle_c2_slice(E):
+    """The W1-streaming kernel (forced with enova_set_score_kernel) on the
+    benchmark detector."""
+    X = synth.metric_trace(4, 800, 16, seed=9)
+    w = synth.detector_weights(64, 16, 128, 16, seed=9)
+    m, s, _ = O.series_stats(X, 400)
+    d = E.PreparedDetector(w)
+    with E.force_score_kernel("stream"):
+        sc, md = E.score_windows(cuda(X), d, cuda(m), cuda(s))
+    rs, rmd = O.score_windows(X, w, m, s, 63, 800)
+    assert_scores(sc.cpu().numpy(), rs, "stream-kernel scores")
+    assert_md(md.cpu().numpy(), rmd)
 
 
 ROW_SHAPES = [(32, 8, 32, 4), (64, 16, 128, 16), (64, 16, 64, 5), (2, 8, 32, 1), (10, 16, 128, 9),
@@ -145,14 +131,10 @@ ROW_SHAPES = [(32, 8, 32, 4), (64, 16, 128, 16), (64, 16, 64, 5), (2, 8, 32, 1),
 
 @pytest.mark.parametrize("W,M,H,Z", ROW_SHAPES, ids=lambda v: str(v))
 def test_row_kernel_matches_oracle_and_pair_kernel(E, W, M, H, Z):
-    """The instance-batched row kernel (forced by ENOVA_SCORE_KERNEL=rows, in a
-    fresh process) on multi-window ranges with ragged tiles: within tolerance of
+    """The instance-batched row kernel (forced with enova_set_score_kernel) on
+    multi-window ranges with ragged tiles: within tolerance of
     the oracle, and BIT-identical to the windowed CTA-pair kernel (same epilogue
     arithmetic and window-sum association), so streamed and batch scores agree."""
-    import os
-    import subprocess
-    import sys
-    import tempfile
     N, T = 5, 300 + W
     seed = 7 * W + M + H + Z
     X = synth.metric_trace(N, T, M, seed=seed)
@@ -162,27 +144,10 @@ def test_row_kernel_matches_oracle_and_pair_kernel(E, W, M, H, Z):
     det = E.PreparedDetector(wts)
     sc_p, md_p = E.score_windows(cuda(X), det, cuda(mean), cuda(std), tb, te)
     fl_p = E.detect(cuda(X), det, cuda(mean), cuda(std), {"z_q": 2.0}, tb, te)
-    with tempfile.TemporaryDirectory() as d:
-        code = (
-            "import numpy as np, torch, sys\n"
-            "sys.path.insert(0, '.')\n"
-            "import paper_2407_09486_b200 as E\n"
-            "from paper_2407_09486_b200 import synth\n"
-            "from oracle import enova_oracle as O\n"
-            f"X = synth.metric_trace({N}, {T}, {M}, seed={seed})\n"
-            f"w = synth.detector_weights({W}, {M}, {H}, {Z}, seed={seed})\n"
-            f"m, s, _ = O.series_stats(X, {T // 2})\n"
-            "d = E.PreparedDetector(w)\n"
-            "c = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()\n"
-            f"sc, md = E.score_windows(c(X), d, c(m), c(s), {tb}, {te})\n"
-            f"fl = E.detect(c(X), d, c(m), c(s), {{'z_q': 2.0}}, {tb}, {te})\n"
-            f"np.savez('{d}/r.npz', sc=sc.cpu().numpy(), md=md.cpu().numpy(), fl=fl.cpu().numpy())\n")
-        env = dict(os.environ, ENOVA_SCORE_KERNEL="rows")
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                           timeout=300)
-        assert r.returncode == 0, r.stdout + r.stderr
-        got = np.load(f"{d}/r.npz")
+    with E.force_score_kernel("rows"):
+        sc_r, md_r = E.score_windows(cuda(X), det, cuda(mean), cuda(std), tb, te)
+        fl_r = E.detect(cuda(X), det, cuda(mean), cuda(std), {"z_q": 2.0}, tb, te)
+    got = dict(sc=sc_r.cpu().numpy(), md=md_r.cpu().numpy(), fl=fl_r.cpu().numpy())
     rs, rmd = O.score_windows(X, wts, mean, std, tb, te)
     assert_scores(got["sc"], rs, "row-kernel scores")
     assert_md(got["md"], rmd)
@@ -593,7 +558,7 @@ def test_spot_ticks_match_oracle(E, refit_every):
     ticks = [synth.score_mixture(2000, seed=22, offset=2000 * k) for k in range(10)]
     ticks[4][[7, 900]] = 80.0                        # anomalies never enter the model
     ref = O.spot_ticks(init, ticks, refit_every=refit_every)
-    spot = E.Spot(2_000_000)
+    spot = E.Spot(200_000, stream_peaks=20_000)
     spot.calibrate(cuda(init))
     z0 = spot.threshold()
     r0 = O.pot_threshold(init)
@@ -611,6 +576,35 @@ def test_spot_ticks_match_oracle(E, refit_every):
         assert got["n"] == rthr["n"] and got["n_peaks"] == rthr["n_peaks"], (k, got, rthr)
         assert got["t"] == rthr["t"]
         assert abs(got["z_q"] - rthr["z_q"]) <= 1e-9 * rthr["z_q"], (k, got["z_q"], rthr["z_q"])
+
+
+def test_spot_capacity_overflow_reported(E):
+    """Peaks beyond the SPOT capacity are not silently dropped: the refit after
+    the overflow (and every later one) reports ENOVA_ERR_WORKSPACE with a NaN
+    z_q instead of fitting the truncated peak set; a new calibration clears it."""
+    init = synth.score_mixture(50_000, seed=31)
+    spot = E.Spot(50_000, stream_peaks=100)
+    spot.calibrate(cuda(init))
+    base = spot.threshold()
+    t = base["t"]
+    tick = cuda(np.full(300, t + 0.5, np.float32))        # 300 normal peaks > capacity 100
+    spot.update(tick, torch.zeros(300, dtype=torch.int8, device="cuda"))
+    spot.refit()
+    with pytest.raises(E.EnovaError):
+        spot.threshold()
+    raw = spot.thr.cpu().numpy().tobytes()
+    from paper_2407_09486_b200._lib import Threshold
+    th = Threshold.from_buffer_copy(raw)
+    assert math.isnan(th.z_q) and th.reserved == 9      # ENOVA_ERR_WORKSPACE
+    spot.refit()                                          # still reported
+    with pytest.raises(E.EnovaError):
+        spot.threshold()
+    spot.calibrate(cuda(init))                            # a new calibration clears it
+    assert spot.threshold()["z_q"] == base["z_q"]
+    # within capacity: no error
+    spot.update(cuda(np.full(50, t + 0.5, np.float32)), torch.zeros(50, dtype=torch.int8, device="cuda"))
+    spot.refit()
+    assert spot.threshold()["n_peaks"] == base["n_peaks"] + 50
 
 
 # ------------------------------------------------------- full-size configs ----
