@@ -30,7 +30,7 @@
  *    ENOVA_ERR_NCCL; enova_last_error() returns a thread-local detail string.
  *    No C++ exception crosses the ABI.
  *  - Fast-path envelope (else ENOVA_ERR_UNSUPPORTED, there is no fallback):
- *    M == 8 or M % 16 == 0 (M <= 64); W even, 2 <= W <= 256; H in {32, 64, 128};
+ *    M in {8, 16, 32, 64}; W even, 2 <= W <= 256; H in {32, 64, 128};
  *    1 <= Z <= 16.
  *  - Precision is part of the contract (R-17): the detector is defined on fp16
  *    tensor-core operands.  enc_w1, enc_wmu, enc_wlv and dec_w1 are rounded to
@@ -361,6 +361,21 @@ enova_status enova_comm_create_local(enova_comm_t *comms, int world, int device)
  * it allocates and frees 256 B of device scratch, so keep it off the hot path). */
 enova_status enova_comm_sum_i64(enova_comm_t comm, int64_t in, int64_t *out, void *stream);
 void enova_comm_destroy(enova_comm_t comm);
+/* Failure handling of the fleet collectives (SURVEY §5, §8b conventions).
+ * Every host-side wait on a communicator is bounded by its timeout (default
+ * 300 s; enova_comm_set_timeout, seconds > 0): enova_fit_threshold with a
+ * communicator, enova_comm_sum_i64 and enova_comm_wait poll the stream and
+ * ncclCommGetAsyncError instead of blocking in cudaStreamSynchronize.  An
+ * asynchronous NCCL error or an expired timeout (a peer rank died or stalled)
+ * aborts the communicator (ncclCommAbort: no rank stays blocked in a
+ * collective) and returns ENOVA_ERR_NCCL; every later call on it returns
+ * ENOVA_ERR_NCCL too, and enova_comm_destroy only frees the handle.  The local
+ * backend bounds its host rendezvous the same way.
+ * enova_comm_wait(comm, stream): bounded wait for the work enqueued on `stream`
+ * (e.g. a captured fleet step replayed with fit_threshold_comm_async inside)
+ * before reading its results on the host. */
+enova_status enova_comm_set_timeout(enova_comm_t comm, double seconds);
+enova_status enova_comm_wait(enova_comm_t comm, void *stream);
 
 /* ------------------------------------------------------------- misc ---- */
 const char *enova_status_string(enova_status s);

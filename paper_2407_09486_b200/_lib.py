@@ -32,7 +32,7 @@ EXPORTS = (
     "enova_spot_update", "enova_spot_refit", "enova_stream_step",
     "enova_threshold_comm_workspace_bytes", "enova_fit_threshold_comm_async",
     "enova_comm_create_local", "enova_comm_sum_i64", "enova_set_score_kernel",
-    "enova_flag_scores_async",
+    "enova_flag_scores_async", "enova_comm_set_timeout", "enova_comm_wait",
 )
 
 
@@ -125,6 +125,8 @@ def lib() -> C.CDLL:
             "enova_kernel_launches": (C.c_uint64, []),
             "enova_set_score_kernel": (C.c_int, [C.c_int]),
             "enova_flag_scores_async": (C.c_int, [vp, vp, i64, vp, vp, vp]),
+            "enova_comm_set_timeout": (C.c_int, [vp, dbl]),
+            "enova_comm_wait": (C.c_int, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

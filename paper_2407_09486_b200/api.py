@@ -571,6 +571,16 @@ class Comm:
         check(lib().enova_comm_create_local(hs, int(world), int(device)))
         return [Comm(hs[r], r, world, local=True) for r in range(world)]
 
+    def set_timeout(self, seconds: float):
+        """Bound of every host-side wait on this communicator (default 300 s)."""
+        check(lib().enova_comm_set_timeout(C.c_void_p(self.handle), float(seconds)))
+
+    def wait(self, stream=None):
+        """Bounded wait for the work enqueued on `stream`: a dead peer or an async
+        NCCL error raises ENOVA_ERR_NCCL (the communicator is aborted) instead of
+        hanging."""
+        check(lib().enova_comm_wait(C.c_void_p(self.handle), _stream_ptr(stream)))
+
     def sum_i64(self, value: int, stream=None) -> int:
         """Synchronous sum of one integer over the ranks (collective)."""
         out = C.c_int64()
@@ -725,6 +735,8 @@ class Pipeline:
         self.graph.replay()
 
     def result(self) -> PipelineResult:
+        if self.comm is not None and not self.comm.local:
+            self.comm.wait()          # bounded: a dead peer raises instead of hanging
         nd = check_stats_diag(self.diag)
         thr = threshold_from_device(self.thr)
         return PipelineResult(self.mean, self.std, nd, self.cal, thr, self.flags, self.scores,

@@ -88,7 +88,7 @@ static enova_status check_detector(const enova_detector *det, DetLayout *L) {
     return ENOVA_ERR_INVALID_ARGUMENT;
   }
   if (!det_layout(det->window, det->n_metrics, det->hidden, det->latent, L)) {
-    set_error("detector shape outside the fast-path envelope (M==8 or M%16==0<=64, W even "
+    set_error("detector shape outside the fast-path envelope (M in {8, 16, 32, 64}, W even "
               "2..256, H in {32,64,128}, 1<=Z<=16)");
     return ENOVA_ERR_UNSUPPORTED;
   }

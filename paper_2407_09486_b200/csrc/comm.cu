@@ -6,13 +6,17 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "common.cuh"
 
 namespace {
+
+constexpr double kDefaultCommTimeoutS = 300.0;
 
 typedef int ncclResult_t;
 typedef void *ncclComm_t;
@@ -21,6 +25,7 @@ struct ncclUniqueId {
 };
 enum { ncclInt64 = 4, ncclUint64 = 5, ncclFloat32 = 7, ncclFloat64 = 8 };
 enum { ncclSum = 0 };
+enum { ncclSuccess = 0, ncclInProgress = 7 };
 
 struct Nccl {
   bool ok = false;
@@ -34,6 +39,8 @@ struct Nccl {
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   const char *(*GetErrorString)(ncclResult_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
+  ncclResult_t (*CommAbort)(ncclComm_t);
 };
 
 Nccl &nccl() {
@@ -61,6 +68,8 @@ Nccl &nccl() {
     SYM(GroupStart, "ncclGroupStart");
     SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
+    SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    SYM(CommAbort, "ncclCommAbort");
 #undef SYM
     n.ok = true;
   });
@@ -86,24 +95,41 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0;
   unsigned long long gen = 0;
+  bool broken = false;               // a rank timed out at a rendezvous: the group is dead
   const void *src[kMaxLocal] = {};
   cudaEvent_t ready[kMaxLocal] = {}, done[kMaxLocal] = {};
   void *stage[kMaxLocal] = {};
   std::mutex coop_m;                 // held from comm_coop_begin to comm_coop_end
   cudaEvent_t coop_last = nullptr;   // completion of the previous cooperative launch
   bool coop_recorded = false;
-  void barrier() {
+  // host rendezvous of the ranks, bounded by timeout_s: false if a rank did not
+  // arrive in time (the group is then broken for every rank)
+  bool barrier(double timeout_s) {
     std::unique_lock<std::mutex> l(m);
+    if (broken) return false;
     const unsigned long long g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(l, [&] { return gen != g; });
+      return true;
     }
+    const bool ok = cv.wait_for(l, std::chrono::duration<double>(timeout_s),
+                                [&] { return gen != g || broken; });
+    if (!ok || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
 };
+
+static enova_status local_broken(enova_comm_t c) {
+  c->aborted = true;
+  set_error("local communicator: a rank did not reach the rendezvous within the timeout");
+  return ENOVA_ERR_NCCL;
+}
 
 struct LocalSrcs {
   const unsigned long long *p[kMaxLocal];
@@ -126,7 +152,7 @@ static enova_status local_enter(enova_comm_t c, const void *send, cudaStream_t s
   LocalGroup *G = c->local;
   G->src[c->rank] = send;
   ENOVA_CUDA_TRY(cudaEventRecord(G->ready[c->rank], st));
-  G->barrier();
+  if (!G->barrier(c->timeout_s)) return local_broken(c);
   for (int q = 0; q < G->world; ++q) ENOVA_CUDA_TRY(cudaStreamWaitEvent(st, G->ready[q], 0));
   return ENOVA_OK;
 }
@@ -136,7 +162,7 @@ static enova_status local_enter(enova_comm_t c, const void *send, cudaStream_t s
 static enova_status local_leave(enova_comm_t c, cudaStream_t st) {
   LocalGroup *G = c->local;
   ENOVA_CUDA_TRY(cudaEventRecord(G->done[c->rank], st));
-  G->barrier();
+  if (!G->barrier(c->timeout_s)) return local_broken(c);
   for (int q = 0; q < G->world; ++q) ENOVA_CUDA_TRY(cudaStreamWaitEvent(st, G->done[q], 0));
   return ENOVA_OK;
 }
@@ -179,14 +205,76 @@ static enova_status local_allreduce_u64(enova_comm_t c, const void *send, void *
 }
 
 // ------------------------------------------------------------- public ----
+static enova_status check_alive(enova_comm_t c) {
+  if (c->aborted) {
+    set_error("communicator was aborted after an earlier failure or timeout");
+    return ENOVA_ERR_NCCL;
+  }
+  return ENOVA_OK;
+}
+
+static void abort_comm(enova_comm_t c) {
+  if (!c->aborted && c->nccl && nccl().ok) nccl().CommAbort(c->nccl);
+  c->aborted = true;
+}
+
+enova_status comm_wait(enova_comm_t c, cudaStream_t st) {
+  if (enova_status r = check_alive(c)) return r;
+  cudaEvent_t ev;
+  ENOVA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(ev, st);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    set_error(std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+    return ENOVA_ERR_CUDA;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  enova_status out = ENOVA_OK;
+  while (true) {
+    e = cudaEventQuery(ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) {
+      set_error(std::string("stream failed while waiting on the communicator: ") +
+                cudaGetErrorString(e));
+      out = ENOVA_ERR_CUDA;
+      break;
+    }
+    if (c->nccl) {
+      ncclResult_t ae = ncclSuccess;
+      const ncclResult_t qr = nccl().CommGetAsyncError(c->nccl, &ae);
+      if (qr != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+        set_error(std::string("NCCL asynchronous error: ") +
+                  nccl().GetErrorString(qr != ncclSuccess ? qr : ae));
+        abort_comm(c);
+        out = ENOVA_ERR_NCCL;
+        break;
+      }
+    }
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > c->timeout_s) {
+      set_error("communicator wait exceeded its timeout (a peer rank is gone or stalled); "
+                "communicator aborted");
+      abort_comm(c);
+      out = ENOVA_ERR_NCCL;
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  cudaEventDestroy(ev);
+  return out;
+}
+
 enova_status comm_allreduce_u64_sum(enova_comm_t c, const void *send, void *recv, size_t count,
                                     cudaStream_t st) {
+  if (enova_status r0 = check_alive(c)) return r0;
   if (c->local) return local_allreduce_u64(c, send, recv, count, st);
   ncclResult_t r = nccl().AllReduce(send, recv, count, ncclUint64, ncclSum, c->nccl, st);
   return r ? nccl_fail(r, "ncclAllReduce") : ENOVA_OK;
 }
 
 enova_status comm_allgather_i64(enova_comm_t c, const void *send, void *recv, cudaStream_t st) {
+  if (enova_status r0 = check_alive(c)) return r0;
   if (c->local) return local_allgather(c, send, recv, 8, st);
   ncclResult_t r = nccl().AllGather(send, recv, 1, ncclInt64, c->nccl, st);
   return r ? nccl_fail(r, "ncclAllGather") : ENOVA_OK;
@@ -194,6 +282,7 @@ enova_status comm_allgather_i64(enova_comm_t c, const void *send, void *recv, cu
 
 enova_status comm_allgather_f32(enova_comm_t c, const void *send, void *recv, size_t count,
                                 cudaStream_t st) {
+  if (enova_status r0 = check_alive(c)) return r0;
   if (c->local) return local_allgather(c, send, recv, count * 4, st);
   ncclResult_t r = nccl().AllGather(send, recv, count, ncclFloat32, c->nccl, st);
   return r ? nccl_fail(r, "ncclAllGather") : ENOVA_OK;
@@ -234,7 +323,7 @@ enova_status comm_sum_i64_sync(enova_comm_t c, int64_t in, int64_t *out, void *s
   enova_status r = comm_allreduce_u64_sum(c, scratch, scratch, 1, st);
   if (r) return r;
   ENOVA_CUDA_TRY(cudaMemcpyAsync(&v, scratch, 8, cudaMemcpyDeviceToHost, st));
-  ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+  if ((r = comm_wait(c, st))) return r;
   *out = (int64_t)v;
   return ENOVA_OK;
 }
@@ -242,6 +331,23 @@ enova_status comm_sum_i64_sync(enova_comm_t c, int64_t in, int64_t *out, void *s
 }  // namespace enova
 
 extern "C" {
+
+enova_status enova_comm_set_timeout(enova_comm_t comm, double seconds) {
+  if (!comm || !(seconds > 0.0)) {
+    enova::set_error("enova_comm_set_timeout: comm required, seconds > 0");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  comm->timeout_s = seconds;
+  return ENOVA_OK;
+}
+
+enova_status enova_comm_wait(enova_comm_t comm, void *stream) {
+  if (!comm) {
+    enova::set_error("enova_comm_wait: comm is NULL");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  return enova::comm_wait(comm, static_cast<cudaStream_t>(stream));
+}
 
 enova_status enova_comm_unique_id(void *out128) {
   if (!out128) {
@@ -283,6 +389,8 @@ enova_status enova_comm_create(enova_comm_t *comm, int rank, int world, const vo
   h->rank = rank;
   h->world = world;
   h->device = device;
+  h->timeout_s = kDefaultCommTimeoutS;
+  h->aborted = false;
   *comm = h;
   return ENOVA_OK;
 }
@@ -329,6 +437,8 @@ enova_status enova_comm_create_local(enova_comm_t *comms, int world, int device)
     h->rank = q;
     h->world = world;
     h->device = device;
+    h->timeout_s = kDefaultCommTimeoutS;
+    h->aborted = false;
     comms[q] = h;
   }
   return ENOVA_OK;
@@ -352,8 +462,8 @@ void enova_comm_destroy(enova_comm_t comm) {
       if (G->coop_last) cudaEventDestroy(G->coop_last);
       delete G;
     }
-  } else if (nccl().ok && comm->nccl) {
-    nccl().CommDestroy(comm->nccl);
+  } else if (nccl().ok && comm->nccl && !comm->aborted) {
+    nccl().CommDestroy(comm->nccl);   // (an aborted communicator is already freed)
   }
   delete comm;
 }

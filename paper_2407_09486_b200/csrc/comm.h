@@ -23,6 +23,8 @@ struct enova_comm_s {
   void *nccl;                 // ncclComm_t (NCCL backend), else null
   enova::LocalGroup *local;   // local backend, else null
   int rank, world, device;
+  double timeout_s;           // bound of every host-side wait on this communicator
+  bool aborted;               // a failure or timeout aborted it: every later call fails
 };
 
 namespace enova {
@@ -40,6 +42,11 @@ enova_status comm_allgather_f32(enova_comm_t c, const void *send, void *recv, si
 // No-ops for NCCL (one rank per device).
 enova_status comm_coop_begin(enova_comm_t c, cudaStream_t st);
 enova_status comm_coop_end(enova_comm_t c, cudaStream_t st);
+// Bounded host wait for everything enqueued on `st` so far: polls the stream and,
+// for NCCL, ncclCommGetAsyncError; an asynchronous NCCL error or a wait longer
+// than the communicator's timeout aborts the communicator (ncclCommAbort, so no
+// rank stays blocked inside a collective) and returns ENOVA_ERR_NCCL.
+enova_status comm_wait(enova_comm_t c, cudaStream_t st);
 // synchronous sum of one host int64 over the ranks (setup-time use); scratch:
 // >= 8 bytes of device memory
 enova_status comm_sum_i64_sync(enova_comm_t c, int64_t in, int64_t *out, void *scratch,

@@ -26,7 +26,10 @@ struct DetLayout {
 
 // Returns false if the detector is outside the fast-path envelope.
 static inline bool det_layout(int W, int M, int H, int Z, DetLayout *L) {
-  if (!(M == 8 || (M % 16 == 0 && M <= 64))) return false;
+  // M / 4 metric groups must be a power of two: the staging threads of the
+  // score kernels map (sample, group) by shifts and reduce a sample's groups with
+  // an xor-shuffle tree (M = 48 was accepted before round 2 and scored wrongly)
+  if (!(M == 8 || M == 16 || M == 32 || M == 64)) return false;
   if (W < 2 || W > 256 || (W % 2) != 0) return false;
   if (!(H == 32 || H == 64 || H == 128)) return false;
   if (Z < 1 || Z > 16) return false;

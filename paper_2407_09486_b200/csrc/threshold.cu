@@ -1401,7 +1401,7 @@ enova_status fit_threshold(const float *scores, int64_t n_local, double q0, doub
                                       n_global_max, st)))
       return r;
     ENOVA_CUDA_TRY(cudaMemcpyAsync(out, od, sizeof(*out), cudaMemcpyDeviceToHost, st));
-    ENOVA_CUDA_TRY(cudaStreamSynchronize(st));
+    if ((r = comm_wait(comm, st))) return r;   // bounded: a dead peer -> ENOVA_ERR_NCCL
     if ((r = status_error(out->reserved))) return r;
     out->reserved = 0;
     return ENOVA_OK;

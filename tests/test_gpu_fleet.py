@@ -214,3 +214,43 @@ def test_local_comm_c2_scale_fleet_threshold(E):
             c.destroy()
     assert all(x == single for x in res)
     assert single["n"] == n_inst * per and single["n_peaks"] >= 10
+
+
+def test_dead_peer_times_out_instead_of_hanging(E):
+    """A rank that never reaches the collective (a dead peer): the waiting rank's
+    fleet threshold returns ENOVA_ERR_NCCL once the communicator's timeout
+    expires, the communicator is aborted, and every later call fails fast
+    (include/enova.h failure handling; SURVEY §5 failure detection)."""
+    import time
+    comms = E.Comm.create_local(2)
+    try:
+        for c in comms:
+            c.set_timeout(1.0)
+        s = torch.from_numpy(synth.score_mixture(100_000, seed=5)).cuda()
+        t0 = time.monotonic()
+        with pytest.raises(E.EnovaError) as ei:
+            E.fit_threshold(s, 0.98, 1e-3, comm=comms[0], n_global_max=200_000)   # rank 1 absent
+        assert ei.value.name == "ENOVA_ERR_NCCL"
+        assert time.monotonic() - t0 < 30
+        with pytest.raises(E.EnovaError) as ei:
+            comms[0].sum_i64(1)
+        assert ei.value.name == "ENOVA_ERR_NCCL"
+        with pytest.raises(E.EnovaError) as ei:
+            comms[0].set_timeout(0.0)
+        assert ei.value.name == "ENOVA_ERR_INVALID_ARGUMENT"
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()
+
+
+def test_nccl_world1_wait_ok(E):
+    comm = E.Comm.create(0, 1, torch.cuda.current_device())
+    try:
+        comm.set_timeout(30.0)
+        x = torch.ones(1 << 20, device="cuda")
+        (x * 2).sum()
+        comm.wait()                     # bounded wait on the current stream: returns
+        assert comm.sum_i64(7) == 7
+    finally:
+        comm.destroy()
