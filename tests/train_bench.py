@@ -1,0 +1,64 @@
+"""The NEXT-3 detection benchmark protocol (R-25):
+test helpers shared by the oracle test and the GPU test (data preparation and
+evaluation bookkeeping only -- no method arithmetic beyond calling the
+implementations under test).
+
+  * trace: synth.spec_benchmark(N, T) -- correlated 8-dim Gaussian normals,
+    level-shift anomaly segments (~1% of points), half of the segments labelled;
+  * detector: W = 2 windows of the M = 8 metrics, H = 32, Z = 4 (SPEC S:547's
+    7 -> 32 -> 4 network on Table II's metrics + KV);
+  * training set: every window ending in [W-1, T_cal), l = -1 if its end point
+    lies in a LABELLED anomaly segment, else +1 (unlabelled anomalies stay +1:
+    the contamination Eq. 9 is designed for);
+  * threshold: POT (q0 = 0.98, q = 1e-3) on the scores of the calibration
+    windows whose end point is normal ("normal calibration data");
+  * evaluation: flags of the windows ending in [T_cal, T) against the labels at
+    their end times, point-adjusted, and the false-positive
+    rate on the normal detection points (<= 2 q).
+"""
+import numpy as np
+
+from paper_2407_09486_b200 import synth
+
+W, M, H, Z = 2, 8, 32, 4
+N, T = 16, 8000
+TCAL = T // 2
+SEED = 0x5EC
+
+
+def data():
+    X, lab, tl = synth.spec_benchmark(N, T, seed=SEED, return_train_labels=True)
+    return X, lab, tl
+
+
+def train_labels(tl):
+    """l per calibration window (ending at t in [W-1, TCAL)), flattened [N * nw]."""
+    return tl[:, W - 1:TCAL].astype(np.float64).reshape(-1)
+
+
+def normal_cal_mask(lab):
+    return (lab[:, W - 1:TCAL] == 0)
+
+
+def schedule(n_windows, epochs, batch):
+    """(order, n_steps): the epochs' permutations concatenated, each epoch padded
+    with -1 to a whole number of batches."""
+    per = -(-n_windows // batch) * batch
+    order = np.full(epochs * per, -1, dtype=np.int64)
+    for e in range(epochs):
+        order[e * per:e * per + n_windows] = synth.epoch_order(n_windows, SEED, e)
+    return order, epochs * per // batch
+
+
+def noise(n_steps, batch):
+    return np.concatenate([synth.noise_normal(batch, Z, SEED, s) for s in range(n_steps)])
+
+
+def evaluate(flags, lab, q=1e-3):
+    from oracle import enova_oracle as O
+    tp, fp, fn, tn = O.fleet_point_adjusted_counts(lab, flags, TCAL)
+    p, r, f1 = O.precision_recall_f1(tp, fp, fn)
+    normal = lab[:, TCAL:TCAL + flags.shape[1]] == 0
+    fpr = float((flags[normal] != 0).mean())
+    return dict(tp=tp, fp=fp, fn=fn, tn=tn, precision=p, recall=r, f1=f1, fp_rate_normal=fpr,
+                fp_rate_bound=2 * q)
