@@ -341,6 +341,63 @@ enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels
                                          int64_t t_begin, int64_t n_windows,
                                          uint64_t *counts_dev, void *stream);
 
+/* ------------------------------------------------------ NEXT-3, training ----
+ * Semi-supervised training of the detector by Eq. 9:
+ *   L = 1/B sum_i l_i log p(x_i | z_i) - (1 + l_i)/2 beta(k) KL(q(z|x_i) || N(0, I))
+ * with l_i = +1 (normal or unlabelled) / -1 (labelled anomaly), the single-sample
+ * reparameterised z_i = mu_i + exp(lv_i / 2) eps_i (eps an input, device fp32
+ * [batch][latent]), the unit-variance Gaussian likelihood log p = -1/2 ||x -
+ * m'(z)||^2 - D/2 log 2 pi and beta(k) from a PI controller
+ * on the batch's mean KL of normal rows (R-24):
+ *   e = KL - kl_setpoint, I += e while unclamped, beta = clamp(kp e + ki I, 0, beta_max)
+ * (beta_mode 1: beta = beta_fixed).  Adam ascent on L (lr, adam_beta1/2,
+ * adam_eps).  A window row is the score kernels' detector input x of the window
+ * with id g = instance * nw + (t - t_begin) of the series range (nw = t_end -
+ * t_begin); ids < 0 or >= n_instances * nw are padding rows (ignored; B counts
+ * the valid rows).  The trainer owns its fp32 master parameters, Adam moments,
+ * PI state, activations (max_batch rows) and a cuBLAS handle -- all allocated
+ * at create (setup time; the step never allocates).  The GEMMs run in cuBLAS
+ * (fp32 FFMA by default; enova_trainer_set_math(t, 1) allows TF32 tensor cores);
+ * the element-wise / row-wise work and every reduction are the library's own
+ * deterministic kernels.  All calls are stream-ordered on `stream`.
+ *   enova_trainer_load:  parameters <- det (device fp32 tensors, include layouts);
+ *                        Adam moments, step count and PI integral reset, beta = beta0.
+ *   enova_trainer_store: parameters -> det's tensors (device fp32, WRITTEN).
+ *   enova_train_step:    one Eq. 9 step on the `batch` rows ids (device int64)
+ *                        with labels indexed BY WINDOW ID (device int8 [n_instances
+ *                        * nw], +1 / -1) and eps, then Adam + PI update; stats_out (optional, device
+ *                        fp64 [4]) = {L, beta used, mean KL of normal rows, their
+ *                        mean log p - KL}.
+ *   enova_train_gradient: dL/dtheta at the given beta, no update (parity checks):
+ *                        grad_out device fp32 [enova_trainer_param_offsets(t, off)]
+ *                        with tensor i of (enc_w1, enc_b1, enc_wmu, enc_bmu, enc_wlv,
+ *                        enc_blv, dec_w1, dec_b1, dec_w2, dec_b2) at offset off[i].
+ * Errors: ENOVA_ERR_INVALID_ARGUMENT for shapes / NULL inputs / batch outside
+ * [1, max_batch]; ENOVA_ERR_CUDA for allocation, cuBLAS or launch failures. */
+typedef struct enova_trainer_s *enova_trainer_t;
+typedef struct {
+  double lr, adam_beta1, adam_beta2, adam_eps;
+  double kl_setpoint, kp, ki, beta_max;
+  int32_t beta_mode;        /* 0 = PI controller, 1 = fixed beta_fixed */
+  int32_t reserved;
+  double beta_fixed;
+} enova_train_config;
+enova_status enova_trainer_create(enova_trainer_t *out, int32_t window, int32_t n_metrics,
+                                  int32_t hidden, int32_t latent, int32_t max_batch, int device);
+void enova_trainer_destroy(enova_trainer_t t);
+int64_t enova_trainer_param_offsets(enova_trainer_t t, int64_t *offsets10);
+enova_status enova_trainer_set_math(enova_trainer_t t, int32_t math);
+enova_status enova_trainer_load(enova_trainer_t t, const enova_detector *det, double beta0,
+                                void *stream);
+enova_status enova_trainer_store(enova_trainer_t t, const enova_detector *det, void *stream);
+enova_status enova_train_step(enova_trainer_t t, const enova_series *series, const int64_t *ids,
+                              const int8_t *labels, int32_t batch, const float *eps,
+                              const enova_train_config *cfg, double *stats_out, void *stream);
+enova_status enova_train_gradient(enova_trainer_t t, const enova_series *series,
+                                  const int64_t *ids, const int8_t *labels, int32_t batch,
+                                  const float *eps, double beta, float *grad_out,
+                                  double *stats_out, void *stream);
+
 /* ------------------------------------------------------------ comm (§8e) ----
  * NCCL communicator for the fleet-wide threshold.  Rank 0 creates the 128-byte
  * unique id; the caller broadcasts it (e.g. torch.distributed) and every rank

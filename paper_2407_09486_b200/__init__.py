@@ -14,7 +14,7 @@ __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold"
            "threshold_from_device", "threshold_to_device", "check_stats_diag", "Pipeline",
            "StatsWorkspace", "StreamRing", "point_adjusted_counts", "point_adjusted_f1", "select_flagged",
            "explain_windows", "Spot", "force_score_kernel",
-           "flag_scores_async"]
+           "flag_scores_async", "Trainer", "train_config"]
 
 
 def __getattr__(name):

@@ -33,6 +33,9 @@ EXPORTS = (
     "enova_threshold_comm_workspace_bytes", "enova_fit_threshold_comm_async",
     "enova_comm_create_local", "enova_comm_sum_i64", "enova_set_score_kernel",
     "enova_flag_scores_async", "enova_comm_set_timeout", "enova_comm_wait",
+    "enova_trainer_create", "enova_trainer_destroy", "enova_trainer_param_offsets",
+    "enova_trainer_set_math", "enova_trainer_load", "enova_trainer_store", "enova_train_step",
+    "enova_train_gradient",
 )
 
 
@@ -51,6 +54,13 @@ class Detector(C.Structure):
                 ("enc_wlv", C.c_void_p), ("enc_blv", C.c_void_p),
                 ("dec_w1", C.c_void_p), ("dec_b1", C.c_void_p),
                 ("dec_w2", C.c_void_p), ("dec_b2", C.c_void_p)]
+
+
+class TrainConfig(C.Structure):
+    _fields_ = [("lr", C.c_double), ("adam_beta1", C.c_double), ("adam_beta2", C.c_double),
+                ("adam_eps", C.c_double), ("kl_setpoint", C.c_double), ("kp", C.c_double),
+                ("ki", C.c_double), ("beta_max", C.c_double), ("beta_mode", C.c_int32),
+                ("reserved", C.c_int32), ("beta_fixed", C.c_double)]
 
 
 class Series(C.Structure):
@@ -126,6 +136,14 @@ def lib() -> C.CDLL:
             "enova_set_score_kernel": (C.c_int, [C.c_int]),
             "enova_flag_scores_async": (C.c_int, [vp, vp, i64, vp, vp, vp]),
             "enova_comm_set_timeout": (C.c_int, [vp, dbl]),
+            "enova_trainer_create": (C.c_int, [P(vp), i32, i32, i32, i32, i32, C.c_int]),
+            "enova_trainer_destroy": (None, [vp]),
+            "enova_trainer_param_offsets": (i64, [vp, P(i64)]),
+            "enova_trainer_set_math": (C.c_int, [vp, i32]),
+            "enova_trainer_load": (C.c_int, [vp, P(Detector), dbl, vp]),
+            "enova_trainer_store": (C.c_int, [vp, P(Detector), vp]),
+            "enova_train_step": (C.c_int, [vp, P(Series), vp, vp, i32, vp, P(TrainConfig), vp, vp]),
+            "enova_train_gradient": (C.c_int, [vp, P(Series), vp, vp, i32, vp, dbl, vp, vp, vp]),
             "enova_comm_wait": (C.c_int, [vp, vp]),
         }
         for name, (res, args) in sig.items():

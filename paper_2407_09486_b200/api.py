@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Detector, Series, Threshold, check, lib
+from ._lib import Detector, Series, Threshold, TrainConfig, check, lib
 
 _WEIGHT_KEYS = ("enc_w1", "enc_b1", "enc_wmu", "enc_bmu", "enc_wlv", "enc_blv",
                 "dec_w1", "dec_b1", "dec_w2", "dec_b2")
@@ -741,3 +741,137 @@ class Pipeline:
         thr = threshold_from_device(self.thr)
         return PipelineResult(self.mean, self.std, nd, self.cal, thr, self.flags, self.scores,
                               self.md, self.cal_md, self.cal_flags)
+
+
+# ------------------------------------------------------------------ NEXT-3 ----
+TRAIN_PARAMS = _WEIGHT_KEYS
+
+
+def train_config(lr=1e-3, latent=4, kl_setpoint=None, kp=0.01, ki=0.001, beta_max=1.0,
+                 beta_fixed=None, adam_beta1=0.9, adam_beta2=0.999, adam_eps=1e-8) -> TrainConfig:
+    """Eq. 9 training constants (SPEC.md:548-550 defaults; R-24): PI
+    setpoint 0.5 * latent nats unless given; beta_fixed switches the PI off."""
+    c = TrainConfig()
+    c.lr, c.adam_beta1, c.adam_beta2, c.adam_eps = lr, adam_beta1, adam_beta2, adam_eps
+    c.kl_setpoint = 0.5 * latent if kl_setpoint is None else kl_setpoint
+    c.kp, c.ki, c.beta_max = kp, ki, beta_max
+    c.beta_mode = 0 if beta_fixed is None else 1
+    c.beta_fixed = 0.0 if beta_fixed is None else beta_fixed
+    return c
+
+
+class Trainer:
+    """NEXT-3: Eq. 9 training state on one GPU (enova_trainer_*): fp32 master
+    parameters, Adam moments, the PI-controlled beta, activations for up to
+    max_batch windows, and a cuBLAS handle for the GEMMs."""
+
+    def __init__(self, window: int, n_metrics: int, hidden: int, latent: int, max_batch: int,
+                 device=None):
+        dev = torch.device(device or "cuda")
+        self.device = dev
+        self.W, self.M, self.H, self.Z, self.max_batch = window, n_metrics, hidden, latent, max_batch
+        h = C.c_void_p()
+        check(lib().enova_trainer_create(C.byref(h), window, n_metrics, hidden, latent, max_batch,
+                                         dev.index if dev.index is not None else
+                                         torch.cuda.current_device()))
+        self.handle = h.value
+        off = (C.c_int64 * 10)()
+        self.n_params = int(lib().enova_trainer_param_offsets(C.c_void_p(self.handle), off))
+        self.offsets = list(off)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def _shapes(self):
+        D, H, Z = self.W * self.M, self.H, self.Z
+        return {"enc_w1": (H, D), "enc_b1": (H,), "enc_wmu": (Z, H), "enc_bmu": (Z,),
+                "enc_wlv": (Z, H), "enc_blv": (Z,), "dec_w1": (H, Z), "dec_b1": (H,),
+                "dec_w2": (D, H), "dec_b2": (D,)}
+
+    def _struct(self, tensors: dict) -> Detector:
+        return Detector(self.W, self.M, self.H, self.Z, *[tensors[k].data_ptr() for k in _WEIGHT_KEYS])
+
+    def set_math(self, tf32: bool):
+        check(lib().enova_trainer_set_math(C.c_void_p(self.handle), 1 if tf32 else 0))
+
+    def load(self, weights: dict, beta0: float = 0.0, stream=None):
+        t = {}
+        for k in _WEIGHT_KEYS:
+            v = weights[k]
+            if isinstance(v, np.ndarray):
+                v = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32))
+            t[k] = v.to(device=self.device, dtype=torch.float32).contiguous()
+        self._loaded = t          # keep alive until the stream-ordered copies ran
+        check(lib().enova_trainer_load(C.c_void_p(self.handle), C.byref(self._struct(t)),
+                                       float(beta0), _stream_ptr(stream)))
+
+    def weights(self, stream=None) -> dict:
+        """The current parameters as a detector weight dict (device fp32 tensors)."""
+        out = {k: torch.empty(sh, dtype=torch.float32, device=self.device)
+               for k, sh in self._shapes().items()}
+        check(lib().enova_trainer_store(C.c_void_p(self.handle), C.byref(self._struct(out)),
+                                        _stream_ptr(stream)))
+        out.update(window=self.W, n_metrics=self.M, hidden=self.H, latent=self.Z)
+        return out
+
+    def _args(self, metrics, mean, std, t_begin, t_end, ids, labels, eps):
+        s = _series(metrics, mean, std, t_begin, t_end)
+        _require_cuda(ids, "ids", torch.int64)
+        _require_cuda(labels, "labels", torch.int8)
+        _require_cuda(eps, "eps")
+        B = ids.numel()
+        if labels.numel() != s.n_instances * max(s.t_end - s.t_begin, 0) or eps.numel() != B * self.Z:
+            raise ValueError("ids [B], labels [n_windows of the range] (by window id), eps [B, latent]")
+        if not labels.is_contiguous() or not ids.is_contiguous() or not eps.is_contiguous():
+            raise ValueError("ids, labels and eps must be contiguous")
+        return s, B
+
+    def step(self, metrics, mean, std, t_begin, t_end, ids, labels, eps, cfg: TrainConfig,
+             stream=None):
+        s, B = self._args(metrics, mean, std, t_begin, t_end, ids, labels, eps)
+        check(lib().enova_train_step(C.c_void_p(self.handle), C.byref(s), C.c_void_p(ids.data_ptr()),
+                                     C.c_void_p(labels.data_ptr()), B, C.c_void_p(eps.data_ptr()),
+                                     C.byref(cfg), C.c_void_p(self.stats.data_ptr()),
+                                     _stream_ptr(stream)))
+        return self.stats
+
+    def gradient(self, metrics, mean, std, t_begin, t_end, ids, labels, eps, beta: float,
+                 stream=None) -> dict:
+        s, B = self._args(metrics, mean, std, t_begin, t_end, ids, labels, eps)
+        g = torch.empty(self.n_params, dtype=torch.float32, device=self.device)
+        check(lib().enova_train_gradient(C.c_void_p(self.handle), C.byref(s),
+                                         C.c_void_p(ids.data_ptr()), C.c_void_p(labels.data_ptr()),
+                                         B, C.c_void_p(eps.data_ptr()), float(beta),
+                                         C.c_void_p(g.data_ptr()), C.c_void_p(self.stats.data_ptr()),
+                                         _stream_ptr(stream)))
+        out = {}
+        for k, o in zip(_WEIGHT_KEYS, self.offsets):
+            sh = self._shapes()[k]
+            out[k] = g[o:o + int(np.prod(sh))].view(sh)
+        return out
+
+    def fit(self, metrics, mean, std, t_begin, t_end, labels_per_window: torch.Tensor,
+            order: torch.Tensor, eps: torch.Tensor, batch: int, cfg: TrainConfig,
+            history: bool = False, stream=None):
+        """Every step of a schedule: order [steps * batch] window ids (-1 = padding)
+        and eps [steps * batch, latent] (device), labels_per_window [n_windows] int8
+        (+1 / -1) of the series range.  Returns the per-step stats [steps, 4] (device)
+        when history is set."""
+        steps = order.numel() // batch
+        hist = torch.empty((steps, 4), dtype=torch.float64, device=self.device) if history else None
+        for k in range(steps):
+            sl = slice(k * batch, (k + 1) * batch)
+            st = self.step(metrics, mean, std, t_begin, t_end, order[sl], labels_per_window,
+                           eps[sl], cfg, stream=stream)
+            if hist is not None:
+                hist[k].copy_(st)
+        return hist
+
+    def destroy(self):
+        if getattr(self, "handle", None):
+            lib().enova_trainer_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:   # noqa: BLE001 -- interpreter shutdown
+            pass

@@ -72,7 +72,9 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
     with open(stamp, "w") as f:
         f.write(" ".join(extra))
     if _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lcudart"]
+        cuda_lib = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64")
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lcudart", "-lcublas",
+               "-L", cuda_lib, "-Xlinker", "-rpath", "-Xlinker", cuda_lib]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
