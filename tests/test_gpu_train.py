@@ -121,17 +121,17 @@ def test_spec_benchmark_f1_on_gpu(E):
     mean, std, _ = E.compute_stats(Xc, TB.TCAL)
     nw = TB.TCAL - (W - 1)
     l = cuda(TB.train_labels(tl).astype(np.int8))
-    order, steps = TB.schedule(X.shape[0] * nw, 10, 64)
-    eps = TB.noise(steps, 64)
+    order, steps = TB.schedule(X.shape[0] * nw, TB.EPOCHS, TB.BATCH)
+    eps = TB.noise(steps, TB.BATCH)
     w0 = synth.detector_weights(W, M, H, Z, seed=TB.SEED)
-    tr = E.Trainer(W, M, H, Z, max_batch=64)
-    cfg = E.train_config(lr=3e-3, latent=Z)
+    tr = E.Trainer(W, M, H, Z, max_batch=TB.BATCH)
+    cfg = E.train_config(lr=TB.LR, latent=Z)
     try:
         tr.load(w0)
         import time
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hist = tr.fit(Xc, mean, std, W - 1, TB.TCAL, l, cuda(order), cuda(eps), 64, cfg,
+        hist = tr.fit(Xc, mean, std, W - 1, TB.TCAL, l, cuda(order), cuda(eps), TB.BATCH, cfg,
                       history=True)
         torch.cuda.synchronize()
         train_s = time.perf_counter() - t0
@@ -146,7 +146,7 @@ def test_spec_benchmark_f1_on_gpu(E):
     pa = E.point_adjusted_f1(cuda(lab), flags, TB.TCAL)
     ev = TB.evaluate(flags.cpu().numpy(), lab)
     assert (pa["tp"], pa["fp"], pa["fn"], pa["tn"]) == (ev["tp"], ev["fp"], ev["fn"], ev["tn"])
-    rep = {"benchmark": "SPEC S:544 synthetic (16 x 8000, W=2, M=8, H=32, Z=4), 10 epochs, batch 64",
+    rep = {"benchmark": f"SPEC S:544 synthetic (16 x 8000, W=2, M=8, H=32, Z=4), {TB.EPOCHS} epochs, batch {TB.BATCH}, Adam {TB.LR}",
            "train_s": train_s, "steps": steps, "final_beta": float(hist[-1, 1]),
            "z_q": thr["z_q"], **ev}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -154,8 +154,8 @@ def test_training_curve_non_decreasing():
 
 
 def test_spec_benchmark_point_adjusted_f1():
-    """S:544 / S:701 at the oracle level: Eq. 9 training (10 epochs, batch 64,
-    Adam 3e-3, PI beta) on the synthetic benchmark's contaminated calibration
+    """S:544 / S:701 at the oracle level: Eq. 9 training (tests/train_bench.py
+    schedule: 30 epochs, batch 64, Adam 3e-3, PI beta) on the synthetic benchmark's contaminated calibration
     half with 50% of the anomaly segments labelled, POT on the normal
     calibration windows, then detection on the second half: point-adjusted
     F1 >= 0.90 and a held-out normal false-positive rate <= 2 q."""
@@ -166,9 +166,9 @@ def test_spec_benchmark_point_adjusted_f1():
     x = O.normalise_x16(X, mean, std)
     win = O.window_matrix(x, TB.W, TB.W - 1, TB.TCAL).reshape(-1, TB.W * TB.M)
     l = TB.train_labels(tl)
-    order, steps = TB.schedule(len(win), 10, 64)
+    order, steps = TB.schedule(len(win), TB.EPOCHS, TB.BATCH)
     w0 = synth.detector_weights(TB.W, TB.M, TB.H, TB.Z, seed=TB.SEED)
-    p, hist = T.train(w0, win, l, order, TB.noise(steps, 64), 64, lr=3e-3)
+    p, hist = T.train(w0, win, l, order, TB.noise(steps, TB.BATCH), TB.BATCH, lr=TB.LR)
     wts = dict(w0)
     wts.update({k: p[k].astype(np.float32) for k in T.PARAMS})
     cal, _ = O.score_windows(X, wts, mean, std, TB.W - 1, TB.TCAL)
