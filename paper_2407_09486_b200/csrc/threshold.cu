@@ -1245,11 +1245,6 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
     ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kMaxYCacheBytes));
-#ifdef ENOVA_POT_CARVEOUT
-    ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot,
-                                        cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        (int)cudaSharedmemCarveoutMaxShared));
-#endif
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   // the fit partitions N_t <= cap peaks into nb contiguous slices
