@@ -341,6 +341,54 @@ enova_status enova_point_adjusted_counts(const int8_t *labels, int64_t ld_labels
                                          int64_t t_begin, int64_t n_windows,
                                          uint64_t *counts_dev, void *stream);
 
+/* ------------------------------------------------------------ the step ----
+ * One pass of the whole hot path over one batch, as
+ * ONE stream-ordered, graph-capturable call: statistics over [0, t_cal_end) ->
+ * scores + MD of the calibration windows (ending in [W-1, t_cal_end)) -> the
+ * (fleet-wide with `comm`) POT threshold on them -> scores + MD of the
+ * detection windows (ending in [t_cal_end, T)) -> the flags of EVERY window
+ * (PAPER.md:282, 297).  The step object owns a high-priority side stream and
+ * two events (created at setup).  enova_step_configure(step, pot_ctas,
+ * concurrent_instances): pot_ctas = 0 runs the stages in sequence (the fit on
+ * every SM); pot_ctas > 0 (even) runs the fit on pot_ctas CTAs in 2-CTA
+ * clusters on the side stream while the detection scores of the first
+ * concurrent_instances instances run on the remaining TPCs, then the rest of
+ * the detection scores, then one flag launch for all windows.  Outputs are
+ * identical in both modes except for the fit's summation order (deterministic
+ * for a given pot_ctas).  All buffers are caller-owned device memory in the
+ * layouts of the single calls above (mean/std [N][M]; cal_* [N][t_cal_end-W+1];
+ * scores/md/flags [N][T-t_cal_end]; thr_dev an enova_threshold); stats_diag is
+ * the device int64[2] of enova_compute_stats_async.  n_global / n_global_max:
+ * the calibration score count over all ranks / the threshold workspace sizing
+ * (single GPU: both N*(t_cal_end-W+1) or larger).  Errors of the single calls
+ * propagate unchanged; the overlapped mode needs scores and md. */
+typedef struct enova_step_s *enova_step_t;
+typedef struct {
+  const enova_series *series;        /* metrics; norm_mean / norm_std / t_begin / t_end ignored */
+  int64_t t_cal_end;
+  const enova_detector *det;
+  const void *det_ws;
+  size_t det_ws_bytes;
+  double init_quantile, risk_q;
+  enova_comm_t comm;                 /* NULL = single GPU */
+  int64_t n_global, n_global_max;
+  float *mean, *std;
+  int64_t *stats_diag;
+  void *stats_ws;
+  size_t stats_ws_bytes;
+  float *cal_scores, *cal_md;
+  int8_t *cal_flags;
+  enova_threshold *thr_dev;
+  void *thr_ws;
+  size_t thr_ws_bytes;
+  float *scores, *md;
+  int8_t *flags;
+} enova_step_args;
+enova_status enova_step_create(enova_step_t *out, int device);
+enova_status enova_step_configure(enova_step_t step, int32_t pot_ctas, int64_t concurrent_instances);
+enova_status enova_step_enqueue(enova_step_t step, const enova_step_args *args, void *stream);
+void enova_step_destroy(enova_step_t step);
+
 /* ------------------------------------------------------ NEXT-3, training ----
  * Semi-supervised training of the detector by Eq. 9:
  *   L = 1/B sum_i l_i log p(x_i | z_i) - (1 + l_i)/2 beta(k) KL(q(z|x_i) || N(0, I))

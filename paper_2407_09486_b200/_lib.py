@@ -35,7 +35,8 @@ EXPORTS = (
     "enova_flag_scores_async", "enova_comm_set_timeout", "enova_comm_wait",
     "enova_trainer_create", "enova_trainer_destroy", "enova_trainer_param_offsets",
     "enova_trainer_set_math", "enova_trainer_load", "enova_trainer_store", "enova_train_step",
-    "enova_train_gradient",
+    "enova_train_gradient", "enova_step_create", "enova_step_configure", "enova_step_enqueue",
+    "enova_step_destroy",
 )
 
 
@@ -61,6 +62,18 @@ class TrainConfig(C.Structure):
                 ("adam_eps", C.c_double), ("kl_setpoint", C.c_double), ("kp", C.c_double),
                 ("ki", C.c_double), ("beta_max", C.c_double), ("beta_mode", C.c_int32),
                 ("reserved", C.c_int32), ("beta_fixed", C.c_double)]
+
+
+class StepArgs(C.Structure):
+    _fields_ = [("series", C.c_void_p), ("t_cal_end", C.c_int64), ("det", C.c_void_p),
+                ("det_ws", C.c_void_p), ("det_ws_bytes", C.c_size_t),
+                ("init_quantile", C.c_double), ("risk_q", C.c_double), ("comm", C.c_void_p),
+                ("n_global", C.c_int64), ("n_global_max", C.c_int64),
+                ("mean", C.c_void_p), ("std", C.c_void_p), ("stats_diag", C.c_void_p),
+                ("stats_ws", C.c_void_p), ("stats_ws_bytes", C.c_size_t),
+                ("cal_scores", C.c_void_p), ("cal_md", C.c_void_p), ("cal_flags", C.c_void_p),
+                ("thr_dev", C.c_void_p), ("thr_ws", C.c_void_p), ("thr_ws_bytes", C.c_size_t),
+                ("scores", C.c_void_p), ("md", C.c_void_p), ("flags", C.c_void_p)]
 
 
 class Series(C.Structure):
@@ -137,6 +150,10 @@ def lib() -> C.CDLL:
             "enova_flag_scores_async": (C.c_int, [vp, vp, i64, vp, vp, vp]),
             "enova_comm_set_timeout": (C.c_int, [vp, dbl]),
             "enova_trainer_create": (C.c_int, [P(vp), i32, i32, i32, i32, i32, C.c_int]),
+            "enova_step_create": (C.c_int, [P(vp), C.c_int]),
+            "enova_step_configure": (C.c_int, [vp, i32, i64]),
+            "enova_step_enqueue": (C.c_int, [vp, P(StepArgs), vp]),
+            "enova_step_destroy": (None, [vp]),
             "enova_trainer_destroy": (None, [vp]),
             "enova_trainer_param_offsets": (i64, [vp, P(i64)]),
             "enova_trainer_set_math": (C.c_int, [vp, i32]),

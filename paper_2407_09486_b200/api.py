@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Detector, Series, Threshold, TrainConfig, check, lib
+from ._lib import Detector, Series, StepArgs, Threshold, TrainConfig, check, lib
 
 _WEIGHT_KEYS = ("enc_w1", "enc_b1", "enc_wmu", "enc_bmu", "enc_wlv", "enc_blv",
                 "dec_w1", "dec_b1", "dec_w2", "dec_b2")
@@ -669,8 +669,13 @@ class Pipeline:
 
     def __init__(self, det: PreparedDetector, n_instances: int, n_steps: int, t_cal_end: int,
                  init_quantile: float = 0.98, risk_q: float = 1e-3, return_scores: bool = True,
-                 device=None, comm: "Comm | None" = None):
+                 device=None, comm: "Comm | None" = None, overlap: bool = True,
+                 pot_ctas: int = 32, concurrent_instances: int | None = None):
         dev = torch.device(device or "cuda")
+        # the overlapped step (enova_step: the fit on pot_ctas CTAs next to the
+        # detection scores) needs the detection scores and MD buffers
+        overlap = overlap and not (comm is not None and comm.local)
+        return_scores = return_scores or overlap
         W, M = det.window, det.n_metrics
         self.det, self.N, self.T, self.M, self.tcal = det, int(n_instances), int(n_steps), M, int(t_cal_end)
         self.q0, self.q = float(init_quantile), float(risk_q)
@@ -695,24 +700,53 @@ class Pipeline:
             self.thr_ws = ThresholdWorkspace(max(self.cal.numel(), 1), self.q0, dev)
         self.graph = None
         self._graph_input = None
+        h = C.c_void_p()
+        check(lib().enova_step_create(C.byref(h), dev.index if dev.index is not None
+                                      else torch.cuda.current_device()))
+        self._step = h.value
+        self.overlap = bool(overlap)
+        if concurrent_instances is None:
+            concurrent_instances = (2 * N) // 5 if overlap else 0
+        self.configure(pot_ctas if overlap else 0, concurrent_instances)
+
+    def configure(self, pot_ctas: int, concurrent_instances: int):
+        """Overlap of the fit with the detection scores (enova_step_configure):
+        pot_ctas = 0 runs the stages in sequence."""
+        check(lib().enova_step_configure(C.c_void_p(self._step), int(pot_ctas),
+                                         int(concurrent_instances)))
+        self.pot_ctas, self.concurrent_instances = int(pot_ctas), int(concurrent_instances)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_step", None):
+                lib().enova_step_destroy(C.c_void_p(self._step))
+                self._step = None
+        except Exception:   # noqa: BLE001 -- interpreter shutdown
+            pass
 
     def enqueue(self, metrics: torch.Tensor, stream=None):
+        """One step (enova_step_enqueue): stats -> calibration scores + MD -> fit
+        (fleet-wide with a communicator) -> detection scores + MD -> every flag."""
         if tuple(metrics.shape) != (self.N, self.T, self.M):
             raise ValueError(f"metrics must be [{self.N}, {self.T}, {self.M}]")
-        W = self.det.window
-        compute_stats_async(metrics, self.tcal, out=(self.mean, self.std), diag=self.diag,
-                            workspace=self.stats_ws, stream=stream)
-        score_windows(metrics, self.det, self.mean, self.std, W - 1, self.tcal,
-                      out=(self.cal, self.cal_md), stream=stream)
-        if self.comm is not None:
-            fit_threshold_comm_async(self.cal, self.n_global, self.comm, self.q0, self.q,
-                                     workspace=self.thr_ws, out=self.thr, stream=stream)
-        else:
-            fit_threshold_async(self.cal, self.q0, self.q, workspace=self.thr_ws, out=self.thr,
-                                stream=stream)
-        flag_scores_async(self.cal, self.cal_md, self.thr, out=self.cal_flags, stream=stream)
-        detect_async(metrics, self.det, self.mean, self.std, self.thr, self.tcal, self.T,
-                     out=(self.flags, self.scores, self.md), stream=stream)
+        s = _series(metrics)
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        a = StepArgs()
+        a.series = C.cast(C.pointer(s), C.c_void_p)
+        a.t_cal_end = self.tcal
+        a.det = C.cast(C.pointer(self.det.struct), C.c_void_p)
+        a.det_ws, a.det_ws_bytes = self.det.ws.data_ptr(), self.det.ws_bytes
+        a.init_quantile, a.risk_q = self.q0, self.q
+        a.comm = self.comm.handle if self.comm is not None else None
+        a.n_global, a.n_global_max = self.n_global, self.thr_ws.n_global_max
+        a.mean, a.std, a.stats_diag = ptr(self.mean), ptr(self.std), ptr(self.diag)
+        a.stats_ws, a.stats_ws_bytes = self.stats_ws.buf.data_ptr(), self.stats_ws.nbytes
+        a.cal_scores, a.cal_md, a.cal_flags = ptr(self.cal), ptr(self.cal_md), ptr(self.cal_flags)
+        a.thr_dev = ptr(self.thr)
+        a.thr_ws, a.thr_ws_bytes = self.thr_ws.buf.data_ptr(), self.thr_ws.nbytes
+        a.scores, a.md, a.flags = ptr(self.scores), ptr(self.md), ptr(self.flags)
+        self._args_keep = (s, a)
+        check(lib().enova_step_enqueue(C.c_void_p(self._step), C.byref(a), _stream_ptr(stream)))
 
     def capture(self, metrics: torch.Tensor):
         """Record one step on `metrics` (a fixed device buffer) into a CUDA graph."""

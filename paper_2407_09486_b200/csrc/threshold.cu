@@ -1236,6 +1236,16 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
 // ------------------------------------------------------------- driver ----
 constexpr int kMaxYCacheBytes = 160 * 1024;
 
+// Grid of the next fits (0 = one CTA per SM) and their cluster size: the step
+// orchestration (step.cu) runs a reduced fit grid next to the detection scores.
+// The result depends on the grid only through the fit's summation order
+// (deterministic for a given grid, within the parity tolerance of any other).
+static thread_local int g_pot_ctas = 0, g_pot_cluster = 0;
+void set_pot_grid(int ctas, int cluster) {
+  g_pot_ctas = ctas;
+  g_pot_cluster = cluster;
+}
+
 static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool reset_barrier = false) {
   PotArgs c = a;
   static bool attr_set[64] = {};   // per device (function attributes are per context)
@@ -1254,14 +1264,33 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
   const size_t dyn = (a.first <= P_FIT && a.last >= P_FIT) ? (size_t)cap_vals * 8 : 0;
   if (dyn == 0) c.ycache_cap = 0;
   if (reset_barrier) ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->bar_count, 0, sizeof(unsigned int), st));
-  void *args[] = {(void *)&c};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(kPotThreads);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  int na = 1;
+  if (g_pot_cluster > 1 && nb % g_pot_cluster == 0) {
+    // whole TPCs: the CTAs of a reduced fit grid take SM pairs, so a concurrent
+    // CTA-pair score launch keeps every other TPC
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = (unsigned)g_pot_cluster;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   count_launch();
-  ENOVA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_pot, dim3(nb), dim3(kPotThreads),
-                                             args, dyn, st));
+  ENOVA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pot, c));
   return ENOVA_OK;
 }
 
 static int pot_grid() {
+  if (g_pot_ctas > 0) return g_pot_ctas < kMaxCtas ? g_pot_ctas : kMaxCtas;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
