@@ -746,11 +746,21 @@ def run_windows(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    # one step = pipe.enqueue(X): stats_async -> calibration scores -> POT threshold
-    # (device-resident; with a communicator the stream-ordered collective fit)
-    # -> flags / scores / MD.  The step is captured once into a CUDA graph and
-    # replayed (one graph launch per step), NCCL collectives included.
+    # one step = pipe.enqueue(X) = enova_step_enqueue: stats -> calibration scores +
+    # MD -> POT threshold (with a communicator the stream-ordered collective fit)
+    # overlapped with the detection scores + MD -> the flags of every window.  The
+    # step is captured once into a CUDA graph and replayed (one graph launch per
+    # step), NCCL collectives included.  Pipeline.tune picks the overlap
+    # configuration (fit grid, detection instances scored next to it) by time;
+    # every configuration gives the same scores, MD and flags.
     use_graph = True   # with a communicator too: the NCCL collectives are captured
+    tuned = pipe.tune(X)
+    if world > 1:   # the same fit grid on every rank (z_q bit-identical across ranks)
+        cfg_t = torch.tensor([tuned["pot_ctas"], tuned["concurrent_instances"]], dtype=torch.int64,
+                             device=dev)
+        dist.broadcast(cfg_t, 0)
+        pipe.configure(int(cfg_t[0]), int(cfg_t[1]))
+        tuned = dict(tuned, pot_ctas=int(cfg_t[0]), concurrent_instances=int(cfg_t[1]))
     l0 = _lib.lib().enova_kernel_launches()
     pipe.enqueue(X)
     torch.cuda.synchronize()
@@ -932,6 +942,7 @@ def run_windows(args, rank, world, local_rank):
             # trace in and its flags out
             X2 = X.clone()   # capture warms up on real data
             pipe2 = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
+            pipe2.configure(pipe.pot_ctas, pipe.concurrent_instances)
             pipe2.capture(X2)
             mk = lambda: (torch.empty(tuple(pipe.cal_flags.shape), dtype=torch.int8).pin_memory(),
                           torch.empty(tuple(pipe.flags.shape), dtype=torch.int8).pin_memory())
@@ -1028,6 +1039,15 @@ def run_windows(args, rank, world, local_rank):
                            "with a score, an MD and a flag",
             },
             "stage_ms": stage_ms,
+            "stage_ms_note": "each stage alone, eager, in sequence (the step overlaps the fit "
+                             "with the detection scores: see step_overlap)",
+            "step_overlap": {"pot_ctas": tuned["pot_ctas"],
+                             "concurrent_instances": tuned["concurrent_instances"],
+                             "tuning_ms": {f"{p_}/{c_}": round(m_, 4)
+                                           for p_, c_, m_ in tuned.get("candidates", [])},
+                             "note": "enova_step: the POT fit on pot_ctas CTAs (2-CTA clusters) "
+                                     "on a side stream next to the detection scores of the "
+                                     "first concurrent_instances instances; (0, 0) = sequential"},
             "next_rows": extras,
             "step_mode": "CUDA graph replay (1 graph launch/step)" if use_graph else "eager",
             "threshold": {"z_q": thr["z_q"], "t": thr["t"], "gamma": thr["gamma"],

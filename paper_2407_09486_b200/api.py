@@ -716,6 +716,43 @@ class Pipeline:
                                          int(concurrent_instances)))
         self.pot_ctas, self.concurrent_instances = int(pot_ctas), int(concurrent_instances)
 
+    def tune(self, metrics: torch.Tensor, candidates=None, reps: int = 5) -> dict:
+        """Pick the fastest step configuration on `metrics` (a fixed device buffer):
+        each candidate (pot_ctas, concurrent_instances) -- (0, 0) is the sequential
+        order -- is captured and replayed `reps` times; every candidate gives the
+        same scores, MD and flags (the fit differs only in summation order), so
+        the choice is by time alone.  Leaves the winner configured and captured."""
+        if self.comm is not None and self.comm.local:
+            return {"pot_ctas": 0, "concurrent_instances": 0, "ms": None}
+        N = self.N
+        if candidates is None:
+            candidates = [(0, 0)]
+            if self.overlap:
+                for pot in (24, 32):
+                    for frac in (0.15, 0.3, 0.45, 0.6, 0.75):
+                        candidates.append((pot, int(frac * N)))
+        s = torch.cuda.current_stream(metrics.device)
+        best, timings = None, []
+        for pot, conc in candidates:
+            self.configure(pot, conc)
+            self.capture(metrics)
+            self.replay()
+            s.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(reps):
+                self.replay()
+            b.record(s)
+            s.synchronize()
+            ms = a.elapsed_time(b) / reps
+            timings.append((pot, conc, ms))
+            if best is None or ms < best[2]:
+                best = (pot, conc, ms)
+        self.configure(best[0], best[1])
+        self.capture(metrics)
+        return {"pot_ctas": best[0], "concurrent_instances": best[1], "ms": best[2],
+                "candidates": timings}
+
     def __del__(self):
         try:
             if getattr(self, "_step", None):

@@ -43,8 +43,10 @@ def main():
     t0, r0 = time_pipe(base, X, flush)
     ref = (r0.scores.clone(), r0.md.clone(), r0.flags.clone(), r0.cal_flags.clone(), r0.threshold)
     print(f"{wl} sequential: {t0 * 1e3:.1f} us  z_q {r0.threshold['z_q']:.9f}", flush=True)
-    for pot in (16, 32, 48):
-        for frac in (0.2, 0.3, 0.4, 0.5):
+    pots = [int(v) for v in os.environ.get('POTS', '16,32,48').split(',')]
+    fracs = [float(v) for v in os.environ.get('FRACS', '0.2,0.3,0.4,0.5').split(',')]
+    for pot in pots:
+        for frac in fracs:
             p = E.Pipeline(det, N, T, T // 2, pot_ctas=pot, concurrent_instances=int(frac * N))
             t, r = time_pipe(p, X, flush)
             same = (torch.equal(r.scores, ref[0]) and torch.equal(r.md, ref[1]))
