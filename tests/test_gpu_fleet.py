@@ -144,8 +144,8 @@ def test_local_comm_pipeline_matches_single_gpu(E):
     tcal = T // 2
     det = E.PreparedDetector(wts)
     Xd = torch.from_numpy(X).cuda()
-    ref = E.Pipeline(det, X.shape[0], T, tcal)
-    ref.enqueue(Xd)
+    ref = E.Pipeline(det, X.shape[0], T, tcal, overlap=False)   # the fit on the full grid,
+    ref.enqueue(Xd)                                              # like the local ranks'
     r0 = ref.result()
     rows = [(0, 3), (3, 4), (4, 10)]
     comms = E.Comm.create_local(3, 0)

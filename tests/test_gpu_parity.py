@@ -414,8 +414,12 @@ def test_stream_ring_matches_batch_and_oracle(E, W, M, H, Z, N):
 
 # ------------------------------------------- stream-ordered / graph path ----
 def test_async_pipeline_matches_sync_and_oracle(E):
-    """Pipeline (stats_async -> scores -> fit_threshold_async -> detect_async) gives
-    bitwise the same result as the synchronous calls, eagerly and as a CUDA graph."""
+    """Pipeline (enova_step: stats -> calibration scores + MD -> fit -> detection
+    scores + MD -> every flag) in sequence gives bitwise the result of the
+    synchronous calls, eagerly and as a CUDA graph; the overlapped step (the fit
+    on a reduced grid next to the detection scores) gives the same scores, MD,
+    flags and calibration flags bit for bit and z_q up to the fit's summation
+    order (1e-12)."""
     W, M, H, Z = 64, 16, 128, 16
     N, T = 12, 3000
     X = synth.metric_trace(N, T, M, seed=51)
@@ -423,7 +427,7 @@ def test_async_pipeline_matches_sync_and_oracle(E):
     det = E.PreparedDetector(wts)
     Xc = cuda(X)
     ref = E.run_pipeline(Xc, det, T // 2)
-    pipe = E.Pipeline(det, N, T, T // 2)
+    pipe = E.Pipeline(det, N, T, T // 2, overlap=False)
     pipe.enqueue(Xc)
     res = pipe.result()
     assert res.threshold == ref.threshold
@@ -431,6 +435,7 @@ def test_async_pipeline_matches_sync_and_oracle(E):
     assert torch.equal(res.cal_scores, ref.cal_scores)
     assert torch.equal(res.flags, ref.flags) and torch.equal(res.scores, ref.scores)
     assert torch.equal(res.md, ref.md)
+    assert torch.equal(res.cal_md, ref.cal_md) and torch.equal(res.cal_flags, ref.cal_flags)
     pipe.flags.zero_()
     pipe.capture(Xc)
     for _ in range(2):
@@ -439,6 +444,16 @@ def test_async_pipeline_matches_sync_and_oracle(E):
     assert res2.threshold == ref.threshold and torch.equal(res2.flags, ref.flags)
     o = O.pot_threshold(ref.cal_scores.cpu().numpy(), 0.98, 1e-3)
     assert abs(res2.threshold["z_q"] - o["z_q"]) <= 1e-9 * o["z_q"]
+    for pot, conc in ((24, 5), (32, 12), (16, 0)):
+        po = E.Pipeline(det, N, T, T // 2, pot_ctas=pot, concurrent_instances=conc)
+        po.capture(Xc)
+        po.replay()
+        r3 = po.result()
+        assert torch.equal(r3.scores, ref.scores) and torch.equal(r3.md, ref.md)
+        assert torch.equal(r3.flags, ref.flags) and torch.equal(r3.cal_flags, ref.cal_flags)
+        assert r3.threshold["t"] == ref.threshold["t"]
+        assert r3.threshold["n_peaks"] == ref.threshold["n_peaks"]
+        assert abs(r3.threshold["z_q"] - ref.threshold["z_q"]) <= 1e-12 * ref.threshold["z_q"]
 
 
 def test_async_failures_are_reported_on_device(E):
