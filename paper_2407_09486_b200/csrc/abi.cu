@@ -32,6 +32,7 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
                                  size_t ws_bytes, cudaStream_t st);
 size_t stats_workspace_bytes(int64_t n, int m);
 void set_forced_kernel(int k);
+int64_t pot_sampled_offset();
 enova_status apply_flags(const float *scores, const float *md, int64_t n,
                          const enova_threshold *thr_dev, int8_t *flags, cudaStream_t st);
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
@@ -170,6 +171,9 @@ int enova_abi_version(void) { return ENOVA_ABI_VERSION; }
 void enova_internal_set_trace(void *dev_buf) { enova::set_pair_trace(dev_buf); }
 // diagnostic (not in enova.h): where k_pot writes its %globaltimer phase stamps
 // in the threshold workspace (PotGlobal is at offset 0)
+// diagnostic (not in enova.h): byte offset of the int flag "the last selection ran
+// on the sampled candidates" in the threshold workspace
+int64_t enova_internal_pot_sampled_offset(void) { return enova::pot_sampled_offset(); }
 void enova_internal_pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
   enova::pot_stamp_offsets(n_off, st_off);
 }

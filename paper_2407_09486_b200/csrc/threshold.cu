@@ -57,7 +57,16 @@ constexpr double kCertRel = 5e-12;
 
 enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
 // phase program of k_pot
-enum { P_HIST0 = 0, P_HIST1 = 1, P_HIST2 = 2, P_COMPACT = 3, P_FIT = 4 };
+enum { P_SAMPLE = 0, P_SCAN = 1, P_HIST0 = 2, P_HIST1 = 3, P_HIST2 = 4, P_COMPACT = 5, P_FIT = 6 };
+// sampled candidate selection (single GPU, n >= kSampleMinN): P_SAMPLE picks a
+// key lo from a strided sample so that >= (1 - q0) + 8 sigma of the scores lie
+// at or above it; P_SCAN is the ONE full pass: it counts the keys below lo and
+// compacts the others (the candidates, ~2.4% of n) stably into this CTA's
+// segment; the radix passes and the peak compaction then read only the
+// candidates.  Exact: if the count below lo exceeds k (a sample that
+// misjudged the quantile) every CTA falls back to the full passes.
+constexpr int kSampleN = 2048;                 // samples per CTA
+constexpr int64_t kSampleMinN = int64_t(1) << 22;
 
 // Device-global state of one fit_threshold call.  The first kHeaderBytes of the
 // workspace (this struct and histogram 0) are zeroed by one memset per call;
@@ -79,6 +88,7 @@ struct PotGlobal {
                                      // until the next calibration fit zeroes the header)
   int pad2;
   int n_stamps, fit_passes;
+  int sampled, pad3;                 // the last selection ran on the sampled candidates
   unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
   unsigned long long t_first_start, t_last_end;   // over all CTAs (diagnostic)
 };
@@ -98,7 +108,9 @@ struct FitState {
 
 struct ThrLayout {
   size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yslot, outdev, yall, header, total;
+  size_t shist, cand, cand_n;   // sampled selection: sample histograms, candidates, per-CTA counts
   int64_t cap;
+  bool sampled;                 // workspace holds the candidate buffer
 };
 
 // world == 0: single-GPU layout.  world >= 1 (communicator): this rank's tail as
@@ -115,8 +127,9 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0, int world = 0) {
   if (L.cap > n_max) L.cap = n_max;
   if (L.cap < 16) L.cap = 16;
   L.glob = take(sizeof(PotGlobal));
+  L.shist = take(2 * kBins * 8);                    // sample histograms (zeroed per call)
   L.hist = take(3 * kBins * 8);
-  L.header = L.hist + kBins * 8;                    // PotGlobal + histogram 0
+  L.header = L.hist + kBins * 8;                    // PotGlobal + sample histograms + histogram 0
   L.counts = take(kMaxCtas * 8);
   L.part = take((size_t)2 * kSums * kMaxPts * kMaxCtas * 8);
   L.nbuf = take(16);
@@ -125,6 +138,11 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0, int world = 0) {
   L.yslot = take((size_t)world * (size_t)L.cap * 4);
   L.outdev = take(world ? sizeof(enova_threshold) : 0);
   L.yall = take((size_t)L.cap * 8);
+  // candidates: one segment of ceil(chunk / 4) * 4 scores per CTA (a segment can
+  // hold its CTA's whole chunk, so it never overflows)
+  L.sampled = (world == 0 && n_max >= kSampleMinN);
+  L.cand = take(L.sampled ? ((size_t)n_max + 4u * kMaxCtas) * 4 : 0);
+  L.cand_n = take(L.sampled ? (size_t)kMaxCtas * 2 * 8 : 0);
   L.total = o;
   return L;
 }
@@ -151,6 +169,9 @@ struct PotArgs {
   double q0;
   int ycache_cap;           // Y values per CTA held in dynamic shared memory
   const long long *n_dev;   // NEXT-2 refit: n read from device (g->n_spot), else a.n
+  unsigned long long *shist; // [2][kBins] sample histograms
+  float *cand;              // sampled selection: per-CTA candidate segments, else null
+  long long *cand_n;        // [kMaxCtas] candidates, [kMaxCtas] keys below lo, per CTA
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -219,14 +240,13 @@ struct SelS {
 // the selected 22-bit bucket (*above), so the peak count of the CTA follows
 // from its own histogram once the last digit is chosen (no counting pass).
 __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned int *h,
-                          int *above_smem) {
+                          int *above_smem, const float *src, int64_t len) {
   const int shift = (pass == 0) ? 21 : (pass == 1) ? 10 : 0;
   const int nbins = (pass == 2) ? 1024 : 2048;
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
   if (threadIdx.x == 0) *above_smem = 0;
   __syncthreads();
-  int64_t b0, b1;
-  score_chunk(a.n_local, &b0, &b1);
+  const int64_t b0 = 0, b1 = len;
   const unsigned int prefix = sel.prefix, mask = sel.mask;
   const unsigned int bucket_hi = prefix | ~mask;   // pass 2: largest key of the bucket
   int above = 0;
@@ -241,10 +261,10 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
       if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
     }
   };
-  const bool al = (reinterpret_cast<uintptr_t>(a.scores + b0) & 15) == 0;
+  const bool al = (reinterpret_cast<uintptr_t>(src + b0) & 15) == 0;
   int64_t tail0 = b0;
   if (al) {
-    const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
+    const float4 *x4 = reinterpret_cast<const float4 *>(src + b0);
     const int64_t n4 = (b1 - b0) / 4;
     // two register batches of 4 float4 ping-pong: batch k+1 is in flight while
     // batch k is binned (8 x 128-bit loads outstanding per thread)
@@ -279,7 +299,7 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
   }
   for (int64_t i0 = tail0; i0 < b1; i0 += blockDim.x) {
     const int64_t i = i0 + threadIdx.x;
-    add(i < b1 ? __ldg(a.scores + i) : 0.f, i < b1);
+    add(i < b1 ? __ldg(src + i) : 0.f, i < b1);
   }
   if (pass == 2) {
 #pragma unroll
@@ -295,10 +315,10 @@ __device__ void hist_pass(const PotArgs &a, const SelS &sel, int pass, unsigned 
 // Every CTA reads the (complete) histogram of `pass` and finds the digit that
 // holds rank k_rem: 512 threads x 4 bins, block exclusive scan.
 __device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned long long *wtot,
-                             int *found) {
+                             int *found, const unsigned long long *hist_override = nullptr) {
   const int shift = (pass == 0) ? 21 : (pass == 1) ? 10 : 0;
   const int nbins = (pass == 2) ? 1024 : 2048;
-  const unsigned long long *gh = a.hist + (size_t)pass * kBins;
+  const unsigned long long *gh = hist_override ? hist_override : a.hist + (size_t)pass * kBins;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned long long c[4];
 #pragma unroll
@@ -346,6 +366,169 @@ __device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned lon
   __syncthreads();
 }
 
+// ------------------------------------------------------- sampled select ----
+// P_SAMPLE: CTA b keys kSampleN evenly spaced scores of its chunk into shared
+// memory; two grid-wide histogram levels (top 11 bits, then the next 11 of the
+// chosen bucket) locate the sample's order statistic at q0 - delta, delta = 8
+// sample standard deviations + 2/S; lo = the lowest key of that 22-bit bucket.
+__device__ int64_t sample_total(const PotArgs &a) {   // every CTA's sample size, summed
+  int64_t tot = 0;
+  const int64_t chunk = ((a.n_local + gridDim.x - 1) / gridDim.x + 3) / 4 * 4;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    const int64_t b0 = min(a.n_local, (int64_t)b * chunk), b1 = min(a.n_local, b0 + chunk);
+    tot += min((int64_t)kSampleN, b1 - b0);
+  }
+  return tot;
+}
+
+__device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsigned int *sk,
+                             int &ns_out, unsigned long long *wtot, int *found,
+                             unsigned int &epoch, long long *s_tot) {
+  int64_t b0, b1;
+  score_chunk(a.n_local, &b0, &b1);
+  const int64_t len = b1 - b0;
+  const int ns = (int)min((int64_t)kSampleN, len);
+  for (int j = threadIdx.x; j < ns; j += blockDim.x)
+    sk[j] = f2key(__ldg(a.scores + b0 + (int64_t)j * len / ns));
+  if (threadIdx.x == 0) {
+    const int64_t S = sample_total(a);
+    const double q0 = a.q0;
+    const double delta = 8.0 * sqrt(q0 * (1.0 - q0) / (double)S) + 2.0 / (double)S;
+    const double qs = q0 - delta;
+    s_tot[0] = qs > 0.0 ? (long long)floor(qs * (double)S) : 0;
+    ssel.prefix = 0;
+    ssel.mask = 0;
+    ssel.k_rem = (unsigned long long)s_tot[0];
+  }
+  for (int level = 0; level < 2; ++level) {
+    const int shift = level == 0 ? 21 : 10;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+      const unsigned int k = sk[j];
+      if ((k & ssel.mask) == ssel.prefix) atomicAdd(&h[(k >> shift) & (kBins - 1)], 1u);
+    }
+    __syncthreads();
+    unsigned long long *gh = a.shist + (size_t)level * kBins;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
+      if (h[i]) atomicAdd(gh + i, (unsigned long long)h[i]);
+    grid_sync(a.g, epoch);
+    stamp(a.g);
+    select_digit(a, ssel, level, wtot, found, gh);
+  }
+  ns_out = ns;
+}
+
+// P_SCAN: the one full pass over this CTA's chunk -- count the keys below lo,
+// compact the rest (the candidates) stably (index order) into the CTA's segment
+// a.cand + blockIdx.x * seg_cap.  4 float4 loads in flight per thread; the
+// order within a batch is (load slot, thread, element) = index order.
+__device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t seg_cap,
+                           long long *out_n) {
+  int64_t b0, b1;
+  score_chunk(a.n_local, &b0, &b1);
+  const float *src = a.scores + b0;
+  const int64_t len = b1 - b0;
+  float *dst = a.cand + (size_t)blockIdx.x * seg_cap;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long base = 0, below = 0;
+  const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  auto batch = [&](const float (&v)[4][4], const bool (&ok)[4][4]) {
+    int cnt[4], incl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      cnt[u] = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool c = ok[u][e] && f2key(v[u][e]) >= lo;
+        cnt[u] += c;
+        below += (ok[u][e] && !c);
+      }
+      incl[u] = cnt[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl[u], o);
+        if (lane >= o) incl[u] += y;
+      }
+      if (lane == 31) wc[u * kPotWarps + warp] = incl[u];
+    }
+    __syncthreads();
+    long long off_u = base;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int before_w = 0, all = 0;
+      for (int w = 0; w < kPotWarps; ++w) {
+        const int vv = wc[u * kPotWarps + w];
+        before_w += (w < warp) ? vv : 0;
+        all += vv;
+      }
+      long long o = off_u + before_w + incl[u] - cnt[u];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (ok[u][e] && f2key(v[u][e]) >= lo) dst[o++] = v[u][e];
+      off_u += all;
+    }
+    base = off_u;
+    __syncthreads();
+  };
+  int64_t tail0 = 0;
+  if (al) {
+    const float4 *x4 = reinterpret_cast<const float4 *>(src);
+    const int64_t n4 = len / 4;
+    const int64_t step = 4 * (int64_t)blockDim.x;
+    float4 nq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = u * blockDim.x + threadIdx.x;
+      nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int64_t i0 = 0; i0 < n4; i0 += step) {   // next batch in flight while this one scatters
+      float v[4][4];
+      bool ok[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool g = i0 + u * blockDim.x + threadIdx.x < n4;
+        v[u][0] = nq[u].x; v[u][1] = nq[u].y; v[u][2] = nq[u].z; v[u][3] = nq[u].w;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ok[u][e] = g;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + step + u * blockDim.x + threadIdx.x;
+        nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      batch(v, ok);
+    }
+    tail0 = 4 * n4;
+  }
+  for (int64_t i0 = tail0; i0 < len; i0 += 16 * blockDim.x) {
+    float v[4][4];
+    bool ok[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + (int64_t)u * 4 * blockDim.x + 4 * threadIdx.x + e;
+        ok[u][e] = i < len;
+        v[u][e] = ok[u][e] ? __ldg(src + i) : 0.f;
+      }
+    batch(v, ok);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+  if (lane == 0) wc[warp] = (int)below;   // < 2^31 per warp
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long bl = 0;
+    for (int w = 0; w < kPotWarps; ++w) bl += wc[w];
+    out_n[0] = base;   // candidates of this CTA
+    out_n[1] = bl;     // keys below lo
+    a.cand_n[blockIdx.x] = base;
+    a.cand_n[kMaxCtas + blockIdx.x] = bl;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- K4 ----
 // Stable compaction of the peaks Y = s - t (s > t) of this rank in index order.
 // The CTA's peak count is known without reading the scores: keys above the
@@ -354,9 +537,9 @@ __device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned lon
 // per-CTA counts; the scatter then keeps 4 float4 loads in flight per thread
 // and orders the output by (load slot, thread, element) = index order.
 __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h, int above,
-                        bool have_hist, int *wcnt, long long *cta_base, unsigned int &epoch) {
-  int64_t b0, b1;
-  score_chunk(a.n_local, &b0, &b1);
+                        bool have_hist, int *wcnt, long long *cta_base, unsigned int &epoch,
+                        const float *src, int64_t len) {
+  const int64_t b0 = 0, b1 = len;
   const float t = sel.t;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c = 0;
@@ -370,7 +553,7 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + u * blockDim.x + threadIdx.x;
-        v[u] = (i < b1) ? __ldg(a.scores + i) : -INFINITY;
+        v[u] = (i < b1) ? __ldg(src + i) : -INFINITY;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) c += (v[u] > t);
@@ -407,7 +590,7 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
   __syncthreads();
   long long base = cta_base[0];
   const double td = (double)t;
-  const bool al = (reinterpret_cast<uintptr_t>(a.scores + b0) & 15) == 0;
+  const bool al = (reinterpret_cast<uintptr_t>(src + b0) & 15) == 0;
   int *wc = wcnt;   // [4][kPotWarps]
   auto scatter4 = [&](const float (&v)[4][4], const bool (&ok)[4][4]) {
     int cnt[4];
@@ -455,7 +638,7 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
   };
   int64_t tail0 = b0;
   if (al) {
-    const float4 *x4 = reinterpret_cast<const float4 *>(a.scores + b0);
+    const float4 *x4 = reinterpret_cast<const float4 *>(src + b0);
     const int64_t n4 = (b1 - b0) / 4;
     // the next batch's 4 float4 are loaded before this batch is scattered
     const int64_t step = 4 * (int64_t)blockDim.x;
@@ -495,7 +678,7 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
       for (int e = 0; e < 4; ++e) {
         const int64_t i = i0 + (int64_t)u * 4 * blockDim.x + 4 * threadIdx.x + e;
         ok[u][e] = i < b1;
-        v[u][e] = ok[u][e] ? __ldg(a.scores + i) : 0.f;
+        v[u][e] = ok[u][e] ? __ldg(src + i) : 0.f;
       }
     scatter4(v, ok);
   }
@@ -1124,7 +1307,10 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
 }
 
 union PotShared {
-  unsigned int h[kBins];
+  struct {
+    unsigned int h[kBins];
+    unsigned int sk[kSampleN];   // P_SAMPLE: this CTA's sample keys
+  } s;
   FitShared fit;
 };
 
@@ -1137,6 +1323,10 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
   __shared__ int wcnt[4 * kPotWarps];
   __shared__ int above;
   __shared__ long long s_off[kMaxWorld + 1];
+  __shared__ SelS ssel;            // sampled selection state
+  __shared__ long long s_tot[2];
+  __shared__ int cmode;            // 1: the radix passes run on the candidates
+  __shared__ long long my_n[2];    // this CTA's candidates / keys below lo
   PotGlobal *g = a.g;
   unsigned int epoch = 0;   // grid barriers passed in this launch
   bool spot_skip = false;
@@ -1151,7 +1341,8 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
     atomicMax(&g->t_first_start, ~t0);   // stored complemented: max(~t) = ~min(t)
   }
   if (threadIdx.x == 0) {
-    if (a.first == P_HIST0) {
+    cmode = 0;
+    if (a.first <= P_HIST0) {
       sel.prefix = 0;
       sel.mask = 0;
       sel.k_rem = a.k;
@@ -1164,23 +1355,73 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
     }
   }
   __syncthreads();
+  // the slice the radix passes and the compaction read: this CTA's candidate
+  // segment (sampled selection) or its chunk of the scores
+  const int64_t seg_cap = a.cand ? ((a.n_local + gridDim.x - 1) / gridDim.x + 3) / 4 * 4 : 0;
+  auto slice = [&](const float *&src, int64_t &len) {
+    if (cmode) {
+      src = a.cand + (size_t)blockIdx.x * seg_cap;
+      len = my_n[0];
+    } else {
+      int64_t b0, b1;
+      score_chunk(a.n_local, &b0, &b1);
+      src = a.scores + b0;
+      len = b1 - b0;
+    }
+  };
   for (int ph = a.first; ph <= a.last; ++ph) {
     if (ph > a.first) grid_sync(g, epoch);
     stamp(g);
-    if (ph == P_HIST0) {
+    if (ph == P_SAMPLE) {
+      int ns = 0;
+      sample_phase(a, ssel, sh.s.h, sh.s.sk, ns, wtot, reinterpret_cast<int *>(found), epoch, s_tot);
+    } else if (ph == P_SCAN) {
+      scan_phase(a, ssel.prefix, wcnt, seg_cap, my_n);
+      grid_sync(g, epoch);
+      stamp(g);
+      // every CTA: keys below lo over the grid (fixed order) -> candidate mode
+      // iff the k-th order statistic is among the candidates
+      if (threadIdx.x == 0) {
+        long long below = 0;
+        for (int b = 0; b < (int)gridDim.x; ++b)
+          below += *(volatile long long *)(a.cand_n + kMaxCtas + b);
+        cmode = (unsigned long long)below <= a.k ? 1 : 0;
+        if (cmode) sel.k_rem = a.k - (unsigned long long)below;
+        if (blockIdx.x == 0) g->sampled = cmode;
+      }
+      __syncthreads();
+      // P_HIST0 follows without a barrier of its own: it reads only this CTA's
+      // segment (written above) and its histogram was zeroed by the header memset
+      ph = P_HIST0;
+      const float *src;
+      int64_t len;
+      slice(src, len);
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kBins; i += gridDim.x * blockDim.x)
+        a.hist[kBins + i] = 0ull;
+      hist_pass(a, sel, 0, sh.s.h, &above, src, len);
+    } else if (ph == P_HIST0) {
       // zero what is not covered by the per-call header memset (first used
       // after the next barrier)
       unsigned long long *h12 = a.hist + kBins;
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kBins;
            i += gridDim.x * blockDim.x)
         h12[i] = 0ull;
-      hist_pass(a, sel, 0, sh.h, &above);
+      const float *src;
+      int64_t len;
+      slice(src, len);
+      hist_pass(a, sel, 0, sh.s.h, &above, src, len);
     } else if (ph == P_HIST1 || ph == P_HIST2) {
-      select_digit(a, sel, ph - 1, wtot, reinterpret_cast<int *>(found));
-      hist_pass(a, sel, ph, sh.h, &above);
+      const float *src;
+      int64_t len;
+      slice(src, len);
+      select_digit(a, sel, ph - P_HIST1, wtot, reinterpret_cast<int *>(found));
+      hist_pass(a, sel, ph - P_HIST0, sh.s.h, &above, src, len);
     } else if (ph == P_COMPACT) {
+      const float *src;
+      int64_t len;
+      slice(src, len);
       select_digit(a, sel, 2, wtot, reinterpret_cast<int *>(found));
-      compact(a, sel, sh.h, above, a.first < P_COMPACT, wcnt, cta_base, epoch);
+      compact(a, sel, sh.s.h, above, a.first < P_COMPACT, wcnt, cta_base, epoch, src, len);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         g->t = sel.t;
         g->nt_local = cta_base[1];
@@ -1317,7 +1558,11 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.counts_all = comm ? reinterpret_cast<const long long *>(b + L.counts_all) : nullptr;
   a.world = 0;
   a.cap = L.cap;
-  a.first = P_HIST0;
+  a.shist = reinterpret_cast<unsigned long long *>(b + L.shist);
+  a.cand = (!comm && L.sampled) ? reinterpret_cast<float *>(b + L.cand) : nullptr;
+  a.cand_n = (!comm && L.sampled) ? reinterpret_cast<long long *>(b + L.cand_n) : nullptr;
+  // single GPU with a large score vector: the sampled one-pass selection
+  a.first = (a.cand && scores && n_local >= kSampleMinN) ? P_SAMPLE : P_HIST0;
   a.last = P_FIT;
   a.out_dev = nullptr;
   a.n_dev = nullptr;
@@ -1490,6 +1735,8 @@ size_t threshold_workspace_bytes(int64_t n_max, double q0, int world) {
 }
 
 // diagnostic: byte offsets of PotGlobal.n_stamps / .stamps in the threshold workspace
+int64_t pot_sampled_offset() { return (int64_t)offsetof(PotGlobal, sampled); }
+
 void pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
   *n_off = (int64_t)offsetof(PotGlobal, n_stamps);
   *st_off = (int64_t)offsetof(PotGlobal, stamps);

@@ -350,3 +350,74 @@ def test_exact_mode_deviation_reported(E):
         # flag disagreement outside the band
         assert math.isfinite(out[k]["max"]) and out[k]["median"] < 1e-3
         assert out[k]["flag_mismatch_outside_band"] == 0
+
+
+# ----------------------------------------------- sampled one-pass selection ----
+def _sampled_flag(E, ws):
+    import ctypes as C
+    from paper_2407_09486_b200 import _lib
+    L = _lib.lib()
+    L.enova_internal_pot_sampled_offset.restype = C.c_int64
+    off = int(L.enova_internal_pot_sampled_offset())
+    return int(ws.buf[off:off + 4].cpu().numpy().view(np.int32)[0])
+
+
+@pytest.mark.parametrize("kind", ["mixture", "sorted", "reversed", "ties", "blocks"])
+def test_sampled_selection_exact(E, kind):
+    """n >= 2^22 takes the sampled path (strided sample -> lo, ONE full pass
+    compacting the candidates, radix passes on the candidates only).  The
+    threshold must equal the oracle's on any ordering of the scores --
+    including sorted input (every candidate in the last CTAs) and heavy ties
+    at the quantile -- with t, n, N_t exact and z_q within 1e-9."""
+    n = (1 << 22) + 12345
+    r = np.random.default_rng(17)
+    s = synth.score_mixture(n, seed=5)
+    if kind == "sorted":
+        s = np.sort(s)
+    elif kind == "reversed":
+        s = np.sort(s)[::-1].copy()
+    elif kind == "ties":
+        s = np.round(s, 1).astype(np.float32)
+    elif kind == "blocks":        # the tail concentrated in a few contiguous blocks
+        s = np.sort(s)
+        cut = int(0.97 * n)
+        tail = s[cut:].copy()
+        s = s[:cut]
+        r.shuffle(s)
+        pos = [int(p * len(s)) for p in (0.1, 0.55, 0.9)]
+        parts = np.array_split(tail, 3)
+        for p, t in sorted(zip(pos, parts), reverse=True):
+            s = np.concatenate([s[:p], t, s[p:]])
+    ws = E.ThresholdWorkspace(n)
+    g = E.fit_threshold(cuda(s), 0.98, 1e-3, workspace=ws)
+    assert _sampled_flag(E, ws) == 1, "the sampled path should have run"
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    assert g["t"] == o["t"] and g["n"] == o["n"] and g["n_peaks"] == o["n_peaks"]
+    assert abs(g["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
+    # and identical to the full-pass selection of a workspace without candidates
+    # (the same scores in a vector too short for sampling would change n: compare
+    # the fit inputs instead -- t and N_t above are exact)
+
+
+def test_sampled_selection_fallback(E):
+    """A sample that misjudges the quantile: a score vector whose strided sample
+    points all fall on small values while the real 98% quantile is high (values
+    at the sample's stride positions are zero) -- the count below lo exceeds k,
+    every CTA falls back to the full passes, and the result is still exact."""
+    n = 1 << 22
+    s = synth.score_mixture(n, seed=9)
+    nb = torch.cuda.get_device_properties(0).multi_processor_count
+    chunk = ((n + nb - 1) // nb + 3) // 4 * 4
+    idx = []
+    for b in range(nb):
+        b0, b1 = min(n, b * chunk), min(n, b * chunk + chunk)
+        ln = b1 - b0
+        ns = min(2048, ln)
+        idx.extend(b0 + np.arange(ns, dtype=np.int64) * ln // ns)
+    s[np.array(idx)] = 100.0                   # every sampled score at the top
+    ws = E.ThresholdWorkspace(n)
+    g = E.fit_threshold(cuda(s), 0.98, 1e-3, workspace=ws)
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    assert g["t"] == o["t"] and g["n_peaks"] == o["n_peaks"]
+    assert abs(g["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
+    assert _sampled_flag(E, ws) == 0, "lo above the quantile must fall back"
