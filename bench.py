@@ -543,23 +543,32 @@ def run_threshold_sweep(args, rank, world, local_rank):
     thr = E.threshold_from_device(thr_dev)
     value = n_total * args.steps / (tot * 1e-3)
     # phase split of one k_pot launch from its %globaltimer stamps (CTA 0):
-    # [0] radix pass 0 ... [3] compaction, [5] fit start, [-1] end
+    # [0] launch entry ... [fit_stamp] start of the GPD fit, [-1] end
     phases = None
     if comm is None:
         import ctypes as C
         step()
         torch.cuda.synchronize()
+        L_ = _lib.lib()
         no, so = C.c_int64(), C.c_int64()
-        _lib.lib().enova_internal_pot_stamp_offsets(C.byref(no), C.byref(so))
+        L_.enova_internal_pot_stamp_offsets(C.byref(no), C.byref(so))
+        L_.enova_internal_pot_fit_stamp_offset.restype = C.c_int64
+        L_.enova_internal_pot_sampled_offset.restype = C.c_int64
+        fo = int(L_.enova_internal_pot_fit_stamp_offset())
+        sp = int(L_.enova_internal_pot_sampled_offset())
         head = ws.buf[:so.value + 8 * 96].cpu().numpy()
         ns = int(head[no.value:no.value + 4].view(np.int32)[0])
+        fs = int(head[fo:fo + 4].view(np.int32)[0])
+        sampled = int(head[sp:sp + 4].view(np.int32)[0])
         st = head[so.value:so.value + 8 * min(ns, 95)].view(np.uint64).astype(np.int64)
-        if ns >= 7:
-            sel_us = (st[5] - st[0]) / 1e3
-            fit_us = (st[-1] - st[5]) / 1e3
-            moved = 4 * 4.0 * n + 8.0 * thr["n_peaks"]        # 3 radix reads + scatter read + Y write
-            phases = {"select_compact_us": sel_us, "fit_us": fit_us,
-                      "select_bytes_moved": moved,
+        if ns >= 4 and 0 < fs < ns:
+            sel_us = (st[fs] - st[0]) / 1e3
+            fit_us = (st[ns - 1] - st[fs]) / 1e3
+            # bytes the selection must move: one read of the scores + the peaks out;
+            # the sampled path also writes and re-reads the ~2.4% candidates
+            moved = 4.0 * n + 8.0 * thr["n_peaks"]
+            phases = {"select_compact_us": sel_us, "fit_us": fit_us, "sampled_selection": bool(sampled),
+                      "select_bytes_algorithmic": moved,
                       "select_achieved_GBps": moved / (sel_us * 1e-6) / 1e9,
                       "select_hbm_frac": moved / (sel_us * 1e-6) / 1e9 / load_peaks()["hbm"],
                       "fit_grid_points": 128, "fit_peaks": thr["n_peaks"],

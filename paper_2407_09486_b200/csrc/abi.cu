@@ -33,6 +33,7 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
 size_t stats_workspace_bytes(int64_t n, int m);
 void set_forced_kernel(int k);
 int64_t pot_sampled_offset();
+int64_t pot_fit_stamp_offset();
 enova_status apply_flags(const float *scores, const float *md, int64_t n,
                          const enova_threshold *thr_dev, int8_t *flags, cudaStream_t st);
 enova_status launch_score(const enova_series *s, const DetLayout &L, const void *det_ws,
@@ -174,6 +175,8 @@ void enova_internal_set_trace(void *dev_buf) { enova::set_pair_trace(dev_buf); }
 // diagnostic (not in enova.h): byte offset of the int flag "the last selection ran
 // on the sampled candidates" in the threshold workspace
 int64_t enova_internal_pot_sampled_offset(void) { return enova::pot_sampled_offset(); }
+// diagnostic: byte offset of the int "stamp index at the start of the fit"
+int64_t enova_internal_pot_fit_stamp_offset(void) { return enova::pot_fit_stamp_offset(); }
 void enova_internal_pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
   enova::pot_stamp_offsets(n_off, st_off);
 }

@@ -88,7 +88,8 @@ struct PotGlobal {
                                      // until the next calibration fit zeroes the header)
   int pad2;
   int n_stamps, fit_passes;
-  int sampled, pad3;                 // the last selection ran on the sampled candidates
+  int sampled, fit_stamp;            // the last selection ran on the sampled candidates;
+                                     // stamp index at the start of the fit (diagnostic)
   unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
   unsigned long long t_first_start, t_last_end;   // over all CTAs (diagnostic)
 };
@@ -1429,6 +1430,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
         if (cta_base[1] > a.cap) g->status = ENOVA_ERR_WORKSPACE;
       }
     } else if (ph == P_FIT) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) g->fit_stamp = s_nstamp - 1;
       // SPOT refit with no peak added since the last fit: the model is unchanged
       // (the cited Algorithm 1 refits only when a peak arrives) -- keep the threshold
       spot_full = a.n_dev && *(volatile int *)&g->spot_overflow != 0;
@@ -1639,8 +1641,8 @@ enova_status fit_threshold_comm_async(const float *scores, int64_t n_local, int6
   for (int p = P_HIST0; p <= P_HIST2; ++p) {
     a.first = a.last = p;
     if ((r = launch_pot_comm(a, nb, st, p > P_HIST0, comm))) return r;
-    r = comm_allreduce_u64_sum(comm, a.hist + (size_t)p * kBins, a.hist + (size_t)p * kBins,
-                               (size_t)kBins, st);
+    r = comm_allreduce_u64_sum(comm, a.hist + (size_t)(p - P_HIST0) * kBins,
+                               a.hist + (size_t)(p - P_HIST0) * kBins, (size_t)kBins, st);
     if (r) return r;
   }
   a.first = a.last = P_COMPACT;
@@ -1736,6 +1738,7 @@ size_t threshold_workspace_bytes(int64_t n_max, double q0, int world) {
 
 // diagnostic: byte offsets of PotGlobal.n_stamps / .stamps in the threshold workspace
 int64_t pot_sampled_offset() { return (int64_t)offsetof(PotGlobal, sampled); }
+int64_t pot_fit_stamp_offset() { return (int64_t)offsetof(PotGlobal, fit_stamp); }
 
 void pot_stamp_offsets(int64_t *n_off, int64_t *st_off) {
   *n_off = (int64_t)offsetof(PotGlobal, n_stamps);

@@ -414,7 +414,8 @@ def test_sampled_selection_fallback(E):
         ln = b1 - b0
         ns = min(2048, ln)
         idx.extend(b0 + np.arange(ns, dtype=np.int64) * ln // ns)
-    s[np.array(idx)] = 100.0                   # every sampled score at the top
+    idx = np.array(idx)
+    s[idx] = 100.0 + np.arange(len(idx), dtype=np.float32) * 1e-3   # every sampled score on top
     ws = E.ThresholdWorkspace(n)
     g = E.fit_threshold(cuda(s), 0.98, 1e-3, workspace=ws)
     o = O.pot_threshold(s, 0.98, 1e-3)
