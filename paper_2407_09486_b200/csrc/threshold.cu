@@ -422,8 +422,12 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
 
 // P_SCAN: the one full pass over this CTA's chunk -- count the keys below lo,
 // compact the rest (the candidates) stably (index order) into the CTA's segment
-// a.cand + blockIdx.x * seg_cap.  4 float4 loads in flight per thread; the
-// order within a batch is (load slot, thread, element) = index order.
+// a.cand + blockIdx.x * seg_cap.  Warp w streams its own contiguous sub-range
+// of the chunk (4 float4 loads in flight per lane) and appends its candidates
+// to its own region [w * sub, ...) of the segment with warp-level prefix sums
+// only (no CTA barrier in the loop); the runs are then moved down to their
+// final, contiguous positions in warp order (each run is read before the
+// position it is written to: destination <= source).
 __device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t seg_cap,
                            long long *out_n) {
   int64_t b0, b1;
@@ -432,102 +436,100 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t s
   const int64_t len = b1 - b0;
   float *dst = a.cand + (size_t)blockIdx.x * seg_cap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  long long base = 0, below = 0;
-  const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  auto batch = [&](const float (&v)[4][4], const bool (&ok)[4][4]) {
-    int cnt[4], incl[4];
+  // warp sub-ranges: multiples of 4 scores (float4-aligned when the chunk is)
+  const int64_t sub = ((len + kPotWarps - 1) / kPotWarps + 3) / 4 * 4;
+  const int64_t w0 = min(len, (int64_t)warp * sub), w1 = min(len, w0 + sub);
+  float *wdst = dst + w0;
+  long long cnt = 0, below = 0;   // warp-uniform cnt
+  const bool al = (reinterpret_cast<uintptr_t>(src + w0) & 15) == 0;
+  // the leading nv (0..4) elements of q are scores, in index order after the
+  // previous lanes' elements
+  auto put4 = [&](const float4 q, int nv) {
+    const float e4[4] = {q.x, q.y, q.z, q.w};
+    int c = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      cnt[u] = 0;
+    for (int e = 0; e < 4; ++e) c += (e < nv && f2key(e4[e]) >= lo);
+    below += nv - c;
+    int incl = c;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool c = ok[u][e] && f2key(v[u][e]) >= lo;
-        cnt[u] += c;
-        below += (ok[u][e] && !c);
-      }
-      incl[u] = cnt[u];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl[u], o);
-        if (lane >= o) incl[u] += y;
-      }
-      if (lane == 31) wc[u * kPotWarps + warp] = incl[u];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    __syncthreads();
-    long long off_u = base;
+    long long o = cnt + incl - c;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int before_w = 0, all = 0;
-      for (int w = 0; w < kPotWarps; ++w) {
-        const int vv = wc[u * kPotWarps + w];
-        before_w += (w < warp) ? vv : 0;
-        all += vv;
-      }
-      long long o = off_u + before_w + incl[u] - cnt[u];
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (ok[u][e] && f2key(v[u][e]) >= lo) dst[o++] = v[u][e];
-      off_u += all;
-    }
-    base = off_u;
-    __syncthreads();
+    for (int e = 0; e < 4; ++e)
+      if (e < nv && f2key(e4[e]) >= lo) wdst[o++] = e4[e];
+    cnt += __shfl_sync(0xffffffffu, incl, 31);
   };
-  int64_t tail0 = 0;
+  int64_t tail0 = w0;
   if (al) {
-    const float4 *x4 = reinterpret_cast<const float4 *>(src);
-    const int64_t n4 = len / 4;
-    const int64_t step = 4 * (int64_t)blockDim.x;
+    const float4 *x4 = reinterpret_cast<const float4 *>(src + w0);
+    const int64_t n4 = (w1 - w0) / 4;
     float4 nq[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t i = u * blockDim.x + threadIdx.x;
+      const int64_t i = u * 32 + lane;
       nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int64_t i0 = 0; i0 < n4; i0 += step) {   // next batch in flight while this one scatters
-      float v[4][4];
-      bool ok[4][4];
+    for (int64_t i0 = 0; i0 < n4; i0 += 128) {   // warp-uniform trip count
+      float4 cur[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nq[u];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const bool g = i0 + u * blockDim.x + threadIdx.x < n4;
-        v[u][0] = nq[u].x; v[u][1] = nq[u].y; v[u][2] = nq[u].z; v[u][3] = nq[u].w;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) ok[u][e] = g;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + step + u * blockDim.x + threadIdx.x;
+        const int64_t i = i0 + 128 + u * 32 + lane;
         nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      batch(v, ok);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) put4(cur[u], (i0 + u * 32 + lane < n4) ? 4 : 0);
     }
-    tail0 = 4 * n4;
+    tail0 = w0 + 4 * n4;
   }
-  for (int64_t i0 = tail0; i0 < len; i0 += 16 * blockDim.x) {
-    float v[4][4];
-    bool ok[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t i = i0 + (int64_t)u * 4 * blockDim.x + 4 * threadIdx.x + e;
-        ok[u][e] = i < len;
-        v[u][e] = ok[u][e] ? __ldg(src + i) : 0.f;
-      }
-    batch(v, ok);
+  for (int64_t i0 = tail0; i0 < w1; i0 += 128) {   // ragged / unaligned: 4 scalars per lane
+    const int64_t i = i0 + 4 * lane;
+    float4 q;
+    q.x = i < w1 ? __ldg(src + i) : 0.f;
+    q.y = i + 1 < w1 ? __ldg(src + i + 1) : 0.f;
+    q.z = i + 2 < w1 ? __ldg(src + i + 2) : 0.f;
+    q.w = i + 3 < w1 ? __ldg(src + i + 3) : 0.f;
+    put4(q, (int)max((int64_t)0, min((int64_t)4, w1 - i)));
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
-  if (lane == 0) wc[warp] = (int)below;   // < 2^31 per warp
+  __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
+  if (lane == 0) {
+    wcount[warp] = cnt;
+    wbelow[warp] = below;
+  }
   __syncthreads();
+  // move run w (at w * sub) down to its final position, in warp order
+  long long pos = wcount[0];
+  for (int w = 1; w < kPotWarps; ++w) {
+    const long long c = wcount[w];
+    if (warp == w) {
+      const float *from = dst + (int64_t)w * sub;
+      float *to = dst + pos;
+      for (long long i = 0; i < c; i += 32) {   // chunk read before write: to <= from
+        const float v = (i + lane < c) ? from[i + lane] : 0.f;
+        __syncwarp();
+        if (i + lane < c) to[i + lane] = v;
+        __syncwarp();
+      }
+    }
+    pos += c;
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     long long bl = 0;
-    for (int w = 0; w < kPotWarps; ++w) bl += wc[w];
-    out_n[0] = base;   // candidates of this CTA
+    for (int w = 0; w < kPotWarps; ++w) bl += wbelow[w];
+    out_n[0] = pos;    // candidates of this CTA
     out_n[1] = bl;     // keys below lo
-    a.cand_n[blockIdx.x] = base;
+    a.cand_n[blockIdx.x] = pos;
     a.cand_n[kMaxCtas + blockIdx.x] = bl;
   }
   __syncthreads();
+  (void)wc;
 }
 
 // ---------------------------------------------------------------- K4 ----

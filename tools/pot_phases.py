@@ -15,7 +15,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2407_09486_b200 as E  # noqa: E402
 from paper_2407_09486_b200 import synth  # noqa: E402
 
-OFF_NSTAMPS, OFF_STAMPS = 112, 120
+
+
+def _offsets():
+    import ctypes as C
+    from paper_2407_09486_b200 import _lib
+    no, so = C.c_int64(), C.c_int64()
+    _lib.lib().enova_internal_pot_stamp_offsets(C.byref(no), C.byref(so))
+    return no.value, so.value
 
 
 def report(scores, label, reps=5):
@@ -32,6 +39,7 @@ def report(scores, label, reps=5):
         b.record()
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
+    OFF_NSTAMPS, OFF_STAMPS = _offsets()
     head = ws.buf[:OFF_STAMPS + 8 * 98].cpu().numpy()
     n = int(head[OFF_NSTAMPS:OFF_NSTAMPS + 4].view(np.int32)[0])
     passes = int(head[OFF_NSTAMPS + 4:OFF_NSTAMPS + 8].view(np.int32)[0])
