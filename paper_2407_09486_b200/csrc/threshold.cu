@@ -422,33 +422,42 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
 
 // P_SCAN: the one full pass over this CTA's chunk -- count the keys below lo,
 // compact the rest (the candidates) stably (index order) into the CTA's segment
-// a.cand + blockIdx.x * seg_cap.  Warp w streams its own contiguous sub-range
-// of the chunk (4 float4 loads in flight per lane) and appends its candidates
-// to its own region [w * sub, ...) of the segment with warp-level prefix sums
-// only (no CTA barrier in the loop); the runs are then moved down to their
-// final, contiguous positions in warp order (each run is read before the
-// position it is written to: destination <= source).
-__device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t seg_cap,
-                           long long *out_n) {
+// a.cand + blockIdx.x * seg_cap.  Warp w owns a contiguous sub-range of the
+// chunk and streams it through its own 4-stage ring of 2 KB bulk copies
+// (cp.async.bulk + mbarrier; 16 warps x 8 KB = 128 KB in flight per SM, what
+// HBM needs at one CTA per SM), appending its candidates to its own region
+// [w * sub, ...) of the segment with warp-level prefix sums only (no CTA
+// barrier in the loop); the runs are then moved down to their final,
+// contiguous positions in warp order (each run is read before the position it
+// is written to: destination <= source).
+constexpr int kScanStages = 4, kScanStageF = 512;                  // floats per stage
+constexpr uint32_t kScanRingBytes = kPotWarps * kScanStages * kScanStageF * 4;   // 128 KB
+
+__device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, long long *out_n) {
+  extern __shared__ __align__(128) double dsm_scan[];   // k_pot's dynamic shared memory
+  __shared__ uint64_t sbar[kPotWarps][kScanStages];
+  __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
   int64_t b0, b1;
   score_chunk(a.n_local, &b0, &b1);
   const float *src = a.scores + b0;
   const int64_t len = b1 - b0;
   float *dst = a.cand + (size_t)blockIdx.x * seg_cap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // warp sub-ranges: multiples of 4 scores (float4-aligned when the chunk is)
+  // warp sub-ranges: multiples of 4 scores (16 B aligned when the chunk is)
   const int64_t sub = ((len + kPotWarps - 1) / kPotWarps + 3) / 4 * 4;
   const int64_t w0 = min(len, (int64_t)warp * sub), w1 = min(len, w0 + sub);
   float *wdst = dst + w0;
-  long long cnt = 0, below = 0;   // warp-uniform cnt
-  const bool al = (reinterpret_cast<uintptr_t>(src + w0) & 15) == 0;
-  // the leading nv (0..4) elements of q are scores, in index order after the
-  // previous lanes' elements
-  auto put4 = [&](const float4 q, int nv) {
+  float *ring = reinterpret_cast<float *>(dsm_scan) + (size_t)warp * kScanStages * kScanStageF;
+  long long cnt = 0, below = 0;   // cnt warp-uniform
+  auto put4 = [&](const float4 q, int nv) {   // leading nv (0..4) elements are scores
     const float e4[4] = {q.x, q.y, q.z, q.w};
+    bool cand[4];
     int c = 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) c += (e < nv && f2key(e4[e]) >= lo);
+    for (int e = 0; e < 4; ++e) {
+      cand[e] = e < nv && f2key(e4[e]) >= lo;
+      c += cand[e];
+    }
     below += nv - c;
     int incl = c;
 #pragma unroll
@@ -459,34 +468,42 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t s
     long long o = cnt + incl - c;
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (e < nv && f2key(e4[e]) >= lo) wdst[o++] = e4[e];
+      if (cand[e]) wdst[o++] = e4[e];
     cnt += __shfl_sync(0xffffffffu, incl, 31);
   };
-  int64_t tail0 = w0;
-  if (al) {
-    const float4 *x4 = reinterpret_cast<const float4 *>(src + w0);
-    const int64_t n4 = (w1 - w0) / 4;
-    float4 nq[4];
+  const bool al = (reinterpret_cast<uintptr_t>(src + w0) & 15) == 0;
+  const int64_t nbulk = al ? (w1 - w0) / 4 * 4 : 0;                 // floats through the ring
+  const int64_t nst = (nbulk + kScanStageF - 1) / kScanStageF;
+  if (lane == 0)
+    for (int k = 0; k < kScanStages; ++k) mbar_init(&sbar[warp][k], 1);
+  fence_mbar_init();
+  __syncwarp();
+  auto issue = [&](int64_t st) {
+    const int slot = (int)(st % kScanStages);
+    const uint32_t bytes =
+        (uint32_t)(min((int64_t)kScanStageF, nbulk - st * kScanStageF) * 4);
+    mbar_arrive_expect_tx(&sbar[warp][slot], bytes);
+    bulk_g2s(ring + slot * kScanStageF, src + w0 + st * kScanStageF, bytes, &sbar[warp][slot]);
+  };
+  if (lane == 0)
+    for (int64_t st = 0; st < min((int64_t)kScanStages, nst); ++st) issue(st);
+  for (int64_t st = 0; st < nst; ++st) {
+    const int slot = (int)(st % kScanStages);
+    mbar_wait(&sbar[warp][slot], (uint32_t)((st / kScanStages) & 1));
+    const int64_t nf = min((int64_t)kScanStageF, nbulk - st * kScanStageF);   // multiple of 4
+    const float4 *r4 = reinterpret_cast<const float4 *>(ring + slot * kScanStageF);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = u * 32 + lane;
-      nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < kScanStageF / 128; ++u) {
+      const int i4 = u * 32 + lane;
+      const bool ok = 4 * i4 < nf;
+      const float4 q = ok ? r4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      put4(q, ok ? 4 : 0);
     }
-    for (int64_t i0 = 0; i0 < n4; i0 += 128) {   // warp-uniform trip count
-      float4 cur[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cur[u] = nq[u];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + 128 + u * 32 + lane;
-        nq[u] = (i < n4) ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) put4(cur[u], (i0 + u * 32 + lane < n4) ? 4 : 0);
-    }
-    tail0 = w0 + 4 * n4;
+    fence_proxy_async_smem();   // this warp's reads of the slot before the next bulk write
+    __syncwarp();
+    if (lane == 0 && st + kScanStages < nst) issue(st + kScanStages);
   }
-  for (int64_t i0 = tail0; i0 < w1; i0 += 128) {   // ragged / unaligned: 4 scalars per lane
+  for (int64_t i0 = w0 + nbulk; i0 < w1; i0 += 128) {   // unaligned or ragged rest
     const int64_t i = i0 + 4 * lane;
     float4 q;
     q.x = i < w1 ? __ldg(src + i) : 0.f;
@@ -497,7 +514,6 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t s
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
-  __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
   if (lane == 0) {
     wcount[warp] = cnt;
     wbelow[warp] = below;
@@ -529,7 +545,6 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int *wc, int64_t s
     a.cand_n[kMaxCtas + blockIdx.x] = bl;
   }
   __syncthreads();
-  (void)wc;
 }
 
 // ---------------------------------------------------------------- K4 ----
@@ -1379,7 +1394,7 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       int ns = 0;
       sample_phase(a, ssel, sh.s.h, sh.s.sk, ns, wtot, reinterpret_cast<int *>(found), epoch, s_tot);
     } else if (ph == P_SCAN) {
-      scan_phase(a, ssel.prefix, wcnt, seg_cap, my_n);
+      scan_phase(a, ssel.prefix, seg_cap, my_n);
       grid_sync(g, epoch);
       stamp(g);
       // every CTA: keys below lo over the grid (fixed order) -> candidate mode
@@ -1506,8 +1521,9 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
   const int64_t per_cta = (a.cap + nb - 1) / nb;
   const int64_t cap_vals = per_cta < kMaxYCacheBytes / 8 ? per_cta : kMaxYCacheBytes / 8;
   c.ycache_cap = (int)cap_vals;
-  const size_t dyn = (a.first <= P_FIT && a.last >= P_FIT) ? (size_t)cap_vals * 8 : 0;
+  size_t dyn = (a.first <= P_FIT && a.last >= P_FIT) ? (size_t)cap_vals * 8 : 0;
   if (dyn == 0) c.ycache_cap = 0;
+  if (a.first <= P_SCAN && a.last >= P_SCAN && dyn < kScanRingBytes) dyn = kScanRingBytes;
   if (reset_barrier) ENOVA_CUDA_TRY(cudaMemsetAsync(&a.g->bar_count, 0, sizeof(unsigned int), st));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nb);
