@@ -55,7 +55,17 @@ constexpr int kSums = 6;              // P, L, dP, dL, d2P, d2L per evaluation p
 // root blurred the sign test
 constexpr double kCertRel = 5e-12;
 
-enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3 };
+enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_GRIDFIX = 5 };
+// Large tails (N_t >= kGrid32MinPeaks): the 128-point scan grid is evaluated in
+// ONE pass of mixed precision (PH_GRID32) -- points with |x| Ymax <= 1e-3 from
+// six fp64 power sums of Y/Ymax (the log1p and 1/(1+t) series, 1e-18 truncation),
+// points with x Ymax < -0.9 in fp64, the rest in fp32 with fp64 accumulation and
+// an error bound: a sign is accepted when |w32| > 1e-5 (|P| + |L| + |P L|), else
+// that point is re-evaluated in fp64 (PH_GRIDFIX).  The signs, hence the
+// brackets, are those of the fp64 scan wherever the fp64 scan itself resolves
+// them; the Halley refinement that follows is fp64 as before.
+constexpr int64_t kGrid32MinPeaks = 100000;
+constexpr int kPow = 6;   // power sums of u = Y / Ymax for the series points
 // phase program of k_pot
 enum { P_SAMPLE = 0, P_SCAN = 1, P_HIST0 = 2, P_HIST1 = 3, P_HIST2 = 4, P_COMPACT = 5, P_FIT = 6 };
 // sampled candidate selection (single GPU, n >= kSampleMinN): P_SAMPLE picks a
@@ -88,6 +98,8 @@ struct PotGlobal {
                                      // until the next calibration fit zeroes the header)
   int pad2;
   int n_stamps, fit_passes;
+  unsigned int sample_lo;            // P_SAMPLE's candidate bound (key), read by k_pot_scan
+  int pad4;
   int sampled, fit_stamp;            // the last selection ran on the sampled candidates;
                                      // stamp index at the start of the fit (diagnostic)
   unsigned long long stamps[kMaxStamps];   // %globaltimer of CTA 0 at phase boundaries (diagnostic)
@@ -99,6 +111,12 @@ struct FitState {
   double t, q, ybar, ymin, ymax;
   int phase, npts, nslots, iters, overflow, converged, nrefine, method, nroots;
   double xs[kMaxPts], w[kMaxPts], L[kMaxPts], dw[kMaxPts], ddw[kMaxPts];
+  double P[kMaxPts];          // mean -xY/(1+xY) of the last pass (certification bound)
+  // PH_GRID32 / PH_GRIDFIX: the full scan grid, w at its points, how each point
+  // is evaluated (0 fp32 certified, 1 series, 2 fp64), evaluation-list <-> grid
+  double gx[kMaxPts], gw[kMaxPts], pm[kPow + 1];
+  int gmode[kMaxPts], gidx[kMaxPts], ginv[kMaxPts];
+  int ngrid, n64, n32, nfix;
   int triple;                 // REFINE evaluates (x, x(1-d), x(1+d)) per root (certifying)
   int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
@@ -535,6 +553,15 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
   __syncthreads();
 }
 
+// The scan as its own (non-cooperative) launch between the sampling launch and
+// the selection + fit launch: its register budget is its own (inside the
+// phase-program kernel the loop ran at ~1.3 TB/s), same grid and partition.
+__global__ void __launch_bounds__(kPotThreads, 1) k_pot_scan(PotArgs a) {
+  __shared__ long long n2[2];
+  const unsigned int lo = *(volatile unsigned int *)&a.g->sample_lo;
+  scan_phase(a, lo, ((a.n_local + gridDim.x - 1) / gridDim.x + 3) / 4 * 4, n2);
+}
+
 // ---------------------------------------------------------------- K4 ----
 // Stable compaction of the peaks Y = s - t (s > t) of this rank in index order.
 // The CTA's peak count is known without reading the scores: keys above the
@@ -704,8 +731,75 @@ __device__ void compact(const PotArgs &a, const SelS &sel, const unsigned int *h
 //          root); pick the best; z_q.
 __device__ void controller(FitState *f, int *scratch) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int phase = f->phase;   // read by all threads before any write below
+  int phase = f->phase;   // read by all threads before any write below
   __syncthreads();
+  if (phase == PH_GRID32 || phase == PH_GRIDFIX) {
+    // w at every scan-grid point: series / fp64 / certified fp32 (GRID32), or the
+    // fp64 re-evaluations of the uncertain fp32 points (GRIDFIX)
+    const int ng = f->ngrid;
+    if (phase == PH_GRID32) {
+      if (tid < ng) {
+        const int mode = f->gmode[tid];
+        if (mode == 1) {
+          // series in t = z u, z = x Ymax, u = Y / Ymax (|t| <= 1e-3):
+          //   P = sum_m (-1)^m z^m <u^m>,  L = sum_m (-1)^(m+1) z^m <u^m> / m,
+          //   P + L = sum_{m>=2} (-1)^m (1 - 1/m) z^m <u^m>  (no O(z) cancellation)
+          const double z = f->gx[tid] * f->ymax;
+          double P = 0.0, L = 0.0, PL = 0.0, zm = 1.0;
+          for (int m = 1; m <= kPow; ++m) {
+            zm *= z;
+            const double tm = zm * f->pm[m];
+            const double sg = (m & 1) ? -1.0 : 1.0;
+            P += sg * tm;
+            L -= sg * tm / m;
+            if (m >= 2) PL += sg * tm * (1.0 - 1.0 / m);
+          }
+          f->gw[tid] = PL + P * L;
+        } else {
+          const int li = f->ginv[tid];
+          const double w = f->w[li];
+          f->gw[tid] = w;
+          if (mode == 0) {
+            const double P = f->P[li], L = f->L[li];
+            const double bound = 1e-5 * (fabs(P) + fabs(L) + fabs(P * L));
+            if (!(fabs(w) > bound)) f->gmode[tid] = 3;   // uncertain: fp64 re-evaluation
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int nf = 0;
+        for (int g = 0; g < ng; ++g)
+          if (f->gmode[g] == 3) {
+            f->gidx[nf] = g;
+            f->xs[nf] = f->gx[g];
+            f->gmode[g] = 2;
+            ++nf;
+          }
+        f->nfix = nf;
+        if (nf > 0) {
+          f->npts = nf;
+          f->phase = PH_GRIDFIX;
+        }
+      }
+      __syncthreads();
+      if (f->nfix > 0) return;   // one more (fp64) pass over Y
+    } else {
+      if (tid < f->nfix) f->gw[f->gidx[tid]] = f->w[tid];
+      __syncthreads();
+    }
+    // the whole grid, in grid order, for the bracket scan
+    if (tid < ng) {
+      f->xs[tid] = f->gx[tid];
+      f->w[tid] = f->gw[tid];
+    }
+    if (tid == 0) {
+      f->npts = ng;
+      f->phase = PH_GRID;
+    }
+    __syncthreads();
+    phase = PH_GRID;
+  }
   if (phase == PH_GRID) {
     const int npts = f->npts;
     bool ex = false, br = false;
@@ -970,6 +1064,36 @@ __device__ void setup_grid(FitState *f) {
     f->npts = (b > a) ? 2 * kGrid : kGrid;
     f->phase = PH_GRID;
   }
+  if (f->nt >= kGrid32MinPeaks) {
+    __syncthreads();
+    if (k == 0) {
+      // evaluation list: the fp64 points first, then the fp32 points; series
+      // points are not evaluated over Y (power sums)
+      const int ng = f->npts;
+      int n64 = 0, n32 = 0;
+      for (int g = 0; g < ng; ++g) {
+        const double z = f->xs[g] * ymax;
+        f->gx[g] = f->xs[g];
+        f->gmode[g] = (fabs(z) <= 1e-3) ? 1 : (z < -0.9) ? 2 : 0;
+        n64 += f->gmode[g] == 2;
+        n32 += f->gmode[g] == 0;
+      }
+      int i64 = 0, i32 = n64;
+      for (int g = 0; g < ng; ++g) {
+        const int li = f->gmode[g] == 2 ? i64++ : f->gmode[g] == 0 ? i32++ : -1;
+        f->ginv[g] = li;
+        if (li >= 0) {
+          f->gidx[li] = g;
+          f->xs[li] = f->gx[g];
+        }
+      }
+      f->ngrid = ng;
+      f->n64 = n64;
+      f->n32 = n32;
+      f->npts = n64 + n32;
+      f->phase = PH_GRID32;
+    }
+  }
 }
 
 // ---- fp64 kernels of the w(x) sums: reciprocal and log1p ----------------
@@ -1073,11 +1197,91 @@ __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t
       for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
 }
 
+// fp32 log1p(t), t > -1, given v = fl(1 + t) and r ~ 1/v: log(v) + c/v with c =
+// t - (v - 1) the rounding error of v; log(v) = e ln2 + 2 atanh(s), v = 2^e m,
+// m in [sqrt(1/2), sqrt(2)), s = (m - 1)/(m + 1), |s| <= 0.1716, atanh by its
+// odd series to s^9 (truncation < 3e-9).  A few ulp relative over the range the
+// certified scan uses it on (t >= -0.9).
+__device__ __forceinline__ float log1p_f32(float t, float v, float r) {
+  const float c = t - (v - 1.f);
+  int bits = __float_as_int(v);
+  int e = ((bits >> 23) & 0xff) - 127;
+  bits = (bits & 0x007fffff) | 0x3f800000;
+  if (bits > 0x3fb504f3) {   // m > sqrt(2): halve
+    bits -= 0x00800000;
+    ++e;
+  }
+  const float m = __int_as_float(bits);
+  float ip;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ip) : "f"(m + 1.f));
+  const float sn = (m - 1.f) * ip;
+  const float s2 = sn * sn;
+  float q = 1.f / 9.f;
+  q = fmaf(q, s2, 1.f / 7.f);
+  q = fmaf(q, s2, 0.2f);
+  q = fmaf(q, s2, 1.f / 3.f);
+  const float at = fmaf(sn * s2, q, sn);   // atanh(s)
+  return fmaf((float)e, 0.6931471805599453f, fmaf(2.f, at, c * r));
+}
+
+// fp32 terms of the P and L sums for up to 4 scan points; fp32 partials over 8
+// terms are flushed into fp64 accumulators (so the sum error stays at the
+// terms' own rounding, ~1e-7 relative).
+__device__ __forceinline__ void eval_bundle32(const double *Y, int64_t s0, int64_t s1,
+                                              const double (&x)[4], int nu,
+                                              double (&acc)[4][kSums]) {
+  float xf[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    xf[u] = (float)x[u];
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
+  }
+  float pp[4] = {0.f, 0.f, 0.f, 0.f}, ll[4] = {0.f, 0.f, 0.f, 0.f};
+  int run = 0;
+  for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
+    const float y = (float)Y[i];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u < nu) {
+        const float t = xf[u] * y;
+        const float v = 1.f + t;
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+        pp[u] = fmaf(-t, r, pp[u]);
+        ll[u] += log1p_f32(t, v, r);
+      }
+    }
+    if (++run == 8) {
+      run = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u][0] += (double)pp[u];
+        acc[u][1] += (double)ll[u];
+        pp[u] = 0.f;
+        ll[u] = 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    acc[u][0] += (double)pp[u];
+    acc[u][1] += (double)ll[u];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
+}
+
 struct FitShared {
   FitState f;
   LogTab tab;
   int scratch[32];
   double sred[kMaxPts][kSums];   // per warp item partial sums [item][k]
+  double powp[kPotWarps][kPow];  // PH_GRID32: per-warp power sums of Y / Ymax
   double red[kSums][kMaxPts];    // grid totals after the barrier
 };
 
@@ -1212,21 +1416,29 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
     double *pw = a.part + (size_t)(pass & 1) * kSums * kMaxPts * kMaxCtas;
     const int npts = f.npts;
     const bool deriv = (phase == PH_REFINE);
+    const bool mixed = (phase == PH_GRID32);
     const int nk = deriv ? kSums : 2;
-    const int nbund = (npts + 3) / 4;
+    // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones
+    const int n64 = mixed ? f.n64 : npts;
+    const int nb64 = (n64 + 3) / 4;
+    const int nbund = mixed ? nb64 + (f.n32 + 3) / 4 : (npts + 3) / 4;
     const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
     const int items = nbund * slices;
     for (int it = warp; it < items; it += kPotWarps) {
       const int bnd = it % nbund, sl = it / nbund;
       const int64_t len = c1 - c0;
       const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
+      const bool f32 = mixed && bnd >= nb64;
+      const int base = f32 ? n64 + 4 * (bnd - nb64) : 4 * bnd;
+      const int nu = min(4, (f32 ? n64 + f.n32 : (mixed ? n64 : npts)) - base);
       double x[4];
-      const int nu = min(4, npts - 4 * bnd);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[4 * bnd + u] : 0.0;
+      for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[base + u] : 0.0;
       double acc[4][kSums];
       if (deriv)
         eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
+      else if (f32)
+        eval_bundle32(Y, s0, s1, x, nu, acc);
       else
         eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
       if (lane == 0) {
@@ -1234,10 +1446,36 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
         for (int u = 0; u < 4; ++u)
           if (u < nu)
 #pragma unroll
-            for (int k = 0; k < kSums; ++k) S.sred[sl * npts + 4 * bnd + u][k] = acc[u][k];
+            for (int k = 0; k < kSums; ++k) S.sred[sl * npts + base + u][k] = acc[u][k];
+      }
+    }
+    if (mixed) {   // power sums of u = Y / Ymax for the series points (fp64, fixed order)
+      const double iy = 1.0 / f.ymax;
+      double q[kPow];
+#pragma unroll
+      for (int m = 0; m < kPow; ++m) q[m] = 0.0;
+      for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+        const double u = Y[i] * iy;
+        double pw_ = u;
+#pragma unroll
+        for (int m = 0; m < kPow; ++m) {
+          q[m] += pw_;
+          pw_ *= u;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < kPow; ++m) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) q[m] += __shfl_xor_sync(0xffffffffu, q[m], o);
+        if (lane == 0) S.powp[warp][m] = q[m];
       }
     }
     __syncthreads();
+    if (mixed && threadIdx.x < kPow) {   // CTA partial power sums -> partial row 2
+      double sp = 0.0;
+      for (int w = 0; w < kPotWarps; ++w) sp += S.powp[w][threadIdx.x];
+      pw[((size_t)2 * kMaxPts + threadIdx.x) * kMaxCtas + blockIdx.x] = sp;
+    }
     // CTA partial per (k, point): slices summed in order
     for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
       const int k = i / npts, pt = i % npts;
@@ -1251,13 +1489,14 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
     // grid totals, fixed order: one warp per (k, point), 4 items in flight per warp
     {
       constexpr int kJ = (kMaxCtas + 31) / 32;
-      const int nitems = nk * npts;
+      const int nitems = nk * npts + (mixed ? kPow : 0);   // + the power sums (row 2)
       for (int i0 = 4 * warp; i0 < nitems; i0 += 4 * kPotWarps) {
         double v[4][kJ];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int i = i0 + q;
-          const int k = i / npts, pt = i % npts;
+          const bool extra = i >= nk * npts;
+          const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
           const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
 #pragma unroll
           for (int j = 0; j < kJ; ++j) {
@@ -1273,7 +1512,10 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
 #pragma unroll
           for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
           const int i = i0 + q;
-          if (lane == 0 && i < nitems) S.red[i / npts][i % npts] = sum;
+          if (lane == 0 && i < nitems) {
+            if (i >= nk * npts) S.red[2][i - nk * npts] = sum;
+            else S.red[i / npts][i % npts] = sum;
+          }
         }
       }
     }
@@ -1284,6 +1526,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
       const double Pm = S.red[0][pt] / N, Lm = S.red[1][pt] / N;
       f.w[pt] = Pm + Lm + Pm * Lm;
       f.L[pt] = Lm;
+      f.P[pt] = Pm;
       if (deriv) {
         const double dPm = S.red[2][pt] / N, dLm = S.red[3][pt] / N;
         const double d2Pm = S.red[4][pt] / N, d2Lm = S.red[5][pt] / N;
@@ -1291,6 +1534,8 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
         f.ddw[pt] = d2Pm + d2Lm + d2Pm * Lm + 2.0 * dPm * dLm + Pm * d2Lm;
       }
     }
+    if (mixed && threadIdx.x == 0)
+      for (int m = 1; m <= kPow; ++m) f.pm[m] = S.red[2][m - 1] / (double)nt;   // mean u^m
     __syncthreads();
     stamp(a.g);
     controller(&f, S.scratch);
@@ -1381,10 +1626,14 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
     if (ph == P_SAMPLE) {
       int ns = 0;
       sample_phase(a, ssel, sh.s.h, sh.s.sk, ns, wtot, reinterpret_cast<int *>(found), epoch, s_tot);
+      if (blockIdx.x == 0 && threadIdx.x == 0) g->sample_lo = ssel.prefix;
     } else if (ph == P_SCAN) {
-      scan_phase(a, ssel.prefix, seg_cap, my_n);
-      grid_sync(g, epoch);
-      stamp(g);
+      // the candidates were compacted by k_pot_scan (previous launch): this
+      // CTA's counts
+      if (threadIdx.x == 0) {
+        my_n[0] = *(volatile long long *)(a.cand_n + blockIdx.x);
+        my_n[1] = *(volatile long long *)(a.cand_n + kMaxCtas + blockIdx.x);
+      }
       // every CTA: keys below lo over the grid (fixed order) -> candidate mode
       // iff the k-th order statistic is among the candidates
       if (threadIdx.x == 0) {
@@ -1495,6 +1744,31 @@ void set_pot_grid(int ctas, int cluster) {
 }
 
 static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool reset_barrier = false) {
+  if (a.first == P_SAMPLE && a.last > P_SAMPLE) {
+    // sampled selection: sampling launch -> k_pot_scan -> selection + fit launch
+    PotArgs s1 = a;
+    s1.last = P_SAMPLE;
+    enova_status r = launch_pot(s1, nb, st, reset_barrier);
+    if (r) return r;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(kPotThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (g_pot_cluster > 1 && nb % g_pot_cluster == 0) {
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)g_pot_cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
+    count_launch();
+    ENOVA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pot_scan, a));
+    PotArgs s3 = a;
+    s3.first = P_SCAN;
+    return launch_pot(s3, nb, st, true);
+  }
   PotArgs c = a;
   static bool attr_set[64] = {};   // per device (function attributes are per context)
   int dev = 0;
