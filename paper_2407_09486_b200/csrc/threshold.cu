@@ -448,7 +448,8 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
 // 3.4 TB/s vs 2.6 TB/s for a shuffle-scan compaction at one CTA per SM,
 // tools/ubench_scan.cu).  The runs are then moved down to their final,
 // contiguous positions in warp order (destination <= source, read before write).
-__device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, long long *out_n) {
+__device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, long long *out_n,
+                           float *stage, int stage_cap) {
   __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
   int64_t b0, b1;
   score_chunk(a.n_local, &b0, &b1);
@@ -525,22 +526,36 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
     wbelow[warp] = below;
   }
   __syncthreads();
-  // move run w (at w * sub) down to its final position, in warp order
-  long long pos = wcount[0];
-  for (int w = 1; w < kPotWarps; ++w) {
-    const long long c = wcount[w];
-    if (warp == w) {
-      const float *from = dst + (int64_t)w * sub;
-      float *to = dst + pos;
-      for (long long i = 0; i < c; i += 32) {   // chunk read before write: to <= from
-        const float v = (i + lane < c) ? from[i + lane] : 0.f;
-        __syncwarp();
-        if (i + lane < c) to[i + lane] = v;
-        __syncwarp();
-      }
-    }
-    pos += c;
+  // runs -> one contiguous, index-ordered segment.  Common case (the CTA's
+  // candidates fit the staging smem): every warp copies its run to its final
+  // offset in shared memory at once, then the CTA writes the segment back
+  // (parallel, no dependent round trips).  Otherwise the runs are moved down in
+  // warp order, 512 threads per chunk, each chunk read before it is written
+  // (destination <= source).
+  long long pos = 0, mypos = 0;
+  for (int w = 0; w < kPotWarps; ++w) {
+    if (w == warp) mypos = pos;
+    pos += wcount[w];
+  }
+  if (pos <= (long long)stage_cap) {
+    const float *from = dst + (int64_t)warp * sub;
+    for (long long i = lane; i < cnt; i += 32) stage[mypos + i] = from[i];
     __syncthreads();
+    for (long long i = threadIdx.x; i < pos; i += blockDim.x) dst[i] = stage[i];
+  } else {
+    long long p2 = wcount[0];
+    for (int w = 1; w < kPotWarps; ++w) {
+      const long long c = wcount[w];
+      const float *from = dst + (int64_t)w * sub;
+      float *to = dst + p2;
+      for (long long i = 0; i < c; i += blockDim.x) {
+        const float v = (i + threadIdx.x < c) ? from[i + threadIdx.x] : 0.f;
+        __syncthreads();
+        if (i + threadIdx.x < c) to[i + threadIdx.x] = v;
+        __syncthreads();
+      }
+      p2 += c;
+    }
   }
   if (threadIdx.x == 0) {
     long long bl = 0;
@@ -556,10 +571,13 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
 // The scan as its own (non-cooperative) launch between the sampling launch and
 // the selection + fit launch: its register budget is its own (inside the
 // phase-program kernel the loop ran at ~1.3 TB/s), same grid and partition.
+constexpr int kScanStageBytes = 200 * 1024;   // k_pot_scan's staging smem (51 200 candidates)
 __global__ void __launch_bounds__(kPotThreads, 1) k_pot_scan(PotArgs a) {
+  extern __shared__ float scan_stage[];
   __shared__ long long n2[2];
   const unsigned int lo = *(volatile unsigned int *)&a.g->sample_lo;
-  scan_phase(a, lo, ((a.n_local + gridDim.x - 1) / gridDim.x + 3) / 4 * 4, n2);
+  scan_phase(a, lo, ((a.n_local + gridDim.x - 1) / gridDim.x + 3) / 4 * 4, n2, scan_stage,
+             kScanStageBytes / 4);
 }
 
 // ---------------------------------------------------------------- K4 ----
@@ -1763,6 +1781,16 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
       cfg.attrs = at;
       cfg.numAttrs = 1;
     }
+    static bool scan_attr[64] = {};
+    int dv = 0;
+    ENOVA_CUDA_TRY(cudaGetDevice(&dv));
+    if (dv < 0 || dv >= 64 || !scan_attr[dv]) {
+      ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot_scan,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kScanStageBytes));
+      if (dv >= 0 && dv < 64) scan_attr[dv] = true;
+    }
+    cfg.dynamicSmemBytes = kScanStageBytes;
     count_launch();
     ENOVA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pot_scan, a));
     PotArgs s3 = a;
