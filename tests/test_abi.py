@@ -64,9 +64,13 @@ def test_workspace_sizing_and_envelope(L):
     b = L.enova_threshold_workspace_bytes(10**6, 0.98)
     assert a > b > 0
     assert a >= 8 * int(0.02 * 10**8)            # the fp64 tail the fit runs on
-    for w in (1, 2, 8):                              # + this rank's fp32 tail + w gathered slots
-        c = L.enova_threshold_comm_workspace_bytes(10**8, 0.98, w)
-        assert c >= a + 4 * int(0.02 * 10**8) * (w + 1)
+    assert a >= 4 * 10**8                        # n >= 2^22: sampled selection's candidate segments
+    for n in (10**6, 10**8):
+        for w in (1, 2, 8):                          # fp64 tail + this rank's fp32 tail + w gathered slots
+            c = L.enova_threshold_comm_workspace_bytes(n, 0.98, w)
+            assert c >= 8 * int(0.02 * n) + 4 * int(0.02 * n) * (w + 1)
+    # the communicator path runs the full radix passes (no candidate buffer)
+    assert L.enova_threshold_comm_workspace_bytes(10**6, 0.98, 1) >= b
 
 
 def test_validation_before_any_launch(L):
