@@ -1047,6 +1047,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
         __threadfence_block();   // own pushed sample before this thread's cp.async reads
       } else {
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();   // reconverge after the per-row push (bar.sync is .aligned)
         named_bar_sync(5, kRowThreads + 32);
       }
     }

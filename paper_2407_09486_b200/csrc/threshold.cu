@@ -376,12 +376,14 @@ __device__ void select_digit(const PotArgs &a, SelS &sel, int pass, unsigned lon
     before += c[u];
   }
   __syncthreads();
-  const unsigned int digit = (unsigned int)found[0];
-  const unsigned long long below = reinterpret_cast<unsigned long long *>(found)[1];
-  sel.prefix |= digit << shift;
-  sel.mask |= (unsigned int)(nbins - 1) << shift;
-  sel.k_rem = k - below;
-  if (pass == 2) sel.t = key2f(sel.prefix);
+  if (tid == 0) {   // sel is shared: one writer (every thread read k before the barrier)
+    const unsigned int digit = (unsigned int)found[0];
+    const unsigned long long below = reinterpret_cast<unsigned long long *>(found)[1];
+    sel.prefix |= digit << shift;
+    sel.mask |= (unsigned int)(nbins - 1) << shift;
+    sel.k_rem = k - below;
+    if (pass == 2) sel.t = key2f(sel.prefix);
+  }
   __syncthreads();
 }
 
