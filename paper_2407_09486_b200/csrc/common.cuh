@@ -363,6 +363,40 @@ __device__ __forceinline__ void mma_f16_pair_warp_x4(uint32_t d_tmem, uint64_t a
       "l"(adesc), "l"(bdesc), "r"(idesc), "l"(astep), "l"(bstep)
       : "memory");
 }
+// as mma_f16_pair_warp_x4, the first MMA accumulating only if acc_first != 0
+// (starts an accumulator from zero)
+__device__ __forceinline__ void mma_f16_pair_warp_x4a(uint32_t d_tmem, uint64_t adesc,
+                                                      uint64_t bdesc, uint32_t idesc,
+                                                      uint64_t astep, uint64_t bstep,
+                                                      uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred e, t, p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 a1, %1, %4;\n\tadd.s64 a2, a1, %4;\n\tadd.s64 a3, a2, %4;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, b1, %5;\n\tadd.s64 b3, b2, %5;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "l"(astep), "l"(bstep), "r"(acc_first)
+      : "memory");
+}
+// D[tmem] (+)= A[TMEM] B[smem]^T over a CTA pair ("TS" form): A row m of the pair
+// tile is lane m mod 128 of CTA m / 128 at the same TMEM address in both CTAs;
+// for kind::f16 a K=16 step spans 8 columns of packed fp16 pairs (k = 2c in the
+// low half).  Layout checked by tools/ubench_ts.cu.
+__device__ __forceinline__ void mma_ts_pair_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_pair_warp(uint64_t *bar, uint16_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

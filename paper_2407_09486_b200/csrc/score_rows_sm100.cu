@@ -17,10 +17,11 @@
 //             raw loads run kRPF K-steps ahead in registers.
 //   GEMM1   : tcgen05.mma cta_group::1 kind::f16 M=128 N=H K=16 per step, A from
 //             the ring, B = W1's back-to-back K-step image streamed through a
-//             4-stage bulk-copy ring; the TMEM accumulator is pre-loaded with b1.
-//   epilogue: E1 (tanh -> h hi/lo), GEMM2 (heads), E2 (KL, mu hi/lo), GEMM3
-//             (decoder, accumulator re-armed with b3), E3 (MD by the column-sum
-//             identity, flag) -- the same element-wise arithmetic (epilogue.cuh)
+//             4-stage bulk-copy ring; the TMEM accumulator starts from zero.
+//   epilogue: E1 (tanh(acc + b1) -> h hi/lo), GEMM2 (heads), E2 (KL, mu hi/lo),
+//             GEMM3 (decoder, from zero in the GEMM1 columns), E3 (MD by the
+//             column-sum identity with tanh(acc + b3), flag) -- the same
+//             element-wise arithmetic (epilogue.cuh)
 //             and the same window-sum association as the windowed CTA-pair
 //             kernel, so a streamed window scores bit-identically to the same
 //             window scored in a batch.
@@ -134,7 +135,7 @@ struct WinSum {
   }
 };
 
-// E1 (encoder tanh -> h hi/lo; GEMM1 columns re-armed with b3), E2 (KL score,
+// E1 (encoder tanh -> h hi/lo), E2 (KL score,
 // mu hi/lo), E3 (MD by the column-sum identity, flag) for one row of a row
 // tile -- the CTA-pair kernel's element-wise arithmetic (epilogue.cuh) in the
 // same association.  Row threads of warps 0-3; GEMM2/GEMM3 are issued by the
@@ -143,7 +144,8 @@ struct WinSum {
 template <int H, int ZP, class Bars, class SxFn>
 __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane, int r, int64_t row,
                                               bool valid, SxFn &&sx_fn, uint8_t *region,
-                                              uint8_t *mubuf, const float *b3s, const float *wbs,
+                                              uint8_t *mubuf, const float *b1cs,
+                                              const float *b3s, const float *wbs,
                                               const float *bmls, Bars &B, int Z, int D,
                                               const double *bbar, float *scores, float *md_out,
                                               int8_t *flags, double z_q, const double *z_q_dev,
@@ -164,21 +166,21 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     (void)tr;
 #endif
   };
-    // ---- E1: h = tanh(acc) -> hi/lo fp16 A images; re-arm acc with b3 ----
+    // ---- E1: h = tanh(acc + b1) -> hi/lo fp16 A images ----
     const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
     mbar_wait_sleep(&B.g1_done, 0);
     stamp(6);
     tc_fence_after();
 #pragma unroll 1
     for (int c16 = 0; c16 < H; c16 += 16) {
-      float v[16];
+      float v[16], bc[16];
       tmem_ld16(lane_addr + c16, v);
+      lds16(b1cs + c16, bc);
       tmem_wait_ld();
-      tmem_fill_cols<16>(lane_addr + c16, b3s + c16);
 #pragma unroll
       for (int e8 = 0; e8 < 16; e8 += 8) {
         uint32_t hi[4], lo[4];
-        e1_tanh_split8(v + e8, hi, lo);   // acc = W1 x + b1 (bias preloaded)
+        e1_tanh_split8_b(v + e8, bc + e8, hi, lo);   // acc = W1 x (from zero)
         const size_t off = kmajor_step_offset(r, c16 + e8, kRR);
         *reinterpret_cast<uint4 *>(region + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4 *>(region + kRR * H * 2 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
@@ -257,10 +259,11 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
         const float4 ww = *reinterpret_cast<const float4 *>(wbs + c32 + k);
-        d4[0] = fmaf(ww.x, tanh_mufu(v[k]), d4[0]);
-        d4[1] = fmaf(ww.y, tanh_mufu(v[k + 1]), d4[1]);
-        d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2]), d4[2]);
-        d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3]), d4[3]);
+        const float4 bb = *reinterpret_cast<const float4 *>(b3s + c32 + k);
+        d4[0] = fmaf(ww.x, tanh_mufu(v[k] + bb.x), d4[0]);   // acc = W3 mu (from zero)
+        d4[1] = fmaf(ww.y, tanh_mufu(v[k + 1] + bb.y), d4[1]);
+        d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2] + bb.z), d4[2]);
+        d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3] + bb.w), d4[3]);
       }
     }
     const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
@@ -279,7 +282,7 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
         tmem_wait_ld();
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float a3 = tanh_2mufu(v[k]);
+          const float a3 = tanh_2mufu(v[k] + b3s[c16 + k]);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (j < M) dm[j] = fmaf(wbarm_s[j * H + c16 + k], a3, dm[j]);
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     fence_mbar_init();
   }
   for (int i = tid; i < H; i += blockDim.x) {
-    b1s[i] = p.b1[i];
+    b1s[i] = __fmul_rn(p.b1[i], kTwoLog2e);   // E1 exponent bias (GEMM1 starts from zero)
     b3s[i] = p.b3[i];
     wbs[i] = p.wbar[i];
   }
@@ -354,16 +357,6 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = B.tmem_slot;
-
-  if (warp < 4) {
-    // GEMM1 accumulator of this row pre-loaded with b1 (GEMM1 accumulates on top)
-    const uint32_t la = tmem + ((uint32_t)(warp * 32) << 16);
-    tmem_fill_cols<H>(la, b1s);
-    tmem_wait_st();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (warp == kRProdWarp) {
     // ---------------- W1 ring producer (+ heads / W3 images once) ----------------
@@ -394,7 +387,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
       const uint64_t ad = make_sdesc(aa + a * kRAStepBytes, kRR * 16, 128);
       const uint64_t bd = make_sdesc(
           ra + st * SL.w_stage_bytes + (q % kRWStageSteps) * 32 * H, 16 * H, 128);
-      mma_f16_warp(tmem, ad, bd, idesc1, 1u);
+      mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
       mma_commit_warp(&B.a_empty[a]);
       if (q % kRWStageSteps == kRWStageSteps - 1 || q == p.nsteps - 1) mma_commit_warp(&B.w_empty[st]);
       if (q == p.nsteps - 1) mma_commit_warp(&B.g1_done);
@@ -424,7 +417,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     if (lane == 0) {
       const uint32_t idesc3 = make_idesc_f16(128, H);
       const uint64_t bd = make_sdesc(smem_u32(w3s), 16 * H, 128);
-      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 1u);
+      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 0u);
       mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf) + kRR * 16 * 2, 16 * kRR, 128), bd, idesc3, 1u);
       mma_commit(&B.g3_done);
     }
@@ -525,7 +518,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     const float sx = ws.acc0 + ws.acc1;
 
     rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, [&]() { return sx; }, region, mubuf,
-                         b3s, wbs, bmls, B,
+                         b1s, b3s, wbs, bmls, B,
                          p.Z, p.D, p.bbar, p.scores, p.md, p.flags, p.z_q, p.z_q_dev, nullptr,
                          kExplain ? wbarm_s : nullptr, kExplain ? xsum : nullptr, p.bbarm,
                          p.md_metric, M, p.W);
@@ -921,7 +914,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     fence_mbar_init();
   }
   for (int i = tid; i < H; i += blockDim.x) {
-    b1s[i] = p.b1[i];
+    b1s[i] = __fmul_rn(p.b1[i], kTwoLog2e);   // E1 exponent bias (GEMM1 starts from zero)
     b3s[i] = p.b3[i];
     wbs[i] = p.wbar[i];
   }
@@ -933,13 +926,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = B.tmem_slot;
-  if (warp < 4) {
-    tmem_fill_cols<H>(tmem + ((uint32_t)(warp * 32) << 16), b1s);
-    tmem_wait_st();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (warp == kRProdWarp) {
     // ---------------- producer: W1 ring (bulk) + A ring (TMA from the fp16 ring) ----------------
@@ -992,7 +978,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       }
       const uint64_t ad = make_sdesc_sw128(aa + a * kSAStageBytes + j * 32);
       const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
-      mma_f16_warp(tmem, ad, bd, idesc1, 1u);
+      mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
       if (lane == 0 && q == 0) stamp(3);
       if (lane == 0 && q == p.nsteps - 1) stamp(4);
       if (j == kSAK - 1 || q == p.nsteps - 1) {
@@ -1024,7 +1010,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     if (lane == 0) {
       const uint32_t idesc3 = make_idesc_f16(128, H);
       const uint64_t bd = make_sdesc(smem_u32(w3s), 16 * H, 128);
-      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 1u);
+      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 0u);
       mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf) + kRR * 16 * 2, 16 * kRR, 128), bd, idesc3, 1u);
       mma_commit(&B.g3_done);
     }
@@ -1138,7 +1124,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       return sx;
     };
     if (r == 0) stamp(5);
-    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx_fn, region, mubuf, b3s, wbs, bmls, B,
+    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx_fn, region, mubuf, b1s, b3s, wbs, bmls, B,
                          p.Z, p.D, p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr);
   }
   tc_fence_before();
