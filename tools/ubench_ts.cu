@@ -94,7 +94,7 @@ __global__ void __cluster_dims__(2, 1, 1) kcheck(const __half *A, const __half *
 }
 
 // throughput: nmma back-to-back M256 N K16 MMAs, A from TMEM (TS) or smem (SS)
-template <int N, bool TS>
+template <int N, bool TS, int NACC = 1>
 __global__ void __cluster_dims__(2, 1, 1) kbench(int nmma, unsigned long long *out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t done;
@@ -113,8 +113,9 @@ __global__ void __cluster_dims__(2, 1, 1) kbench(int nmma, unsigned long long *o
     unsigned long long t0 = clock64();
     for (int q = 0; q < nmma; ++q) {
       const uint64_t bd = make_sdesc(b + (q & 7) * 2048, 16 * (N / 2), 128);
-      if (TS) mma_ts_pair(tmem, tmem + 256 + 8 * (q & 15), bd, id, q > 0);
-      else mma_f16_pair(tmem, make_sdesc(a + (q & 7) * 4096, 2048, 128), bd, id, q > 0);
+      const uint32_t d = tmem + (uint32_t)((q % NACC) * N);   // NACC independent accumulators
+      if (TS) mma_ts_pair(d, tmem + 256 + 8 * (q & 15), bd, id, q >= NACC);
+      else mma_f16_pair(d, make_sdesc(a + (q & 7) * 4096, 2048, 128), bd, id, q >= NACC);
     }
     mma_commit_pair(&done, 3);
     mbar_wait(&done, 0);
@@ -160,13 +161,13 @@ static int check() {
   return bad;
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int NACC = 1>
 static double bench() {
   unsigned long long *d, h = 0;
   cudaMalloc(&d, 8);
-  cudaFuncSetAttribute(kbench<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(kbench<N, TS, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   const int n = 4096;
-  for (int rep = 0; rep < 2; ++rep) kbench<N, TS><<<2, 128, 65536>>>(n, d);
+  for (int rep = 0; rep < 2; ++rep) kbench<N, TS, NACC><<<2, 128, 65536>>>(n, d);
   cudaDeviceSynchronize();
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   cudaFree(d);
@@ -177,6 +178,11 @@ int main() {
   int bad = check<32, 1>() + check<32, 8>() + check<128, 2>();
   printf("cycles per M256 K16 MMA: N=128 SS %.1f TS %.1f | N=32 SS %.1f TS %.1f\n", bench<128, false>(),
          bench<128, true>(), bench<32, false>(), bench<32, true>());
+  printf("independent accumulators (TS): N=32 x2 %.1f x4 %.1f x8 %.1f | N=64 x1 %.1f x2 %.1f | N=16 x1 %.1f x4 %.1f | N=256 x1 %.1f\n",
+         bench<32, true, 2>(), bench<32, true, 4>(), bench<32, true, 8>(), bench<64, true, 1>(),
+         bench<64, true, 2>(), bench<16, true, 1>(), bench<16, true, 4>(), bench<256, true, 1>());
+  printf("independent accumulators (SS): N=32 x4 %.1f | N=128 x2 %.1f\n", bench<32, false, 4>(),
+         bench<128, false, 2>());
   printf("%s\n", bad ? "TS LAYOUT MISMATCH" : "TS layout ok");
   return bad != 0;
 }
