@@ -4,27 +4,33 @@
 // (PAPER.md:282); per-dimension z-score with stats from the training horizon
 // reused at inference, std floored at 1e-6 (R-4).
 //
-// One HBM pass, one wave: a persistent grid of 2 CTAs per SM splits the
+// One HBM pass, one wave: a persistent grid of one CTA per SM splits the
 // flattened (instance, sample) space of the calibration horizon into equal
-// contiguous ranges, so every CTA streams the same number of samples with
-// coalesced 128-bit loads (4 in flight per thread) whatever the fleet shape --
-// no ragged last wave.  A range covers one or more instance SEGMENTS; for each
-// segment the threads accumulate the SHIFTED sums S1 = sum(x - K), S2 =
-// sum((x - K)^2) in fp64, with K = the series' first sample (the same shift in
-// every segment, so segment sums simply add), the CTA reduces them in a fixed
-// order and stores them in the instance's contributor slot (contributor c =
-// this CTA's index minus the instance's first CTA).  The last contributor of
-// an instance (ticket) combines the slots in contributor order: mean = K +
-// S1/n, var = S2/n - (S1/n)^2.  With fp32 data and K inside the series' range
-// this equals the two-pass fp64 result to ~1e-16 relative, far below the fp32
-// rounding that follows; the result depends on the grid only through the
-// contributor split (deterministic for a device).
+// contiguous ranges, so every CTA streams the same number of samples whatever
+// the fleet shape -- no ragged last wave.  The bytes arrive by bulk copy: a
+// producer warp walks the CTA's range as chunks of <= 16 KB inside one instance
+// segment and keeps kStatsStages chunks in flight (cp.async.bulk into a shared
+// memory ring, mbarrier complete_tx), so the HBM latency is covered without
+// register-held loads; 512 consumer threads accumulate from shared memory.
+// For each instance SEGMENT of the range the consumers accumulate the SHIFTED
+// sums S1 = sum(x - K), S2 = sum((x - K)^2) in fp64, with K = the series' first
+// sample (the same shift in every segment, so segment sums simply add), reduce
+// them in a fixed order and store them in the instance's contributor slot
+// (contributor c = this CTA's index minus the instance's first CTA).  The last
+// contributor of an instance (ticket) combines the slots in contributor order:
+// mean = K + S1/n, var = S2/n - (S1/n)^2.  With fp32 data and K inside the
+// series' range this equals the two-pass fp64 result to ~1e-16 relative, far
+// below the fp32 rounding that follows; the result depends on the grid only
+// through the contributor split (deterministic for a device).
 #include "common.cuh"
 
 namespace enova {
 
-constexpr int kStatsThreads = 512;
-constexpr int kStatsMaxGrid = 512;   // 2 CTAs per SM on <= 256 SMs (workspace sizing)
+constexpr int kStatsThreads = 512;              // consumers
+constexpr int kStatsBlock = kStatsThreads + 32; // + the producer warp
+constexpr int kStatsMaxGrid = 512;   // <= 256 SMs x 2 (workspace sizing)
+constexpr int kStatsStages = 6;
+constexpr uint32_t kStatsChunkBytes = 16384;
 
 // contributors of one instance: a CTA range holds >= floor(N T / nb) >= 64
 // samples, so an instance of T samples meets at most ceil(nb / N) + 2 ranges
@@ -45,98 +51,150 @@ __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t S, int nb) {
   return ((x + 1) * nb - 1) / S;
 }
 
+// the chunk sequence of a CTA range (walked identically by producer and consumers):
+// chunk = [c0, c1) of the flattened space inside one instance, <= cs samples
+struct ChunkWalk {
+  int64_t pos, r1, T_cal, cs;
+  __device__ __forceinline__ bool next(int64_t &c0, int64_t &c1) {
+    if (pos >= r1) return false;
+    c0 = pos;
+    const int64_t seg_end = min(r1, (pos / T_cal + 1) * T_cal);
+    c1 = min(seg_end, pos + cs);
+    pos = c1;
+    return true;
+  }
+};
+
 template <bool kPow2Group>
-__global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
+__global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     const float *__restrict__ X, int64_t ld, int M, int64_t N, int64_t T_cal,
     float *__restrict__ mean_out, float *__restrict__ std_out, unsigned long long *diag,
     unsigned int *ticket, double *slots, int64_t max_contrib) {
-  extern __shared__ double red[];  // [nwarps or nslots][2][M]
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t full[kStatsStages], empty[kStatsStages];
   __shared__ bool last;
+  __shared__ int bad_any;
+  double *red = reinterpret_cast<double *>(sm + kStatsStages * kStatsChunkBytes);  // [rows][2][M]
   const int G = M / 4;
-  const int g = threadIdx.x % G;
-  const int slot = threadIdx.x / G;
-  const int nslots = blockDim.x / G;
+  const int nslots = kStatsThreads / G;
+  const int active = nslots * G;       // consumer threads with a (slot, g)
   const int nb = gridDim.x;
   const int64_t S = N * T_cal;
   const int64_t r0 = (int64_t)blockIdx.x * S / nb, r1 = (int64_t)(blockIdx.x + 1) * S / nb;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bad = 0;
-  for (int64_t seg0 = r0; seg0 < r1;) {
-    const int64_t inst = seg0 / T_cal;
-    const int64_t t0 = seg0 - inst * T_cal;
-    const int64_t seg1 = min(r1, (inst + 1) * T_cal);
-    const int64_t t1 = t0 + (seg1 - seg0);
-    const float4 *base = reinterpret_cast<const float4 *>(X + inst * ld);
-    const float4 K = __ldg(base + g);   // shift: the series' first sample
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-    auto acc = [&](const float4 v) {
-      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-      const double d0 = (double)v.x - K.x, d1 = (double)v.y - K.y, d2 = (double)v.z - K.z,
-                   d3 = (double)v.w - K.w;
-      a0 += d0; a1 += d1; a2 += d2; a3 += d3;
-      q0 = fma(d0, d0, q0); q1 = fma(d1, d1, q1); q2 = fma(d2, d2, q2); q3 = fma(d3, d3, q3);
-    };
-    for (int64_t t = t0 + slot; t < t1; t += 4 * nslots) {   // 4 x 128-bit loads in flight
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (t + u * nslots < t1) v[u] = __ldg(base + (t + u * nslots) * G + g);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (t + u * nslots < t1) acc(v[u]);
+  const int64_t cs = max((int64_t)1, (int64_t)(kStatsChunkBytes / (4u * (uint32_t)M)));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < kStatsStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kStatsThreads / 32);
     }
+    bad_any = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= kStatsThreads) {
+    // ---------------- producer warp: bulk copies, kStatsStages chunks ahead ----------------
+    if (lane == 0) {
+      ChunkWalk w{r0, r1, T_cal, cs};
+      int64_t c0, c1;
+      for (int k = 0; w.next(c0, c1); ++k) {
+        const int sg = k % kStatsStages;
+        if (k >= kStatsStages) mbar_wait(&empty[sg], ((k / kStatsStages) - 1) & 1);
+        const int64_t inst = c0 / T_cal, t = c0 - inst * T_cal;
+        const uint32_t bytes = (uint32_t)(c1 - c0) * 4u * (uint32_t)M;
+        mbar_arrive_expect_tx(&full[sg], bytes);
+        bulk_g2s(sm + (size_t)sg * kStatsChunkBytes, X + inst * ld + t * M, bytes, &full[sg]);
+      }
+    }
+    return;   // the consumers never wait on the producer warp with a CTA barrier
+  }
+  // ---------------- consumers ----------------
+  const int g = tid % G;
+  const int slot = tid / G;
+  const bool act = tid < active;
+  int bad = 0;
+  ChunkWalk w{r0, r1, T_cal, cs};
+  int64_t c0, c1;
+  int k = 0;
+  bool have = w.next(c0, c1);
+  while (have) {
+    const int64_t inst = c0 / T_cal;
+    const float4 K = __ldg(reinterpret_cast<const float4 *>(X + inst * ld) + (act ? g : 0));
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+    // every chunk of this segment
+    do {
+      const int sg = k % kStatsStages;
+      mbar_wait(&full[sg], (k / kStatsStages) & 1);
+      const float4 *src = reinterpret_cast<const float4 *>(sm + (size_t)sg * kStatsChunkBytes);
+      const int n = (int)(c1 - c0);
+      if (act) {
+#pragma unroll 4
+        for (int t = slot; t < n; t += nslots) {
+          const float4 v = src[t * G + g];
+          bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+          const double d0 = (double)v.x - K.x, d1 = (double)v.y - K.y, d2 = (double)v.z - K.z,
+                       d3 = (double)v.w - K.w;
+          a0 += d0; a1 += d1; a2 += d2; a3 += d3;
+          q0 = fma(d0, d0, q0); q1 = fma(d1, d1, q1); q2 = fma(d2, d2, q2); q3 = fma(d3, d3, q3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sg]);
+      ++k;
+      have = w.next(c0, c1);
+    } while (have && c0 / T_cal == inst);
+    // ---- the segment's sums: fixed-order reduction, contributor slot, ticket ----
     double v8[8] = {a0, a1, a2, a3, q0, q1, q2, q3};
     int nred;   // partial sums per output left in red[] (summed below in index order)
     if (kPow2Group) {
-      // G a power of two <= 32 (M in {8, ..., 128}), full warps: fixed-order
-      // shuffle tree over the slots of a warp (lanes with the same g), then one
-      // row of red[] per warp
+      // G a power of two <= 32 (M in {8, ..., 128}): fixed-order shuffle tree
+      // over the slots of a warp (lanes with the same g), one row of red[] per warp
       for (int o = G; o < 32; o <<= 1)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v8[k] += __shfl_xor_sync(0xffffffffu, v8[k], o);
+        for (int q = 0; q < 8; ++q) v8[q] += __shfl_xor_sync(0xffffffffu, v8[q], o);
       if (lane < G) {
         double *r = red + (size_t)warp * 2 * M;
         r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
         r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
       }
-      nred = blockDim.x >> 5;
+      nred = kStatsThreads >> 5;
     } else {
-      // any G (M a multiple of 4 up to 256, partial last warp allowed): one row
-      // of red[] per slot, then a fixed-order pairwise tree over the slots in
-      // shared memory (row s += row s + half), so the result does not depend on
-      // warp boundaries
-      double *r = red + (size_t)slot * 2 * M;
-      r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
-      r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
+      // any G (M a multiple of 4 up to 256): one row of red[] per slot, then a
+      // fixed-order pairwise tree over the slots in shared memory (row s += row
+      // s + half), so the result does not depend on warp boundaries
+      if (act) {
+        double *r = red + (size_t)slot * 2 * M;
+        r[4 * g + 0] = v8[0]; r[4 * g + 1] = v8[1]; r[4 * g + 2] = v8[2]; r[4 * g + 3] = v8[3];
+        r[M + 4 * g + 0] = v8[4]; r[M + 4 * g + 1] = v8[5]; r[M + 4 * g + 2] = v8[6]; r[M + 4 * g + 3] = v8[7];
+      }
       int rows = nslots;
       while (rows > 1) {
         const int half = (rows + 1) >> 1;
-        __syncthreads();
-        for (int e = threadIdx.x; e < (rows - half) * 2 * M; e += blockDim.x)
+        named_bar_sync(1, kStatsThreads);
+        for (int e = tid; e < (rows - half) * 2 * M; e += kStatsThreads)
           red[e] += red[(size_t)half * 2 * M + e];
         rows = half;
       }
       nred = 1;
     }
-    __syncthreads();
+    named_bar_sync(1, kStatsThreads);
     const int64_t first = cta_of(inst * T_cal, S, nb);
     const int64_t ncontrib = cta_of((inst + 1) * T_cal - 1, S, nb) - first + 1;
     const int64_t c = blockIdx.x - first;   // contributor index of this CTA
     double *pc = slots + ((size_t)inst * max_contrib + c) * 2 * M;
-    for (int e = threadIdx.x; e < 2 * M; e += blockDim.x) {   // fixed-order sum over rows
-      double s = 0;
-      for (int k = 0; k < nred; ++k) s += red[(size_t)k * 2 * M + e];
-      pc[e] = s;
+    for (int e = tid; e < 2 * M; e += kStatsThreads) {   // fixed-order sum over rows
+      double sacc = 0;
+      for (int q = 0; q < nred; ++q) sacc += red[(size_t)q * 2 * M + e];
+      pc[e] = sacc;
     }
     // the last contributor of this instance combines the slots in order
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      last = (atomicAdd(ticket + inst, 1u) == (unsigned)ncontrib - 1);
-    __syncthreads();
+    named_bar_sync(1, kStatsThreads);
+    if (tid == 0) last = (atomicAdd(ticket + inst, 1u) == (unsigned)ncontrib - 1);
+    named_bar_sync(1, kStatsThreads);
     if (last) {
       __threadfence();
-      for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      for (int j = tid; j < M; j += kStatsThreads) {
         const double *p0 = slots + (size_t)inst * max_contrib * 2 * M;
         double s1 = 0, s2 = 0;
         for (int64_t q = 0; q < ncontrib; ++q) {
@@ -157,11 +215,11 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_series_stats(
         std_out[inst * M + j] = (float)sd;
       }
     }
-    __syncthreads();   // red[] and `last` are reused by the next segment
-    seg0 = seg1;
+    named_bar_sync(1, kStatsThreads);   // red[] and `last` are reused by the next segment
   }
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0 && bad) atomicAdd(diag + 1, 1ull);   // CTAs with a non-finite sample
+  if (bad) atomicOr(&bad_any, 1);
+  named_bar_sync(1, kStatsThreads);
+  if (tid == 0 && bad_any) atomicAdd(diag + 1, 1ull);   // CTAs with a non-finite sample
 }
 
 // diag[0] = series whose std was floored, diag[1] = CTAs whose range held a
@@ -182,25 +240,23 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   int dev = 0, sms = 148;
   ENOVA_CUDA_TRY(cudaGetDevice(&dev));
   ENOVA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // one wave of 2 CTAs per SM, each with an equal share of the N * T_cal samples
-  // (at least 64 samples per CTA)
+  // one wave of one CTA per SM, each with an equal share of the N * T_cal
+  // samples (at least 64 samples per CTA)
   const int64_t S = N * t_cal_end;
-  int64_t nb = 2 * (int64_t)sms;
+  int64_t nb = sms;
   if (nb > kStatsMaxGrid) nb = kStatsMaxGrid;
   if (nb > S / 64) nb = S / 64;
   if (nb < 1) nb = 1;
   const int G = M / 4;
-  const int nthreads = G * (kStatsThreads / G);
-  const int nslots = nthreads / G;
+  const int nslots = kStatsThreads / G;
   if (diag_dev) ENOVA_CUDA_TRY(cudaMemsetAsync(diag_dev, 0, 2 * sizeof(unsigned long long), st));
   ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, 256 + (size_t)N * 4, st));   // diag (own) + tickets
   const bool pow2 = (G & (G - 1)) == 0 && G <= 32;
-  const size_t smem = (size_t)(pow2 ? nthreads / 32 : nslots) * 2 * M * sizeof(double);
+  const size_t smem = (size_t)kStatsStages * kStatsChunkBytes +
+                      (size_t)(pow2 ? kStatsThreads / 32 : nslots) * 2 * M * sizeof(double);
   auto kern = pow2 ? k_series_stats<true> : k_series_stats<false>;
-  if (smem > 48 * 1024)
-    ENOVA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-  ENOVA_LAUNCH(kern, (unsigned)nb, nthreads, smem, st, s->metrics, s->ld_instance, M, N,
+  ENOVA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ENOVA_LAUNCH(kern, (unsigned)nb, kStatsBlock, smem, st, s->metrics, s->ld_instance, M, N,
                t_cal_end, mean, stdv, diag, ticket, slots, stats_max_contrib(N));
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
