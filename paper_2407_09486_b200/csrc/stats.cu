@@ -29,8 +29,8 @@ namespace enova {
 constexpr int kStatsThreads = 512;              // consumers
 constexpr int kStatsBlock = kStatsThreads + 32; // + the producer warp
 constexpr int kStatsMaxGrid = 512;   // <= 256 SMs x 2 (workspace sizing)
-constexpr int kStatsStages = 6;
-constexpr uint32_t kStatsChunkBytes = 16384;
+constexpr int kStatsStages = 5;
+constexpr uint32_t kStatsChunkBytes = 32768;
 
 // contributors of one instance: a CTA range holds >= floor(N T / nb) >= 64
 // samples, so an instance of T samples meets at most ceil(nb / N) + 2 ranges
@@ -52,14 +52,21 @@ __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t S, int nb) {
 }
 
 // the chunk sequence of a CTA range (walked identically by producer and consumers):
-// chunk = [c0, c1) of the flattened space inside one instance, <= cs samples
+// chunk = [c0, c1) of the flattened space inside instance `inst`, <= cs samples;
+// one 64-bit division per range, none per chunk
 struct ChunkWalk {
-  int64_t pos, r1, T_cal, cs;
-  __device__ __forceinline__ bool next(int64_t &c0, int64_t &c1) {
+  int64_t pos, r1, T_cal, cs, inst, full_end;
+  __device__ __forceinline__ ChunkWalk(int64_t r0, int64_t r1_, int64_t T, int64_t cs_)
+      : pos(r0), r1(r1_), T_cal(T), cs(cs_), inst(r0 / T), full_end((r0 / T + 1) * T) {}
+  __device__ __forceinline__ bool next(int64_t &c0, int64_t &c1, int64_t &ci) {
     if (pos >= r1) return false;
+    if (pos >= full_end) {   // next instance segment
+      ++inst;
+      full_end += T_cal;
+    }
     c0 = pos;
-    const int64_t seg_end = min(r1, (pos / T_cal + 1) * T_cal);
-    c1 = min(seg_end, pos + cs);
+    c1 = min(min(r1, full_end), pos + cs);
+    ci = inst;
     pos = c1;
     return true;
   }
@@ -95,12 +102,12 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
   if (tid >= kStatsThreads) {
     // ---------------- producer warp: bulk copies, kStatsStages chunks ahead ----------------
     if (lane == 0) {
-      ChunkWalk w{r0, r1, T_cal, cs};
-      int64_t c0, c1;
-      for (int k = 0; w.next(c0, c1); ++k) {
+      ChunkWalk w(r0, r1, T_cal, cs);
+      int64_t c0, c1, inst;
+      for (int k = 0; w.next(c0, c1, inst); ++k) {
         const int sg = k % kStatsStages;
         if (k >= kStatsStages) mbar_wait(&empty[sg], ((k / kStatsStages) - 1) & 1);
-        const int64_t inst = c0 / T_cal, t = c0 - inst * T_cal;
+        const int64_t t = c0 - inst * T_cal;
         const uint32_t bytes = (uint32_t)(c1 - c0) * 4u * (uint32_t)M;
         mbar_arrive_expect_tx(&full[sg], bytes);
         bulk_g2s(sm + (size_t)sg * kStatsChunkBytes, X + inst * ld + t * M, bytes, &full[sg]);
@@ -113,12 +120,12 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
   const int slot = tid / G;
   const bool act = tid < active;
   int bad = 0;
-  ChunkWalk w{r0, r1, T_cal, cs};
-  int64_t c0, c1;
+  ChunkWalk w(r0, r1, T_cal, cs);
+  int64_t c0, c1, ci;
   int k = 0;
-  bool have = w.next(c0, c1);
+  bool have = w.next(c0, c1, ci);
   while (have) {
-    const int64_t inst = c0 / T_cal;
+    const int64_t inst = ci;
     const float4 K = __ldg(reinterpret_cast<const float4 *>(X + inst * ld) + (act ? g : 0));
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
     // every chunk of this segment
@@ -141,8 +148,8 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sg]);
       ++k;
-      have = w.next(c0, c1);
-    } while (have && c0 / T_cal == inst);
+      have = w.next(c0, c1, ci);
+    } while (have && ci == inst);
     // ---- the segment's sums: fixed-order reduction, contributor slot, ticket ----
     double v8[8] = {a0, a1, a2, a3, q0, q1, q2, q3};
     int nred;   // partial sums per output left in red[] (summed below in index order)
