@@ -190,6 +190,24 @@ enova_status enova_fit_threshold_comm_async(const float *scores, int64_t n_local
                                             enova_comm_t comm, enova_threshold *out_dev,
                                             void *ws, size_t ws_bytes, void *stream);
 
+/* Distributed-fit variant: the same selection
+ * phases and collectives, then every rank fits the GPD on ITS OWN tail -- no
+ * tail gather: one cooperative launch per fit step (statistics, grid scan,
+ * certified refinement passes, candidates; a fixed sequence of 17 launches,
+ * steps after convergence return at once) with an all-gather of the ranks'
+ * pass totals (6 KB per rank) between steps, summed by every rank in rank
+ * order.  z_q is bit-identical across the ranks of one communicator and equal
+ * across world sizes up to the fp64 summation order (the replicated
+ * enova_fit_threshold_comm_async is bit-identical across world sizes).  The
+ * fit's work per rank is its own tail: the replicated fit's Amdahl term at large
+ * world sizes.  Workspace, arguments, out_dev and status as
+ * enova_fit_threshold_comm_async. */
+enova_status enova_fit_threshold_dist_async(const float *scores, int64_t n_local,
+                                            int64_t n_global, int64_t n_global_max,
+                                            double init_quantile, double risk_q,
+                                            enova_comm_t comm, enova_threshold *out_dev,
+                                            void *ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------ a-2..a-6 ----
  * Score every window of the series range and flag it ("An anomaly is
  * detected if the KL-divergence ... exceeds this threshold", MD decides
@@ -386,6 +404,10 @@ typedef struct {
 } enova_step_args;
 enova_status enova_step_create(enova_step_t *out, int device);
 enova_status enova_step_configure(enova_step_t step, int32_t pot_ctas, int64_t concurrent_instances);
+/* fit_mode (communicator steps): 0 = replicated fit on the gathered tails
+ * (enova_fit_threshold_comm_async, default), 1 = distributed fit
+ * (enova_fit_threshold_dist_async). */
+enova_status enova_step_set_fit_mode(enova_step_t step, int32_t fit_mode);
 enova_status enova_step_enqueue(enova_step_t step, const enova_step_args *args, void *stream);
 void enova_step_destroy(enova_step_t step);
 

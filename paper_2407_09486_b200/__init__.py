@@ -10,6 +10,7 @@ Seeded synthetic inputs live in ``paper_2407_09486_b200.synth``.
 __all__ = ["PreparedDetector", "compute_stats", "score_windows", "fit_threshold", "detect",
            "ring_push", "ring_view", "Comm", "ThresholdWorkspace", "run_pipeline",
            "EnovaError", "compute_stats_async", "fit_threshold_async", "fit_threshold_comm_async",
+           "fit_threshold_dist_async",
            "detect_async",
            "threshold_from_device", "threshold_to_device", "check_stats_diag", "Pipeline",
            "StatsWorkspace", "StreamRing", "point_adjusted_counts", "point_adjusted_f1", "select_flagged",

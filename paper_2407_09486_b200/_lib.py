@@ -36,7 +36,7 @@ EXPORTS = (
     "enova_trainer_create", "enova_trainer_destroy", "enova_trainer_param_offsets",
     "enova_trainer_set_math", "enova_trainer_load", "enova_trainer_store", "enova_train_step",
     "enova_train_gradient", "enova_step_create", "enova_step_configure", "enova_step_enqueue",
-    "enova_step_destroy",
+    "enova_step_destroy", "enova_fit_threshold_dist_async", "enova_step_set_fit_mode",
 )
 
 
@@ -152,6 +152,9 @@ def lib() -> C.CDLL:
             "enova_trainer_create": (C.c_int, [P(vp), i32, i32, i32, i32, i32, C.c_int]),
             "enova_step_create": (C.c_int, [P(vp), C.c_int]),
             "enova_step_configure": (C.c_int, [vp, i32, i64]),
+            "enova_step_set_fit_mode": (C.c_int, [vp, i32]),
+            "enova_fit_threshold_dist_async": (C.c_int, [vp, i64, i64, i64, dbl, dbl, vp, vp, vp,
+                                                         sz, vp]),
             "enova_step_enqueue": (C.c_int, [vp, P(StepArgs), vp]),
             "enova_step_destroy": (None, [vp]),
             "enova_trainer_destroy": (None, [vp]),

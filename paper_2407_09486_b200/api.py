@@ -652,6 +652,29 @@ def run_pipeline(metrics: torch.Tensor, det: PreparedDetector, t_cal_end: int,
     return PipelineResult(mean, std, nd, cal, thr, flags, sc, md, cal_md, cal_flags)
 
 
+def fit_threshold_dist_async(scores: torch.Tensor, n_global: int, comm: "Comm",
+                             init_quantile: float = 0.98, risk_q: float = 1e-3, *,
+                             workspace: ThresholdWorkspace | None = None, out=None,
+                             stream=None) -> torch.Tensor:
+    """The distributed-fit variant of fit_threshold_comm_async
+    (enova_fit_threshold_dist_async): every rank fits on its own tail with the
+    ranks' pass totals all-gathered between fit steps.  Returns the DEVICE
+    enova_threshold (identical on every rank)."""
+    _require_cuda(scores, "scores")
+    flat = scores.reshape(-1)
+    if not flat.is_contiguous():
+        flat = flat.contiguous()
+    if workspace is None:
+        workspace = ThresholdWorkspace(n_global, init_quantile, scores.device, world=comm.world)
+    thr = out if out is not None else torch.zeros(THRESHOLD_BYTES, dtype=torch.uint8,
+                                                  device=scores.device)
+    check(lib().enova_fit_threshold_dist_async(
+        C.c_void_p(flat.data_ptr()), flat.numel(), int(n_global), workspace.n_global_max,
+        float(init_quantile), float(risk_q), C.c_void_p(comm.handle), C.c_void_p(thr.data_ptr()),
+        C.c_void_p(workspace.buf.data_ptr()), workspace.nbytes, _stream_ptr(stream)))
+    return thr
+
+
 class Pipeline:
     """The whole hot path for a fixed fleet shape, preallocated and stream-ordered:
     stats over [0, t_cal_end) -> calibration scores and MD -> single-GPU POT
@@ -670,7 +693,8 @@ class Pipeline:
     def __init__(self, det: PreparedDetector, n_instances: int, n_steps: int, t_cal_end: int,
                  init_quantile: float = 0.98, risk_q: float = 1e-3, return_scores: bool = True,
                  device=None, comm: "Comm | None" = None, overlap: bool = True,
-                 pot_ctas: int = 32, concurrent_instances: int | None = None):
+                 pot_ctas: int = 32, concurrent_instances: int | None = None,
+                 fit_mode: str = "replicated"):
         dev = torch.device(device or "cuda")
         # the overlapped step (enova_step: the fit on pot_ctas CTAs next to the
         # detection scores) needs the detection scores and MD buffers
@@ -704,6 +728,11 @@ class Pipeline:
         check(lib().enova_step_create(C.byref(h), dev.index if dev.index is not None
                                       else torch.cuda.current_device()))
         self._step = h.value
+        if fit_mode not in ("replicated", "distributed"):
+            raise ValueError("fit_mode must be 'replicated' or 'distributed'")
+        self.fit_mode = fit_mode
+        check(lib().enova_step_set_fit_mode(C.c_void_p(self._step),
+                                            1 if fit_mode == "distributed" else 0))
         self.overlap = bool(overlap)
         if concurrent_instances is None:
             concurrent_instances = (2 * N) // 5 if overlap else 0

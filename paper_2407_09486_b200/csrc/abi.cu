@@ -46,6 +46,10 @@ enova_status fit_threshold_async(const float *scores, int64_t n, double q0, doub
                                  enova_threshold *out_dev, void *ws, size_t ws_bytes,
                                  int64_t n_global_max, cudaStream_t st);
 size_t threshold_workspace_bytes(int64_t n_max, double q0, int world);
+enova_status fit_threshold_dist_async(const float *scores, int64_t n_local, int64_t n, double q0,
+                                      double q, enova_comm_t comm, enova_threshold *out_dev,
+                                      void *ws, size_t ws_bytes, int64_t n_global_max,
+                                      cudaStream_t st);
 enova_status fit_threshold_comm_async(const float *scores, int64_t n_local, int64_t n, double q0,
                                       double q, enova_comm_t comm, enova_threshold *out_dev,
                                       void *ws, size_t ws_bytes, int64_t n_global_max,
@@ -366,6 +370,31 @@ enova_status enova_fit_threshold_comm_async(const float *scores, int64_t n_local
   enova_status r = sticky();
   if (r) return r;
   return fit_threshold_comm_async(scores, n_local, n_global, init_quantile, risk_q, comm, out_dev,
+                                  ws, ws_bytes, n_global_max, static_cast<cudaStream_t>(stream));
+}
+
+enova_status enova_fit_threshold_dist_async(const float *scores, int64_t n_local, int64_t n_global,
+                                            int64_t n_global_max, double init_quantile,
+                                            double risk_q, enova_comm_t comm,
+                                            enova_threshold *out_dev, void *ws, size_t ws_bytes,
+                                            void *stream) {
+  if (!comm || !out_dev || n_local < 0 || (n_local > 0 && !scores) || n_global < 1 ||
+      !aligned(out_dev, 8)) {
+    set_error("bad fit_threshold_dist_async arguments");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (!(init_quantile >= 0.0 && init_quantile < 1.0) || !(risk_q > 0.0 && risk_q < 1.0)) {
+    set_error("init_quantile must be in [0,1) and risk_q in (0,1)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  if (n_global_max < n_global) n_global_max = n_global;
+  if (!ws || !aligned(ws, 256)) {
+    set_error("threshold workspace missing or misaligned");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = sticky();
+  if (r) return r;
+  return fit_threshold_dist_async(scores, n_local, n_global, init_quantile, risk_q, comm, out_dev,
                                   ws, ws_bytes, n_global_max, static_cast<cudaStream_t>(stream));
 }
 

@@ -27,6 +27,7 @@ struct enova_step_s {
   cudaEvent_t fork, join;
   int pot_ctas;                 // 0: sequential (fit on every SM, then detection)
   int64_t concurrent_instances; // detection instances scored next to the fit
+  int fit_mode;                 // communicator: 0 replicated fit, 1 distributed fit
 };
 
 namespace enova {
@@ -61,6 +62,7 @@ enova_status enova_step_create(enova_step_t *out, int device) {
   enova_step_s *s = new enova_step_s();
   s->device = device;
   s->pot_ctas = 0;
+  s->fit_mode = 0;
   s->concurrent_instances = 0;
   cudaError_t e = cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
   int lo = 0, hi = 0;
@@ -94,6 +96,15 @@ enova_status enova_step_configure(enova_step_t s, int32_t pot_ctas, int64_t conc
   }
   s->pot_ctas = pot_ctas;
   s->concurrent_instances = concurrent_instances;
+  return ENOVA_OK;
+}
+
+enova_status enova_step_set_fit_mode(enova_step_t s, int32_t fit_mode) {
+  if (!s || fit_mode < 0 || fit_mode > 1) {
+    set_error("enova_step_set_fit_mode: fit_mode 0 (replicated) or 1 (distributed)");
+    return ENOVA_ERR_INVALID_ARGUMENT;
+  }
+  s->fit_mode = fit_mode;
   return ENOVA_OK;
 }
 
@@ -138,6 +149,10 @@ enova_status enova_step_enqueue(enova_step_t s, const enova_step_args *a, void *
   det.t_begin = tcal;
   det.t_end = T;
   auto fit = [&](cudaStream_t fs) -> enova_status {
+    if (a->comm && s->fit_mode == 1)
+      return enova_fit_threshold_dist_async(a->cal_scores, n_cal, a->n_global, a->n_global_max,
+                                            a->init_quantile, a->risk_q, a->comm, a->thr_dev,
+                                            a->thr_ws, a->thr_ws_bytes, fs);
     if (a->comm)
       return enova_fit_threshold_comm_async(a->cal_scores, n_cal, a->n_global, a->n_global_max,
                                             a->init_quantile, a->risk_q, a->comm, a->thr_dev,

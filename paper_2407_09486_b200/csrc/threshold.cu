@@ -128,6 +128,7 @@ struct FitState {
 struct ThrLayout {
   size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yslot, outdev, yall, header, total;
   size_t shist, cand, cand_n;   // sampled selection: sample histograms, candidates, per-CTA counts
+  size_t fstate, xsend, xrecv;  // distributed fit (communicator layouts)
   int64_t cap;
   bool sampled;                 // workspace holds the candidate buffer
 };
@@ -157,6 +158,9 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0, int world = 0) {
   L.yslot = take((size_t)world * (size_t)L.cap * 4);
   L.outdev = take(world ? sizeof(enova_threshold) : 0);
   L.yall = take((size_t)L.cap * 8);
+  L.fstate = take(world ? sizeof(FitState) : 0);
+  L.xsend = take(world ? (size_t)kSums * kMaxPts * 8 : 0);
+  L.xrecv = take((size_t)world * kSums * kMaxPts * 8);
   // candidates: one segment of ceil(chunk / 4) * 4 scores per CTA (a segment can
   // hold its CTA's whole chunk, so it never overflows)
   L.sampled = (world == 0 && n_max >= kSampleMinN);
@@ -191,6 +195,11 @@ struct PotArgs {
   unsigned long long *shist; // [2][kBins] sample histograms
   float *cand;              // sampled selection: per-CTA candidate segments, else null
   long long *cand_n;        // [kMaxCtas] candidates, [kMaxCtas] keys below lo, per CTA
+  // distributed fit (communicator path): step of this launch (-1: not distributed)
+  int dfit_step, dfit_last;
+  double *xsend;            // [kSums * kMaxPts] this rank's totals of the step
+  const double *xrecv;      // [world][kSums * kMaxPts] gathered totals
+  FitState *fstate;         // the fit's state between launches
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -1342,27 +1351,262 @@ __device__ int64_t pack_tails(const PotArgs &a, long long *s_off) {
   return nt;
 }
 
+// ---- the fit's building blocks (shared by the one-launch fit and the
+// distributed per-pass launches) ----
+
+// this CTA's slice [c0, c1) of a tail of nt values
+__device__ __forceinline__ void fit_slice(int64_t nt, int64_t &c0, int64_t &c1) {
+  const int nb = gridDim.x;
+  const int64_t chunk = (nt + nb - 1) / nb;
+  c0 = min(nt, (int64_t)blockIdx.x * chunk);
+  c1 = min(nt, c0 + chunk);
+}
+
+// Y statistics of this CTA's slice -> partial buffer rows 0..2 (sum, min, max);
+// stages the slice in shared memory when it fits.  src = the fp64 tail.
+__device__ void fit_stats_partials(const PotArgs &a, FitShared &S, const double *src, int64_t c0,
+                                   int64_t c1, bool cached, double *ycache) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s = 0.0, mn = INFINITY, mx = -INFINITY;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const double y = src[i];   // written by this kernel / launch: coherent load
+    if (cached) ycache[i - c0] = y;
+    s += y;
+    mn = fmin(mn, y);
+    mx = fmax(mx, y);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    S.sred[warp][0] = s;
+    S.sred[warp][1] = mn;
+    S.sred[warp][2] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
+    for (int w = 0; w < kPotWarps; ++w) {
+      ts += S.sred[w][0];
+      tmn = fmin(tmn, S.sred[w][1]);
+      tmx = fmax(tmx, S.sred[w][2]);
+    }
+    a.part[0 * kMaxCtas + blockIdx.x] = ts;
+    a.part[1 * kMaxCtas + blockIdx.x] = tmn;
+    a.part[2 * kMaxCtas + blockIdx.x] = tmx;
+  }
+}
+
+// grid totals of the statistics partials (fixed order; warp 0 of every CTA)
+__device__ void fit_stats_totals(const PotArgs &a, double &ts, double &tmn, double &tmx) {
+  const int lane = threadIdx.x & 31, nb = gridDim.x;
+  ts = 0.0;
+  tmn = INFINITY;
+  tmx = -INFINITY;
+  for (int b = lane; b < nb; b += 32) {
+    ts += *(volatile double *)(a.part + b);
+    tmn = fmin(tmn, *(volatile double *)(a.part + kMaxCtas + b));
+    tmx = fmax(tmx, *(volatile double *)(a.part + 2 * kMaxCtas + b));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ts += __shfl_xor_sync(0xffffffffu, ts, o);
+    tmn = fmin(tmn, __shfl_xor_sync(0xffffffffu, tmn, o));
+    tmx = fmax(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+  }
+}
+
+// one evaluation pass over this CTA's slice at the points of f (list order):
+// CTA partials per (k, point) -> pw ([kSums][kMaxPts][kMaxCtas])
+__device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int64_t c1,
+                                  double *pw) {
+  FitState &f = S.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int phase = f.phase;
+  const int npts = f.npts;
+  const bool deriv = (phase == PH_REFINE);
+  const bool mixed = (phase == PH_GRID32);
+  const int nk = deriv ? kSums : 2;
+  // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones
+  const int n64 = mixed ? f.n64 : npts;
+  const int nb64 = (n64 + 3) / 4;
+  const int nbund = mixed ? nb64 + (f.n32 + 3) / 4 : (npts + 3) / 4;
+  const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
+  const int items = nbund * slices;
+  for (int it = warp; it < items; it += kPotWarps) {
+    const int bnd = it % nbund, sl = it / nbund;
+    const int64_t len = c1 - c0;
+    const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
+    const bool f32 = mixed && bnd >= nb64;
+    const int base = f32 ? n64 + 4 * (bnd - nb64) : 4 * bnd;
+    const int nu = min(4, (f32 ? n64 + f.n32 : (mixed ? n64 : npts)) - base);
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[base + u] : 0.0;
+    double acc[4][kSums];
+    if (deriv)
+      eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
+    else if (f32)
+      eval_bundle32(Y, s0, s1, x, nu, acc);
+    else
+      eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < nu)
+#pragma unroll
+          for (int k = 0; k < kSums; ++k) S.sred[sl * npts + base + u][k] = acc[u][k];
+    }
+  }
+  if (mixed) {   // power sums of u = Y / Ymax for the series points (fp64, fixed order)
+    const double iy = 1.0 / f.ymax;
+    double q[kPow];
+#pragma unroll
+    for (int m = 0; m < kPow; ++m) q[m] = 0.0;
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const double u = Y[i] * iy;
+      double pw_ = u;
+#pragma unroll
+      for (int m = 0; m < kPow; ++m) {
+        q[m] += pw_;
+        pw_ *= u;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kPow; ++m) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) q[m] += __shfl_xor_sync(0xffffffffu, q[m], o);
+      if (lane == 0) S.powp[warp][m] = q[m];
+    }
+  }
+  __syncthreads();
+  if (mixed && threadIdx.x < kPow) {   // CTA partial power sums -> partial row 2
+    double sp = 0.0;
+    for (int w = 0; w < kPotWarps; ++w) sp += S.powp[w][threadIdx.x];
+    pw[((size_t)2 * kMaxPts + threadIdx.x) * kMaxCtas + blockIdx.x] = sp;
+  }
+  // CTA partial per (k, point): slices summed in order
+  for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
+    const int k = i / npts, pt = i % npts;
+    double s = 0.0;
+    for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
+    pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
+  }
+}
+
+// grid totals of one pass (after the barrier), fixed order: one warp per
+// (k, point), 4 items in flight per warp -> S.red
+__device__ void fit_eval_totals(FitShared &S, const double *pw) {
+  FitState &f = S.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nb = gridDim.x;
+  const int npts = f.npts;
+  const bool mixed = (f.phase == PH_GRID32);
+  const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+  constexpr int kJ = (kMaxCtas + 31) / 32;
+  const int nitems = nk * npts + (mixed ? kPow : 0);   // + the power sums (row 2)
+  for (int i0 = 4 * warp; i0 < nitems; i0 += 4 * kPotWarps) {
+    double v[4][kJ];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q;
+      const bool extra = i >= nk * npts;
+      const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
+      const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int b = lane + 32 * j;
+        v[q][j] = (i < nitems && b < nb) ? *(volatile const double *)(src + b) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double sum = 0.0;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) sum += v[q][j];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const int i = i0 + q;
+      if (lane == 0 && i < nitems) {
+        if (i >= nk * npts) S.red[2][i - nk * npts] = sum;
+        else S.red[i / npts][i % npts] = sum;
+      }
+    }
+  }
+}
+
+// means of the pass totals in S.red -> w (and derivatives) at the list points,
+// then the controller (next points, roots, candidates, z_q)
+__device__ void fit_finish_pass(FitShared &S) {
+  FitState &f = S.f;
+  const int npts = f.npts;
+  const bool deriv = (f.phase == PH_REFINE);
+  const bool mixed = (f.phase == PH_GRID32);
+  const double N = (double)f.nt;
+  if (threadIdx.x < npts) {
+    const int pt = threadIdx.x;
+    const double Pm = S.red[0][pt] / N, Lm = S.red[1][pt] / N;
+    f.w[pt] = Pm + Lm + Pm * Lm;
+    f.L[pt] = Lm;
+    f.P[pt] = Pm;
+    if (deriv) {
+      const double dPm = S.red[2][pt] / N, dLm = S.red[3][pt] / N;
+      const double d2Pm = S.red[4][pt] / N, d2Lm = S.red[5][pt] / N;
+      f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
+      f.ddw[pt] = d2Pm + d2Lm + d2Pm * Lm + 2.0 * dPm * dLm + Pm * d2Lm;
+    }
+  }
+  if (mixed && threadIdx.x == 0)
+    for (int m = 1; m <= kPow; ++m) f.pm[m] = S.red[2][m - 1] / N;   // mean u^m
+  __syncthreads();
+  controller(&f, S.scratch);
+}
+
+// the fit's result -> PotGlobal (CTA 0, thread 0)
+__device__ void fit_publish(const PotArgs &a, const FitState &f) {
+  PotGlobal *g = a.g;
+  g->gamma = f.gamma;
+  g->sigma = f.sigma;
+  g->z_q = f.z_q;
+  g->method = f.method;
+  g->nroots = f.nroots;
+  g->overflow = f.overflow;
+  g->converged = f.converged;
+  g->fit_passes = f.iters;
+  int st = ENOVA_OK;
+  if (f.overflow) st = ENOVA_ERR_UNSUPPORTED;
+  else if (!f.converged) st = ENOVA_ERR_UNSUPPORTED;
+  g->status = st;
+}
+
+// f's run-wide fields from the Y statistics
+__device__ void fit_init_state(const PotArgs &a, FitState &f, int64_t nt, double ts, double tmn,
+                               double tmx) {
+  f.nt = nt;
+  f.n = a.n_dev ? *(volatile const long long *)a.n_dev : a.n;
+  f.t = (double)*(volatile float *)&a.g->t;
+  f.q = a.q;
+  f.overflow = 0;
+  f.converged = 0;
+  f.iters = 0;
+  f.phase = PH_GRID;
+  f.ybar = ts / (double)nt;
+  f.ymin = tmn;
+  f.ymax = tmx;
+}
+
 __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const int64_t nt) {
   FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nb = gridDim.x;
   if (nt < 10 || nt > a.cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       a.g->status = (nt < 10) ? ENOVA_ERR_TOO_FEW_EXCEEDANCES : ENOVA_ERR_WORKSPACE;
     return;   // uniform over the grid
   }
-  if (threadIdx.x == 0) {
-    f.nt = nt;
-    f.n = a.n_dev ? *(volatile const long long *)a.n_dev : a.n;
-    f.t = (double)*(volatile float *)&a.g->t;
-    f.q = a.q;
-    f.overflow = 0;
-    f.converged = 0;
-    f.iters = 0;
-    f.phase = PH_GRID;
-  }
-  const int64_t chunk = (nt + nb - 1) / nb;
-  const int64_t c0 = min(nt, (int64_t)blockIdx.x * chunk), c1 = min(nt, c0 + chunk);
+  int64_t c0, c1;
+  fit_slice(nt, c0, c1);
   // this CTA's slice of Y is staged in shared memory by the Y-statistics pass
   // (every later pass reads it from there); global reads if it does not fit
   extern __shared__ double ycache[];
@@ -1371,209 +1615,170 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
   fill_logtab(S.tab);   // first read after the next barrier
 
   // ---- Ybar, Ymin, Ymax (pass 0, partial buffer 0) ----
-  {
-    double s = 0.0, mn = INFINITY, mx = -INFINITY;
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const double y = a.yfit[i];   // written by this kernel's compaction: coherent load
-      if (cached) ycache[i - c0] = y;
-      s += y;
-      mn = fmin(mn, y);
-      mx = fmax(mx, y);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (lane == 0) {
-      S.sred[warp][0] = s;
-      S.sred[warp][1] = mn;
-      S.sred[warp][2] = mx;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
-      for (int w = 0; w < kPotWarps; ++w) {
-        ts += S.sred[w][0];
-        tmn = fmin(tmn, S.sred[w][1]);
-        tmx = fmax(tmx, S.sred[w][2]);
-      }
-      a.part[0 * kMaxCtas + blockIdx.x] = ts;
-      a.part[1 * kMaxCtas + blockIdx.x] = tmn;
-      a.part[2 * kMaxCtas + blockIdx.x] = tmx;
-    }
-    grid_sync(a.g, epoch);
-    stamp(a.g);
-    if (warp == 0) {
-      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
-      for (int b = lane; b < nb; b += 32) {
-        ts += *(volatile double *)(a.part + b);
-        tmn = fmin(tmn, *(volatile double *)(a.part + kMaxCtas + b));
-        tmx = fmax(tmx, *(volatile double *)(a.part + 2 * kMaxCtas + b));
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        ts += __shfl_xor_sync(0xffffffffu, ts, o);
-        tmn = fmin(tmn, __shfl_xor_sync(0xffffffffu, tmn, o));
-        tmx = fmax(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
-      }
-      if (lane == 0) {
-        f.ybar = ts / (double)nt;
-        f.ymin = tmn;
-        f.ymax = tmx;
-      }
-    }
-    __syncthreads();
-    setup_grid(&f);
-    __syncthreads();
+  fit_stats_partials(a, S, a.yfit, c0, c1, cached, ycache);
+  grid_sync(a.g, epoch);
+  stamp(a.g);
+  if (warp == 0) {
+    double ts, tmn, tmx;
+    fit_stats_totals(a, ts, tmn, tmx);
+    if (lane == 0) fit_init_state(a, f, nt, ts, tmn, tmx);
   }
+  __syncthreads();
+  setup_grid(&f);
+  __syncthreads();
 
   // ---- evaluation passes (partials double-buffered: one barrier per pass) ----
   for (int pass = 1;; ++pass) {
-    const int phase = f.phase;
-    if (phase == PH_DONE) break;
+    if (f.phase == PH_DONE) break;
     double *pw = a.part + (size_t)(pass & 1) * kSums * kMaxPts * kMaxCtas;
-    const int npts = f.npts;
-    const bool deriv = (phase == PH_REFINE);
-    const bool mixed = (phase == PH_GRID32);
-    const int nk = deriv ? kSums : 2;
-    // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones
-    const int n64 = mixed ? f.n64 : npts;
-    const int nb64 = (n64 + 3) / 4;
-    const int nbund = mixed ? nb64 + (f.n32 + 3) / 4 : (npts + 3) / 4;
-    const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
-    const int items = nbund * slices;
-    for (int it = warp; it < items; it += kPotWarps) {
-      const int bnd = it % nbund, sl = it / nbund;
-      const int64_t len = c1 - c0;
-      const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
-      const bool f32 = mixed && bnd >= nb64;
-      const int base = f32 ? n64 + 4 * (bnd - nb64) : 4 * bnd;
-      const int nu = min(4, (f32 ? n64 + f.n32 : (mixed ? n64 : npts)) - base);
-      double x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[base + u] : 0.0;
-      double acc[4][kSums];
-      if (deriv)
-        eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
-      else if (f32)
-        eval_bundle32(Y, s0, s1, x, nu, acc);
-      else
-        eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (u < nu)
-#pragma unroll
-            for (int k = 0; k < kSums; ++k) S.sred[sl * npts + base + u][k] = acc[u][k];
-      }
-    }
-    if (mixed) {   // power sums of u = Y / Ymax for the series points (fp64, fixed order)
-      const double iy = 1.0 / f.ymax;
-      double q[kPow];
-#pragma unroll
-      for (int m = 0; m < kPow; ++m) q[m] = 0.0;
-      for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-        const double u = Y[i] * iy;
-        double pw_ = u;
-#pragma unroll
-        for (int m = 0; m < kPow; ++m) {
-          q[m] += pw_;
-          pw_ *= u;
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < kPow; ++m) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) q[m] += __shfl_xor_sync(0xffffffffu, q[m], o);
-        if (lane == 0) S.powp[warp][m] = q[m];
-      }
-    }
-    __syncthreads();
-    if (mixed && threadIdx.x < kPow) {   // CTA partial power sums -> partial row 2
-      double sp = 0.0;
-      for (int w = 0; w < kPotWarps; ++w) sp += S.powp[w][threadIdx.x];
-      pw[((size_t)2 * kMaxPts + threadIdx.x) * kMaxCtas + blockIdx.x] = sp;
-    }
-    // CTA partial per (k, point): slices summed in order
-    for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
-      const int k = i / npts, pt = i % npts;
-      double s = 0.0;
-      for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
-      pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
-    }
+    fit_eval_partials(S, Y, c0, c1, pw);
     stamp(a.g);
     grid_sync(a.g, epoch);
     stamp(a.g);
-    // grid totals, fixed order: one warp per (k, point), 4 items in flight per warp
-    {
-      constexpr int kJ = (kMaxCtas + 31) / 32;
-      const int nitems = nk * npts + (mixed ? kPow : 0);   // + the power sums (row 2)
-      for (int i0 = 4 * warp; i0 < nitems; i0 += 4 * kPotWarps) {
-        double v[4][kJ];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = i0 + q;
-          const bool extra = i >= nk * npts;
-          const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
-          const double *src = pw + ((size_t)k * kMaxPts + pt) * kMaxCtas;
-#pragma unroll
-          for (int j = 0; j < kJ; ++j) {
-            const int b = lane + 32 * j;
-            v[q][j] = (i < nitems && b < nb) ? *(volatile const double *)(src + b) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double sum = 0.0;
-#pragma unroll
-          for (int j = 0; j < kJ; ++j) sum += v[q][j];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          const int i = i0 + q;
-          if (lane == 0 && i < nitems) {
-            if (i >= nk * npts) S.red[2][i - nk * npts] = sum;
-            else S.red[i / npts][i % npts] = sum;
-          }
-        }
-      }
-    }
+    fit_eval_totals(S, pw);
     __syncthreads();
-    if (threadIdx.x < npts) {
-      const int pt = threadIdx.x;
-      const double N = (double)nt;
-      const double Pm = S.red[0][pt] / N, Lm = S.red[1][pt] / N;
-      f.w[pt] = Pm + Lm + Pm * Lm;
-      f.L[pt] = Lm;
-      f.P[pt] = Pm;
-      if (deriv) {
-        const double dPm = S.red[2][pt] / N, dLm = S.red[3][pt] / N;
-        const double d2Pm = S.red[4][pt] / N, d2Lm = S.red[5][pt] / N;
-        f.dw[pt] = dPm + dLm + dPm * Lm + Pm * dLm;
-        f.ddw[pt] = d2Pm + d2Lm + d2Pm * Lm + 2.0 * dPm * dLm + Pm * d2Lm;
-      }
-    }
-    if (mixed && threadIdx.x == 0)
-      for (int m = 1; m <= kPow; ++m) f.pm[m] = S.red[2][m - 1] / (double)nt;   // mean u^m
-    __syncthreads();
-    stamp(a.g);
-    controller(&f, S.scratch);
+    fit_finish_pass(S);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    PotGlobal *g = a.g;
-    g->gamma = f.gamma;
-    g->sigma = f.sigma;
-    g->z_q = f.z_q;
-    g->method = f.method;
-    g->nroots = f.nroots;
-    g->overflow = f.overflow;
-    g->converged = f.converged;
-    g->fit_passes = f.iters;
-    int st = ENOVA_OK;
-    if (f.overflow) st = ENOVA_ERR_UNSUPPORTED;
-    else if (!f.converged) st = ENOVA_ERR_UNSUPPORTED;
-    g->status = st;
+  if (blockIdx.x == 0 && threadIdx.x == 0) fit_publish(a, f);
+}
+
+// ---- distributed fit (SURVEY §8e "distributed-fit variant") ----
+// Each rank fits on its OWN tail only: one launch per evaluation pass; between
+// launches the ranks' pass totals (this rank's CTA partials summed in CTA
+// order) are all-gathered and every rank sums them in rank order, so every
+// rank sees the same totals, runs the same controller and ends with the same
+// z_q (bit-identical across ranks; across world sizes equal up to the fp64
+// summation order, like the replicated fit across grid sizes).
+//   step 0: this rank's Y = raw tail - t (fp64), its statistics -> xsend
+//   step s >= 1: combine the gathered totals (stats at s = 1), finish the pass
+//   (controller), evaluate the next pass over the local tail -> xsend
+// f persists in global memory between launches (CTA 0 stores, all CTAs load).
+constexpr int kDfitLen = kSums * kMaxPts;   // doubles per rank per exchange
+
+__device__ void fstate_copy(FitState *dst, const FitState *src) {
+  const int n = (int)(sizeof(FitState) / 8);
+  const long long *s = reinterpret_cast<const long long *>(src);
+  long long *d = reinterpret_cast<long long *>(dst);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = *(volatile const long long *)(s + i);
+}
+
+__device__ void dfit_step(const PotArgs &a, FitShared &S, unsigned int &epoch) {
+  FitState &f = S.f;
+  PotGlobal *g = a.g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ntl = *(volatile long long *)&g->nt_local;   // this rank's peaks
+  int64_t c0, c1;
+  fit_slice(ntl, c0, c1);
+  extern __shared__ double ycache[];
+  const bool cached = (c1 - c0) <= (int64_t)a.ycache_cap;
+  double *Yl = a.ydst;   // this rank's fp64 tail
+  if (a.dfit_step == 0) {
+    const double td = (double)*(volatile float *)&g->t;
+    for (int64_t i = c0 + threadIdx.x; i < c1 && ntl <= a.cap; i += blockDim.x)
+      Yl[i] = (double)a.ylocal[i] - td;
+    __syncthreads();
+    fit_stats_partials(a, S, Yl, c0, c1, false, ycache);
+    grid_sync(g, epoch);
+    if (blockIdx.x == 0 && warp == 0) {
+      double ts, tmn, tmx;
+      fit_stats_totals(a, ts, tmn, tmx);
+      if (lane == 0) {
+        a.xsend[0] = ts;
+        a.xsend[1] = tmn;
+        a.xsend[2] = tmx;
+        a.xsend[3] = (double)ntl;
+      }
+    }
+    return;
+  }
+  // ---- s >= 1: the gathered totals of the previous exchange ----
+  if (a.dfit_step == 1) {
+    if (threadIdx.x == 0) {
+      double ts = 0.0, tmn = INFINITY, tmx = -INFINITY;
+      long long nt = 0;
+      bool over = false;   // a rank's tail overflowed its workspace (same on every rank)
+      for (int r = 0; r < a.world; ++r) {   // rank order
+        const double *x = a.xrecv + (size_t)r * kDfitLen;
+        ts += x[0];
+        tmn = fmin(tmn, x[1]);
+        tmx = fmax(tmx, x[2]);
+        nt += (long long)x[3];
+        over = over || x[3] > (double)a.cap;
+      }
+      f.nt = over ? 0 : nt;
+      if (!over && nt >= 10) fit_init_state(a, f, nt, ts, tmn, tmx);
+      else f.phase = PH_DONE;
+      if (blockIdx.x == 0) {
+        g->nt_fit = nt;
+        if (f.nt < 10) g->status = over ? ENOVA_ERR_WORKSPACE : ENOVA_ERR_TOO_FEW_EXCEEDANCES;
+      }
+    }
+    __syncthreads();
+    if (f.nt < 10) {
+      if (blockIdx.x == 0) {   // later steps see PH_DONE
+        const int n = (int)(sizeof(FitState) / 8);
+        const long long *src = reinterpret_cast<const long long *>(&f);
+        long long *dst = reinterpret_cast<long long *>(a.fstate);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+      }
+      return;
+    }
+    fill_logtab(S.tab);
+    setup_grid(&f);
+    __syncthreads();
+  } else {
+    fstate_copy(&f, a.fstate);
+    __syncthreads();
+    if (f.phase == PH_DONE || f.nt < 10) return;   // converged in an earlier step
+    fill_logtab(S.tab);
+    // S.red = the ranks' pass totals summed in rank order
+    const int npts = f.npts;
+    const bool mixed = (f.phase == PH_GRID32);
+    const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+    for (int i = threadIdx.x; i < nk * npts + (mixed ? kPow : 0); i += blockDim.x) {
+      const bool extra = i >= nk * npts;
+      const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
+      double sum = 0.0;
+      for (int r = 0; r < a.world; ++r) sum += a.xrecv[(size_t)r * kDfitLen + k * kMaxPts + pt];
+      S.red[k][pt] = sum;
+    }
+    __syncthreads();
+    fit_finish_pass(S);
+    __syncthreads();
+  }
+  if (f.phase == PH_DONE) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) fit_publish(a, f);
+  } else {
+    // the next pass over this rank's tail
+    const double *Y = Yl;
+    if (cached) {
+      for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) ycache[i - c0] = Yl[i];
+      Y = (const double *)ycache - c0;
+    }
+    __syncthreads();
+    double *pw = a.part;
+    fit_eval_partials(S, Y, c0, c1, pw);
+    grid_sync(g, epoch);
+    if (blockIdx.x == 0) {
+      fit_eval_totals(S, pw);
+      __syncthreads();
+      const int npts = f.npts;
+      const bool mixed = (f.phase == PH_GRID32);
+      const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+      for (int i = threadIdx.x; i < nk * npts + (mixed ? kPow : 0); i += blockDim.x) {
+        const bool extra = i >= nk * npts;
+        const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
+        a.xsend[k * kMaxPts + pt] = S.red[k][pt];
+      }
+      if (a.dfit_last && threadIdx.x == 0) g->status = ENOVA_ERR_UNSUPPORTED;   // not converged
+    }
+  }
+  if (blockIdx.x == 0) {   // the state the next step finishes from
+    __syncthreads();
+    const int n = (int)(sizeof(FitState) / 8);
+    const long long *src = reinterpret_cast<const long long *>(&f);
+    long long *dst = reinterpret_cast<long long *>(a.fstate);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   }
 }
 
@@ -1711,9 +1916,13 @@ __global__ void __launch_bounds__(kPotThreads, 1) k_pot(PotArgs a) {
       spot_skip = !spot_full && a.n_dev &&
                   *(volatile long long *)&g->nt_fit == *(volatile long long *)&g->nt_refit;
       if (!spot_skip && !spot_full) {
-        const int64_t nt = a.yslot ? pack_tails(a, s_off)
-                                   : (int64_t)*(volatile long long *)&g->nt_fit;
-        fit(a, sh.fit, epoch, nt);
+        if (a.dfit_step >= 0) {
+          dfit_step(a, sh.fit, epoch);
+        } else {
+          const int64_t nt = a.yslot ? pack_tails(a, s_off)
+                                     : (int64_t)*(volatile long long *)&g->nt_fit;
+          fit(a, sh.fit, epoch, nt);
+        }
       }
     }
   }
@@ -1877,6 +2086,11 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.last = P_FIT;
   a.out_dev = nullptr;
   a.n_dev = nullptr;
+  a.dfit_step = -1;
+  a.dfit_last = 0;
+  a.xsend = comm ? reinterpret_cast<double *>(b + L.xsend) : nullptr;
+  a.xrecv = comm ? reinterpret_cast<const double *>(b + L.xrecv) : nullptr;
+  a.fstate = comm ? reinterpret_cast<FitState *>(b + L.fstate) : nullptr;
   return a;
 }
 
@@ -1963,6 +2177,60 @@ enova_status fit_threshold_comm_async(const float *scores, int64_t n_local, int6
   a.first = a.last = P_FIT;
   a.out_dev = out_dev;
   return launch_pot_comm(a, nb, st, true, comm);
+}
+
+// Distributed fit (SURVEY §8e variant): the same selection phases, then each
+// rank fits on its own tail -- no tail gather -- with one cooperative launch per
+// fit step and an all-gather of the ranks' pass totals (6 KB per rank) between
+// steps (dfit_step above).  A fixed launch sequence (graph-capturable): step 0
+// + kDfitSteps steps; steps after convergence exit at once.
+constexpr int kDfitSteps = 16;
+enova_status fit_threshold_dist_async(const float *scores, int64_t n_local, int64_t n, double q0,
+                                      double q, enova_comm_t comm, enova_threshold *out_dev,
+                                      void *ws, size_t ws_bytes, int64_t n_global_max,
+                                      cudaStream_t st) {
+  char *b = static_cast<char *>(ws);
+  if (comm->world > kMaxWorld) {
+    set_error("communicator larger than 256 ranks");
+    return ENOVA_ERR_UNSUPPORTED;
+  }
+  const ThrLayout L = thr_layout(n_global_max, q0, comm->world);
+  if (ws_bytes < L.total) {
+    set_error("threshold workspace too small (size it with the communicator's world size)");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  enova_status r = check_k(n, q0);
+  if (r) return r;
+  if (n > n_global_max || n_local > n) {
+    set_error("total score count exceeds n_global_max used to size the workspace");
+    return ENOVA_ERR_WORKSPACE;
+  }
+  PotArgs a = make_args(scores, n_local, n, q0, q, b, L, true);
+  a.world = comm->world;
+  const int nb = pot_grid();
+  ENOVA_CUDA_TRY(cudaMemsetAsync(b, 0, L.header, st));
+  for (int p = P_HIST0; p <= P_HIST2; ++p) {
+    a.first = a.last = p;
+    if ((r = launch_pot_comm(a, nb, st, p > P_HIST0, comm))) return r;
+    r = comm_allreduce_u64_sum(comm, a.hist + (size_t)(p - P_HIST0) * kBins,
+                               a.hist + (size_t)(p - P_HIST0) * kBins, (size_t)kBins, st);
+    if (r) return r;
+  }
+  a.first = a.last = P_COMPACT;
+  if ((r = launch_pot_comm(a, nb, st, true, comm))) return r;
+  a.first = a.last = P_FIT;
+  for (int step = 0; step <= kDfitSteps; ++step) {
+    a.dfit_step = step;
+    a.dfit_last = step == kDfitSteps;
+    a.out_dev = a.dfit_last ? out_dev : nullptr;
+    if ((r = launch_pot_comm(a, nb, st, true, comm))) return r;
+    if (step < kDfitSteps) {
+      r = comm_allgather_f32(comm, reinterpret_cast<const float *>(a.xsend), b + L.xrecv,
+                             (size_t)2 * kSums * kMaxPts, st);
+      if (r) return r;
+    }
+  }
+  return ENOVA_OK;
 }
 
 // Host syncs: single GPU one (the result).  With a communicator one more (the

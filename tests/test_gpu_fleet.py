@@ -254,3 +254,133 @@ def test_nccl_world1_wait_ok(E):
         assert comm.sum_i64(7) == 7
     finally:
         comm.destroy()
+
+
+def _dist_fit(E, sd, parts, world, n_global, q0=0.98, q=1e-3):
+    comms = E.Comm.create_local(world, 0)
+    try:
+        def rank(r, st):
+            thr = E.fit_threshold_dist_async(sd[parts[r][0]:parts[r][1]], n_global, comms[r],
+                                             q0, q, stream=st)
+            st.synchronize()
+            return E.threshold_from_device(thr)
+        return run_ranks(world, rank)
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+@pytest.mark.parametrize("world,cuts", [(1, []), (2, [0.5]), (3, [0.2, 0.9]),
+                                        (4, [0.25, 0.25, 0.6])])
+def test_distributed_fit_matches_oracle_and_ranks_agree(E, world, cuts):
+    """The distributed-fit variant (enova_fit_threshold_dist_async):
+    each rank fits on its own tail with the pass totals all-gathered -- every
+    rank gets the same threshold (bit for bit), t / N_t exact, z_q within the
+    1e-9 parity tolerance of the oracle and of the replicated fit."""
+    s = synth.score_mixture(400_000, seed=31 + world)
+    sd = torch.from_numpy(s).cuda()
+    parts = shard(s.size, world, cuts)
+    res = _dist_fit(E, sd, parts, world, s.size)
+    for r in range(1, world):
+        assert res[r] == res[0], (r, res[r], res[0])
+    single = E.fit_threshold(sd, 0.98, 1e-3)
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    d = res[0]
+    assert d["t"] == o["t"] and d["n_peaks"] == o["n_peaks"] and d["n"] == s.size
+    assert abs(d["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"]), (d, o)
+    assert abs(d["z_q"] - single["z_q"]) <= 1e-9 * abs(single["z_q"])
+    assert d["method"] == single["method"]
+
+
+def test_distributed_fit_large_tail_and_edge_cases(E):
+    """c5-like tail (2M-score mixture -> 40k peaks, the certified fp32 grid
+    path) on 3 ranks with every peak on the last rank; too few exceedances on
+    every rank -> the same error on every rank."""
+    s = np.sort(synth.score_mixture(2_000_000, seed=77))
+    sd = torch.from_numpy(s).cuda()
+    parts = shard(s.size, 3, [0.3, 0.6])
+    res = _dist_fit(E, sd, parts, 3, s.size)
+    assert res[0] == res[1] == res[2]
+    o = O.pot_threshold(s, 0.98, 1e-3)
+    assert res[0]["n_peaks"] == o["n_peaks"] and res[0]["t"] == o["t"]
+    assert abs(res[0]["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
+    z = torch.zeros(20_000, dtype=torch.float32, device="cuda")
+    comms = E.Comm.create_local(2, 0)
+    try:
+        def rank(r, st):
+            thr = E.fit_threshold_dist_async(z[r * 10_000:(r + 1) * 10_000], 20_000, comms[r],
+                                             0.98, 1e-3, stream=st)
+            st.synchronize()
+            try:
+                E.threshold_from_device(thr)
+            except E.EnovaError as e:
+                return e.name
+            return "ok"
+        st = run_ranks(2, rank)
+    finally:
+        for c in comms:
+            c.destroy()
+    assert st == ["ENOVA_ERR_TOO_FEW_EXCEEDANCES"] * 2
+
+
+def test_distributed_fit_pipeline(E):
+    """Sharded Pipelines with fit_mode='distributed' (3 in-process ranks, uneven
+    shards): the same threshold on every rank, within 1e-9 of the single-GPU
+    pipeline's; flags / scores / MD rows equal the single-GPU pipeline's
+    (identical z_q in practice; asserted outside the R-19 band)."""
+    X, wts = _fleet(n_inst=10, seed_off=9)
+    T = X.shape[1]
+    tcal = T // 2
+    det = E.PreparedDetector(wts)
+    Xd = torch.from_numpy(X).cuda()
+    ref = E.Pipeline(det, X.shape[0], T, tcal, overlap=False)
+    ref.enqueue(Xd)
+    r0 = ref.result()
+    rows = [(0, 3), (3, 4), (4, 10)]
+    comms = E.Comm.create_local(3, 0)
+    try:
+        def rank(r, st):
+            a, b = rows[r]
+            p = E.Pipeline(det, b - a, T, tcal, comm=comms[r], fit_mode="distributed")
+            p.enqueue(Xd[a:b].contiguous(), stream=st)
+            st.synchronize()
+            res = p.result()
+            return (res.threshold, res.flags.cpu(), res.scores.cpu())
+        res = run_ranks(3, rank)
+    finally:
+        for c in comms:
+            c.destroy()
+    z0 = r0.threshold["z_q"]
+    for r, (a, b) in enumerate(rows):
+        thr, fl, sc = res[r]
+        assert thr == res[0][0]
+        assert abs(thr["z_q"] - z0) <= 1e-9 * abs(z0)
+        assert torch.equal(sc, r0.scores[a:b].cpu())
+        far = (sc.double() - z0).abs() > 1e-3 * abs(z0)
+        assert torch.equal(fl[far], r0.flags[a:b].cpu()[far])
+
+
+def test_distributed_fit_nccl_world1_graph(E):
+    """The NCCL backend with the distributed fit: the whole step (17 fit-step
+    launches and the all-gathers between them) captured in one CUDA graph;
+    equal to the eager distributed step bit for bit."""
+    X, wts = _fleet(n_inst=6, seed_off=4)
+    T = X.shape[1]
+    tcal = T // 2
+    det = E.PreparedDetector(wts)
+    Xd = torch.from_numpy(X).cuda()
+    comm = E.Comm.create(0, 1, torch.cuda.current_device())
+    try:
+        p = E.Pipeline(det, X.shape[0], T, tcal, comm=comm, fit_mode="distributed")
+        p.enqueue(Xd)
+        eager = p.result()
+        th_e, fl_e = dict(eager.threshold), eager.flags.clone()
+        p.capture(Xd)
+        p.replay()
+        g = p.result()
+    finally:
+        comm.destroy()
+    assert g.threshold == th_e
+    assert torch.equal(g.flags, fl_e)
+    o = O.detect_pipeline(X, wts, tcal)
+    assert abs(th_e["z_q"] - o["threshold"]["z_q"]) <= 1e-6 * abs(o["threshold"]["z_q"])
