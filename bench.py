@@ -513,6 +513,8 @@ def run_threshold_sweep(args, rank, world, local_rank):
     def enqueue():
         if comm is None:
             E.fit_threshold_async(scores, workspace=ws, out=thr_dev)
+        elif args.fit == "distributed":   # per-rank tails, pass totals all-gathered
+            E.fit_threshold_dist_async(scores, n_total, comm, workspace=ws, out=thr_dev)
         else:   # stream-ordered collective fit: captured with its NCCL calls
             E.fit_threshold_comm_async(scores, n_total, comm, workspace=ws, out=thr_dev)
     l0 = _lib.lib().enova_kernel_launches()
@@ -610,6 +612,7 @@ def run_threshold_sweep(args, rank, world, local_rank):
             "config": {"workload": f"c5: {n_total} scores (99.9% 0.5*chi2_16 + 0.1% GPD tail), "
                                    f"q0=0.98, q=1e-3", "scores": n_total,
                        "parallelism": f"score-sharded x{world}",
+                       "fit": args.fit if comm is not None else "single-GPU",
                        "l2": "inputs 400 MB > L2 (no flush needed)"},
             "threshold": {k_: thr[k_] for k_ in ("t", "gamma", "sigma", "z_q", "n_peaks")},
             "phases": phases,
@@ -632,6 +635,10 @@ def run_threshold_sweep(args, rank, world, local_rank):
 
 
 def main():
+    # NCCL prints its version banner on stdout at communicator creation when
+    # NCCL_DEBUG=VERSION: keep stdout to the one JSON line
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -646,6 +653,10 @@ def main():
                     help="host-side multi-rank plumbing only (gloo, no GPU, no kernels): "
                          "shards, barrier, max-over-ranks timing and the JSON line")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--fit", default="replicated", choices=["replicated", "distributed"],
+                    help="fleet threshold fit with a communicator (N > 1): every rank fits the "
+                         "gathered tail (replicated) or its own tail with pass totals all-gathered "
+                         "(distributed, SURVEY §8e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -749,7 +760,7 @@ def run_windows(args, rank, world, local_rank):
     n_cal_local = N * (tcal - (W - 1))
     n_det_local = N * (T - tcal)
     wins_local = n_cal_local + n_det_local
-    pipe = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
+    pipe = E.Pipeline(det, N, T, tcal, device=dev, comm=comm, fit_mode=args.fit)
     cal, mean, std = pipe.cal, pipe.mean, pipe.std
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -950,7 +961,7 @@ def run_windows(args, rank, world, local_rank):
             # step-k graph on the compute stream; every step still copies its whole
             # trace in and its flags out
             X2 = X.clone()   # capture warms up on real data
-            pipe2 = E.Pipeline(det, N, T, tcal, device=dev, comm=comm)
+            pipe2 = E.Pipeline(det, N, T, tcal, device=dev, comm=comm, fit_mode=args.fit)
             pipe2.configure(pipe.pot_ctas, pipe.concurrent_instances)
             pipe2.capture(X2)
             mk = lambda: (torch.empty(tuple(pipe.cal_flags.shape), dtype=torch.int8).pin_memory(),
@@ -1042,6 +1053,7 @@ def run_windows(args, rank, world, local_rank):
                             f"H={H} Z={Z}; T_cal={tcal}; fleet-wide POT threshold",
                 "instances_per_gpu": N, "global_instances": N * world, "T": T, "M": M, "W": W,
                 "windows_per_step": wins_local * world, "parallelism": f"instance-sharded x{world}",
+                "fit": args.fit if world > 1 else "single-GPU",
                 "l2": f"flushed between steps (256 MiB zero-fill, untimed); inputs {Xh.nbytes / 1e6:.0f} MB/GPU > L2",
                 "precision": "fp16 operands (x, weights), fp32 accumulate, h/mu hi+lo fp16",
                 "outputs": "every window of the trace (calibration and detection) ends the step "
