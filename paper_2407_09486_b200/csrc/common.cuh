@@ -308,6 +308,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// non-.aligned form: valid when the participating warps reach the barrier
+// from different code paths / after divergent code
+__device__ __forceinline__ void named_bar_sync_na(uint32_t id, uint32_t nthreads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     }
   } else if (warp == kSAWarp) {
     // ---------------- A producer: one TMA box (kSAK K-steps x 128 instances) per group ----------------
-    if (!kCpAsyncA && p.sample) named_bar_sync(5, kRowThreads + 32);   // fused ingest: wait for the pushes
+    if (!kCpAsyncA && p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
     if (!kCpAsyncA && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
@@ -1033,8 +1033,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
         __threadfence_block();   // own pushed sample before this thread's cp.async reads
       } else {
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();   // reconverge after the per-row push (bar.sync is .aligned)
-        named_bar_sync(5, kRowThreads + 32);
+        __syncwarp();   // reconverge after the per-row push
+        named_bar_sync_na(5, kRowThreads + 32);
       }
     }
     // cp.async A loading: this row's window, group g = 64 fp16 (128 B) at element
