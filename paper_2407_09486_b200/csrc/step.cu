@@ -170,7 +170,9 @@ enova_status enova_step_enqueue(enova_step_t s, const enova_step_args *a, void *
   // overlapped: fork the fit onto the side stream with a reduced grid
   ENOVA_CUDA_TRY(cudaEventRecord(s->fork, st));
   ENOVA_CUDA_TRY(cudaStreamWaitEvent(s->aux, s->fork, 0));
-  set_pot_grid(s->pot_ctas, 2);
+  // a fit grid of <= 16 CTAs runs as one cluster (cluster barriers instead of
+  // grid barriers through global memory); larger grids as whole TPCs
+  set_pot_grid(s->pot_ctas, s->pot_ctas <= 16 ? s->pot_ctas : 2);
   r = fit(s->aux);
   set_pot_grid(0, 0);
   if (r) return r;

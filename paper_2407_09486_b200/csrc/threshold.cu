@@ -217,8 +217,18 @@ __device__ __forceinline__ float key2f(unsigned int k) {
 // b * gridDim.x: one release-add per CTA, then acquire-polls of the same word
 // -- no fences, no second hop through a generation flag.
 __device__ __forceinline__ void grid_sync(PotGlobal *g, unsigned int &epoch) {
-  __syncthreads();
   ++epoch;
+  uint32_t ncta;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+  if (ncta == gridDim.x) {
+    // the whole grid is one thread-block cluster (a reduced fit grid of <= 16
+    // CTAs): the hardware cluster barrier, release / acquire at cluster scope,
+    // orders the global-memory partials like the counter barrier below
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    return;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int target = epoch * gridDim.x;
     unsigned int *p = &g->bar_count;
@@ -1999,6 +2009,8 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
       ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot_scan,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kScanStageBytes));
+      ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot_scan,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       if (dv >= 0 && dv < 64) scan_attr[dv] = true;
     }
     cfg.dynamicSmemBytes = kScanStageBytes;
@@ -2016,6 +2028,9 @@ static enova_status launch_pot(const PotArgs &a, int nb, cudaStream_t st, bool r
     ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kMaxYCacheBytes));
+    // a reduced fit grid may be ONE cluster of up to 16 CTAs (grid_sync)
+    ENOVA_CUDA_TRY(cudaFuncSetAttribute((const void *)k_pot,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   // the fit partitions N_t <= cap peaks into nb contiguous slices

@@ -444,7 +444,7 @@ def test_async_pipeline_matches_sync_and_oracle(E):
     assert res2.threshold == ref.threshold and torch.equal(res2.flags, ref.flags)
     o = O.pot_threshold(ref.cal_scores.cpu().numpy(), 0.98, 1e-3)
     assert abs(res2.threshold["z_q"] - o["z_q"]) <= 1e-9 * o["z_q"]
-    for pot, conc in ((24, 5), (32, 12), (16, 0)):
+    for pot, conc in ((24, 5), (32, 12), (16, 0), (8, 3)):
         po = E.Pipeline(det, N, T, T // 2, pot_ctas=pot, concurrent_instances=conc)
         po.capture(Xc)
         po.replay()
