@@ -43,6 +43,7 @@ constexpr int kPotWarps = kPotThreads / 32;
 constexpr int kMaxCtas = 256;
 constexpr int kMaxWorld = 256;        // ranks of one communicator (fleet threshold)
 constexpr int kMaxPts = 128;
+constexpr int kMaxSl = 4;             // Y slices per point bundle in the mixed grid pass
 constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
 constexpr int kMaxRefinePasses = 60;
@@ -428,8 +429,16 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
   score_chunk(a.n_local, &b0, &b1);
   const int64_t len = b1 - b0;
   const int ns = (int)min((int64_t)kSampleN, len);
-  for (int j = threadIdx.x; j < ns; j += blockDim.x)
-    sk[j] = f2key(__ldg(a.scores + b0 + (int64_t)j * len / ns));
+  // sample j at floor(j len / ns): 32-bit arithmetic when j len < 2^32 (the same
+  // integer), the 64-bit division only for chunks above 2M scores
+  if (len <= (int64_t)(0xffffffffu / kSampleN)) {
+    const uint32_t l32 = (uint32_t)len, n32 = (uint32_t)ns;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x)
+      sk[j] = f2key(__ldg(a.scores + b0 + (uint32_t)j * l32 / n32));
+  } else {
+    for (int j = threadIdx.x; j < ns; j += blockDim.x)
+      sk[j] = f2key(__ldg(a.scores + b0 + (int64_t)j * len / ns));
+  }
   if (threadIdx.x == 0) {
     const int64_t S = sample_total(a);
     const double q0 = a.q0;
@@ -1260,28 +1269,32 @@ __device__ __forceinline__ float log1p_f32(float t, float v, float r) {
   q = fmaf(q, s2, 0.2f);
   q = fmaf(q, s2, 1.f / 3.f);
   const float at = fmaf(sn * s2, q, sn);   // atanh(s)
-  return fmaf((float)e, 0.6931471805599453f, fmaf(2.f, at, c * r));
+  // (float)e without an I2F (XU): 1.5 * 2^23 + e is exact for |e| < 2^22
+  const float ef = __int_as_float(0x4B400000 + e) - 12582912.f;
+  return fmaf(ef, 0.6931471805599453f, fmaf(2.f, at, c * r));
 }
 
-// fp32 terms of the P and L sums for up to 4 scan points; fp32 partials over 8
-// terms are flushed into fp64 accumulators (so the sum error stays at the
-// terms' own rounding, ~1e-7 relative).
+// fp32 terms of the P and L sums for up to kW scan points; fp32 partials over
+// 16 terms are flushed into fp64 accumulators (so the sum error stays ~1e-6
+// relative, inside the certification bound 1e-5 (|P| + |L| + |P L|)).  One fp64
+// -> fp32 conversion of Y per element serves all kW points.
+template <int kW>
 __device__ __forceinline__ void eval_bundle32(const double *Y, int64_t s0, int64_t s1,
-                                              const double (&x)[4], int nu,
-                                              double (&acc)[4][kSums]) {
-  float xf[4];
+                                              const double *x, int nu, double (&acc)[kW][2]) {
+  float xf[kW];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    xf[u] = (float)x[u];
-#pragma unroll
-    for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
+  for (int u = 0; u < kW; ++u) {
+    xf[u] = (u < nu) ? (float)x[u] : 0.f;
+    acc[u][0] = acc[u][1] = 0.0;
   }
-  float pp[4] = {0.f, 0.f, 0.f, 0.f}, ll[4] = {0.f, 0.f, 0.f, 0.f};
+  float pp[kW], ll[kW];
+#pragma unroll
+  for (int u = 0; u < kW; ++u) pp[u] = ll[u] = 0.f;
   int run = 0;
   for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
     const float y = (float)Y[i];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kW; ++u) {
       if (u < nu) {
         const float t = xf[u] * y;
         const float v = 1.f + t;
@@ -1291,10 +1304,10 @@ __device__ __forceinline__ void eval_bundle32(const double *Y, int64_t s0, int64
         ll[u] += log1p_f32(t, v, r);
       }
     }
-    if (++run == 8) {
+    if (++run == 16) {
       run = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kW; ++u) {
         acc[u][0] += (double)pp[u];
         acc[u][1] += (double)ll[u];
         pp[u] = 0.f;
@@ -1303,12 +1316,12 @@ __device__ __forceinline__ void eval_bundle32(const double *Y, int64_t s0, int64
     }
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kW; ++u) {
     acc[u][0] += (double)pp[u];
     acc[u][1] += (double)ll[u];
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < kW; ++u)
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -1319,7 +1332,7 @@ struct FitShared {
   FitState f;
   LogTab tab;
   int scratch[32];
-  double sred[kMaxPts][kSums];   // per warp item partial sums [item][k]
+  double sred[kMaxSl * kMaxPts][kSums];   // per warp item partial sums [slice * npts + pt][k]
   double powp[kPotWarps][kPow];  // PH_GRID32: per-warp power sums of Y / Ymax
   double red[kSums][kMaxPts];    // grid totals after the barrier
 };
@@ -1440,27 +1453,56 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   const bool deriv = (phase == PH_REFINE);
   const bool mixed = (phase == PH_GRID32);
   const int nk = deriv ? kSums : 2;
-  // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones
+  // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones.
+  // Warp items = (bundle, Y slice).  The mixed grid pass cuts every bundle into
+  // slices (~4 items per warp) and an fp64 bundle into 4x as many as an fp32 one
+  // (its evaluation costs ~4x), so the CTA's warps finish together.
+  constexpr int kWB = 8;   // points per fp32 bundle (one Y conversion serves 8 points)
   const int n64 = mixed ? f.n64 : npts;
   const int nb64 = (n64 + 3) / 4;
-  const int nbund = mixed ? nb64 + (f.n32 + 3) / 4 : (npts + 3) / 4;
-  const int slices = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
-  const int items = nbund * slices;
+  const int nbund = mixed ? nb64 + (f.n32 + kWB - 1) / kWB : (npts + 3) / 4;
+  int sA, sB;   // slices of an A (fp64-type) and a B (fp32) bundle
+  if (mixed) {
+    sB = min(kMaxSl, max(1, (4 * kPotWarps + nbund - 1) / max(nbund, 1)));
+    sA = min(kMaxSl, 4 * sB);
+  } else {
+    sA = sB = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
+  }
+  const int nA = nb64, nB = nbund - nb64;
+  const int itemsA = nA * sA, items = itemsA + nB * sB;
   for (int it = warp; it < items; it += kPotWarps) {
-    const int bnd = it % nbund, sl = it / nbund;
+    const bool isA = it < itemsA;
+    const int j = isA ? it : it - itemsA;
+    const int bnd = isA ? j % nA : nA + j % nB, sl = isA ? j / nA : j / nB;
+    const int slices = isA ? sA : sB;
     const int64_t len = c1 - c0;
     const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
     const bool f32 = mixed && bnd >= nb64;
-    const int base = f32 ? n64 + 4 * (bnd - nb64) : 4 * bnd;
-    const int nu = min(4, (f32 ? n64 + f.n32 : (mixed ? n64 : npts)) - base);
+    // points split evenly over the bundles of a type (a refine pass's 6 points:
+    // 3 + 3, not 4 + 2, so the warps' items cost the same)
+    if (f32) {
+      const int b = bnd - nb64;
+      const int base = n64 + b * f.n32 / nB, nu = n64 + (b + 1) * f.n32 / nB - base;
+      double acc[kWB][2];
+      eval_bundle32<kWB>(Y, s0, s1, f.xs + base, nu, acc);
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < kWB; ++u)
+          if (u < nu) {
+            S.sred[sl * npts + base + u][0] = acc[u][0];
+            S.sred[sl * npts + base + u][1] = acc[u][1];
+          }
+      }
+      continue;
+    }
+    const int nAp = mixed ? n64 : npts;
+    const int base = bnd * nAp / nA, nu = (bnd + 1) * nAp / nA - base;
     double x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[base + u] : 0.0;
     double acc[4][kSums];
     if (deriv)
       eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
-    else if (f32)
-      eval_bundle32(Y, s0, s1, x, nu, acc);
     else
       eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
     if (lane == 0) {
@@ -1502,6 +1544,7 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
     const int k = i / npts, pt = i % npts;
     double s = 0.0;
+    const int slices = (pt < n64) ? sA : sB;   // list order: A bundles' points first
     for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
     pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
   }
