@@ -43,7 +43,6 @@ constexpr int kPotWarps = kPotThreads / 32;
 constexpr int kMaxCtas = 256;
 constexpr int kMaxWorld = 256;        // ranks of one communicator (fleet threshold)
 constexpr int kMaxPts = 128;
-constexpr int kMaxSl = 4;             // Y slices per point bundle in the mixed grid pass
 constexpr int kMaxSlots = 64;
 constexpr int kGrid = 64;
 constexpr int kMaxRefinePasses = 60;
@@ -56,16 +55,24 @@ constexpr int kSums = 6;              // P, L, dP, dL, d2P, d2L per evaluation p
 // root blurred the sign test
 constexpr double kCertRel = 5e-12;
 
-enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_GRIDFIX = 5 };
+enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_GRIDFIX = 5,
+       PH_GRIDBIN = 6 };
 // Large tails (N_t >= kGrid32MinPeaks): the 128-point scan grid is evaluated in
-// ONE pass of mixed precision (PH_GRID32) -- points with |x| Ymax <= 1e-3 from
-// six fp64 power sums of Y/Ymax (the log1p and 1/(1+t) series, 1e-18 truncation),
-// points with x Ymax < -0.9 in fp64, the rest in fp32 with fp64 accumulation and
-// an error bound: a sign is accepted when |w32| > 1e-5 (|P| + |L| + |P L|), else
-// that point is re-evaluated in fp64 (PH_GRIDFIX).  The signs, hence the
-// brackets, are those of the fp64 scan wherever the fp64 scan itself resolves
-// them; the Halley refinement that follows is fp64 as before.
+// two passes (PH_GRID32, PH_GRIDBIN) -- points with |x| Ymax <= 1e-3 from six
+// fp64 power sums of Y/Ymax (the log1p and 1/(1+t) series, 1e-18 truncation),
+// points with x Ymax < -0.9 in fp64 over Y (PH_GRID32, which also bins Y), the
+// rest over a log-binned histogram of Y (PH_GRIDBIN): per bin the count, sum and
+// sum of squares, each term evaluated at the bin mean with the exact
+// second-order correction 1/2 f''(ybar_b) sum (y - ybar_b)^2 -- 2048 bins per
+// octave (relative width 3.4e-4), so the remainder is third order (<= 1e-7 of
+// the sums even at x Ymax = -0.9) -- and an error bound: a sign is accepted when
+// |w| > 1e-6 (|P| + |L| + |P L|), else that point is re-evaluated in fp64 over
+// Y (PH_GRIDFIX).  The signs, hence the brackets, are those of the fp64 scan
+// wherever the fp64 scan itself resolves them; the Halley refinement that
+// follows is fp64 over Y as before.
 constexpr int64_t kGrid32MinPeaks = 100000;
+constexpr int kMaxBins = 131072;          // binned grid pass: bins of log2(Y) (x3 fp64 each)
+constexpr double kBinsPerOctave = 2048.0;
 constexpr int kPow = 6;   // power sums of u = Y / Ymax for the series points
 // phase program of k_pot
 enum { P_SAMPLE = 0, P_SCAN = 1, P_HIST0 = 2, P_HIST1 = 3, P_HIST2 = 4, P_COMPACT = 5, P_FIT = 6 };
@@ -118,6 +125,8 @@ struct FitState {
   double gx[kMaxPts], gw[kMaxPts], pm[kPow + 1];
   int gmode[kMaxPts], gidx[kMaxPts], ginv[kMaxPts];
   int ngrid, n64, n32, nfix;
+  double bin_l0, bin_k;       // PH_GRIDBIN: bin b holds log2(Y) in [l0 + b/k, l0 + (b+1)/k)
+  int nbins;
   int triple;                 // REFINE evaluates (x, x(1-d), x(1+d)) per root (certifying)
   int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
@@ -130,6 +139,8 @@ struct ThrLayout {
   size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yslot, outdev, yall, header, total;
   size_t shist, cand, cand_n;   // sampled selection: sample histograms, candidates, per-CTA counts
   size_t fstate, xsend, xrecv;  // distributed fit (communicator layouts)
+  size_t bins;                  // binned grid pass: [kMaxBins][3] fp64 (count, sum, sum of squares)
+  bool has_bins;
   int64_t cap;
   bool sampled;                 // workspace holds the candidate buffer
 };
@@ -162,6 +173,8 @@ static inline ThrLayout thr_layout(int64_t n_max, double q0, int world = 0) {
   L.fstate = take(world ? sizeof(FitState) : 0);
   L.xsend = take(world ? (size_t)kSums * kMaxPts * 8 : 0);
   L.xrecv = take((size_t)world * kSums * kMaxPts * 8);
+  L.has_bins = L.cap >= kGrid32MinPeaks;
+  L.bins = take(L.has_bins ? (size_t)kMaxBins * 3 * 8 : 0);
   // candidates: one segment of ceil(chunk / 4) * 4 scores per CTA (a segment can
   // hold its CTA's whole chunk, so it never overflows)
   L.sampled = (world == 0 && n_max >= kSampleMinN);
@@ -201,6 +214,7 @@ struct PotArgs {
   double *xsend;            // [kSums * kMaxPts] this rank's totals of the step
   const double *xrecv;      // [world][kSums * kMaxPts] gathered totals
   FitState *fstate;         // the fit's state between launches
+  double *bins;             // [kMaxBins][3] binned grid pass (null below kGrid32MinPeaks)
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -781,9 +795,9 @@ __device__ void controller(FitState *f, int *scratch) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int phase = f->phase;   // read by all threads before any write below
   __syncthreads();
-  if (phase == PH_GRID32 || phase == PH_GRIDFIX) {
-    // w at every scan-grid point: series / fp64 / certified fp32 (GRID32), or the
-    // fp64 re-evaluations of the uncertain fp32 points (GRIDFIX)
+  if (phase == PH_GRID32 || phase == PH_GRIDBIN || phase == PH_GRIDFIX) {
+    // w at every scan-grid point: series / fp64 (GRID32), certified binned
+    // (GRIDBIN), or the fp64 re-evaluations of the uncertain binned points (GRIDFIX)
     const int ng = f->ngrid;
     if (phase == PH_GRID32) {
       if (tid < ng) {
@@ -803,18 +817,38 @@ __device__ void controller(FitState *f, int *scratch) {
             if (m >= 2) PL += sg * tm * (1.0 - 1.0 / m);
           }
           f->gw[tid] = PL + P * L;
-        } else {
-          const int li = f->ginv[tid];
-          const double w = f->w[li];
-          f->gw[tid] = w;
-          if (mode == 0) {
-            const double P = f->P[li], L = f->L[li];
-            const double bound = 1e-5 * (fabs(P) + fabs(L) + fabs(P * L));
-            if (!(fabs(w) > bound)) f->gmode[tid] = 3;   // uncertain: fp64 re-evaluation
-          }
+        } else if (mode == 2) {
+          f->gw[tid] = f->w[f->ginv[tid]];
         }
       }
       __syncthreads();
+      if (tid == 0) {   // the binned points' evaluation list (grid order)
+        int nb = 0;
+        for (int g = 0; g < ng; ++g)
+          if (f->gmode[g] == 0) {
+            f->gidx[nb] = g;
+            f->xs[nb] = f->gx[g];
+            ++nb;
+          }
+        f->npts = nb;
+        if (nb > 0) f->phase = PH_GRIDBIN;
+      }
+      __syncthreads();
+      if (f->phase == PH_GRIDBIN) return;   // one more pass, over the bins
+    } else if (phase == PH_GRIDBIN) {
+      if (tid < f->npts) {
+        const int g = f->gidx[tid];
+        const double w = f->w[tid], P = f->P[tid], L = f->L[tid];
+        f->gw[g] = w;
+        // the binned sums carry a third-order remainder <= ~3e-8 of |P| + |L| (bin
+        // width 3.4e-4, x Ymax >= -0.9) and fp64 rounding: a 1e-6 bound leaves a
+        // 30x margin
+        const double bound = 1e-6 * (fabs(P) + fabs(L) + fabs(P * L));
+        if (!(fabs(w) > bound)) f->gmode[g] = 3;   // uncertain: fp64 re-evaluation
+      }
+      __syncthreads();
+    }
+    if (phase == PH_GRID32 || phase == PH_GRIDBIN) {
       if (tid == 0) {
         int nf = 0;
         for (int g = 0; g < ng; ++g)
@@ -1138,8 +1172,16 @@ __device__ void setup_grid(FitState *f) {
       f->ngrid = ng;
       f->n64 = n64;
       f->n32 = n32;
-      f->npts = n64 + n32;
+      f->npts = n64;   // PH_GRID32 evaluates the fp64 points; the rest over the bins
       f->phase = PH_GRID32;
+      // bins of log2(Y) over [Ymin, Ymax]: kBinsPerOctave per octave, fewer if the
+      // range spans more than kMaxBins / kBinsPerOctave octaves
+      const double l0 = log2(ymin), oct = fmax(log2(ymax) - l0, 1e-9);
+      double bk = kBinsPerOctave;
+      if (oct * bk > (double)(kMaxBins - 2)) bk = (double)(kMaxBins - 2) / oct;
+      f->bin_l0 = l0;
+      f->bin_k = bk;
+      f->nbins = min(kMaxBins, (int)ceil(oct * bk) + 1);
     }
   }
 }
@@ -1245,83 +1287,37 @@ __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t
       for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
 }
 
-// fp32 log1p(t), t > -1, given v = fl(1 + t) and r ~ 1/v: log(v) + c/v with c =
-// t - (v - 1) the rounding error of v; log(v) = e ln2 + 2 atanh(s), v = 2^e m,
-// m in [sqrt(1/2), sqrt(2)), s = (m - 1)/(m + 1), |s| <= 0.1716, atanh by its
-// odd series to s^9 (truncation < 3e-9).  A few ulp relative over the range the
-// certified scan uses it on (t >= -0.9).
-__device__ __forceinline__ float log1p_f32(float t, float v, float r) {
-  const float c = t - (v - 1.f);
-  int bits = __float_as_int(v);
-  int e = ((bits >> 23) & 0xff) - 127;
-  bits = (bits & 0x007fffff) | 0x3f800000;
-  if (bits > 0x3fb504f3) {   // m > sqrt(2): halve
-    bits -= 0x00800000;
-    ++e;
-  }
-  const float m = __int_as_float(bits);
-  float ip;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ip) : "f"(m + 1.f));
-  const float sn = (m - 1.f) * ip;
-  const float s2 = sn * sn;
-  float q = 1.f / 9.f;
-  q = fmaf(q, s2, 1.f / 7.f);
-  q = fmaf(q, s2, 0.2f);
-  q = fmaf(q, s2, 1.f / 3.f);
-  const float at = fmaf(sn * s2, q, sn);   // atanh(s)
-  // (float)e without an I2F (XU): 1.5 * 2^23 + e is exact for |e| < 2^22
-  const float ef = __int_as_float(0x4B400000 + e) - 12582912.f;
-  return fmaf(ef, 0.6931471805599453f, fmaf(2.f, at, c * r));
-}
-
-// fp32 terms of the P and L sums for up to kW scan points; fp32 partials over
-// 16 terms are flushed into fp64 accumulators (so the sum error stays ~1e-6
-// relative, inside the certification bound 1e-5 (|P| + |L| + |P L|)).  One fp64
-// -> fp32 conversion of Y per element serves all kW points.
-template <int kW>
-__device__ __forceinline__ void eval_bundle32(const double *Y, int64_t s0, int64_t s1,
-                                              const double *x, int nu, double (&acc)[kW][2]) {
-  float xf[kW];
+// PH_GRIDBIN: sums of the P and L terms of up to 4 points over the bins
+// [b0, b1) (lanes over bins): per bin n f(x m) + 1/2 f''(x m) x^2 S2 with m the
+// bin mean and S2 = sum (y - m)^2 -- f = log1p, f'' = -1/(1+u)^2; P's term
+// -u/(1+u), its second derivative 2/(1+u)^3.
+__device__ __forceinline__ void eval_bins(const double *bins, int b0, int b1,
+                                          const double (&x)[4], int nu,
+                                          double (&acc)[4][kSums], const LogTab &T) {
 #pragma unroll
-  for (int u = 0; u < kW; ++u) {
-    xf[u] = (u < nu) ? (float)x[u] : 0.f;
-    acc[u][0] = acc[u][1] = 0.0;
-  }
-  float pp[kW], ll[kW];
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
-  for (int u = 0; u < kW; ++u) pp[u] = ll[u] = 0.f;
-  int run = 0;
-  for (int64_t i = s0 + (threadIdx.x & 31); i < s1; i += 32) {
-    const float y = (float)Y[i];
+    for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
+  for (int b = b0 + (threadIdx.x & 31); b < b1; b += 32) {
+    const double n = __ldcg(bins + 3 * b);
+    if (n == 0.0) continue;
+    const double s = __ldcg(bins + 3 * b + 1), q = __ldcg(bins + 3 * b + 2);
+    const double m = s / n;
+    const double s2 = fmax(q - s * m, 0.0);
 #pragma unroll
-    for (int u = 0; u < kW; ++u) {
+    for (int u = 0; u < 4; ++u) {
       if (u < nu) {
-        const float t = xf[u] * y;
-        const float v = 1.f + t;
-        float r;
-        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-        pp[u] = fmaf(-t, r, pp[u]);
-        ll[u] += log1p_f32(t, v, r);
-      }
-    }
-    if (++run == 16) {
-      run = 0;
-#pragma unroll
-      for (int u = 0; u < kW; ++u) {
-        acc[u][0] += (double)pp[u];
-        acc[u][1] += (double)ll[u];
-        pp[u] = 0.f;
-        ll[u] = 0.f;
+        const double xm = x[u] * m;
+        const double v = 1.0 + xm;
+        const double r = rcp_nr(v);
+        const double c2 = x[u] * x[u] * r * r * s2;   // x^2 S2 / (1 + x m)^2
+        acc[u][0] = fma(n, -xm * r, fma(c2, r, acc[u][0]));
+        acc[u][1] = fma(n, log1p_fast(xm, v, r, T), fma(-0.5, c2, acc[u][1]));
       }
     }
   }
 #pragma unroll
-  for (int u = 0; u < kW; ++u) {
-    acc[u][0] += (double)pp[u];
-    acc[u][1] += (double)ll[u];
-  }
-#pragma unroll
-  for (int u = 0; u < kW; ++u)
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -1332,7 +1328,7 @@ struct FitShared {
   FitState f;
   LogTab tab;
   int scratch[32];
-  double sred[kMaxSl * kMaxPts][kSums];   // per warp item partial sums [slice * npts + pt][k]
+  double sred[kMaxPts][kSums];   // per warp item partial sums [slice * npts + pt][k]
   double powp[kPotWarps][kPow];  // PH_GRID32: per-warp power sums of Y / Ymax
   double red[kSums][kMaxPts];    // grid totals after the barrier
 };
@@ -1423,6 +1419,15 @@ __device__ void fit_stats_partials(const PotArgs &a, FitShared &S, const double 
   }
 }
 
+// the binned grid pass's histogram starts empty: every CTA zeroes its slice
+// (first written after the next grid barrier)
+__device__ __forceinline__ void zero_bins(double *bins) {
+  if (!bins) return;
+  const int n = kMaxBins * 3;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    bins[i] = 0.0;
+}
+
 // grid totals of the statistics partials (fixed order; warp 0 of every CTA)
 __device__ void fit_stats_totals(const PotArgs &a, double &ts, double &tmn, double &tmx) {
   const int lane = threadIdx.x & 31, nb = gridDim.x;
@@ -1445,64 +1450,43 @@ __device__ void fit_stats_totals(const PotArgs &a, double &ts, double &tmn, doub
 // one evaluation pass over this CTA's slice at the points of f (list order):
 // CTA partials per (k, point) -> pw ([kSums][kMaxPts][kMaxCtas])
 __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int64_t c1,
-                                  double *pw) {
+                                  double *pw, double *bins) {
   FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int phase = f.phase;
   const int npts = f.npts;
   const bool deriv = (phase == PH_REFINE);
   const bool mixed = (phase == PH_GRID32);
+  const bool binned = (phase == PH_GRIDBIN);
   const int nk = deriv ? kSums : 2;
-  // bundles of 4 list points; PH_GRID32: the fp64 points' bundles, then the fp32 ones.
-  // Warp items = (bundle, Y slice).  The mixed grid pass cuts every bundle into
-  // slices (~4 items per warp) and an fp64 bundle into 4x as many as an fp32 one
-  // (its evaluation costs ~4x), so the CTA's warps finish together.
-  constexpr int kWB = 8;   // points per fp32 bundle (one Y conversion serves 8 points)
-  const int n64 = mixed ? f.n64 : npts;
-  const int nb64 = (n64 + 3) / 4;
-  const int nbund = mixed ? nb64 + (f.n32 + kWB - 1) / kWB : (npts + 3) / 4;
-  int sA, sB;   // slices of an A (fp64-type) and a B (fp32) bundle
-  if (mixed) {
-    sB = min(kMaxSl, max(1, (4 * kPotWarps + nbund - 1) / max(nbund, 1)));
-    sA = min(kMaxSl, 4 * sB);
-  } else {
-    sA = sB = (nbund >= kPotWarps) ? 1 : kPotWarps / max(nbund, 1);
+  // PH_GRIDBIN: the list points over this CTA's slice of the bins, not over Y
+  if (binned) {
+    const int nbn = f.nbins, nbk = gridDim.x;
+    const int b0 = (int)((int64_t)blockIdx.x * nbn / nbk), b1 = (int)((int64_t)(blockIdx.x + 1) * nbn / nbk);
+    c0 = b0;
+    c1 = b1;
   }
-  const int nA = nb64, nB = nbund - nb64;
-  const int itemsA = nA * sA, items = itemsA + nB * sB;
+  // bundles of 4 list points (PH_GRID32: the fp64 points; the rest of the grid
+  // is evaluated over the bins).  Warp items = (bundle, Y slice); the points are
+  // spread evenly over the bundles (a refine pass's 6 points: 3 + 3, not 4 + 2)
+  const int n64 = mixed ? f.n64 : npts;
+  const int nA = (n64 + 3) / 4;
+  const int sA = (nA >= kPotWarps) ? 1 : kPotWarps / max(nA, 1);
+  const int items = nA * sA;
   for (int it = warp; it < items; it += kPotWarps) {
-    const bool isA = it < itemsA;
-    const int j = isA ? it : it - itemsA;
-    const int bnd = isA ? j % nA : nA + j % nB, sl = isA ? j / nA : j / nB;
-    const int slices = isA ? sA : sB;
+    const int bnd = it % nA, sl = it / nA;
+    const int slices = sA;
     const int64_t len = c1 - c0;
     const int64_t s0 = c0 + len * sl / slices, s1 = c0 + len * (sl + 1) / slices;
-    const bool f32 = mixed && bnd >= nb64;
-    // points split evenly over the bundles of a type (a refine pass's 6 points:
-    // 3 + 3, not 4 + 2, so the warps' items cost the same)
-    if (f32) {
-      const int b = bnd - nb64;
-      const int base = n64 + b * f.n32 / nB, nu = n64 + (b + 1) * f.n32 / nB - base;
-      double acc[kWB][2];
-      eval_bundle32<kWB>(Y, s0, s1, f.xs + base, nu, acc);
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < kWB; ++u)
-          if (u < nu) {
-            S.sred[sl * npts + base + u][0] = acc[u][0];
-            S.sred[sl * npts + base + u][1] = acc[u][1];
-          }
-      }
-      continue;
-    }
-    const int nAp = mixed ? n64 : npts;
-    const int base = bnd * nAp / nA, nu = (bnd + 1) * nAp / nA - base;
+    const int base = bnd * n64 / nA, nu = (bnd + 1) * n64 / nA - base;
     double x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = (u < nu) ? f.xs[base + u] : 0.0;
     double acc[4][kSums];
     if (deriv)
       eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
+    else if (binned)
+      eval_bins(bins, (int)s0, (int)s1, x, nu, acc, S.tab);
     else
       eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
     if (lane == 0) {
@@ -1514,18 +1498,28 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
     }
   }
   if (mixed) {   // power sums of u = Y / Ymax for the series points (fp64, fixed order)
+                 // and the bins of log2(Y) for PH_GRIDBIN (count, sum, sum of squares)
     const double iy = 1.0 / f.ymax;
+    const float l0f = (float)f.bin_l0, bkf = (float)f.bin_k;
+    const int nbn = f.nbins;
     double q[kPow];
 #pragma unroll
     for (int m = 0; m < kPow; ++m) q[m] = 0.0;
     for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const double u = Y[i] * iy;
+      const double y = Y[i];
+      const double u = y * iy;
       double pw_ = u;
 #pragma unroll
       for (int m = 0; m < kPow; ++m) {
         q[m] += pw_;
         pw_ *= u;
       }
+      float lg;
+      asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"((float)y));
+      const int bi = min(max(__float2int_rd((lg - l0f) * bkf), 0), nbn - 1);
+      atomicAdd(bins + 3 * bi, 1.0);
+      atomicAdd(bins + 3 * bi + 1, y);
+      atomicAdd(bins + 3 * bi + 2, y * y);
     }
 #pragma unroll
     for (int m = 0; m < kPow; ++m) {
@@ -1544,8 +1538,7 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
     const int k = i / npts, pt = i % npts;
     double s = 0.0;
-    const int slices = (pt < n64) ? sA : sB;   // list order: A bundles' points first
-    for (int sl = 0; sl < slices; ++sl) s += S.sred[sl * npts + pt][k];
+    for (int sl = 0; sl < sA; ++sl) s += S.sred[sl * npts + pt][k];
     pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
   }
 }
@@ -1669,6 +1662,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
 
   // ---- Ybar, Ymin, Ymax (pass 0, partial buffer 0) ----
   fit_stats_partials(a, S, a.yfit, c0, c1, cached, ycache);
+  if (nt >= kGrid32MinPeaks) zero_bins(a.bins);
   grid_sync(a.g, epoch);
   stamp(a.g);
   if (warp == 0) {
@@ -1684,7 +1678,7 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
   for (int pass = 1;; ++pass) {
     if (f.phase == PH_DONE) break;
     double *pw = a.part + (size_t)(pass & 1) * kSums * kMaxPts * kMaxCtas;
-    fit_eval_partials(S, Y, c0, c1, pw);
+    fit_eval_partials(S, Y, c0, c1, pw, a.bins);
     stamp(a.g);
     grid_sync(a.g, epoch);
     stamp(a.g);
@@ -1731,6 +1725,7 @@ __device__ void dfit_step(const PotArgs &a, FitShared &S, unsigned int &epoch) {
       Yl[i] = (double)a.ylocal[i] - td;
     __syncthreads();
     fit_stats_partials(a, S, Yl, c0, c1, false, ycache);
+    zero_bins(a.bins);
     grid_sync(g, epoch);
     if (blockIdx.x == 0 && warp == 0) {
       double ts, tmn, tmx;
@@ -1810,7 +1805,7 @@ __device__ void dfit_step(const PotArgs &a, FitShared &S, unsigned int &epoch) {
     }
     __syncthreads();
     double *pw = a.part;
-    fit_eval_partials(S, Y, c0, c1, pw);
+    fit_eval_partials(S, Y, c0, c1, pw, a.bins);
     grid_sync(g, epoch);
     if (blockIdx.x == 0) {
       fit_eval_totals(S, pw);
@@ -2149,6 +2144,7 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.xsend = comm ? reinterpret_cast<double *>(b + L.xsend) : nullptr;
   a.xrecv = comm ? reinterpret_cast<const double *>(b + L.xrecv) : nullptr;
   a.fstate = comm ? reinterpret_cast<FitState *>(b + L.fstate) : nullptr;
+  a.bins = L.has_bins ? reinterpret_cast<double *>(b + L.bins) : nullptr;
   return a;
 }
 
