@@ -8,7 +8,7 @@
 // flattened (instance, sample) space of the calibration horizon into equal
 // contiguous ranges, so every CTA streams the same number of samples whatever
 // the fleet shape -- no ragged last wave.  The bytes arrive by bulk copy: a
-// producer warp walks the CTA's range as chunks of <= 16 KB inside one instance
+// producer warp walks the CTA's range as chunks of <= 64 KB inside one instance
 // segment and keeps kStatsStages chunks in flight (cp.async.bulk into a shared
 // memory ring, mbarrier complete_tx), so the HBM latency is covered without
 // register-held loads; 512 consumer threads accumulate from shared memory.
@@ -29,8 +29,10 @@ namespace enova {
 constexpr int kStatsThreads = 512;              // consumers
 constexpr int kStatsBlock = kStatsThreads + 32; // + the producer warp
 constexpr int kStatsMaxGrid = 512;   // <= 256 SMs x 2 (workspace sizing)
-constexpr int kStatsStages = 5;
-constexpr uint32_t kStatsChunkBytes = 32768;
+// 3 x 64 KB in flight per SM (same-box ncu, c2: 5 x 32 KB 25.8 us, 10 x 16 KB
+// 29.5 us, 3 x 64 KB 23.6 us -- the bytes in flight per SM set the rate)
+constexpr int kStatsStages = 3;
+constexpr uint32_t kStatsChunkBytes = 65536;
 
 // contributors of one instance: a CTA range holds >= floor(N T / nb) >= 64
 // samples, so an instance of T samples meets at most ceil(nb / N) + 2 ranges
@@ -194,13 +196,21 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
       for (int q = 0; q < nred; ++q) sacc += red[(size_t)q * 2 * M + e];
       pc[e] = sacc;
     }
-    // the last contributor of this instance combines the slots in order
-    __threadfence();
+    // the last contributor of this instance combines the slots in order: the
+    // ticket is an acq_rel RMW at gpu scope after the CTA barrier -- it releases
+    // this CTA's slot writes (cumulative over the barrier) and, for the last
+    // contributor, acquires every other contributor's (no full fences)
     named_bar_sync(1, kStatsThreads);
-    if (tid == 0) last = (atomicAdd(ticket + inst, 1u) == (unsigned)ncontrib - 1);
+    if (tid == 0) {
+      unsigned int old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "l"(ticket + inst)
+                   : "memory");
+      last = (old == (unsigned)ncontrib - 1);
+    }
     named_bar_sync(1, kStatsThreads);
     if (last) {
-      __threadfence();
       for (int j = tid; j < M; j += kStatsThreads) {
         const double *p0 = slots + (size_t)inst * max_contrib * 2 * M;
         double s1 = 0, s2 = 0;
