@@ -27,9 +27,7 @@
 //             window scored in a batch.
 //
 // Envelope: M in {8, 16} (a K-step holds whole samples), H in {32, 64, 128}.
-#include <cuda.h>
 #include <type_traits>
-#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -648,19 +646,29 @@ enova_status launch_explain_rows(const enova_series *s, const DetLayout &L, cons
 // k are contiguous: slots (k+1) mod W ..) next to its fp32 sample sum
 // s = sum_j x_j (the windowed kernels' association) in [N][2W].  A tick needs
 // no normalisation: the GEMM1 A operand of 4 K-steps for 128 instances is ONE
-// 2-D TMA box (64 fp16 = 128 B per instance x 128 instances, SWIZZLE_128B,
-// 16 KB) consumed by K-major SWIZZLE_128B UMMA descriptors (+32 B per K-step),
-// so the kernel is a TMA -> tcgen05 pipeline plus the shared epilogue.
+// 16 KB bulk copy of the tile's contiguous range of the tiled canonical ring
+// (below), consumed by no-swizzle K-major UMMA descriptors, so the kernel is a
+// bulk-copy -> tcgen05 pipeline plus the shared epilogue.
 // =====================================================================
 
-// Row pitches are padded off powers of two: with the natural pitches (2W*M fp16 =
-// 4 KB, 2W fp32 = 512 B at c4) the 128 instances of a tile hit the same DRAM
-// channel and every A group of the stream kernel was serialised (measured ~1 us
-// per 4-K-step group).  +256 B / +32 B spreads consecutive instances.
-__host__ __device__ inline int64_t stream_pitch(int W, int M) { return (int64_t)2 * W * M + 128; }
+// The fp16 ring is TILED in the UMMA's no-swizzle K-major canonical layout:
+//   [tile of 128 instances][2W slots][M/8 halves][128 rows][8 fp16]
+// so one slot of one tile is M/8 contiguous 2 KB half-blocks, and the A
+// operand of ANY run of K-steps of a tile's windows is ONE contiguous range (a
+// window = slots [s0, s0 + W) of the mirror ring; K-step q = half-blocks
+// s0 M/8 + 2q, +1): the stream kernel moves it with plain 16 KB bulk copies
+// instead of 2-D TMA boxes of 128 scattered 128-B rows (which paced the K loop
+// at ~0.65 us per 4 K-steps).  The fp32 sample-sum ring stays [N][pitch]; its
+// pitch is padded off a power of two (consecutive instances on different DRAM
+// channels).
 __host__ __device__ inline int64_t sums_pitch(int W) { return (int64_t)2 * W + 8; }
+__host__ __device__ inline size_t stream_elem(int64_t i, int s, int j, int W, int M) {
+  return ((((size_t)(i >> 7) * 2 * W + s) * (size_t)(M >> 3) + (size_t)(j >> 3)) << 10) +
+         ((size_t)(i & 127) << 3) + (size_t)(j & 7);
+}
 size_t stream_sums_offset(int64_t n, int W, int M) {
-  return align_up((size_t)n * stream_pitch(W, M) * 2, 256);
+  const size_t tiles = (size_t)((n + 127) / 128);
+  return align_up(tiles * 128 * 2 * W * M * 2, 256);
 }
 size_t stream_ring_bytes(int64_t n, int W, int M) {
   return stream_sums_offset(n, W, M) + (size_t)n * sums_pitch(W) * 4;
@@ -678,11 +686,11 @@ __global__ void k_stream_push(__half *__restrict__ ring16, float *__restrict__ s
   const float4 *xs = reinterpret_cast<const float4 *>(sample + i * M);
   const float4 *ms = reinterpret_cast<const float4 *>(mean + i * M);
   const float4 *ss = reinterpret_cast<const float4 *>(stdv + i * M);
-  __half *r0 = ring16 + (size_t)i * stream_pitch(W, M) + (size_t)slot * M;   // [N][pitch]
-  __half *r1 = r0 + (size_t)W * M;
   float pg[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
+    __half *r0 = ring16 + stream_elem(i, slot, 4 * g, W, M);       // tiled canonical layout
+    __half *r1 = ring16 + stream_elem(i, slot + W, 4 * g, W, M);   // the mirror slot
     const float4 v = __ldg(xs + g), mu = __ldg(ms + g), sd = __ldg(ss + g);
     const float z0 = fminf(fmaxf(div_rn(__fsub_rn(v.x, mu.x), sd.x, __frcp_rn(sd.x)), -1e4f), 1e4f);
     const float z1 = fminf(fmaxf(div_rn(__fsub_rn(v.y, mu.y), sd.y, __frcp_rn(sd.y)), -1e4f), 1e4f);
@@ -691,8 +699,8 @@ __global__ void k_stream_push(__half *__restrict__ ring16, float *__restrict__ s
     uint2 pk;
     pk.x = cvt_pack_f16x2(z0, z1);
     pk.y = cvt_pack_f16x2(z2, z3);
-    *reinterpret_cast<uint2 *>(r0 + 4 * g) = pk;
-    *reinterpret_cast<uint2 *>(r1 + 4 * g) = pk;
+    *reinterpret_cast<uint2 *>(r0) = pk;
+    *reinterpret_cast<uint2 *>(r1) = pk;
     const float2 f01 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.x));
     const float2 f23 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.y));
     pg[g] = (f01.x + f01.y) + (f23.x + f23.y);
@@ -724,50 +732,13 @@ enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sampl
   return ENOVA_OK;
 }
 
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1,
-                                            uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1,
-                                            int c2, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// A ring of the stream kernel: stages of kSAK K-steps = one TMA box of
-// 64 fp16 (128 B, the SWIZZLE_128B atom width) x 128 instances = 16 KB.
+// A ring of the stream kernel: stages of kSAK K-steps = one 16 KB bulk copy of
+// the tile's contiguous canonical-layout range (4 x [2 halves][128 rows][16 B]).
 constexpr int kSAK = 4;
 constexpr int kSAStages = 8;
-constexpr int kSAWarp = 6;                        // A (TMA) producer warp (kCpAsyncA == false)
-// A operand loading of the stream kernel: true = the row threads copy their own
-// window with cp.async (LDGSTS, 16 B, kSADepth groups in flight per thread, manual
-// 128B swizzle); false = one TMA box per group from a producer warp.  Measured:
-// the TMA path paces the K loop at ~0.7 us per 4-K-step group (few boxes in
-// flight per SM), the cp.async path keeps 4x more bytes in flight.
-constexpr bool kCpAsyncA = false;
-constexpr int kSADepth = 4;
+constexpr int kSAWarp = 6;                        // A producer warp
 constexpr int kSThreads = kRThreads + 32;
 constexpr uint32_t kSAStageBytes = kRR * 128;
-
-// K-major SWIZZLE_128B smem descriptor (TMA CU_TENSOR_MAP_SWIZZLE_128B layout):
-// 8-row x 128-B swizzle atoms, SBO = 1024 B between 8-row groups, LBO unused;
-// the K=16 step j of an atom starts at +32 j bytes.
-__device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1 << 16;                    // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
-  d |= (uint64_t)1 << 46;                    // version
-  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
-  return d;
-}
 
 struct StreamParams {
   const float *sums;        // [N][2W] fp32 sample sums
@@ -832,11 +803,11 @@ __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i
   const float4 *xs = reinterpret_cast<const float4 *>(p.sample + i * M);
   const float4 *ms = reinterpret_cast<const float4 *>(p.mean + i * M);
   const float4 *ss = reinterpret_cast<const float4 *>(p.stdv + i * M);
-  __half *r0 = p.ring16 + (size_t)i * stream_pitch(W, M) + (size_t)slot * M;
-  __half *r1 = r0 + (size_t)W * M;
   float pg[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
+    __half *r0 = p.ring16 + stream_elem(i, slot, 4 * g, W, M);
+    __half *r1 = p.ring16 + stream_elem(i, slot + W, 4 * g, W, M);
     const float4 v = __ldg(xs + g), mu = __ldg(ms + g), sd = __ldg(ss + g);
     const float z0 = fminf(fmaxf(div_rn(__fsub_rn(v.x, mu.x), sd.x, __frcp_rn(sd.x)), -1e4f), 1e4f);
     const float z1 = fminf(fmaxf(div_rn(__fsub_rn(v.y, mu.y), sd.y, __frcp_rn(sd.y)), -1e4f), 1e4f);
@@ -845,8 +816,8 @@ __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i
     uint2 pk;
     pk.x = cvt_pack_f16x2(z0, z1);
     pk.y = cvt_pack_f16x2(z2, z3);
-    *reinterpret_cast<uint2 *>(r0 + 4 * g) = pk;
-    *reinterpret_cast<uint2 *>(r1 + 4 * g) = pk;
+    *reinterpret_cast<uint2 *>(r0) = pk;
+    *reinterpret_cast<uint2 *>(r1) = pk;
     const float2 f01 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.x));
     const float2 f23 = __half22float2(*reinterpret_cast<const __half2 *>(&pk.y));
     pg[g] = (f01.x + f01.y) + (f23.x + f23.y);
@@ -860,8 +831,7 @@ __device__ __forceinline__ void stream_push_one(const StreamParams &p, int64_t i
 }
 
 template <int H, int ZP>
-__global__ void __launch_bounds__(kSThreads, 1)
-    k_stream_rows(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+__global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams p) {
   constexpr int N2 = 2 * ZP;
   extern __shared__ __align__(1024) uint8_t smem[];
   const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
@@ -900,9 +870,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
       mbar_init(&B.w_empty[i], 1);
     }
     for (int i = 0; i < kRAStages; ++i) {
-      // TMA: the producer's expect_tx (the TMA completes the bytes); cp.async: one
+      // the producer's expect_tx (the bulk copy completes the bytes)
       // arrival per row warp
-      mbar_init(&B.a_full[i], kCpAsyncA ? kRowThreads / 32 : 1);
+      mbar_init(&B.a_full[i], 1);
       mbar_init(&B.a_empty[i], 1);
     }
     mbar_init(&B.wimg, 1);
@@ -928,9 +898,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
   const uint32_t tmem = B.tmem_slot;
 
   if (warp == kRProdWarp) {
-    // ---------------- producer: W1 ring (bulk) + A ring (TMA from the fp16 ring) ----------------
+    // ---------------- producer: W1 ring (bulk copies) ----------------
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       const uint32_t hb = (uint32_t)N2 * H * 2, w3b = (uint32_t)H * 16 * 2;
       mbar_arrive_expect_tx(&B.wimg, hb + w3b);
       bulk_g2s(heads, p.headsimg, hb, &B.wimg);
@@ -948,17 +917,19 @@ __global__ void __launch_bounds__(kSThreads, 1)
       }
     }
   } else if (warp == kSAWarp) {
-    // ---------------- A producer: one TMA box (kSAK K-steps x 128 instances) per group ----------------
-    if (!kCpAsyncA && p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
-    if (!kCpAsyncA && lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    // ---------------- A producer: one 16 KB bulk copy (kSAK K-steps x 128 instances) per group ----------------
+    if (p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
+    if (lane == 0) {
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+      // this tile's window: half-blocks woff M/8 + 2q, +1 of K-step q (2 KB each)
+      const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
+                            (((size_t)blockIdx.x * 2 * W + woff) * (size_t)(p.M >> 3) << 11);
       for (int g = 0; g < n_groups; ++g) {
         const int a = g % kSAStages;
         if (g >= kSAStages) mbar_wait_sleep(&B.a_empty[a], ((g / kSAStages) - 1) & 1, 64);
-        mbar_arrive_expect_tx(&B.a_full[a], kSAStageBytes);
-        tma_load_2d(astage + a * kSAStageBytes, &tmap, woff * p.M + 16 * kSAK * g, (int)row0,
-                    &B.a_full[a]);
+        const uint32_t bytes = (uint32_t)min(kSAK, p.nsteps - g * kSAK) * 4096u;
+        mbar_arrive_expect_tx(&B.a_full[a], bytes);
+        bulk_g2s(astage + a * kSAStageBytes, tsrc + (size_t)g * kSAStageBytes, bytes, &B.a_full[a]);
         if (g < 20) stamp(16 + g);
         if (g == 0) stamp(1);
         if (g == n_groups - 1) stamp(2);
@@ -976,7 +947,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
         mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
         tc_fence_after();
       }
-      const uint64_t ad = make_sdesc_sw128(aa + a * kSAStageBytes + j * 32);
+      // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
+      const uint64_t ad = make_sdesc(aa + a * kSAStageBytes + j * 4096, 2048, 128);
       const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
       mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
       if (lane == 0 && q == 0) stamp(3);
@@ -1020,7 +992,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const int r = tid;
     const int64_t row = row0 + r;
     const bool valid = row < p.n;
-    if (p.sample) {   // fused ingest of this tick's sample, visible to the TMA (async proxy)
+    if (p.sample) {   // fused ingest of this tick's sample, visible to the bulk copies (async proxy)
       if (valid) {
         switch (p.M) {
           case 8: stream_push_one<2>(p, row); break;
@@ -1029,38 +1001,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
           default: stream_push_one<16>(p, row); break;
         }
       }
-      if constexpr (kCpAsyncA) {
-        __threadfence_block();   // own pushed sample before this thread's cp.async reads
-      } else {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();   // reconverge after the per-row push
-        named_bar_sync_na(5, kRowThreads + 32);
-      }
-    }
-    // cp.async A loading: this row's window, group g = 64 fp16 (128 B) at element
-    // woff*M + 64 g, into stage (g % kSAStages) row r with the 128B swizzle
-    // (16-byte chunk c of row r at c ^ (r & 7); 8-row atoms 1 KB apart)
-    const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
-    const __half *asrc = p.ring16 + (size_t)(valid ? row : 0) * stream_pitch(W, p.M) + (size_t)woff * p.M;
-    const uint32_t adst_row = smem_u32(astage) + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
-    auto issue_group = [&](int g) {
-      const int a = g % kSAStages;
-      const uint32_t dst = adst_row + (uint32_t)a * kSAStageBytes;
-      const __half *src = asrc + 64 * g;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t d = dst + (uint32_t)((c ^ (r & 7)) * 16);
-        const int sz = valid ? 16 : 0;   // zero-fill rows past the fleet
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d),
-                     "l"(src + 8 * c), "r"(sz)
-                     : "memory");
-      }
-    };
-    if constexpr (kCpAsyncA) {
-      for (int g = 0; g < kSADepth; ++g) {
-        if (g < n_groups) issue_group(g);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // pushes -> the bulk copies
+      __syncwarp();   // reconverge after the per-row push
+      named_bar_sync_na(5, kRowThreads + 32);
     }
     const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
     WinSum ws;
@@ -1077,21 +1020,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
       for (int k = 0; k < 17; ++k)
         sv4[k] = (valid && 4 * k < wsh + W) ? __ldg(sp4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    if constexpr (kCpAsyncA) {
-      for (int g = 0; g < n_groups; ++g) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kSADepth - 1) : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&B.a_full[g % kSAStages]);
-        if (r == 0 && g < 20) stamp(16 + g);
-        const int nx = g + kSADepth;
-        if (nx < n_groups) {
-          if (nx >= kSAStages) mbar_wait(&B.a_empty[nx % kSAStages], ((nx / kSAStages) - 1) & 1);
-          issue_group(nx);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
     }
     // (reduced only before E3, where MD needs it: off the E1 / E2 critical path)
     auto sx_fn = [&]() -> float {
@@ -1138,21 +1066,9 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
                            float *md, cudaStream_t st, const float *sample = nullptr,
                            const float *mean = nullptr, const float *stdv = nullptr);
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
-  return fn;
-}
 
 template <int H, int ZP>
-static enova_status launch_stream_t(const CUtensorMap &tm, const StreamParams &p, cudaStream_t st) {
+static enova_status launch_stream_t(const StreamParams &p, cudaStream_t st) {
   const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
   auto kern = k_stream_rows<H, ZP>;
   static thread_local int cached_dev = -1;
@@ -1167,7 +1083,7 @@ static enova_status launch_stream_t(const CUtensorMap &tm, const StreamParams &p
     set_error("too many instances for one launch");
     return ENOVA_ERR_UNSUPPORTED;
   }
-  ENOVA_LAUNCH(kern, (unsigned)tiles, kSThreads, SL.total, st, tm, p);
+  ENOVA_LAUNCH(kern, (unsigned)tiles, kSThreads, SL.total, st, p);
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }
@@ -1177,24 +1093,7 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
                            float *md, cudaStream_t st, const float *sample,
                            const float *mean, const float *stdv) {
   if (n == 0) return ENOVA_OK;
-  auto enc = tensor_map_encoder();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable from the driver");
-    return ENOVA_ERR_CUDA;
-  }
   const int W = L.W, M = L.M;
-  CUtensorMap tm;   // [instance N][2W*M] fp16; box = 64 K-elements (128 B) x 128 instances
-  const cuuint64_t dims[2] = {(cuuint64_t)stream_pitch(W, M), (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)(stream_pitch(W, M) * 2)};
-  const cuuint32_t box[2] = {16 * kSAK, (cuuint32_t)kRR};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ring), dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed for the stream ring");
-    return ENOVA_ERR_CUDA;
-  }
   StreamParams p{};
   const uint8_t *b = static_cast<const uint8_t *>(det_ws);
   p.sums = reinterpret_cast<const float *>(static_cast<const uint8_t *>(ring) +
@@ -1225,12 +1124,12 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
   p.ring16 = const_cast<__half *>(static_cast<const __half *>(ring));
   p.sums_w = const_cast<float *>(p.sums);
   switch (L.H * 100 + L.ZP) {
-    case 3208: return launch_stream_t<32, 8>(tm, p, st);
-    case 3216: return launch_stream_t<32, 16>(tm, p, st);
-    case 6408: return launch_stream_t<64, 8>(tm, p, st);
-    case 6416: return launch_stream_t<64, 16>(tm, p, st);
-    case 12808: return launch_stream_t<128, 8>(tm, p, st);
-    case 12816: return launch_stream_t<128, 16>(tm, p, st);
+    case 3208: return launch_stream_t<32, 8>(p, st);
+    case 3216: return launch_stream_t<32, 16>(p, st);
+    case 6408: return launch_stream_t<64, 8>(p, st);
+    case 6416: return launch_stream_t<64, 16>(p, st);
+    case 12808: return launch_stream_t<128, 8>(p, st);
+    case 12816: return launch_stream_t<128, 16>(p, st);
   }
   set_error("unsupported (H, Z)");
   return ENOVA_ERR_UNSUPPORTED;
