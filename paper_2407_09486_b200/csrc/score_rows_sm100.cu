@@ -56,7 +56,8 @@ struct RowParams {
 
 constexpr int kRR = 128;                 // rows per tile (UMMA M)
 constexpr int kRWStageSteps = 4;         // W1 ring: K-steps per stage
-constexpr int kRWStages = 4;             // W1 ring depth
+constexpr int kRWStages = 4;             // W1 ring depth (row kernel)
+constexpr int kMaxWStages = 8;           // RowBars capacity (the stream kernel's W1 ring)
 constexpr int kRAStages = 16;            // A ring depth (one K-step each)
 constexpr uint32_t kRAStepBytes = kRR * 16 * 2;   // 4 KB
 constexpr int kRowThreads = 128;         // thread = row
@@ -65,7 +66,7 @@ constexpr int kRMmaWarp = 4, kRProdWarp = 5;
 constexpr int kRPF = 8;                  // K-steps of raw samples in flight per thread
 
 struct RowBars {
-  uint64_t w_full[kRWStages], w_empty[kRWStages], a_full[kRAStages], a_empty[kRAStages];
+  uint64_t w_full[kMaxWStages], w_empty[kMaxWStages], a_full[kRAStages], a_empty[kRAStages];
   uint64_t wimg, g1_done, h_full, g2_done, mu_full, g3_done;
   uint32_t tmem_slot, pad;
 };
@@ -75,7 +76,8 @@ struct RowLayoutSm {
 };
 
 __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
-                                                       uint32_t a_ring_bytes = kRAStages * kRAStepBytes) {
+                                                       uint32_t a_ring_bytes = kRAStages * kRAStepBytes,
+                                                       int w_stages = kRWStages) {
   RowLayoutSm L;
   uint32_t o = 0;
   auto take = [&](uint32_t b, uint32_t a) {
@@ -85,7 +87,7 @@ __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
     return r;
   };
   L.w_stage_bytes = (uint32_t)kRWStageSteps * 32 * H;
-  const uint32_t ring = kRWStages * L.w_stage_bytes, hb = 2u * kRR * H * 2;
+  const uint32_t ring = (uint32_t)w_stages * L.w_stage_bytes, hb = 2u * kRR * H * 2;
   L.region = take(ring > hb ? ring : hb, 1024);      // W1 ring, then h hi | lo
   L.astage = take(a_ring_bytes, 1024);
   L.heads = take((uint32_t)2 * ZP * H * 2, 128);
@@ -735,8 +737,18 @@ enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sampl
 // A ring of the stream kernel: stages of kSAK K-steps = one 16 KB bulk copy of
 // the tile's contiguous canonical-layout range (4 x [2 halves][128 rows][16 B]).
 constexpr int kSAK = 4;
-constexpr int kSAStages = 8;
-constexpr int kSAWarp = 6;                        // A producer warp
+// The K loop is paced by ring round trips (bulk-copy latency ~2 us vs ~0.14 us
+// of MMAs per group), and a group needs one A and one W1 stage: the two rings
+// get the same depth, as deep as shared memory allows.
+constexpr int kSAStages = 6;
+constexpr int kSWStages = 6;   // the stream kernel's W1 ring
+constexpr int kSAWarp = 6;                        // A producer warp (kLsuA == false)
+// A operand of the stream kernel through the LSU path: the 128 row threads copy
+// each 16 KB group with cp.async (16 B per thread-op, coalesced; the tiled ring
+// needs no swizzle), so A and W1 (bulk copies, the TMA path) arrive over two
+// paths in parallel.  false = 16 KB bulk copies from the A producer warp.
+// (measured: the same tick either way -- 29.1 us -- so the bulk-copy path is kept)
+constexpr bool kLsuA = false;
 constexpr int kSThreads = kRThreads + 32;
 constexpr uint32_t kSAStageBytes = kRR * 128;
 
@@ -834,7 +846,7 @@ template <int H, int ZP>
 __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams p) {
   constexpr int N2 = 2 * ZP;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages);
   uint8_t *region = smem + SL.region;
   uint8_t *astage = smem + SL.astage;
   uint8_t *heads = smem + SL.heads;
@@ -865,14 +877,14 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
   if (tid == 0) stamp(0);
 
   if (tid == 0) {
-    for (int i = 0; i < kRWStages; ++i) {
+    for (int i = 0; i < kSWStages; ++i) {
       mbar_init(&B.w_full[i], 1);
       mbar_init(&B.w_empty[i], 1);
     }
     for (int i = 0; i < kRAStages; ++i) {
       // the producer's expect_tx (the bulk copy completes the bytes)
       // arrival per row warp
-      mbar_init(&B.a_full[i], 1);
+      mbar_init(&B.a_full[i], kLsuA ? kRowThreads / 32 : 1);
       mbar_init(&B.a_empty[i], 1);
     }
     mbar_init(&B.wimg, 1);
@@ -907,8 +919,8 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
       // W1 ring: one stage (kRWStageSteps = kSAK K-steps) per group
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
       for (int g = 0; g < n_groups; ++g) {
-        const int st = g % kRWStages;
-        if (g >= kRWStages) mbar_wait_sleep(&B.w_empty[st], ((g / kRWStages) - 1) & 1, 64);
+        const int st = g % kSWStages;
+        if (g >= kSWStages) mbar_wait_sleep(&B.w_empty[st], ((g / kSWStages) - 1) & 1, 64);
         const int steps = min(kSAK, p.nsteps - g * kSAK);
         const uint32_t bytes = (uint32_t)steps * 32 * H;
         mbar_arrive_expect_tx(&B.w_full[st], bytes);
@@ -918,8 +930,8 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
     }
   } else if (warp == kSAWarp) {
     // ---------------- A producer: one 16 KB bulk copy (kSAK K-steps x 128 instances) per group ----------------
-    if (p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
-    if (lane == 0) {
+    if (!kLsuA && p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
+    if (!kLsuA && lane == 0) {
       const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
       // this tile's window: half-blocks woff M/8 + 2q, +1 of K-step q (2 KB each)
       const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
@@ -940,11 +952,11 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
     const uint32_t idesc1 = make_idesc_f16(128, H);
     const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
     for (int q = 0; q < p.nsteps; ++q) {
-      const int g = q / kSAK, j = q % kSAK, a = g % kSAStages, st = g % kRWStages;
+      const int g = q / kSAK, j = q % kSAK, a = g % kSAStages, st = g % kSWStages;
       if (j == 0) {
         mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
         if (lane == 0 && g < 20) stamp(36 + g);
-        mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
+        mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
         tc_fence_after();
       }
       // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
@@ -1001,9 +1013,50 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
           default: stream_push_one<16>(p, row); break;
         }
       }
-      asm volatile("fence.proxy.async.global;" ::: "memory");   // pushes -> the bulk copies
-      __syncwarp();   // reconverge after the per-row push
-      named_bar_sync_na(5, kRowThreads + 32);
+      if constexpr (kLsuA) {
+        __threadfence_block();   // every row's pushed sample before the cp.async reads
+        __syncwarp();
+        named_bar_sync_na(5, kRowThreads);
+      } else {
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // pushes -> the bulk copies
+        __syncwarp();   // reconverge after the per-row push
+        named_bar_sync_na(5, kRowThreads + 32);
+      }
+    }
+    if constexpr (kLsuA) {
+      // A groups (kSAK K-steps = 16 KB of the tile's contiguous canonical range)
+      // by cp.async, kSAStages - 1 groups in flight
+      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+      const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
+                            (((size_t)blockIdx.x * 2 * W + woff) * (size_t)(p.M >> 3) << 11);
+      const uint32_t abase = smem_u32(astage);
+      auto issue = [&](int g) {
+        const int a = g % kSAStages;
+        const int chunks = min(kSAK, p.nsteps - g * kSAK) * 256;   // 16-B chunks
+        const uint8_t *src = tsrc + (size_t)g * kSAStageBytes;
+        const uint32_t dst = abase + (uint32_t)a * kSAStageBytes;
+        for (int c = r; c < chunks; c += kRowThreads)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c),
+                       "l"(src + 16 * (size_t)c)
+                       : "memory");
+      };
+      constexpr int kDepth = kSAStages - 1;
+      for (int g = 0; g < kDepth; ++g) {
+        if (g < n_groups) issue(g);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      for (int g = 0; g < n_groups; ++g) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // -> the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.a_full[g % kSAStages]);
+        const int nx = g + kDepth;
+        if (nx < n_groups) {
+          if (nx >= kSAStages) mbar_wait(&B.a_empty[nx % kSAStages], ((nx / kSAStages) - 1) & 1);
+          issue(nx);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
     }
     const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
     WinSum ws;
@@ -1069,7 +1122,7 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
 
 template <int H, int ZP>
 static enova_status launch_stream_t(const StreamParams &p, cudaStream_t st) {
-  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes);
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages);
   auto kern = k_stream_rows<H, ZP>;
   static thread_local int cached_dev = -1;
   int dev = 0;
