@@ -926,6 +926,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
         mbar_arrive_expect_tx(&B.w_full[st], bytes);
         bulk_g2s(region + st * SL.w_stage_bytes, p.w1img + (size_t)g * SL.w_stage_bytes, bytes,
                  &B.w_full[st]);
+        if (g < 16) stamp(56 + g);
       }
     }
   } else if (warp == kSAWarp) {
@@ -957,6 +958,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
         mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
         if (lane == 0 && g < 20) stamp(36 + g);
         mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
+        if (lane == 0 && g < 16) stamp(72 + g);
         tc_fence_after();
       }
       // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]

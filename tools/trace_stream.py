@@ -45,3 +45,5 @@ for i, nm in enumerate(names):
 print("A TMA issued (us):", " ".join(f"{(t[16 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
 print("A ready at MMA (us):", " ".join(f"{(t[36 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
 
+print("W1 stage issued (us):", " ".join(f"{(t[56 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
+print("W1 ready at MMA (us):", " ".join(f"{(t[72 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
