@@ -506,8 +506,7 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
   const int64_t sub = ((len + kPotWarps - 1) / kPotWarps + 3) / 4 * 4;
   const int64_t w0 = min(len, (int64_t)warp * sub), w1 = min(len, w0 + sub);
   float *wdst = dst + w0;
-  long long cnt = 0;   // warp-uniform
-  int below = 0;       // per lane (< 2^31: at most a sub-range)
+  long long cnt = 0;   // warp-uniform; the warp's keys below lo = its range - cnt
   // the leading nv (0..4) elements of q, in index order after the lower lanes'
   auto put4 = [&](const float4 q, int nv) {
     const float e4[4] = {q.x, q.y, q.z, q.w};
@@ -522,10 +521,8 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
     long long o = cnt + __popc(bl[0] & lt) + __popc(bl[1] & lt) + __popc(bl[2] & lt) +
                   __popc(bl[3] & lt);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 4; ++e)
       if (c[e]) wdst[o++] = e4[e];
-      below += (e < nv && !c[e]);
-    }
     cnt += __popc(bl[0]) + __popc(bl[1]) + __popc(bl[2]) + __popc(bl[3]);
   };
   const bool al = (reinterpret_cast<uintptr_t>(src + w0) & 15) == 0;
@@ -563,11 +560,9 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
     q.w = i + 3 < w1 ? __ldg(src + i + 3) : 0.f;
     put4(q, (int)max((int64_t)0, min((int64_t)4, w1 - i)));
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
   if (lane == 0) {
     wcount[warp] = cnt;
-    wbelow[warp] = below;
+    wbelow[warp] = (w1 - w0) - cnt;
   }
   __syncthreads();
   // runs -> one contiguous, index-ordered segment.  Common case (the CTA's
