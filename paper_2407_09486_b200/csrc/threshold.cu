@@ -56,7 +56,19 @@ constexpr int kSums = 6;              // P, L, dP, dL, d2P, d2L per evaluation p
 constexpr double kCertRel = 5e-12;
 
 enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_GRIDFIX = 5,
-       PH_GRIDBIN = 6 };
+       PH_GRIDBIN = 6, PH_BREFINE = 7 };
+// Large tails: before the fp64 (certifying) Halley passes over Y, each bracket's
+// root is located by up to kMaxBinRefine Halley passes over the bins (PH_BREFINE:
+// w and its derivatives from the binned sums, the iterate kept inside the fp64
+// bracket; no sign of a binned w is trusted).  The exact passes then start within
+// the binned model's error (~1e-8 relative) of the root: one Halley step lands
+// within rounding of it and the next pass certifies it -- two passes over Y
+// instead of five from the grid's secant point.
+constexpr int kMaxBinRefine = 4;
+// evaluation sums per point of a pass: P, L (+ first and second derivatives)
+__device__ __forceinline__ int phase_sums(int phase) {
+  return (phase == PH_REFINE || phase == PH_BREFINE) ? kSums : 2;
+}
 // Large tails (N_t >= kGrid32MinPeaks): the 128-point scan grid is evaluated in
 // two passes (PH_GRID32, PH_GRIDBIN) -- points with |x| Ymax <= 1e-3 from six
 // fp64 power sums of Y/Ymax (the log1p and 1/(1+t) series, 1e-18 truncation),
@@ -68,10 +80,10 @@ enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_
 // the sums even at x Ymax = -0.9) -- and an error bound: a sign is accepted when
 // |w| > 1e-6 (|P| + |L| + |P L|), else that point is re-evaluated in fp64 over
 // Y (PH_GRIDFIX).  The signs, hence the brackets, are those of the fp64 scan
-// wherever the fp64 scan itself resolves them; the Halley refinement that
-// follows is fp64 over Y as before.
+// wherever the fp64 scan itself resolves them; the binned Halley passes
+// (PH_BREFINE) only place the start of the certifying fp64 passes over Y.
 constexpr int64_t kGrid32MinPeaks = 100000;
-constexpr int kMaxBins = 131072;          // binned grid pass: bins of log2(Y) (x3 fp64 each)
+constexpr int kMaxBins = 131072;          // binned grid pass: bins of log2(Y) (x3 int64 each)
 constexpr double kBinsPerOctave = 2048.0;
 constexpr int kPow = 6;   // power sums of u = Y / Ymax for the series points
 // phase program of k_pot
@@ -128,10 +140,14 @@ struct FitState {
   double bin_l0, bin_k;       // PH_GRIDBIN: bin b holds log2(Y) in [l0 + b/k, l0 + (b+1)/k)
   int nbins;
   int triple;                 // REFINE evaluates (x, x(1-d), x(1+d)) per root (certifying)
+  int bin_cl;                 // ceil(log2(N_t + 1)): fixed-point headroom of the bin sums
+  int use_bins;               // the bins are filled (N_t >= kGrid32MinPeaks): PH_BREFINE first
+  int biters, pad_b;          // PH_BREFINE passes run
   int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
   int exact[kMaxSlots];
   int refine_idx[kMaxSlots];
+  double lfin[kMaxSlots];     // L at a slot's certified root, when the last refine pass evaluated it
   double gamma, sigma, z_q;
 };
 
@@ -139,7 +155,7 @@ struct ThrLayout {
   size_t glob, hist, counts, part, nbuf, counts_all, ylocal, yslot, outdev, yall, header, total;
   size_t shist, cand, cand_n;   // sampled selection: sample histograms, candidates, per-CTA counts
   size_t fstate, xsend, xrecv;  // distributed fit (communicator layouts)
-  size_t bins;                  // binned grid pass: [kMaxBins][3] fp64 (count, sum, sum of squares)
+  size_t bins;                  // binned passes: [kMaxBins][3] int64 (count, fixed-point sums, see bin_add)
   bool has_bins;
   int64_t cap;
   bool sampled;                 // workspace holds the candidate buffer
@@ -214,7 +230,7 @@ struct PotArgs {
   double *xsend;            // [kSums * kMaxPts] this rank's totals of the step
   const double *xrecv;      // [world][kSums * kMaxPts] gathered totals
   FitState *fstate;         // the fit's state between launches
-  double *bins;             // [kMaxBins][3] binned grid pass (null below kGrid32MinPeaks)
+  unsigned long long *bins; // [kMaxBins][3] binned grid pass (null below kGrid32MinPeaks)
 };
 
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -485,16 +501,28 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
 // P_SCAN: the one full pass over this CTA's chunk -- count the keys below lo,
 // compact the rest (the candidates) stably (index order) into the CTA's segment
 // a.cand + blockIdx.x * seg_cap.  Warp w owns a contiguous sub-range of the
-// chunk, streams it with two ping-ponged register batches of 4 x 128-bit loads
-// per lane (8 in flight) and appends its candidates to its own region
-// [w * sub, ...) of the segment: four ballots per batch slot give every lane
-// its output offset (no shuffle scans, no CTA barrier in the loop; measured
-// 3.4 TB/s vs 2.6 TB/s for a shuffle-scan compaction at one CTA per SM,
-// tools/ubench_scan.cu).  The runs are then moved down to their final,
-// contiguous positions in warp order (destination <= source, read before write).
+// chunk and streams it with two ping-ponged register batches of 4 x 128-bit
+// loads per lane (8 in flight, no CTA barrier in the loop).  Its candidates go
+// to its own run: a slice of the shared staging buffer while they fit (plain
+// shared-memory stores), else -- after one copy of what the slice holds -- its
+// region [w * sub, ...) of the global segment.  When every run stayed in shared
+// memory the warps write them straight to their final offsets (coalesced);
+// otherwise the runs are moved down in warp order (destination <= source, each
+// chunk read before it is written).
+//
+// Output offsets.  Fast path (lo >= 2^31: lo is the key of a float >= +0, the
+// case of every score the detector emits): key(v) >= lo <=> (int)bits(v) >=
+// (int)(lo ^ 2^31) for every bit pattern (negative floats and negative NaNs are
+// negative ints with keys < 2^31 <= lo; positive NaNs are candidates both ways),
+// one integer compare per element; the per-float4 candidate counts of a batch
+// (0..4 each) travel packed in the bytes of one word through ONE warp inclusive
+// scan (a byte's prefix <= 128), giving every lane its offset in (float4 slot,
+// lane, element) = index order.  General path and ragged tails: four ballots per
+// float4 on the keys.
 __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, long long *out_n,
                            float *stage, int stage_cap) {
   __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
+  __shared__ int wspill[kPotWarps];
   int64_t b0, b1;
   score_chunk(a.n_local, &b0, &b1);
   const float *src = a.scores + b0;
@@ -505,10 +533,22 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
   // warp sub-ranges: multiples of 4 scores (16 B aligned when the chunk is)
   const int64_t sub = ((len + kPotWarps - 1) / kPotWarps + 3) / 4 * 4;
   const int64_t w0 = min(len, (int64_t)warp * sub), w1 = min(len, w0 + sub);
-  float *wdst = dst + w0;
-  long long cnt = 0;   // warp-uniform; the warp's keys below lo = its range - cnt
+  unsigned int *wd = reinterpret_cast<unsigned int *>(dst + w0);   // the warp's global region
+  const int wcap = stage_cap / kPotWarps;
+  unsigned int *ws = reinterpret_cast<unsigned int *>(stage) + (size_t)warp * wcap;   // its smem slice
+  bool insm = true;   // warp-uniform: the run is in the smem slice
+  long long cnt = 0;  // warp-uniform; the warp's keys below lo = its range - cnt
+  // before appending up to `more` candidates: leave the smem slice if they may not fit
+  auto reserve = [&](long long more) {
+    if (insm && cnt + more > (long long)wcap) {
+      for (long long i = lane; i < cnt; i += 32) wd[i] = ws[i];
+      __syncwarp();
+      insm = false;
+    }
+  };
   // the leading nv (0..4) elements of q, in index order after the lower lanes'
   auto put4 = [&](const float4 q, int nv) {
+    reserve(128);
     const float e4[4] = {q.x, q.y, q.z, q.w};
     bool c[4];
     unsigned int bl[4];
@@ -520,14 +560,83 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
     // lanes below l hold 4 elements each before this lane's first one
     long long o = cnt + __popc(bl[0] & lt) + __popc(bl[1] & lt) + __popc(bl[2] & lt) +
                   __popc(bl[3] & lt);
+    unsigned int *out = insm ? ws : wd;
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (c[e]) wdst[o++] = e4[e];
+      if (c[e]) out[o++] = __float_as_uint(e4[e]);
     cnt += __popc(bl[0]) + __popc(bl[1]) + __popc(bl[2]) + __popc(bl[3]);
   };
   const bool al = (reinterpret_cast<uintptr_t>(src + w0) & 15) == 0;
   int64_t tail0 = w0;
-  if (al) {
+  if (al && lo >= 0x80000000u && (w1 - w0) / 4 < 0x40000000) {
+    const int lo_i = (int)(lo ^ 0x80000000u);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(src + w0);
+    const int nfull = (int)(((w1 - w0) / 4) & ~(int64_t)127);   // full batches of 4 x 32 float4
+    unsigned int c32 = 0;   // warp-uniform candidate count (< 2^32: the range is)
+    auto ld = [&](uint4 (&v)[4], int i0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(x4 + i0 + u * 32 + lane);
+    };
+    auto proc = [&](const uint4 (&v)[4]) {
+      unsigned int m[4], pk = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        m[u] = ((int)v[u].x >= lo_i ? 1u : 0u) | ((int)v[u].y >= lo_i ? 2u : 0u) |
+               ((int)v[u].z >= lo_i ? 4u : 0u) | ((int)v[u].w >= lo_i ? 8u : 0u);
+        pk += (unsigned int)__popc(m[u]) << (8 * u);
+      }
+      unsigned int sc = pk;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, sc, d);
+        if (lane >= d) sc += t;
+      }
+      const unsigned int tot = __shfl_sync(0xffffffffu, sc, 31), ex = sc - pk;
+      if (tot == 0) return;   // no candidate in the batch (warp-uniform)
+      cnt = c32;
+      reserve((long long)(tot & 0xffu) + ((tot >> 8) & 0xffu) + ((tot >> 16) & 0xffu) + (tot >> 24));
+      unsigned int b = c32;
+      if (insm) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (m[u]) {
+            unsigned int *bp = ws + b + ((ex >> (8 * u)) & 0xffu);
+            if (m[u] & 1u) *bp++ = v[u].x;
+            if (m[u] & 2u) *bp++ = v[u].y;
+            if (m[u] & 4u) *bp++ = v[u].z;
+            if (m[u] & 8u) *bp = v[u].w;
+          }
+          b += (tot >> (8 * u)) & 0xffu;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (m[u]) {
+            unsigned int *bp = wd + b + ((ex >> (8 * u)) & 0xffu);
+            if (m[u] & 1u) *bp++ = v[u].x;
+            if (m[u] & 2u) *bp++ = v[u].y;
+            if (m[u] & 4u) *bp++ = v[u].z;
+            if (m[u] & 8u) *bp = v[u].w;
+          }
+          b += (tot >> (8 * u)) & 0xffu;
+        }
+      }
+      c32 = b;
+    };
+    if (nfull > 0) {
+      uint4 va[4], vb[4];
+      ld(va, 0);
+      for (int i0 = 0; i0 < nfull; i0 += 256) {   // warp-uniform trip count
+        const bool hb = i0 + 128 < nfull;
+        if (hb) ld(vb, i0 + 128);
+        proc(va);
+        if (i0 + 256 < nfull) ld(va, i0 + 256);
+        if (hb) proc(vb);
+      }
+    }
+    cnt = c32;
+    tail0 = w0 + 4 * (int64_t)nfull;
+  } else if (al) {
     const float4 *x4 = reinterpret_cast<const float4 *>(src + w0);
     const int64_t n4 = (w1 - w0) / 4;
     auto ld = [&](float4 (&v)[4], int64_t i0) {
@@ -563,37 +672,48 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
   if (lane == 0) {
     wcount[warp] = cnt;
     wbelow[warp] = (w1 - w0) - cnt;
+    wspill[warp] = insm ? 0 : 1;
   }
   __syncthreads();
-  // runs -> one contiguous, index-ordered segment.  Common case (the CTA's
-  // candidates fit the staging smem): every warp copies its run to its final
-  // offset in shared memory at once, then the CTA writes the segment back
-  // (parallel, no dependent round trips).  Otherwise the runs are moved down in
-  // warp order, 512 threads per chunk, each chunk read before it is written
-  // (destination <= source).
   long long pos = 0, mypos = 0;
+  int spilled = 0;
   for (int w = 0; w < kPotWarps; ++w) {
     if (w == warp) mypos = pos;
     pos += wcount[w];
+    spilled |= wspill[w];
   }
-  if (pos <= (long long)stage_cap) {
-    const float *from = dst + (int64_t)warp * sub;
-    for (long long i = lane; i < cnt; i += 32) stage[mypos + i] = from[i];
-    __syncthreads();
-    for (long long i = threadIdx.x; i < pos; i += blockDim.x) dst[i] = stage[i];
+  if (!spilled) {
+    // every run in shared memory: each warp writes its run at its final offset
+    float *to = dst + mypos;
+    for (long long i = lane; i < cnt; i += 32) to[i] = __uint_as_float(ws[i]);
   } else {
-    long long p2 = wcount[0];
-    for (int w = 1; w < kPotWarps; ++w) {
-      const long long c = wcount[w];
-      const float *from = dst + (int64_t)w * sub;
-      float *to = dst + p2;
-      for (long long i = 0; i < c; i += blockDim.x) {
-        const float v = (i + threadIdx.x < c) ? from[i + threadIdx.x] : 0.f;
-        __syncthreads();
-        if (i + threadIdx.x < c) to[i + threadIdx.x] = v;
-        __syncthreads();
+    // runs -> the global regions [w * sub, ...) first, then one contiguous,
+    // index-ordered segment.  Common case (the CTA's candidates fit the staging
+    // smem): every warp copies its run to its final offset in shared memory at
+    // once, then the CTA writes the segment back.  Otherwise the runs are moved
+    // down in warp order, each chunk read before it is written.
+    if (insm)
+      for (long long i = lane; i < cnt; i += 32) wd[i] = ws[i];
+    __syncthreads();   // every run in global memory; the smem slices are free
+    if (pos <= (long long)stage_cap) {
+      const float *from = dst + (int64_t)warp * sub;
+      for (long long i = lane; i < cnt; i += 32) stage[mypos + i] = from[i];
+      __syncthreads();
+      for (long long i = threadIdx.x; i < pos; i += blockDim.x) dst[i] = stage[i];
+    } else {
+      long long p2 = wcount[0];
+      for (int w = 1; w < kPotWarps; ++w) {
+        const long long c = wcount[w];
+        const float *from = dst + (int64_t)w * sub;
+        float *to = dst + p2;
+        for (long long i = 0; i < c; i += blockDim.x) {
+          const float v = (i + threadIdx.x < c) ? from[i + threadIdx.x] : 0.f;
+          __syncthreads();
+          if (i + threadIdx.x < c) to[i + threadIdx.x] = v;
+          __syncthreads();
+        }
+        p2 += c;
       }
-      p2 += c;
     }
   }
   if (threadIdx.x == 0) {
@@ -929,12 +1049,15 @@ __device__ void controller(FitState *f, int *scratch) {
       for (int w = 0; w < kMaxPts / 32; ++w) nr += scratch[16 + w];
     }
     const bool triple = 3 * nr <= kMaxPts;
+    const bool bref = f->use_bins && nr > 0;   // binned Halley passes first
     if (br && off_h < kMaxSlots) {
       f->refine_idx[off_b] = off_h;
       f->rdone[off_b] = 0;
       double x0 = xk - wk * (xk1 - xk) / (wk1 - wk);   // first iterate: secant point
       if (!(x0 > fmin(xk, xk1) && x0 < fmax(xk, xk1))) x0 = 0.5 * (xk + xk1);
-      if (triple) {
+      if (bref) {
+        f->xs[off_b] = x0;
+      } else if (triple) {
         f->xs[3 * off_b] = x0;
         f->xs[3 * off_b + 1] = x0 * (1.0 - kCertRel);
         f->xs[3 * off_b + 2] = x0 * (1.0 + kCertRel);
@@ -950,8 +1073,46 @@ __device__ void controller(FitState *f, int *scratch) {
       f->nrefine = nr;
       f->triple = triple ? 1 : 0;
       f->converged = (nr == 0) ? 1 : 0;
-      f->npts = (nr > 0) ? (triple ? 3 * nr : nr) : ns;
-      f->phase = (nr > 0) ? PH_REFINE : PH_FINAL;
+      f->npts = (nr > 0) ? ((triple && !bref) ? 3 * nr : nr) : ns;
+      f->phase = (nr > 0) ? (bref ? PH_BREFINE : PH_REFINE) : PH_FINAL;
+      f->biters = 0;
+    }
+    __syncthreads();
+    return;
+  }
+  if (phase == PH_BREFINE) {
+    // binned Halley step per bracket, kept inside the (fp64-certified) bracket;
+    // after convergence to the binned model (or kMaxBinRefine passes) the
+    // iterates start the exact passes
+    const int nr = f->nrefine, it = f->biters;
+    bool conv = true;
+    double xn = 0.0;
+    if (tid < nr) {
+      const int sidx = f->refine_idx[tid];
+      const double x = f->xs[tid], w = f->w[tid], dw = f->dw[tid], ddw = f->ddw[tid];
+      const double a = fmin(f->lo[sidx], f->hi[sidx]), b = fmax(f->lo[sidx], f->hi[sidx]);
+      const double den = 2.0 * dw * dw - w * ddw;
+      xn = (den != 0.0 && isfinite(den)) ? x - 2.0 * w * dw / den : (dw != 0.0 ? x - w / dw : x);
+      if (!(xn > a && xn < b)) xn = (xn <= a) ? 0.5 * (x + a) : 0.5 * (x + b);
+      conv = fabs(xn - x) <= 1e-10 * fabs(x);
+    }
+    const int all_conv = __syncthreads_and(conv);   // every read of xs / w done
+    const bool done = all_conv || it + 1 >= kMaxBinRefine;
+    if (tid < nr) {
+      if (done && f->triple) {
+        f->xs[3 * tid] = xn;
+        f->xs[3 * tid + 1] = xn * (1.0 - kCertRel);
+        f->xs[3 * tid + 2] = xn * (1.0 + kCertRel);
+      } else {
+        f->xs[tid] = xn;
+      }
+    }
+    if (tid == 0) {
+      f->biters = it + 1;
+      if (done) {
+        f->phase = PH_REFINE;
+        f->npts = f->triple ? 3 * nr : nr;
+      }
     }
     __syncthreads();
     return;
@@ -961,12 +1122,13 @@ __device__ void controller(FitState *f, int *scratch) {
     // certification: opposite signs of w at x(1 -+ d) put the root within
     // 2 d |x| = 1e-11 |x| of x in the SAME pass that found it.
     const int nr = f->nrefine, iters = f->iters;
-    bool conv = true;
+    bool conv = true, at_centre = true;
     int sidx = 0;
     double xfin = 0.0;
     if (tid < nr) {
       sidx = f->refine_idx[tid];
       const double x = f->xs[3 * tid];
+      const double lc = f->L[3 * tid];
       xfin = x;
       if (!f->rdone[tid]) {
         const double w = f->w[3 * tid], dw = f->dw[3 * tid], ddw = f->ddw[3 * tid];
@@ -1004,6 +1166,8 @@ __device__ void controller(FitState *f, int *scratch) {
         if (done) {
           f->rdone[tid] = 1;
           f->xs[3 * tid] = xfin;
+          at_centre = (xfin == x);
+          f->lfin[sidx] = lc;
         } else {
           const double den = 2.0 * dw * dw - w * ddw;
           double xn = (den != 0.0 && isfinite(den)) ? x - 2.0 * w * dw / den
@@ -1015,14 +1179,22 @@ __device__ void controller(FitState *f, int *scratch) {
           f->xs[3 * tid + 2] = xn * (1.0 + kCertRel);
           conv = false;
         }
+      } else {
+        f->lfin[sidx] = lc;   // certified in an earlier pass: x is its root, evaluated again
       }
     }
     const int all_conv = __syncthreads_and(conv);
     const bool done = all_conv || iters + 1 >= kMaxRefinePasses;
+    // every slot a refined root whose certified x is the centre point this pass
+    // evaluated: L at the roots is known, the FINAL pass over Y is skipped
+    const bool fused = __syncthreads_and(at_centre) && all_conv && nr == f->nslots;
     if (done) {
       if (tid < nr) f->lo[sidx] = f->xs[3 * tid];
       __syncthreads();
-      if (tid < f->nslots) f->xs[tid] = f->lo[tid];
+      if (tid < f->nslots) {
+        f->xs[tid] = f->lo[tid];
+        if (fused) f->L[tid] = f->lfin[tid];
+      }
     }
     if (tid == 0) {
       f->iters = iters + 1;
@@ -1033,7 +1205,8 @@ __device__ void controller(FitState *f, int *scratch) {
       }
     }
     __syncthreads();
-    return;
+    if (!fused) return;
+    phase = PH_FINAL;   // the candidates' log-likelihoods from the roots' L, now
   }
   if (phase == PH_REFINE) {
     const int nr = f->nrefine, iters = f->iters;
@@ -1140,6 +1313,8 @@ __device__ void setup_grid(FitState *f) {
   if (k == 0) {
     f->npts = (b > a) ? 2 * kGrid : kGrid;
     f->phase = PH_GRID;
+    f->use_bins = 0;
+    f->biters = 0;
   }
   if (f->nt >= kGrid32MinPeaks) {
     __syncthreads();
@@ -1176,6 +1351,8 @@ __device__ void setup_grid(FitState *f) {
       if (oct * bk > (double)(kMaxBins - 2)) bk = (double)(kMaxBins - 2) / oct;
       f->bin_l0 = l0;
       f->bin_k = bk;
+      f->bin_cl = 64 - __clzll((long long)f->nt);   // N_t < 2^cl
+      f->use_bins = 1;
       f->nbins = min(kMaxBins, (int)ceil(oct * bk) + 1);
     }
   }
@@ -1282,23 +1459,63 @@ __device__ __forceinline__ void eval_bundle(const double *Y, int64_t s0, int64_t
       for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
 }
 
-// PH_GRIDBIN: sums of the P and L terms of up to 4 points over the bins
-// [b0, b1) (lanes over bins): per bin n f(x m) + 1/2 f''(x m) x^2 S2 with m the
-// bin mean and S2 = sum (y - m)^2 -- f = log1p, f'' = -1/(1+u)^2; P's term
-// -u/(1+u), its second derivative 2/(1+u)^3.
-__device__ __forceinline__ void eval_bins(const double *bins, int b0, int b1,
+// ---- the log2(Y) bins: deterministic fixed-point sums ----------------------
+// Bin b of log2(Y) has the reference point r_b = 2^(l0 + (b + 1/2)/k) and keeps
+// the count, sum (y - r_b) and sum (y - r_b)^2 of its values as int64 fixed point
+// (integer atomics: exact and order-free, so every run -- and every rank of a
+// replicated fit -- sees the same bin sums bit for bit).  |y - r_b| < 2^(E_b - 8)
+// (E_b = the exponent of r_b; a bin is < 2^-9.4 r_b wide for any k >= 475, the
+// smallest k a float range can need) and a bin holds <= N_t < 2^cl values, so
+// the scales 2^(69 - cl - E_b) and 2^(77 - cl - 2 E_b) keep every sum below 2^61
+// while quantising y - r_b at ~2^(cl - 69) of y (~4e-15 at N_t = 2M).
+__device__ __forceinline__ double pow2i(int k) {   // 2^k, -1022 <= k <= 1023
+  return __hiloint2double((k + 1023) << 20, 0);
+}
+__device__ __forceinline__ double bin_ref(double l0, double bk, int b) {
+  return exp2(l0 + ((double)b + 0.5) / bk);
+}
+__device__ __forceinline__ int exp_of(double v) {   // unbiased exponent of a normal v > 0
+  return ((__double2hiint(v) >> 20) & 0x7ff) - 1023;
+}
+__device__ __forceinline__ void bin_add(unsigned long long *bins, int bi, double y, double l0,
+                                        double bk, int cl) {
+  const double rb = bin_ref(l0, bk, bi);
+  const int E = exp_of(rb);
+  const double d = y - rb;   // exact (Sterbenz: y and r_b within a factor 2)
+  const long long dq = __double2ll_rn(d * pow2i(69 - cl - E));
+  const long long qq = __double2ll_rn((d * d) * pow2i(77 - cl - 2 * E));
+  atomicAdd(bins + 3 * bi, 1ull);
+  atomicAdd(bins + 3 * bi + 1, (unsigned long long)dq);
+  atomicAdd(bins + 3 * bi + 2, (unsigned long long)qq);
+}
+
+// PH_GRIDBIN / PH_BREFINE: sums of the P and L terms of up to 4 points over the
+// bins [b0, b1) (lanes over bins): per bin n f(x m) + 1/2 f''(x m) x^2 S2 with m
+// the bin mean and S2 = sum (y - m)^2 -- f = log1p, f'' = -1/(1+u)^2; P's term
+// -u/(1+u), its second derivative 2/(1+u)^3.  kDeriv (PH_BREFINE) adds the
+// x-derivatives of the sums at zeroth order in the bin spread (sum y and sum y^2
+// exact, 1/(1 + x y) taken at the bin mean): they only steer the binned Halley
+// steps, never a sign or a certified value.
+template <bool kDeriv>
+__device__ __forceinline__ void eval_bins(const unsigned long long *bins, int b0, int b1,
                                           const double (&x)[4], int nu,
-                                          double (&acc)[4][kSums], const LogTab &T) {
+                                          double (&acc)[4][kSums], const LogTab &T, double l0,
+                                          double bk, int cl) {
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
   for (int b = b0 + (threadIdx.x & 31); b < b1; b += 32) {
-    const double n = __ldcg(bins + 3 * b);
-    if (n == 0.0) continue;
-    const double s = __ldcg(bins + 3 * b + 1), q = __ldcg(bins + 3 * b + 2);
-    const double m = s / n;
-    const double s2 = fmax(q - s * m, 0.0);
+    const long long cnt = (long long)__ldcg(bins + 3 * b);
+    if (cnt == 0) continue;
+    const double n = (double)cnt;
+    const double rb = bin_ref(l0, bk, b);
+    const int E = exp_of(rb);
+    const double sd = (double)(long long)__ldcg(bins + 3 * b + 1) * pow2i(E + cl - 69);
+    const double qd = (double)(long long)__ldcg(bins + 3 * b + 2) * pow2i(2 * E + cl - 77);
+    const double dm = sd / n;
+    const double m = rb + dm;
+    const double s2 = fmax(qd - sd * dm, 0.0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (u < nu) {
@@ -1308,13 +1525,22 @@ __device__ __forceinline__ void eval_bins(const double *bins, int b0, int b1,
         const double c2 = x[u] * x[u] * r * r * s2;   // x^2 S2 / (1 + x m)^2
         acc[u][0] = fma(n, -xm * r, fma(c2, r, acc[u][0]));
         acc[u][1] = fma(n, log1p_fast(xm, v, r, T), fma(-0.5, c2, acc[u][1]));
+        if (kDeriv) {
+          const double sy = n * m, sy2 = fma(n * m, m, s2);   // sum y, sum y^2
+          const double r2 = r * r;
+          acc[u][2] -= sy * r2;
+          acc[u][3] += sy * r;
+          acc[u][4] = fma(2.0 * sy2, r2 * r, acc[u][4]);
+          acc[u][5] -= sy2 * r2;
+        }
       }
     }
   }
+  constexpr int nk = kDeriv ? kSums : 2;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < nk; ++k)
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc[u][k] += __shfl_xor_sync(0xffffffffu, acc[u][k], o);
 }
@@ -1416,11 +1642,11 @@ __device__ void fit_stats_partials(const PotArgs &a, FitShared &S, const double 
 
 // the binned grid pass's histogram starts empty: every CTA zeroes its slice
 // (first written after the next grid barrier)
-__device__ __forceinline__ void zero_bins(double *bins) {
+__device__ __forceinline__ void zero_bins(unsigned long long *bins) {
   if (!bins) return;
   const int n = kMaxBins * 3;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    bins[i] = 0.0;
+    bins[i] = 0ull;
 }
 
 // grid totals of the statistics partials (fixed order; warp 0 of every CTA)
@@ -1445,15 +1671,15 @@ __device__ void fit_stats_totals(const PotArgs &a, double &ts, double &tmn, doub
 // one evaluation pass over this CTA's slice at the points of f (list order):
 // CTA partials per (k, point) -> pw ([kSums][kMaxPts][kMaxCtas])
 __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int64_t c1,
-                                  double *pw, double *bins) {
+                                  double *pw, unsigned long long *bins) {
   FitState &f = S.f;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int phase = f.phase;
   const int npts = f.npts;
   const bool deriv = (phase == PH_REFINE);
   const bool mixed = (phase == PH_GRID32);
-  const bool binned = (phase == PH_GRIDBIN);
-  const int nk = deriv ? kSums : 2;
+  const bool binned = (phase == PH_GRIDBIN || phase == PH_BREFINE);
+  const int nk = phase_sums(phase);
   // PH_GRIDBIN: the list points over this CTA's slice of the bins, not over Y
   if (binned) {
     const int nbn = f.nbins, nbk = gridDim.x;
@@ -1480,8 +1706,10 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
     double acc[4][kSums];
     if (deriv)
       eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
+    else if (phase == PH_BREFINE)
+      eval_bins<true>(bins, (int)s0, (int)s1, x, nu, acc, S.tab, f.bin_l0, f.bin_k, f.bin_cl);
     else if (binned)
-      eval_bins(bins, (int)s0, (int)s1, x, nu, acc, S.tab);
+      eval_bins<false>(bins, (int)s0, (int)s1, x, nu, acc, S.tab, f.bin_l0, f.bin_k, f.bin_cl);
     else
       eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
     if (lane == 0) {
@@ -1512,9 +1740,7 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
       float lg;
       asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"((float)y));
       const int bi = min(max(__float2int_rd((lg - l0f) * bkf), 0), nbn - 1);
-      atomicAdd(bins + 3 * bi, 1.0);
-      atomicAdd(bins + 3 * bi + 1, y);
-      atomicAdd(bins + 3 * bi + 2, y * y);
+      bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
     }
 #pragma unroll
     for (int m = 0; m < kPow; ++m) {
@@ -1545,7 +1771,7 @@ __device__ void fit_eval_totals(FitShared &S, const double *pw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nb = gridDim.x;
   const int npts = f.npts;
   const bool mixed = (f.phase == PH_GRID32);
-  const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+  const int nk = phase_sums(f.phase);
   constexpr int kJ = (kMaxCtas + 31) / 32;
   const int nitems = nk * npts + (mixed ? kPow : 0);   // + the power sums (row 2)
   for (int i0 = 4 * warp; i0 < nitems; i0 += 4 * kPotWarps) {
@@ -1583,7 +1809,7 @@ __device__ void fit_eval_totals(FitShared &S, const double *pw) {
 __device__ void fit_finish_pass(FitShared &S) {
   FitState &f = S.f;
   const int npts = f.npts;
-  const bool deriv = (f.phase == PH_REFINE);
+  const bool deriv = phase_sums(f.phase) == kSums;
   const bool mixed = (f.phase == PH_GRID32);
   const double N = (double)f.nt;
   if (threadIdx.x < npts) {
@@ -1777,7 +2003,7 @@ __device__ void dfit_step(const PotArgs &a, FitShared &S, unsigned int &epoch) {
     // S.red = the ranks' pass totals summed in rank order
     const int npts = f.npts;
     const bool mixed = (f.phase == PH_GRID32);
-    const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+    const int nk = phase_sums(f.phase);
     for (int i = threadIdx.x; i < nk * npts + (mixed ? kPow : 0); i += blockDim.x) {
       const bool extra = i >= nk * npts;
       const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
@@ -1807,7 +2033,7 @@ __device__ void dfit_step(const PotArgs &a, FitShared &S, unsigned int &epoch) {
       __syncthreads();
       const int npts = f.npts;
       const bool mixed = (f.phase == PH_GRID32);
-      const int nk = (f.phase == PH_REFINE) ? kSums : 2;
+      const int nk = phase_sums(f.phase);
       for (int i = threadIdx.x; i < nk * npts + (mixed ? kPow : 0); i += blockDim.x) {
         const bool extra = i >= nk * npts;
         const int k = extra ? 2 : i / npts, pt = extra ? i - nk * npts : i % npts;
@@ -2139,7 +2365,7 @@ static PotArgs make_args(const float *scores, int64_t n_local, int64_t n, double
   a.xsend = comm ? reinterpret_cast<double *>(b + L.xsend) : nullptr;
   a.xrecv = comm ? reinterpret_cast<const double *>(b + L.xrecv) : nullptr;
   a.fstate = comm ? reinterpret_cast<FitState *>(b + L.fstate) : nullptr;
-  a.bins = L.has_bins ? reinterpret_cast<double *>(b + L.bins) : nullptr;
+  a.bins = L.has_bins ? reinterpret_cast<unsigned long long *>(b + L.bins) : nullptr;
   return a;
 }
 
