@@ -379,19 +379,28 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_rows(const RowParams p) 
     // ---------------- MMA issuer ----------------
     const uint32_t idesc1 = make_idesc_f16(128, H);
     const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
-    for (int q = 0; q < p.nsteps; ++q) {
-      const int a = q % kRAStages, g = q / kRWStageSteps, st = g % kRWStages;
-      mbar_wait(&B.a_full[a], (q / kRAStages) & 1);
-      if (q % kRWStageSteps == 0) mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
-      tc_fence_after();
-      const uint64_t ad = make_sdesc(aa + a * kRAStepBytes, kRR * 16, 128);
-      const uint64_t bd = make_sdesc(
-          ra + st * SL.w_stage_bytes + (q % kRWStageSteps) * 32 * H, 16 * H, 128);
-      mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
-      mma_commit_warp(&B.a_empty[a]);
-      if (q % kRWStageSteps == kRWStageSteps - 1 || q == p.nsteps - 1) mma_commit_warp(&B.w_empty[st]);
-      if (q == p.nsteps - 1) mma_commit_warp(&B.g1_done);
+    // one iteration per W1 stage, its K-steps unrolled (straight-line waits and
+    // commits: see k_stream_rows)
+    const int n_groups = (p.nsteps + kRWStageSteps - 1) / kRWStageSteps;
+    for (int g = 0; g < n_groups; ++g) {
+      const int st = g % kRWStages;
+      mbar_wait(&B.w_full[st], (g / kRWStages) & 1);
+      const int steps = min(kRWStageSteps, p.nsteps - g * kRWStageSteps);
+#pragma unroll
+      for (int j = 0; j < kRWStageSteps; ++j) {
+        if (j < steps) {
+          const int q = g * kRWStageSteps + j, a = q % kRAStages;
+          mbar_wait(&B.a_full[a], (q / kRAStages) & 1);
+          tc_fence_after();
+          const uint64_t ad = make_sdesc(aa + a * kRAStepBytes, kRR * 16, 128);
+          const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
+          mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
+          mma_commit_warp(&B.a_empty[a]);
+        }
+      }
+      mma_commit_warp(&B.w_empty[st]);
     }
+    mma_commit_warp(&B.g1_done);
     // heads GEMM2: [mu | lv] = (h_hi + h_lo) [Wmu | Wlv]^T, accumulator at column H
     mbar_wait(&B.wimg, 0);
     mbar_wait(&B.h_full, 0);
@@ -952,27 +961,34 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
     // ---------------- MMA issuer (as k_score_rows) ----------------
     const uint32_t idesc1 = make_idesc_f16(128, H);
     const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
-    for (int q = 0; q < p.nsteps; ++q) {
-      const int g = q / kSAK, j = q % kSAK, a = g % kSAStages, st = g % kSWStages;
-      if (j == 0) {
-        mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
-        if (lane == 0 && g < 20) stamp(36 + g);
-        mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
-        if (lane == 0 && g < 16) stamp(72 + g);
-        tc_fence_after();
+    // one iteration per group (its kSAK MMAs unrolled): waits, MMAs, commits in
+    // straight-line code.  A loop over K-steps with the waits at j == 0 and the
+    // commits at j == kSAK - 1 paced the rings at ~1200 cycles per group instead
+    // of ~410 (tools/ubench_c4.cu, k_bis V1 vs V3)
+    const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
+    for (int g = 0; g < n_groups; ++g) {
+      const int a = g % kSAStages, st = g % kSWStages;
+      mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
+      if (lane == 0 && g < 20) stamp(36 + g);
+      mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
+      if (lane == 0 && g < 16) stamp(72 + g);
+      tc_fence_after();
+      const int steps = min(kSAK, p.nsteps - g * kSAK);
+#pragma unroll
+      for (int j = 0; j < kSAK; ++j) {
+        if (j < steps) {
+          // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
+          const uint64_t ad = make_sdesc(aa + a * kSAStageBytes + j * 4096, 2048, 128);
+          const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
+          mma_f16_warp(tmem, ad, bd, idesc1, (g | j) ? 1u : 0u);
+        }
       }
-      // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
-      const uint64_t ad = make_sdesc(aa + a * kSAStageBytes + j * 4096, 2048, 128);
-      const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
-      mma_f16_warp(tmem, ad, bd, idesc1, q > 0 ? 1u : 0u);
-      if (lane == 0 && q == 0) stamp(3);
-      if (lane == 0 && q == p.nsteps - 1) stamp(4);
-      if (j == kSAK - 1 || q == p.nsteps - 1) {
-        mma_commit_warp(&B.a_empty[a]);
-        mma_commit_warp(&B.w_empty[st]);
-      }
-      if (q == p.nsteps - 1) mma_commit_warp(&B.g1_done);
+      if (lane == 0 && g == 0) stamp(3);
+      mma_commit_warp(&B.a_empty[a]);
+      mma_commit_warp(&B.w_empty[st]);
     }
+    if (lane == 0) stamp(4);
+    mma_commit_warp(&B.g1_done);
     mbar_wait(&B.wimg, 0);
     mbar_wait(&B.h_full, 0);
     tc_fence_after();

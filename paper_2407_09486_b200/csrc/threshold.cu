@@ -519,6 +519,10 @@ __device__ void sample_phase(const PotArgs &a, SelS &ssel, unsigned int *h, unsi
 // scan (a byte's prefix <= 128), giving every lane its offset in (float4 slot,
 // lane, element) = index order.  General path and ragged tails: four ballots per
 // float4 on the keys.
+#ifndef ENOVA_SCAN_PF
+#define ENOVA_SCAN_PF 512
+#endif
+constexpr int kScanPf = ENOVA_SCAN_PF;   // float4 (multiple of 256): the scan's L2 prefetch distance
 __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, long long *out_n,
                            float *stage, int stage_cap) {
   __shared__ long long wcount[kPotWarps], wbelow[kPotWarps];
@@ -623,11 +627,24 @@ __device__ void scan_phase(const PotArgs &a, unsigned int lo, int64_t seg_cap, l
       }
       c32 = b;
     };
+    // L2 prefetch kScanPf float4 ahead of the loads (one bulk prefetch of the
+    // warp's next 4 KB per iteration, no registers held): the register batches
+    // then mostly hit L2, so the 8 loads in flight per lane cover its latency
+    const int64_t n4w = (w1 - w0) / 4;
+    auto pf = [&](int64_t i) {
+      if (kScanPf > 0 && lane == 0 && i < n4w) {
+        const uint32_t bytes = (uint32_t)(min((int64_t)256, n4w - i) * 16);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x4 + i), "r"(bytes) : "memory");
+      }
+    };
+    if (kScanPf > 0)
+      for (int64_t i = 0; i < kScanPf; i += 256) pf(i);
     if (nfull > 0) {
       uint4 va[4], vb[4];
       ld(va, 0);
       for (int i0 = 0; i0 < nfull; i0 += 256) {   // warp-uniform trip count
         const bool hb = i0 + 128 < nfull;
+        pf((int64_t)i0 + kScanPf);
         if (hb) ld(vb, i0 + 128);
         proc(va);
         if (i0 + 256 < nfull) ld(va, i0 + 256);
@@ -1905,7 +1922,13 @@ __device__ void fit(const PotArgs &a, FitShared &S, unsigned int &epoch, const i
     stamp(a.g);
     fit_eval_totals(S, pw);
     __syncthreads();
+#ifdef ENOVA_FIT_STAMPS
+    stamp(a.g);
+#endif
     fit_finish_pass(S);
+#ifdef ENOVA_FIT_STAMPS
+    stamp(a.g);
+#endif
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) fit_publish(a, f);
 }

@@ -1,0 +1,454 @@
+// Microbenchmark: the c4 streaming tick's operand ingest.  Each CTA pulls its
+// A rows (distinct per CTA, from a ring of `ring_mb` MB -- L2-warm after the
+// first launch) and the W1 image (shared by every CTA, or halves by CTA parity)
+// through two bulk-copy rings of S x 16 KB stages, as k_stream_rows does; one
+// consumer warp releases the stages (no MMA).  Prints the kernel time (CUDA
+// events, mean of 50 launches) per configuration: what bounds the K loop --
+// per-SM ingest, aggregate bandwidth, or the shared W1 lines.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ubench_c4 tools/ubench_c4.cu
+#include <cstdio>
+#include <cstdint>
+#include "../paper_2407_09486_b200/csrc/common.cuh"
+using namespace enova;
+namespace enova {
+void set_error(const std::string &) {}
+enova_status cuda_status(cudaError_t, const char *) { return ENOVA_ERR_CUDA; }
+void count_launch() {}
+}
+
+constexpr uint32_t CH = 16384;
+__device__ long long g_tr[256];
+__device__ __forceinline__ long long clk() { long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; }
+
+template <int S>
+__global__ void __launch_bounds__(96, 1) k_rings(const uint8_t *__restrict__ A, uint32_t a_bytes,
+                                                 const uint8_t *__restrict__ Wt, uint32_t w_bytes,
+                                                 int w_halves, float *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t afull[S], aempty[S], wfull[S], wempty[S];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1);
+      mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (w_halves & 8) tc_fence_before();
+  __syncthreads();
+  if (w_halves & 8) tc_fence_after();
+  const int na = (int)(a_bytes / CH), nw = (int)(w_bytes / CH);
+  const uint8_t *abase = A + (size_t)blockIdx.x * a_bytes;
+  const uint8_t *wbase = Wt + (w_halves & 1 ? (size_t)(blockIdx.x & 1) * w_bytes : 0);
+  uint8_t *as = sm, *ws = sm + S * CH;
+  const bool trc = (w_halves & 2) && blockIdx.x == 0;
+  if (trc && tid == 0) g_tr[250] = clk();
+  if (warp == 0 && tid == 0) {
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&aempty[s], ((k / S) - 1) & 1);
+      mbar_arrive_expect_tx(&afull[s], CH);
+      bulk_g2s(as + (size_t)s * CH, abase + (size_t)k * CH, CH, &afull[s]);
+      if (trc && k < 32) g_tr[k] = clk();
+    }
+  } else if (warp == 1 && tid == 32) {
+    for (int k = 0; k < nw; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&wempty[s], ((k / S) - 1) & 1);
+      mbar_arrive_expect_tx(&wfull[s], CH);
+      bulk_g2s(ws + (size_t)s * CH, wbase + (size_t)k * CH, CH, &wfull[s]);
+    }
+  } else if (tid == 64 || ((w_halves & 32) && warp == 2)) {
+    const int n = na > nw ? na : nw;
+    float acc = 0.f;
+    for (int k = 0; k < n; ++k) {
+      const int s = k % S;
+      if (k < na) { mbar_wait(&afull[s], (k / S) & 1); if (trc && tid == 64 && k < 32) g_tr[64 + k] = clk(); acc += as[(size_t)s * CH + 5]; if (tid == 64) mbar_arrive(&aempty[s]); }
+      if (k < nw) { mbar_wait(&wfull[s], (k / S) & 1); if (trc && tid == 64 && k < 32) g_tr[128 + k] = clk(); acc += ws[(size_t)s * CH + 7]; if (tid == 64) mbar_arrive(&wempty[s]); }
+    }
+    if (acc == 1.2345f) out[0] = acc;
+  }
+  if (w_halves & 16) __syncthreads();   // every thread waits for the consumer
+  if (w_halves & 4) {   // never true at run time: a tcgen05 alloc/dealloc present in the kernel
+    __shared__ uint32_t slot2;
+    if (warp == 2 && a_bytes == 77u) { tmem_alloc(&slot2, 32); tmem_dealloc(slot2, 32); }
+  }
+}
+
+
+// the same rings with the stream kernel's GEMM1 consuming them: 4 x M128N128K16
+// tcgen05 MMAs per (A, W1) group pair (no-swizzle K-major canonical layouts),
+// committed to the stages' empty barriers
+template <int S>
+__global__ void __launch_bounds__(96, 1) k_rings_mma(const uint8_t *__restrict__ A, uint32_t a_bytes,
+                                                     const uint8_t *__restrict__ Wt, uint32_t w_bytes,
+                                                     int mode, float *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t afull[S], aempty[S], wfull[S], wempty[S], done;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1);
+      mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2 && !(mode & 4)) tmem_alloc(&slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if ((mode & 64) && blockIdx.x == 0 && tid == 0) g_tr[250] = clk();
+  const uint32_t tmem = slot;
+  const int na = (int)(a_bytes / CH);
+  const uint8_t *abase = A + (size_t)blockIdx.x * a_bytes;
+  uint8_t *as = sm, *ws = sm + S * CH;
+  if ((mode & 256) && warp < 2) {
+    // converged producer warps: every lane runs the loop and waits, lane 0 issues
+    uint8_t *dst = warp == 0 ? as : ws;
+    const uint8_t *srcb = warp == 0 ? abase : Wt;
+    uint64_t *full = warp == 0 ? afull : wfull, *empty = warp == 0 ? aempty : wempty;
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+      if ((tid & 31) == 0) {
+        mbar_arrive_expect_tx(&full[s], CH);
+        bulk_g2s(dst + (size_t)s * CH, srcb + (size_t)k * CH, CH, &full[s]);
+        if ((mode & 64) && warp == 0 && blockIdx.x == 0 && k < 32) g_tr[k] = clk();
+      }
+      __syncwarp();
+    }
+  } else if (warp == 0 && tid == 0) {
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) { if (mode & 2) mbar_wait(&aempty[s], ((k / S) - 1) & 1); else mbar_wait_sleep(&aempty[s], ((k / S) - 1) & 1, 64); }
+      mbar_arrive_expect_tx(&afull[s], CH);
+      bulk_g2s(as + (size_t)s * CH, abase + (size_t)k * CH, CH, &afull[s]);
+      if ((mode & 64) && blockIdx.x == 0 && k < 32) g_tr[k] = clk();
+    }
+  } else if (warp == 1 && tid == 32) {
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) { if (mode & 2) mbar_wait(&wempty[s], ((k / S) - 1) & 1); else mbar_wait_sleep(&wempty[s], ((k / S) - 1) & 1, 64); }
+      mbar_arrive_expect_tx(&wfull[s], CH);
+      bulk_g2s(ws + (size_t)s * CH, Wt + (size_t)k * CH, CH, &wfull[s]);
+    }
+  } else if (warp == 2) {
+    const uint32_t idesc = make_idesc_f16(128, 128);
+    const uint32_t aa = smem_u32(as), wa = smem_u32(ws);
+    for (int q = 0; q < 4 * na; ++q) {
+      const int g = q / 4, j = q % 4, s = g % S;
+      if (j == 0) {
+        if (mode & 16) {            // one lane polls (try_wait), the warp reconverges
+          if ((tid & 31) == 0) { mbar_wait(&afull[s], (g / S) & 1); mbar_wait(&wfull[s], (g / S) & 1); }
+          __syncwarp();
+        } else if (mode & 32) {     // every lane polls with test_wait (no suspend)
+          uint64_t *bs[2] = {&afull[s], &wfull[s]};
+          for (int t2 = 0; t2 < 2; ++t2) {
+            uint32_t dn = 0;
+            while (!dn)
+              asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                           : "=r"(dn) : "r"(smem_u32(bs[t2])), "r"((uint32_t)((g / S) & 1)) : "memory");
+          }
+        } else if (mode & 128) {   // back off between polls
+          mbar_wait_sleep(&afull[s], (g / S) & 1, 32);
+          mbar_wait_sleep(&wfull[s], (g / S) & 1, 32);
+        } else {
+          mbar_wait(&afull[s], (g / S) & 1);
+          if ((mode & 64) && blockIdx.x == 0 && (tid & 31) == 0 && g < 32) g_tr[64 + g] = clk();
+          mbar_wait(&wfull[s], (g / S) & 1);
+          if ((mode & 64) && blockIdx.x == 0 && (tid & 31) == 0 && g < 32) g_tr[128 + g] = clk();
+        }
+        if (!(mode & 8)) tc_fence_after();
+      }
+      if (!(mode & 1)) {
+        const uint64_t ad = make_sdesc(aa + s * CH + j * 4096, 2048, 128);
+        const uint64_t bd = make_sdesc(wa + s * CH + j * 4096, 2048, 128);
+        mma_f16_warp(tmem, ad, bd, idesc, q > 0 ? 1u : 0u);
+      }
+      if (j == 3) {
+        if (!(mode & 1)) {
+          mma_commit_warp(&aempty[s]);
+          mma_commit_warp(&wempty[s]);
+        } else if (tid == 64) {
+          mbar_arrive(&aempty[s]);
+          mbar_arrive(&wempty[s]);
+        }
+        __syncwarp();
+      }
+    }
+    if (!(mode & 1)) mma_commit_warp(&done);
+    else if (tid == 64) mbar_arrive(&done);
+    __syncwarp();
+    mbar_wait(&done, 0);
+    tc_fence_after();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2 && !(mode & 4)) tmem_dealloc(tmem, 128);
+  if (tid == 0 && a_bytes == 12345u) out[0] = 1.f;
+}
+
+// bisection kernels: k_rings_mma's structure without tcgen05 (V=0: consumer loop
+// over groups; V=1: consumer loop over K-steps with waits at j == 0 and releases
+// at j == 3, as the MMA warp does; V=2: V=1 + the other lanes of the producer
+// warps parked at a final barrier)
+template <int S, int V>
+__global__ void __launch_bounds__(96, 1) k_bis(const uint8_t *__restrict__ A, uint32_t a_bytes,
+                                               const uint8_t *__restrict__ Wt, float *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t afull[S], aempty[S], wfull[S], wempty[S];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1);
+      mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) g_tr[250] = clk();
+  const int na = (int)(a_bytes / CH);
+  const uint8_t *abase = A + (size_t)blockIdx.x * a_bytes;
+  uint8_t *as = sm, *ws = sm + S * CH;
+  if (warp == 0 && tid == 0) {
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&aempty[s], ((k / S) - 1) & 1);
+      mbar_arrive_expect_tx(&afull[s], CH);
+      bulk_g2s(as + (size_t)s * CH, abase + (size_t)k * CH, CH, &afull[s]);
+    }
+  } else if (warp == 1 && tid == 32) {
+    for (int k = 0; k < na; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&wempty[s], ((k / S) - 1) & 1);
+      mbar_arrive_expect_tx(&wfull[s], CH);
+      bulk_g2s(ws + (size_t)s * CH, Wt + (size_t)k * CH, CH, &wfull[s]);
+    }
+  } else if (warp == 2 && V == 3) {
+    // V0's group loop with the 4 MMAs of each group (M128 N128 K16, TMEM accumulator)
+    __shared__ uint32_t slot;
+    tmem_alloc(&slot, 128);
+    tc_fence_before();
+    __syncwarp();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    const uint32_t idesc = make_idesc_f16(128, 128);
+    const uint32_t aa = smem_u32(as), wa = smem_u32(ws);
+    for (int g = 0; g < na; ++g) {
+      const int s = g % S;
+      mbar_wait(&afull[s], (g / S) & 1);
+      mbar_wait(&wfull[s], (g / S) & 1);
+      tc_fence_after();
+      if (blockIdx.x == 0 && tid == 64 && g < 32) g_tr[64 + g] = clk();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t ad = make_sdesc(aa + s * CH + j * 4096, 2048, 128);
+        const uint64_t bd = make_sdesc(wa + s * CH + j * 4096, 2048, 128);
+        mma_f16_warp(tmem, ad, bd, idesc, (g | j) ? 1u : 0u);
+      }
+      mma_commit_warp(&aempty[s]);
+      mma_commit_warp(&wempty[s]);
+      __syncwarp();
+    }
+    __shared__ uint64_t dn;
+    if (tid == 64) { mbar_init(&dn, 1); fence_mbar_init(); }
+    __syncwarp();
+    mma_commit_warp(&dn);
+    __syncwarp();
+    mbar_wait(&dn, 0);
+    if (blockIdx.x == 0 && tid == 64) g_tr[100] = clk();
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  } else if (warp == 2) {
+    if (V == 0) {
+      for (int g = 0; g < na; ++g) {
+        const int s = g % S;
+        mbar_wait(&afull[s], (g / S) & 1);
+        mbar_wait(&wfull[s], (g / S) & 1);
+        if (blockIdx.x == 0 && tid == 64 && g < 32) g_tr[64 + g] = clk();
+        if (tid == 64) { mbar_arrive(&aempty[s]); mbar_arrive(&wempty[s]); }
+        __syncwarp();
+      }
+    } else {
+      for (int q = 0; q < 4 * na; ++q) {
+        const int g = q / 4, j = q % 4, s = g % S;
+        if (j == 0) {
+          mbar_wait(&afull[s], (g / S) & 1);
+          mbar_wait(&wfull[s], (g / S) & 1);
+          if (blockIdx.x == 0 && tid == 64 && g < 32) g_tr[64 + g] = clk();
+        }
+        if (j == 3) {
+          if (tid == 64) { mbar_arrive(&aempty[s]); mbar_arrive(&wempty[s]); }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  if (V == 2) __syncthreads();
+  if (tid == 0 && a_bytes == 12345u) out[0] = 1.f;
+}
+
+int main() {
+  const size_t ring = (size_t)48 << 20;
+  uint8_t *A, *Wt;
+  float *out;
+  cudaMalloc(&A, ring);
+  cudaMalloc(&Wt, 1 << 20);
+  cudaMalloc(&out, 64);
+  cudaMemset(A, 1, ring);
+  cudaMemset(Wt, 1, 1 << 20);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  constexpr int S = 6;
+  cudaFuncSetAttribute(k_rings<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * S * CH);
+  auto run = [&](const char *name, int ctas, uint32_t a_bytes, uint32_t w_bytes, int halves) {
+    auto launch = [&] { k_rings<S><<<ctas, 96, 2 * S * CH>>>(A, a_bytes, Wt, w_bytes, halves, out); };
+    for (int i = 0; i < 3; ++i) launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int i = 0; i < 50; ++i) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double us = ms * 1e3 / 50;
+    const double per_sm = (double)(a_bytes + w_bytes) / (us * 1e-6) / 1e9;
+    const double agg = per_sm * ctas;
+    printf("%-52s %7.2f us  per-CTA %6.1f GB/s  aggregate %7.1f GB/s  (%s)\n", name, us, per_sm, agg,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  run("empty launch (1 CTA, nothing)", 1, 0, 0, 0);
+  run("1 CTA: A 256K + W 256K", 1, 256 << 10, 256 << 10, 0);
+  run("1 CTA: A 256K only", 1, 256 << 10, 0, 0);
+  run("1 CTA: A 128K + W 128K traced", 1, 128 << 10, 128 << 10, 2);
+  run("1 CTA: A 128K + W 128K (tcgen05 code present)", 1, 128 << 10, 128 << 10, 4);
+  run("1 CTA: A 128K + W 128K (plain)", 1, 128 << 10, 128 << 10, 0);
+  run("1 CTA: A 128K + W 128K (tc fences at start)", 1, 128 << 10, 128 << 10, 8);
+  run("1 CTA: A 128K + W 128K (final __syncthreads)", 1, 128 << 10, 128 << 10, 16);
+  run("1 CTA: A 128K + W 128K (both)", 1, 128 << 10, 128 << 10, 24);
+  auto trace = [&](const char *nm) {
+    long long h[256];
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("%s: A ready:", nm);
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("\n");
+  };
+  run("1 CTA: traced, final __syncthreads", 1, 128 << 10, 128 << 10, 2 | 16);
+  trace("final-sync");
+  run("1 CTA: traced, warp consumer", 1, 128 << 10, 128 << 10, 2 | 32);
+  trace("warp-consumer");
+  run("1 CTA: traced, warp consumer + final sync + fences", 1, 128 << 10, 128 << 10, 2 | 32 | 16 | 8);
+  trace("warp-consumer+sync+fences");
+  auto runb = [&](const char *name, auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * S * CH);
+    for (int i = 0; i < 3; ++i) kern<<<1, 96, 2 * S * CH>>>(A, 128 << 10, Wt, out);
+    cudaDeviceSynchronize();
+    trace(name);
+  };
+  runb("bis V0", k_bis<S, 0>);
+  runb("bis V1", k_bis<S, 1>);
+  runb("bis V2", k_bis<S, 2>);
+  runb("bis V3 (MMAs)", k_bis<S, 3>);
+  {
+    auto kern = k_bis<S, 3>;
+    for (int i = 0; i < 3; ++i) kern<<<1, 96, 2 * S * CH>>>(A, 256 << 10, Wt, out);
+    cudaDeviceSynchronize();
+    long long h[256];
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("V3 256K: A ready:");
+    for (int k = 0; k < 16; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("  MMAs done %lld\n", h[100] - h[250]);
+    for (int i = 0; i < 3; ++i) kern<<<79, 96, 2 * S * CH>>>(A, 256 << 10, Wt, out);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("V3 256K 79 CTAs (CTA 0): A ready:");
+    for (int k = 0; k < 16; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("  MMAs done %lld\n", h[100] - h[250]);
+  }
+  {
+    long long h[256];
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("k_rings trace (cycles from start): A issue:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[k] - h[250]);
+    printf("\n A ready:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("\n W ready:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[128 + k] - h[250]);
+    printf("\n");
+  }
+  run("8 CTAs: A 256K + W 256K", 8, 256 << 10, 256 << 10, 0);
+  run("79 CTAs: A 256K + W 256K (c4 today)", 79, 256 << 10, 256 << 10, 0);
+  run("79 CTAs: A 256K only", 79, 256 << 10, 0, 0);
+  run("79 CTAs: W 256K only (shared)", 79, 0, 256 << 10, 0);
+  run("80 CTAs: A 256K + W half 128K (CTA pairs)", 80, 256 << 10, 128 << 10, 1);
+  run("148 CTAs: A 128K + W 256K", 148, 128 << 10, 256 << 10, 0);
+  run("148 CTAs: A 128K + W half 128K", 148, 128 << 10, 128 << 10, 1);
+  run("148 CTAs: A 144K only", 148, 144 << 10, 0, 0);
+  cudaFuncSetAttribute(k_rings_mma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * S * CH);
+  auto runm = [&](const char *name, int ctas, int mode, uint32_t ab = 256 << 10) {
+    auto launch = [&] { k_rings_mma<S><<<ctas, 96, 2 * S * CH>>>(A, ab, Wt, ab, mode, out); };
+    for (int i = 0; i < 3; ++i) launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int i = 0; i < 50; ++i) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("%-52s %7.2f us  (%s)\n", name, ms * 1e3 / 50, cudaGetErrorString(cudaGetLastError()));
+  };
+  runm("MMA rings: 1 CTA, MMAs, sleeping producers", 1, 0);
+  runm("MMA rings: 1 CTA, no MMA, sleeping producers", 1, 1);
+  runm("MMA rings: 1 CTA, MMAs, spinning producers", 1, 2);
+  runm("MMA rings: 1 CTA, no MMA, spinning producers", 1, 3);
+  runm("MMA rings: 79 CTAs, MMAs, sleeping producers", 79, 0);
+  runm("MMA rings: 79 CTAs, no MMA, sleeping producers", 79, 1);
+  runm("MMA rings: 79 CTAs, MMAs, spinning producers", 79, 2);
+  runm("MMA rings: 79 CTAs, no MMA, spinning producers", 79, 3);
+  runm("MMA rings: 79 CTAs, no MMA, no TMEM alloc", 79, 7);
+  runm("MMA rings: 1 CTA, no MMA, no TMEM alloc", 1, 7);
+  runm("MMA rings: 1 CTA, no MMA, no TMEM, no loop fence", 1, 15);
+  runm("MMA rings: 1 CTA, no MMA, no loop fence", 1, 11);
+  runm("MMA rings: 1 CTA, no MMA, lane-0 try_wait", 1, 1 | 16);
+  runm("MMA rings: 1 CTA, no MMA, test_wait spin", 1, 1 | 32);
+  runm("MMA rings: 1 CTA, MMA, lane-0 try_wait", 1, 16);
+  runm("MMA rings: 1 CTA, MMA, test_wait spin", 1, 32);
+  runm("MMA rings: 79 CTAs, MMA, test_wait spin", 79, 32);
+  runm("MMA rings: 1 CTA, 0 bytes, no MMA, no TMEM", 1, 1 | 4, 0);
+  runm("MMA rings: 1 CTA, 0 bytes, TMEM alloc", 1, 0, 0);
+  runm("MMA rings: 1 CTA, 16 KB, no MMA, no TMEM", 1, 1 | 4, 16384);
+  runm("MMA rings: 1 CTA, 64 KB, no MMA, no TMEM", 1, 1 | 4, 65536);
+  runm("MMA rings: 1 CTA, 128 KB, no MMA, no TMEM", 1, 1 | 4, 131072);
+  runm("MMA rings: 1 CTA, 128 KB, no MMA, no TMEM, traced", 1, 1 | 4 | 64, 131072);
+  runm("MMA rings: 1 CTA, 128 KB, no MMA, sleep-poll consumer", 1, 1 | 4 | 128, 131072);
+  runm("MMA rings: 1 CTA, 256 KB, MMA, converged producers", 1, 256);
+  runm("MMA rings: 79 CTA, 256 KB, MMA, converged producers", 79, 256);
+  runm("MMA rings: 1 CTA, 256 KB, no MMA, converged producers", 1, 256 | 1);
+  runm("MMA rings: 1 CTA, 128 KB, no MMA, converged, traced", 1, 256 | 1 | 4 | 64, 131072);
+  {
+    long long h[256];
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("converged trace: A issue:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[k] - h[250]);
+    printf("\n A ready:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("\n");
+  }
+  runm("MMA rings: 1 CTA, 256 KB, MMA, sleep-poll consumer", 1, 128);
+  runm("MMA rings: 79 CTA, 256 KB, MMA, sleep-poll consumer", 79, 128);
+  {
+    long long h[256];
+    cudaMemcpyFromSymbol(h, g_tr, sizeof(h));
+    printf("trace (cycles from start): A issue:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[k] - h[250]);
+    printf("\n A ready:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[64 + k] - h[250]);
+    printf("\n W ready:");
+    for (int k = 0; k < 8; ++k) printf(" %lld", h[128 + k] - h[250]);
+    printf("\n");
+  }
+  return 0;
+}
