@@ -68,6 +68,7 @@ constexpr int kRPF = 8;                  // K-steps of raw samples in flight per
 struct RowBars {
   uint64_t w_full[kMaxWStages], w_empty[kMaxWStages], a_full[kRAStages], a_empty[kRAStages];
   uint64_t wimg, g1_done, h_full, g2_done, mu_full, g3_done;
+  uint64_t e3_done;   // split epilogue (stream kernel): the helpers' E3 partials are in smem
   uint32_t tmem_slot, pad;
 };
 
@@ -141,7 +142,14 @@ struct WinSum {
 // same association.  Row threads of warps 0-3; GEMM2/GEMM3 are issued by the
 // MMA warp between the h_full / mu_full arrivals and the g2_done / g3_done
 // commits of RowBars.
-template <int H, int ZP, class Bars, class SxFn>
+// kPart: 0 = the whole epilogue of the row; 1 / 2 = the row thread / its helper
+// thread (a warp of the same TMEM lane quadrant) of a split epilogue: E1 over
+// the first / second half of the H columns (element-wise: any split is
+// bit-identical), E2 by the row thread only, E3's four interleaved fma chains
+// (columns k mod 4) as chains 0, 1 / 2, 3 with the helper's (d2 + d3) passed
+// through shared memory (e3part, e3_done) -- the same operations in the same
+// order as kPart 0, so the split epilogue is bit-identical to the whole one.
+template <int H, int ZP, class Bars, class SxFn, int kPart = 0>
 __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane, int r, int64_t row,
                                               bool valid, SxFn &&sx_fn, uint8_t *region,
                                               uint8_t *mubuf, const float *b1cs,
@@ -153,7 +161,7 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
                                               const float *wbarm_s = nullptr,
                                               const float *xsum = nullptr,
                                               const float *bbarm = nullptr, float *md_metric = nullptr,
-                                              int M = 0, int W = 0) {
+                                              int M = 0, int W = 0, float *e3part = nullptr) {
   auto stamp = [&](int slot) {   // diagnostic; compiled in with -DENOVA_TRACE only
 #ifdef ENOVA_TRACE
     if (tr && r == 0) {
@@ -168,11 +176,12 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
   };
     // ---- E1: h = tanh(acc + b1) -> hi/lo fp16 A images ----
     const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-    mbar_wait_sleep(&B.g1_done, 0);
+    mbar_wait_sleep(&B.g1_done, 0, 256);   // (the K loop: long; polling would slow its warps)
     stamp(6);
     tc_fence_after();
+    constexpr int kC0 = kPart == 2 ? H / 2 : 0, kC1 = kPart == 1 ? H / 2 : H;
 #pragma unroll 1
-    for (int c16 = 0; c16 < H; c16 += 16) {
+    for (int c16 = kC0; c16 < kC1; c16 += 16) {
       float v[16], bc[16];
       tmem_ld16(lane_addr + c16, v);
       lds16(b1cs + c16, bc);
@@ -192,9 +201,33 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     __syncwarp();
     if (lane == 0) mbar_arrive(&B.h_full);
     stamp(7);
+    if constexpr (kPart == 2) {
+      // helper: E3 chains 2, 3 -> e3part
+      mbar_wait_sleep(&B.g3_done, 0, 32);
+      tc_fence_after();
+      float d2 = 0.f, d3 = 0.f;
+#pragma unroll 1
+      for (int c32 = 0; c32 < H; c32 += 32) {
+        float v[32];
+        tmem_ld16(lane_addr + c32, *reinterpret_cast<float(*)[16]>(&v[0]));
+        tmem_ld16(lane_addr + c32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          const float4 ww = *reinterpret_cast<const float4 *>(wbs + c32 + k);
+          const float4 bb = *reinterpret_cast<const float4 *>(b3s + c32 + k);
+          d2 = fmaf(ww.z, tanh_mufu(v[k + 2] + bb.z), d2);
+          d3 = fmaf(ww.w, tanh_mufu(v[k + 3] + bb.w), d3);
+        }
+      }
+      e3part[r] = d2 + d3;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.e3_done);
+      return;
+    }
 
     // ---- E2: KL score; mu -> hi/lo fp16 ----
-    mbar_wait_sleep(&B.g2_done, 0, 64);
+    mbar_wait_sleep(&B.g2_done, 0, kPart ? 32 : 64);
     stamp(8);
     tc_fence_after();
     float score;
@@ -246,7 +279,7 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
 
     // ---- E3: MD by the column-sum identity; flag ----
     const float sx = sx_fn();   // window sum (may be computed here, off the E1 path)
-    mbar_wait_sleep(&B.g3_done, 0, 64);
+    mbar_wait_sleep(&B.g3_done, 0, kPart ? 32 : 64);
     stamp(10);
     tc_fence_after();
     float d4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -262,11 +295,20 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
         const float4 bb = *reinterpret_cast<const float4 *>(b3s + c32 + k);
         d4[0] = fmaf(ww.x, tanh_mufu(v[k] + bb.x), d4[0]);   // acc = W3 mu (from zero)
         d4[1] = fmaf(ww.y, tanh_mufu(v[k + 1] + bb.y), d4[1]);
-        d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2] + bb.z), d4[2]);
-        d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3] + bb.w), d4[3]);
+        if constexpr (kPart == 0) {
+          d4[2] = fmaf(ww.z, tanh_mufu(v[k + 2] + bb.z), d4[2]);
+          d4[3] = fmaf(ww.w, tanh_mufu(v[k + 3] + bb.w), d4[3]);
+        }
       }
     }
-    const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+    float d23;
+    if constexpr (kPart == 1) {
+      mbar_wait(&B.e3_done, 0);
+      d23 = e3part[r];
+    } else {
+      d23 = d4[2] + d4[3];
+    }
+    const float dot = (d4[0] + d4[1]) + d23;
     const float mdv = (sx - dot - (float)(*bbar)) / (float)D;
     if (wbarm_s) {
       // NEXT-1: per-metric mean difference MD_j = (sum_tau x_{tau,j} - w_bar_j . a3 -
@@ -746,19 +788,19 @@ enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sampl
 // A ring of the stream kernel: stages of kSAK K-steps = one 16 KB bulk copy of
 // the tile's contiguous canonical-layout range (4 x [2 halves][128 rows][16 B]).
 constexpr int kSAK = 4;
-// The K loop is paced by ring round trips (bulk-copy latency ~2 us vs ~0.14 us
-// of MMAs per group), and a group needs one A and one W1 stage: the two rings
-// get the same depth, as deep as shared memory allows.
+// A group needs one A and one W1 stage: the two rings get the same depth, as
+// deep as shared memory allows (6 x 32 KB in flight per SM; with the MMA warp's
+// straight-line group loop a group takes ~410 cycles, the 4 MMAs' own cost).
 constexpr int kSAStages = 6;
 constexpr int kSWStages = 6;   // the stream kernel's W1 ring
-constexpr int kSAWarp = 6;                        // A producer warp (kLsuA == false)
-// A operand of the stream kernel through the LSU path: the 128 row threads copy
-// each 16 KB group with cp.async (16 B per thread-op, coalesced; the tiled ring
-// needs no swizzle), so A and W1 (bulk copies, the TMA path) arrive over two
-// paths in parallel.  false = 16 KB bulk copies from the A producer warp.
-// (measured: the same tick either way -- 29.1 us -- so the bulk-copy path is kept)
-constexpr bool kLsuA = false;
-constexpr int kSThreads = kRThreads + 32;
+constexpr int kSAWarp = 6;                        // A producer warp
+constexpr int kSHelperWarp0 = 7;                  // warps 7-10: epilogue helpers (TMEM quadrant warp & 3)
+constexpr int kSThreads = kRThreads + 32 + kRowThreads;
+// the helpers' E3 partials reuse the GEMM3 A image (mubuf): GEMM3 has completed
+// (g3_done) before any helper writes
+__device__ __forceinline__ float *e3part_of(uint8_t *smem, const RowLayoutSm &SL) {
+  return reinterpret_cast<float *>(smem + SL.mubuf);
+}
 constexpr uint32_t kSAStageBytes = kRR * 128;
 
 struct StreamParams {
@@ -885,48 +927,37 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
   };
   if (tid == 0) stamp(0);
 
+  // 1. barrier initialisation, then the producers start at once (they need
+  //    nothing else); the consumers (rows, their helpers, the MMA warp) load the
+  //    biases and allocate TMEM meanwhile and meet at their own named barrier
   if (tid == 0) {
     for (int i = 0; i < kSWStages; ++i) {
       mbar_init(&B.w_full[i], 1);
       mbar_init(&B.w_empty[i], 1);
     }
-    for (int i = 0; i < kRAStages; ++i) {
-      // the producer's expect_tx (the bulk copy completes the bytes)
-      // arrival per row warp
-      mbar_init(&B.a_full[i], kLsuA ? kRowThreads / 32 : 1);
+    for (int i = 0; i < kSAStages; ++i) {
+      mbar_init(&B.a_full[i], 1);   // the producer's expect_tx (the bulk copy completes the bytes)
       mbar_init(&B.a_empty[i], 1);
     }
     mbar_init(&B.wimg, 1);
     mbar_init(&B.g1_done, 1);
-    mbar_init(&B.h_full, kRowThreads / 32);
+    mbar_init(&B.h_full, 2 * kRowThreads / 32);   // row warps + helper warps (E1 halves)
     mbar_init(&B.g2_done, 1);
     mbar_init(&B.mu_full, kRowThreads / 32);
     mbar_init(&B.g3_done, 1);
+    mbar_init(&B.e3_done, kRowThreads / 32);
     fence_mbar_init();
   }
-  for (int i = tid; i < H; i += blockDim.x) {
-    b1s[i] = __fmul_rn(p.b1[i], kTwoLog2e);   // E1 exponent bias (GEMM1 starts from zero)
-    b3s[i] = p.b3[i];
-    wbs[i] = p.wbar[i];
-  }
-  for (int i = tid; i < N2; i += blockDim.x) bmls[i] = p.bml[i];
-  for (int i = tid; i < (int)(2 * kRR * 16 * 2 / 16); i += blockDim.x)
-    reinterpret_cast<uint4 *>(mubuf)[i] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) tmem_alloc(&B.tmem_slot, SL.tmem_cols);
-  tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = B.tmem_slot;
+  const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
 
   if (warp == kRProdWarp) {
-    // ---------------- producer: W1 ring (bulk copies) ----------------
+    // ---------------- producer: heads / W3 images, W1 ring (bulk copies) ----------------
     if (lane == 0) {
       const uint32_t hb = (uint32_t)N2 * H * 2, w3b = (uint32_t)H * 16 * 2;
       mbar_arrive_expect_tx(&B.wimg, hb + w3b);
       bulk_g2s(heads, p.headsimg, hb, &B.wimg);
       bulk_g2s(w3s, p.w3img, w3b, &B.wimg);
-      // W1 ring: one stage (kRWStageSteps = kSAK K-steps) per group
-      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
       for (int g = 0; g < n_groups; ++g) {
         const int st = g % kSWStages;
         if (g >= kSWStages) mbar_wait_sleep(&B.w_empty[st], ((g / kSWStages) - 1) & 1, 64);
@@ -940,13 +971,14 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
     }
   } else if (warp == kSAWarp) {
     // ---------------- A producer: one 16 KB bulk copy (kSAK K-steps x 128 instances) per group ----------------
-    if (!kLsuA && p.sample) named_bar_sync_na(5, kRowThreads + 32);   // fused ingest: wait for the pushes
-    if (!kLsuA && lane == 0) {
-      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
-      // this tile's window: half-blocks woff M/8 + 2q, +1 of K-step q (2 KB each)
-      const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
-                            (((size_t)blockIdx.x * 2 * W + woff) * (size_t)(p.M >> 3) << 11);
-      for (int g = 0; g < n_groups; ++g) {
+    // The window's newest sample is its last K-step (last group): only that
+    // group waits for this tick's fused pushes; the older groups stream while
+    // the row threads ingest.
+    const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
+                          (((size_t)blockIdx.x * 2 * W + woff) * (size_t)(p.M >> 3) << 11);
+    for (int g = 0; g < n_groups; ++g) {
+      if (g == n_groups - 1 && p.sample) named_bar_sync_na(5, kRowThreads + 32);
+      if (lane == 0) {
         const int a = g % kSAStages;
         if (g >= kSAStages) mbar_wait_sleep(&B.a_empty[a], ((g / kSAStages) - 1) & 1, 64);
         const uint32_t bytes = (uint32_t)min(kSAK, p.nsteps - g * kSAK) * 4096u;
@@ -956,179 +988,170 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
         if (g == 0) stamp(1);
         if (g == n_groups - 1) stamp(2);
       }
+      __syncwarp();
     }
-  } else if (warp == kRMmaWarp) {
-    // ---------------- MMA issuer (as k_score_rows) ----------------
-    const uint32_t idesc1 = make_idesc_f16(128, H);
-    const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
-    // one iteration per group (its kSAK MMAs unrolled): waits, MMAs, commits in
-    // straight-line code.  A loop over K-steps with the waits at j == 0 and the
-    // commits at j == kSAK - 1 paced the rings at ~1200 cycles per group instead
-    // of ~410 (tools/ubench_c4.cu, k_bis V1 vs V3)
-    const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
-    for (int g = 0; g < n_groups; ++g) {
-      const int a = g % kSAStages, st = g % kSWStages;
-      mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
-      if (lane == 0 && g < 20) stamp(36 + g);
-      mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
-      if (lane == 0 && g < 16) stamp(72 + g);
-      tc_fence_after();
-      const int steps = min(kSAK, p.nsteps - g * kSAK);
-#pragma unroll
-      for (int j = 0; j < kSAK; ++j) {
-        if (j < steps) {
-          // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
-          const uint64_t ad = make_sdesc(aa + a * kSAStageBytes + j * 4096, 2048, 128);
-          const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
-          mma_f16_warp(tmem, ad, bd, idesc1, (g | j) ? 1u : 0u);
-        }
-      }
-      if (lane == 0 && g == 0) stamp(3);
-      mma_commit_warp(&B.a_empty[a]);
-      mma_commit_warp(&B.w_empty[st]);
-    }
-    if (lane == 0) stamp(4);
-    mma_commit_warp(&B.g1_done);
-    mbar_wait(&B.wimg, 0);
-    mbar_wait(&B.h_full, 0);
-    tc_fence_after();
-    if (lane == 0) {
-      const uint32_t idesc2 = make_idesc_f16(128, N2);
-      const uint32_t hb = smem_u32(heads);
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {
-        const uint32_t ab = smem_u32(region) + (uint32_t)pass * (kRR * H * 2);
-        for (int s = 0; s < H / 16; ++s) {
-          const uint64_t ad = make_sdesc(ab + s * (32 * kRR), 16 * kRR, 128);
-          const uint64_t bd = make_sdesc(hb + s * (32 * N2), 16 * N2, 128);
-          mma_f16_ss(tmem + H, ad, bd, idesc2, (pass | s) ? 1u : 0u);
-        }
-      }
-      mma_commit(&B.g2_done);
-    }
-    __syncwarp();
-    mbar_wait(&B.mu_full, 0);
-    tc_fence_after();
-    if (lane == 0) {
-      const uint32_t idesc3 = make_idesc_f16(128, H);
-      const uint64_t bd = make_sdesc(smem_u32(w3s), 16 * H, 128);
-      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 0u);
-      mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf) + kRR * 16 * 2, 16 * kRR, 128), bd, idesc3, 1u);
-      mma_commit(&B.g3_done);
-    }
-    __syncwarp();
   } else {
-    // ---------------- row threads: window sums while GEMM1 runs, then the epilogues ----------------
-    const int r = tid;
-    const int64_t row = row0 + r;
-    const bool valid = row < p.n;
-    if (p.sample) {   // fused ingest of this tick's sample, visible to the bulk copies (async proxy)
-      if (valid) {
-        switch (p.M) {
-          case 8: stream_push_one<2>(p, row); break;
-          case 16: stream_push_one<4>(p, row); break;
-          case 32: stream_push_one<8>(p, row); break;
-          default: stream_push_one<16>(p, row); break;
+    // ---------------- consumers: biases, TMEM ----------------
+    constexpr int kCons = kSThreads - 64;   // rows, MMA warp, helpers
+    const int ctid = warp < kRProdWarp ? tid : tid - 64;
+    for (int i = ctid; i < H; i += kCons) {
+      b1s[i] = __fmul_rn(p.b1[i], kTwoLog2e);   // E1 exponent bias (GEMM1 starts from zero)
+      b3s[i] = p.b3[i];
+      wbs[i] = p.wbar[i];
+    }
+    for (int i = ctid; i < N2; i += kCons) bmls[i] = p.bml[i];
+    for (int i = ctid; i < (int)(2 * kRR * 16 * 2 / 16); i += kCons)
+      reinterpret_cast<uint4 *>(mubuf)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 0) tmem_alloc(&B.tmem_slot, SL.tmem_cols);
+    tc_fence_before();
+    named_bar_sync_na(6, kCons);
+    tc_fence_after();
+    const uint32_t tmem = B.tmem_slot;
+
+    if (warp == kRMmaWarp) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc1 = make_idesc_f16(128, H);
+      const uint32_t aa = smem_u32(astage), ra = smem_u32(region);
+      // one iteration per group (its kSAK MMAs unrolled): waits, MMAs, commits in
+      // straight-line code.  A loop over K-steps with the waits at j == 0 and the
+      // commits at j == kSAK - 1 paced the rings at ~1200 cycles per group instead
+      // of ~410 (tools/ubench_c4.cu, k_bis V1 vs V3)
+      for (int g = 0; g < n_groups; ++g) {
+        const int a = g % kSAStages, st = g % kSWStages;
+        mbar_wait(&B.a_full[a], (g / kSAStages) & 1);
+        if (lane == 0 && g < 20) stamp(36 + g);
+        mbar_wait(&B.w_full[st], (g / kSWStages) & 1);
+        if (lane == 0 && g < 16) stamp(72 + g);
+        tc_fence_after();
+        const int steps = min(kSAK, p.nsteps - g * kSAK);
+#pragma unroll
+        for (int j = 0; j < kSAK; ++j) {
+          if (j < steps) {
+            // K-step j of the stage: [2 halves (LBO 2 KB)][16 row groups (SBO 128 B)][8 rows][16 B]
+            const uint64_t ad = make_sdesc(aa + a * kSAStageBytes + j * 4096, 2048, 128);
+            const uint64_t bd = make_sdesc(ra + st * SL.w_stage_bytes + j * 32 * H, 16 * H, 128);
+            mma_f16_warp(tmem, ad, bd, idesc1, (g | j) ? 1u : 0u);
+          }
         }
+        if (lane == 0 && g == 0) stamp(3);
+        mma_commit_warp(&B.a_empty[a]);
+        mma_commit_warp(&B.w_empty[st]);
       }
-      if constexpr (kLsuA) {
-        __threadfence_block();   // every row's pushed sample before the cp.async reads
-        __syncwarp();
-        named_bar_sync_na(5, kRowThreads);
-      } else {
+      if (lane == 0) stamp(4);
+      mma_commit_warp(&B.g1_done);
+      mbar_wait(&B.wimg, 0);
+      mbar_wait(&B.h_full, 0);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t idesc2 = make_idesc_f16(128, N2);
+        const uint32_t hb = smem_u32(heads);
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          const uint32_t ab = smem_u32(region) + (uint32_t)pass * (kRR * H * 2);
+          for (int s = 0; s < H / 16; ++s) {
+            const uint64_t ad = make_sdesc(ab + s * (32 * kRR), 16 * kRR, 128);
+            const uint64_t bd = make_sdesc(hb + s * (32 * N2), 16 * N2, 128);
+            mma_f16_ss(tmem + H, ad, bd, idesc2, (pass | s) ? 1u : 0u);
+          }
+        }
+        mma_commit(&B.g2_done);
+      }
+      __syncwarp();
+      mbar_wait(&B.mu_full, 0);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t idesc3 = make_idesc_f16(128, H);
+        const uint64_t bd = make_sdesc(smem_u32(w3s), 16 * H, 128);
+        mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf), 16 * kRR, 128), bd, idesc3, 0u);
+        mma_f16_ss(tmem, make_sdesc(smem_u32(mubuf) + kRR * 16 * 2, 16 * kRR, 128), bd, idesc3, 1u);
+        mma_commit(&B.g3_done);
+      }
+      __syncwarp();
+    } else if (warp >= kSHelperWarp0) {
+      // ---------------- helpers: the second E1 half and E3 chains 2, 3 of the rows of their quadrant ----------------
+      const int q4 = warp & 3, r = q4 * 32 + lane;
+      auto no_sx = []() -> float { return 0.f; };
+      rows_epilogue<H, ZP, RowBars, decltype(no_sx) &, 2>(
+          tmem, q4, lane, r, row0 + r, row0 + r < p.n, no_sx, region, mubuf, b1s, b3s, wbs, bmls, B,
+          p.Z, p.D, p.bbar, nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr,
+          nullptr, nullptr, 0, 0, e3part_of(smem, SL));
+    } else {
+      // ---------------- row threads: the fused ingest, window sums, the epilogues ----------------
+      const int r = tid;
+      const int64_t row = row0 + r;
+      const bool valid = row < p.n;
+      if (p.sample) {   // fused ingest of this tick's sample, visible to the bulk copies (async proxy)
+        if (valid) {
+          switch (p.M) {
+            case 8: stream_push_one<2>(p, row); break;
+            case 16: stream_push_one<4>(p, row); break;
+            case 32: stream_push_one<8>(p, row); break;
+            default: stream_push_one<16>(p, row); break;
+          }
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");   // pushes -> the bulk copies
         __syncwarp();   // reconverge after the per-row push
-        named_bar_sync_na(5, kRowThreads + 32);
+        named_bar_arrive(5, kRowThreads + 32);   // the A producer syncs before the last group
       }
-    }
-    if constexpr (kLsuA) {
-      // A groups (kSAK K-steps = 16 KB of the tile's contiguous canonical range)
-      // by cp.async, kSAStages - 1 groups in flight
-      const int n_groups = (p.nsteps + kSAK - 1) / kSAK;
-      const uint8_t *tsrc = reinterpret_cast<const uint8_t *>(p.ring16) +
-                            (((size_t)blockIdx.x * 2 * W + woff) * (size_t)(p.M >> 3) << 11);
-      const uint32_t abase = smem_u32(astage);
-      auto issue = [&](int g) {
-        const int a = g % kSAStages;
-        const int chunks = min(kSAK, p.nsteps - g * kSAK) * 256;   // 16-B chunks
-        const uint8_t *src = tsrc + (size_t)g * kSAStageBytes;
-        const uint32_t dst = abase + (uint32_t)a * kSAStageBytes;
-        for (int c = r; c < chunks; c += kRowThreads)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c),
-                       "l"(src + 16 * (size_t)c)
-                       : "memory");
-      };
-      constexpr int kDepth = kSAStages - 1;
-      for (int g = 0; g < kDepth; ++g) {
-        if (g < n_groups) issue(g);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
-      for (int g = 0; g < n_groups; ++g) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // -> the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&B.a_full[g % kSAStages]);
-        const int nx = g + kDepth;
-        if (nx < n_groups) {
-          if (nx >= kSAStages) mbar_wait(&B.a_empty[nx % kSAStages], ((nx / kSAStages) - 1) & 1);
-          issue(nx);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
-    }
-    const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
-    WinSum ws;
-    ws.init();
-    // window sums: each thread prefetches its row's W per-sample sums as aligned
-    // float4 (W <= 64: 17 x 16 B covering [woff, woff + W), issued now, in flight
-    // while the A groups stream) and folds them in WinSum order before E3
-    const bool pre = W <= 64;
-    const int wsh = woff & 3;   // uniform over the CTA
-    float4 sv4[17];
-    if (pre) {
-      const float4 *sp4 = reinterpret_cast<const float4 *>(
-          p.sums + (size_t)(valid ? row : 0) * sums_pitch(W) + (woff - wsh));
+      const int W8 = W & ~7, nb2 = 2 * (W8 / 16);
+      WinSum ws;
+      ws.init();
+      // window sums: each thread prefetches its row's W per-sample sums as aligned
+      // float4 (W <= 64: 17 x 16 B covering [woff, woff + W), issued now, in flight
+      // while the A groups stream) and folds them in WinSum order before E3
+      const bool pre = W <= 64;
+      const int wsh = woff & 3;   // uniform over the CTA
+      float4 sv4[17];
+      if (pre) {
+        const float4 *sp4 = reinterpret_cast<const float4 *>(
+            p.sums + (size_t)(valid ? row : 0) * sums_pitch(W) + (woff - wsh));
 #pragma unroll
-      for (int k = 0; k < 17; ++k)
-        sv4[k] = (valid && 4 * k < wsh + W) ? __ldg(sp4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    // (reduced only before E3, where MD needs it: off the E1 / E2 critical path)
-    auto sx_fn = [&]() -> float {
-      float sx = 0.f;
-      if (pre && valid) {
-        auto fold = [&](auto shift_c) {
-          constexpr int sh = decltype(shift_c)::value;
+        for (int k = 0; k < 17; ++k)
+          sv4[k] = (valid && 4 * k < wsh + W) ? __ldg(sp4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // (reduced only before E3, where MD needs it: off the E1 / E2 critical path)
+      auto sx_fn = [&]() -> float {
+        float sx = 0.f;
+        if (pre && valid) {
+          auto fold = [&](auto shift_c) {
+            constexpr int sh = decltype(shift_c)::value;
 #pragma unroll
-          for (int tau = 0; tau < 64; ++tau) {
-            if (tau < W) {
-              const int e = tau + sh;
-              const float4 q = sv4[e >> 2];
-              const float v = (e & 3) == 0 ? q.x : (e & 3) == 1 ? q.y : (e & 3) == 2 ? q.z : q.w;
-              ws.push(tau, v, W8, nb2);
+            for (int tau = 0; tau < 64; ++tau) {
+              if (tau < W) {
+                const int e = tau + sh;
+                const float4 q = sv4[e >> 2];
+                const float v = (e & 3) == 0 ? q.x : (e & 3) == 1 ? q.y : (e & 3) == 2 ? q.z : q.w;
+                ws.push(tau, v, W8, nb2);
+              }
             }
+          };
+          switch (wsh) {
+            case 0: fold(std::integral_constant<int, 0>{}); break;
+            case 1: fold(std::integral_constant<int, 1>{}); break;
+            case 2: fold(std::integral_constant<int, 2>{}); break;
+            default: fold(std::integral_constant<int, 3>{}); break;
           }
-        };
-        switch (wsh) {
-          case 0: fold(std::integral_constant<int, 0>{}); break;
-          case 1: fold(std::integral_constant<int, 1>{}); break;
-          case 2: fold(std::integral_constant<int, 2>{}); break;
-          default: fold(std::integral_constant<int, 3>{}); break;
+          sx = ws.acc0 + ws.acc1;
+        } else if (valid) {   // long windows: per-thread loads (the association of WinSum)
+          const float *sp = p.sums + (size_t)row * sums_pitch(W) + woff;
+          for (int tau = 0; tau < W; ++tau) ws.push(tau, __ldg(sp + tau), W8, nb2);
+          sx = ws.acc0 + ws.acc1;
         }
-        sx = ws.acc0 + ws.acc1;
-      } else if (valid) {   // long windows: per-thread loads (the association of WinSum)
-        const float *sp = p.sums + (size_t)row * sums_pitch(W) + woff;
-        for (int tau = 0; tau < W; ++tau) ws.push(tau, __ldg(sp + tau), W8, nb2);
-        sx = ws.acc0 + ws.acc1;
-      }
-      return sx;
-    };
-    if (r == 0) stamp(5);
-    rows_epilogue<H, ZP>(tmem, warp, lane, r, row, valid, sx_fn, region, mubuf, b1s, b3s, wbs, bmls, B,
-                         p.Z, p.D, p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr);
+        return sx;
+      };
+      // the window sum is folded now, while GEMM1 runs (the rows wait for it anyway)
+      const float sx_pre = sx_fn();
+      auto sx_get = [sx_pre]() -> float { return sx_pre; };
+      if (r == 0) stamp(5);
+      rows_epilogue<H, ZP, RowBars, decltype(sx_get) &, 1>(
+          tmem, warp, lane, r, row, valid, sx_get, region, mubuf, b1s, b3s, wbs, bmls, B, p.Z, p.D,
+          p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr, nullptr, nullptr, nullptr, nullptr, 0,
+          0, e3part_of(smem, SL));
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, SL.tmem_cols);
+  if (warp == 0) tmem_dealloc(B.tmem_slot, SL.tmem_cols);
 }
 
 unsigned long long *pair_trace();
