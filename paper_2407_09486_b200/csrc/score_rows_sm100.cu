@@ -78,7 +78,8 @@ struct RowLayoutSm {
 
 __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
                                                        uint32_t a_ring_bytes = kRAStages * kRAStepBytes,
-                                                       int w_stages = kRWStages) {
+                                                       int w_stages = kRWStages,
+                                                       int w_stage_steps = kRWStageSteps) {
   RowLayoutSm L;
   uint32_t o = 0;
   auto take = [&](uint32_t b, uint32_t a) {
@@ -87,7 +88,7 @@ __host__ __device__ inline RowLayoutSm row_smem_layout(int H, int ZP,
     o += b;
     return r;
   };
-  L.w_stage_bytes = (uint32_t)kRWStageSteps * 32 * H;
+  L.w_stage_bytes = (uint32_t)w_stage_steps * 32 * H;
   const uint32_t ring = (uint32_t)w_stages * L.w_stage_bytes, hb = 2u * kRR * H * 2;
   L.region = take(ring > hb ? ring : hb, 1024);      // W1 ring, then h hi | lo
   L.astage = take(a_ring_bytes, 1024);
@@ -785,14 +786,19 @@ enova_status stream_push(void *ring, int64_t n, int W, int M, const float *sampl
   return ENOVA_OK;
 }
 
-// A ring of the stream kernel: stages of kSAK K-steps = one 16 KB bulk copy of
-// the tile's contiguous canonical-layout range (4 x [2 halves][128 rows][16 B]).
-constexpr int kSAK = 4;
+// A ring of the stream kernel: stages of kSAK K-steps = one bulk copy of the
+// tile's contiguous canonical-layout range (kSAK x [2 halves][128 rows][16 B]);
+// the W1 ring's stages hold the same kSAK K-steps.
+#ifndef ENOVA_SAK
+#define ENOVA_SAK 8
+#endif
+constexpr int kSAK = ENOVA_SAK;
 // A group needs one A and one W1 stage: the two rings get the same depth, as
-// deep as shared memory allows (6 x 32 KB in flight per SM; with the MMA warp's
-// straight-line group loop a group takes ~410 cycles, the 4 MMAs' own cost).
-constexpr int kSAStages = 6;
-constexpr int kSWStages = 6;   // the stream kernel's W1 ring
+// deep as shared memory allows (192 KB in flight per SM; with the MMA warp's
+// straight-line group loop a 4-K-step group takes ~410 cycles, the 4 MMAs' own cost).
+constexpr int kSAStages = 24 / kSAK;
+constexpr int kSWStages = kSAStages;   // the stream kernel's W1 ring
+static_assert(kSWStages <= kMaxWStages && kSAStages <= kRAStages, "RowBars capacity");
 constexpr int kSAWarp = 6;                        // A producer warp
 constexpr int kSHelperWarp0 = 7;                  // warps 7-10: epilogue helpers (TMEM quadrant warp & 3)
 constexpr int kSThreads = kRThreads + 32 + kRowThreads;
@@ -801,7 +807,7 @@ constexpr int kSThreads = kRThreads + 32 + kRowThreads;
 __device__ __forceinline__ float *e3part_of(uint8_t *smem, const RowLayoutSm &SL) {
   return reinterpret_cast<float *>(smem + SL.mubuf);
 }
-constexpr uint32_t kSAStageBytes = kRR * 128;
+constexpr uint32_t kSAStageBytes = kRR * 32 * kSAK;
 
 struct StreamParams {
   const float *sums;        // [N][2W] fp32 sample sums
@@ -897,7 +903,7 @@ template <int H, int ZP>
 __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams p) {
   constexpr int N2 = 2 * ZP;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages);
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages, kSAK);
   uint8_t *region = smem + SL.region;
   uint8_t *astage = smem + SL.astage;
   uint8_t *heads = smem + SL.heads;
@@ -970,7 +976,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
       }
     }
   } else if (warp == kSAWarp) {
-    // ---------------- A producer: one 16 KB bulk copy (kSAK K-steps x 128 instances) per group ----------------
+    // ---------------- A producer: one bulk copy (kSAK K-steps x 128 instances) per group ----------------
     // The window's newest sample is its last K-step (last group): only that
     // group waits for this tick's fused pushes; the older groups stream while
     // the row threads ingest.
@@ -1163,7 +1169,7 @@ enova_status stream_detect(const void *ring, int64_t n, int64_t tick, const DetL
 
 template <int H, int ZP>
 static enova_status launch_stream_t(const StreamParams &p, cudaStream_t st) {
-  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages);
+  const RowLayoutSm SL = row_smem_layout(H, ZP, kSAStages * kSAStageBytes, kSWStages, kSAK);
   auto kern = k_stream_rows<H, ZP>;
   static thread_local int cached_dev = -1;
   int dev = 0;
