@@ -1506,15 +1506,15 @@ __device__ __forceinline__ void bin_add(unsigned long long *bins, int bi, double
   atomicAdd(bins + 3 * bi + 2, (unsigned long long)qq);
 }
 
-// PH_GRIDBIN / PH_BREFINE: sums of the P and L terms of up to 4 points over the
-// bins [b0, b1) (lanes over bins): per bin n f(x m) + 1/2 f''(x m) x^2 S2 with m
+// PH_GRIDBIN / PH_BREFINE: sums of the P and L terms of up to 4 points over
+// this CTA's bins (lanes over bins): per bin n f(x m) + 1/2 f''(x m) x^2 S2 with m
 // the bin mean and S2 = sum (y - m)^2 -- f = log1p, f'' = -1/(1+u)^2; P's term
 // -u/(1+u), its second derivative 2/(1+u)^3.  kDeriv (PH_BREFINE) adds the
 // x-derivatives of the sums at zeroth order in the bin spread (sum y and sum y^2
 // exact, 1/(1 + x y) taken at the bin mean): they only steer the binned Halley
 // steps, never a sign or a certified value.
 template <bool kDeriv>
-__device__ __forceinline__ void eval_bins(const unsigned long long *bins, int b0, int b1,
+__device__ __forceinline__ void eval_bins(const unsigned long long *bins, int j0, int j1,
                                           const double (&x)[4], int nu,
                                           double (&acc)[4][kSums], const LogTab &T, double l0,
                                           double bk, int cl) {
@@ -1522,7 +1522,9 @@ __device__ __forceinline__ void eval_bins(const unsigned long long *bins, int b0
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int k = 0; k < kSums; ++k) acc[u][k] = 0.0;
-  for (int b = b0 + (threadIdx.x & 31); b < b1; b += 32) {
+  // this CTA's bins b = blockIdx.x + j gridDim.x, j in [j0, j1) (lanes over j)
+  for (int j = j0 + (threadIdx.x & 31); j < j1; j += 32) {
+    const int b = (int)blockIdx.x + j * (int)gridDim.x;
     const long long cnt = (long long)__ldcg(bins + 3 * b);
     if (cnt == 0) continue;
     const double n = (double)cnt;
@@ -1698,11 +1700,11 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   const bool binned = (phase == PH_GRIDBIN || phase == PH_BREFINE);
   const int nk = phase_sums(phase);
   // PH_GRIDBIN: the list points over this CTA's slice of the bins, not over Y
+  // (bins dealt round-robin: CTA b takes bins b, b + grid, ... -- the occupied
+  // bins cluster in a few octaves, so contiguous slices left most CTAs idle)
   if (binned) {
-    const int nbn = f.nbins, nbk = gridDim.x;
-    const int b0 = (int)((int64_t)blockIdx.x * nbn / nbk), b1 = (int)((int64_t)(blockIdx.x + 1) * nbn / nbk);
-    c0 = b0;
-    c1 = b1;
+    c0 = 0;
+    c1 = (f.nbins - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   }
   // bundles of 4 list points (PH_GRID32: the fp64 points; the rest of the grid
   // is evaluated over the bins).  Warp items = (bundle, Y slice); the points are
