@@ -290,6 +290,12 @@ __global__ void __launch_bounds__(96, 1) k_bis(const uint8_t *__restrict__ A, ui
   if (tid == 0 && a_bytes == 12345u) out[0] = 1.f;
 }
 
+// launch-overhead probes: an empty kernel with D bytes of dynamic shared memory
+__global__ void k_empty(float *out) {
+  extern __shared__ uint8_t sm[];
+  if (threadIdx.x == 0 && out == nullptr) sm[0] = 1;
+}
+
 int main() {
   const size_t ring = (size_t)48 << 20;
   uint8_t *A, *Wt;
@@ -321,6 +327,37 @@ int main() {
            cudaGetErrorString(cudaGetLastError()));
   };
   run("empty launch (1 CTA, nothing)", 1, 0, 0, 0);
+  {
+    cudaFuncSetAttribute(k_empty, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    auto lat = [&](const char *name, int ctas, int thr, int smem, bool graph) {
+      cudaGraphExec_t ge = nullptr;
+      if (graph) {
+        cudaGraph_t g;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        k_empty<<<ctas, thr, smem, st>>>(out);
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+      }
+      auto once = [&] { if (graph) cudaGraphLaunch(ge, st); else k_empty<<<ctas, thr, smem, st>>>(out); };
+      for (int i = 0; i < 5; ++i) once();
+      cudaStreamSynchronize(st);
+      cudaEventRecord(a, st);
+      for (int i = 0; i < 200; ++i) once();
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("%-52s %7.2f us per launch (%s)\n", name, ms * 1e3 / 200, cudaGetErrorString(cudaGetLastError()));
+    };
+    lat("empty: 79 CTAs x 352 thr, 0 smem, stream", 79, 352, 0, false);
+    lat("empty: 79 CTAs x 352 thr, 210 KB smem, stream", 79, 352, 210 * 1024, false);
+    lat("empty: 79 CTAs x 352 thr, 100 KB smem, stream", 79, 352, 100 * 1024, false);
+    lat("empty: 79 CTAs x 352 thr, 0 smem, graph", 79, 352, 0, true);
+    lat("empty: 79 CTAs x 352 thr, 210 KB smem, graph", 79, 352, 210 * 1024, true);
+    lat("empty: 1 CTA x 32 thr, 0 smem, stream", 1, 32, 0, false);
+  }
   run("1 CTA: A 256K + W 256K", 1, 256 << 10, 256 << 10, 0);
   run("1 CTA: A 256K only", 1, 256 << 10, 0, 0);
   run("1 CTA: A 128K + W 128K traced", 1, 128 << 10, 128 << 10, 2);
