@@ -605,6 +605,17 @@ def run_threshold_sweep(args, rank, world, local_rank):
                       "fit_grid_points": 128, "fit_peaks": thr["n_peaks"],
                       "note": "stamps of CTA 0 (globaltimer); the fit is fp64 compute "
                               "(Grimshaw grid + certified Halley passes), not HBM-bound"}
+            if sampled and ns > 4:
+                # the one full pass over the scores (k_pot_scan) runs between the
+                # sampling launch's last stamp [3] and the selection launch's first
+                # [4]: the gap bounds the scan kernel's time (two launch gaps included)
+                gap = (st[4] - st[3]) / 1e3
+                phases["scan"] = {"kernel": "k_pot_scan", "gap_us": gap,
+                                  "achieved_GBps_lower_bound": 4.0 * n / (gap * 1e-6) / 1e9,
+                                  "hbm_frac_lower_bound": 4.0 * n / (gap * 1e-6) / 1e9 / load_peaks()["hbm"],
+                                  "note": "algorithmic bytes = one fp32 read of the scores; the "
+                                          "stamp gap includes the end of the sampling launch, two "
+                                          "launch gaps and the start of the selection launch"}
     peaks = load_peaks()
     ms = tot / args.steps
     achieved = 4.0 * n / (ms * 1e-3) / 1e9                 # algorithmic: one read of the shard
