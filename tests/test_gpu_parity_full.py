@@ -362,7 +362,8 @@ def _sampled_flag(E, ws):
     return int(ws.buf[off:off + 4].cpu().numpy().view(np.int32)[0])
 
 
-@pytest.mark.parametrize("kind", ["mixture", "sorted", "reversed", "ties", "blocks"])
+@pytest.mark.parametrize("kind", ["mixture", "sorted", "reversed", "ties", "blocks", "negative",
+                                  "straddle"])
 def test_sampled_selection_exact(E, kind):
     """n >= 2^22 takes the sampled path (strided sample -> lo, ONE full pass
     compacting the candidates, radix passes on the candidates only).  The
@@ -378,6 +379,11 @@ def test_sampled_selection_exact(E, kind):
         s = np.sort(s)[::-1].copy()
     elif kind == "ties":
         s = np.round(s, 1).astype(np.float32)
+    elif kind == "negative":      # every score < 0: the scan's general (key) path, lo < 2^31
+        s = (s - 60.0).astype(np.float32)
+    elif kind == "straddle":      # the quantile just below 0, the tail crossing 0 (-0.0 included)
+        s = (s - np.float32(np.quantile(s, 0.985))).astype(np.float32)
+        s[::1000] = np.float32(-0.0)
     elif kind == "blocks":        # the tail concentrated in a few contiguous blocks
         s = np.sort(s)
         cut = int(0.97 * n)
@@ -422,6 +428,20 @@ def test_sampled_selection_fallback(E):
     assert g["t"] == o["t"] and g["n_peaks"] == o["n_peaks"]
     assert abs(g["z_q"] - o["z_q"]) <= 1e-9 * abs(o["z_q"])
     assert _sampled_flag(E, ws) == 0, "lo above the quantile must fall back"
+
+
+def test_binned_fit_deterministic(E):
+    """The log2(Y) bins are int64 fixed-point sums (integer atomics, order-free):
+    repeated fits of the same scores -- binned grid pass, binned Halley start,
+    certifying fp64 passes -- give bit-identical thresholds (a replicated fleet
+    fit must agree bit for bit on every rank)."""
+    n = 6_000_000
+    s = cuda(np.random.default_rng(7).gamma(2.0, 1.0, n).astype(np.float32))
+    ws = E.ThresholdWorkspace(n)
+    a = [E.fit_threshold(s, 0.98, 1e-3, workspace=ws) for _ in range(3)]
+    assert a[0]["n_peaks"] >= 100_000
+    for b in a[1:]:
+        assert b["z_q"] == a[0]["z_q"] and b["gamma"] == a[0]["gamma"] and b["sigma"] == a[0]["sigma"]
 
 
 # --------------------------------------------- binned grid pass (N_t >= 1e5) ----
