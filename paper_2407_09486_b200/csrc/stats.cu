@@ -26,13 +26,34 @@
 
 namespace enova {
 
+unsigned long long *pair_trace();
+// diagnostic %globaltimer stamps of CTA 0 (compiled in with -DENOVA_TRACE only)
+__device__ __forceinline__ void k1_stamp(unsigned long long *tr, int slot) {
+#ifdef ENOVA_TRACE
+  if (tr && blockIdx.x == 0 && slot < 96) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[slot] = t;
+  }
+#else
+  (void)tr;
+  (void)slot;
+#endif
+}
+
 constexpr int kStatsThreads = 512;              // consumers
 constexpr int kStatsBlock = kStatsThreads + 32; // + the producer warp
 constexpr int kStatsMaxGrid = 512;   // <= 256 SMs x 2 (workspace sizing)
 // 3 x 64 KB in flight per SM (same-box ncu, c2: 5 x 32 KB 25.8 us, 10 x 16 KB
 // 29.5 us, 3 x 64 KB 23.6 us -- the bytes in flight per SM set the rate)
-constexpr int kStatsStages = 3;
-constexpr uint32_t kStatsChunkBytes = 65536;
+#ifndef ENOVA_STATS_STAGES
+#define ENOVA_STATS_STAGES 3
+#endif
+#ifndef ENOVA_STATS_CHUNK
+#define ENOVA_STATS_CHUNK 65536
+#endif
+constexpr int kStatsStages = ENOVA_STATS_STAGES;
+constexpr uint32_t kStatsChunkBytes = ENOVA_STATS_CHUNK;
 
 // contributors of one instance: a CTA range holds >= floor(N T / nb) >= 64
 // samples, so an instance of T samples meets at most ceil(nb / N) + 2 ranges
@@ -78,7 +99,7 @@ template <bool kPow2Group>
 __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     const float *__restrict__ X, int64_t ld, int M, int64_t N, int64_t T_cal,
     float *__restrict__ mean_out, float *__restrict__ std_out, unsigned long long *diag,
-    unsigned int *ticket, double *slots, int64_t max_contrib) {
+    unsigned int *ticket, double *slots, int64_t max_contrib, unsigned long long *tr) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t full[kStatsStages], empty[kStatsStages];
   __shared__ bool last;
@@ -101,6 +122,7 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) k1_stamp(tr, 0);
   if (tid >= kStatsThreads) {
     // ---------------- producer warp: bulk copies, kStatsStages chunks ahead ----------------
     if (lane == 0) {
@@ -113,6 +135,7 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
         const uint32_t bytes = (uint32_t)(c1 - c0) * 4u * (uint32_t)M;
         mbar_arrive_expect_tx(&full[sg], bytes);
         bulk_g2s(sm + (size_t)sg * kStatsChunkBytes, X + inst * ld + t * M, bytes, &full[sg]);
+        if (k < 24) k1_stamp(tr, 1 + k);
       }
     }
     return;   // the consumers never wait on the producer warp with a CTA barrier
@@ -124,7 +147,7 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
   int bad = 0;
   ChunkWalk w(r0, r1, T_cal, cs);
   int64_t c0, c1, ci;
-  int k = 0;
+  int k = 0, seg = 0;
   bool have = w.next(c0, c1, ci);
   while (have) {
     const int64_t inst = ci;
@@ -134,6 +157,7 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     do {
       const int sg = k % kStatsStages;
       mbar_wait(&full[sg], (k / kStatsStages) & 1);
+      if (tid == 0 && k < 24) k1_stamp(tr, 32 + k);
       const float4 *src = reinterpret_cast<const float4 *>(sm + (size_t)sg * kStatsChunkBytes);
       const int n = (int)(c1 - c0);
       if (act) {
@@ -153,6 +177,7 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
       have = w.next(c0, c1, ci);
     } while (have && ci == inst);
     // ---- the segment's sums: fixed-order reduction, contributor slot, ticket ----
+    if (tid == 0) k1_stamp(tr, 64 + 2 * min(seg, 7));
     double v8[8] = {a0, a1, a2, a3, q0, q1, q2, q3};
     int nred;   // partial sums per output left in red[] (summed below in index order)
     if (kPow2Group) {
@@ -233,10 +258,13 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
       }
     }
     named_bar_sync(1, kStatsThreads);   // red[] and `last` are reused by the next segment
+    if (tid == 0) k1_stamp(tr, 65 + 2 * min(seg, 7));
+    ++seg;
   }
   if (bad) atomicOr(&bad_any, 1);
   named_bar_sync(1, kStatsThreads);
   if (tid == 0 && bad_any) atomicAdd(diag + 1, 1ull);   // CTAs with a non-finite sample
+  if (tid == 0) k1_stamp(tr, 95);
 }
 
 // diag[0] = series whose std was floored, diag[1] = CTAs whose range held a
@@ -274,7 +302,7 @@ enova_status compute_stats_async(const enova_series *s, int64_t t_cal_end, float
   auto kern = pow2 ? k_series_stats<true> : k_series_stats<false>;
   ENOVA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ENOVA_LAUNCH(kern, (unsigned)nb, kStatsBlock, smem, st, s->metrics, s->ld_instance, M, N,
-               t_cal_end, mean, stdv, diag, ticket, slots, stats_max_contrib(N));
+               t_cal_end, mean, stdv, diag, ticket, slots, stats_max_contrib(N), pair_trace());
   ENOVA_CUDA_TRY(cudaGetLastError());
   return ENOVA_OK;
 }
