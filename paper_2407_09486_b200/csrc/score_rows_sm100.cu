@@ -243,20 +243,25 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
         tmem_ld8(hacc + ZP, vl);
       }
       tmem_wait_ld();
+      stamp(12);
+      // every term first (branch-free: independent chains the scheduler can
+      // interleave), then the sum in z order (the same additions as before:
+      // + 0.f for z >= Z leaves kl unchanged, kl >= +0)
+      float mz[ZP], tz[ZP];
+#pragma unroll
+      for (int z = 0; z < ZP; ++z) {
+        const float m = vm[z] + bmls[z];
+        const float t = kl_term2(m, vl[z] + bmls[ZP + z]);
+        mz[z] = z < Z ? m : 0.f;
+        tz[z] = z < Z ? t : 0.f;
+      }
       float kl = 0.f;
+#pragma unroll
+      for (int z = 0; z < ZP; ++z) kl += tz[z];
       uint32_t hi[8], lo[8];
 #pragma unroll
       for (int z = 0; z < ZP; z += 2) {
-        float m2[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          float m = 0.f;
-          if (z + u < Z) {
-            m = vm[z + u] + bmls[z + u];
-            kl += kl_term2(m, vl[z + u] + bmls[ZP + z + u]);
-          }
-          m2[u] = m;
-        }
+        const float m2[2] = {mz[z], mz[z + 1]};
         const uint32_t hp = cvt_pack_f16x2(m2[0], m2[1]);
         const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
         hi[z >> 1] = hp;
@@ -272,9 +277,11 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
       }
       score = fmaxf(0.5f * kl, 0.f);
     }
+    stamp(13);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncwarp();
+    stamp(14);
     if (lane == 0) mbar_arrive(&B.mu_full);
     stamp(9);
 
@@ -1045,8 +1052,14 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
       }
       if (lane == 0) stamp(4);
       mma_commit_warp(&B.g1_done);
+      // (the E-chain waits back off: a spinning MMA warp takes issue slots from
+      // the row warp that shares its SM sub-partition)
       mbar_wait(&B.wimg, 0);
+#ifdef ENOVA_MMA_SPIN
       mbar_wait(&B.h_full, 0);
+#else
+      mbar_wait_sleep(&B.h_full, 0, 32);
+#endif
       tc_fence_after();
       if (lane == 0) {
         const uint32_t idesc2 = make_idesc_f16(128, N2);
@@ -1063,7 +1076,11 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
         mma_commit(&B.g2_done);
       }
       __syncwarp();
+#ifdef ENOVA_MMA_SPIN
       mbar_wait(&B.mu_full, 0);
+#else
+      mbar_wait_sleep(&B.mu_full, 0, 32);
+#endif
       tc_fence_after();
       if (lane == 0) {
         const uint32_t idesc3 = make_idesc_f16(128, H);

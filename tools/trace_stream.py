@@ -42,6 +42,7 @@ names = ["start", "prod: first A TMA", "prod: last A TMA", "mma: first", "mma: l
 print(f"launch {e0.elapsed_time(e1) * 1e3:.1f} us")
 for i, nm in enumerate(names):
     print(f"{nm:22s} {(t[i] - t[0]) / 1e3:8.2f} us")
+print("E2 detail (us): tmem loaded %.2f, KL+pack+stores %.2f, fences+syncwarp %.2f" % tuple((t[i] - t[0]) / 1e3 for i in (12, 13, 14)))
 print("A TMA issued (us):", " ".join(f"{(t[16 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
 print("A ready at MMA (us):", " ".join(f"{(t[36 + g] - t[0]) / 1e3:.2f}" for g in range(16)))
 
