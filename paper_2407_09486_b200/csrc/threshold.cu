@@ -1709,7 +1709,11 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   // bundles of 4 list points (PH_GRID32: the fp64 points; the rest of the grid
   // is evaluated over the bins).  Warp items = (bundle, Y slice); the points are
   // spread evenly over the bundles (a refine pass's 6 points: 3 + 3, not 4 + 2)
+#ifndef ENOVA_AB_NOPOLE   // diagnostic A/B only (results invalid without the pole points)
   const int n64 = mixed ? f.n64 : npts;
+#else
+  const int n64 = mixed ? 0 : npts;
+#endif
   const int nA = (n64 + 3) / 4;
   const int sA = (nA >= kPotWarps) ? 1 : kPotWarps / max(nA, 1);
   const int items = nA * sA;
@@ -1759,7 +1763,11 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
       float lg;
       asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"((float)y));
       const int bi = min(max(__float2int_rd((lg - l0f) * bkf), 0), nbn - 1);
+#ifndef ENOVA_AB_NOBIN   // diagnostic A/B only (results invalid without the bins)
       bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
+#else
+      if (bi == -7) bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
+#endif
     }
 #pragma unroll
     for (int m = 0; m < kPow; ++m) {
