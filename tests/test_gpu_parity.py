@@ -375,7 +375,8 @@ def test_streaming_ring_matches_batch(E):
             assert torch.equal(f[:, 0], fb[:, k - W + 1])
 
 
-@pytest.mark.parametrize("W,M,H,Z,N", [(64, 16, 128, 16, 300), (32, 8, 32, 4, 130), (16, 32, 64, 8, 70)],
+@pytest.mark.parametrize("W,M,H,Z,N", [(64, 16, 128, 16, 300), (32, 8, 32, 4, 130), (16, 32, 64, 8, 70),
+                                       (20, 8, 64, 8, 200), (40, 16, 128, 16, 129)],
                          ids=lambda v: str(v))
 def test_stream_ring_matches_batch_and_oracle(E, W, M, H, Z, N):
     """a-10 fast path: ingest-normalised fp16 ring + TMA-fed row kernel.  Every
