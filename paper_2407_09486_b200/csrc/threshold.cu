@@ -86,6 +86,8 @@ constexpr int64_t kGrid32MinPeaks = 100000;
 constexpr int kMaxBins = 131072;          // binned grid pass: bins of log2(Y) (x3 int64 each)
 constexpr double kBinsPerOctave = 2048.0;
 constexpr int kPow = 6;   // power sums of u = Y / Ymax for the series points
+constexpr int kMaxPole = 8;      // hybrid pole points (the grid has 7 with x Ymax < -0.9)
+constexpr int kPoleList = 96;    // per-warp list of the pass's high Y (flushed when full)
 // phase program of k_pot
 enum { P_SAMPLE = 0, P_SCAN = 1, P_HIST0 = 2, P_HIST1 = 3, P_HIST2 = 4, P_COMPACT = 5, P_FIT = 6 };
 // sampled candidate selection (single GPU, n >= kSampleMinN): P_SAMPLE picks a
@@ -143,6 +145,13 @@ struct FitState {
   int bin_cl;                 // ceil(log2(N_t + 1)): fixed-point headroom of the bin sums
   int use_bins;               // the bins are filled (N_t >= kGrid32MinPeaks): PH_BREFINE first
   int biters, pad_b;          // PH_BREFINE passes run
+  // hybrid pole points (x Ymax < -0.9): the Y of bins >= bin_cb (y >~ Ymax / 2,
+  // where 1 + x y may approach 0) summed exactly in the PH_GRID32 pass (gP, gL:
+  // their mean P and L terms), the bins below bin_cb in PH_GRIDBIN (1 + x y >= ~1/2
+  // there: the binned model's accuracy holds); gmode 4 = pole point awaiting its
+  // binned part
+  int bin_cb, pole_hybrid;
+  double gP[kMaxPts], gL[kMaxPts];
   int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
   int exact[kMaxSlots];
@@ -950,14 +959,20 @@ __device__ void controller(FitState *f, int *scratch) {
           }
           f->gw[tid] = PL + P * L;
         } else if (mode == 2) {
-          f->gw[tid] = f->w[f->ginv[tid]];
+          if (f->pole_hybrid) {   // the exact high-Y part; the binned part follows
+            f->gP[tid] = f->P[f->ginv[tid]];
+            f->gL[tid] = f->L[f->ginv[tid]];
+            f->gmode[tid] = 4;
+          } else {
+            f->gw[tid] = f->w[f->ginv[tid]];
+          }
         }
       }
       __syncthreads();
       if (tid == 0) {   // the binned points' evaluation list (grid order)
         int nb = 0;
         for (int g = 0; g < ng; ++g)
-          if (f->gmode[g] == 0) {
+          if (f->gmode[g] == 0 || f->gmode[g] == 4) {
             f->gidx[nb] = g;
             f->xs[nb] = f->gx[g];
             ++nb;
@@ -970,7 +985,12 @@ __device__ void controller(FitState *f, int *scratch) {
     } else if (phase == PH_GRIDBIN) {
       if (tid < f->npts) {
         const int g = f->gidx[tid];
-        const double w = f->w[tid], P = f->P[tid], L = f->L[tid];
+        double w = f->w[tid], P = f->P[tid], L = f->L[tid];
+        if (f->gmode[g] == 4) {   // pole point: binned low bins + exact high Y
+          P += f->gP[g];
+          L += f->gL[g];
+          w = P + L + P * L;
+        }
         f->gw[g] = w;
         // the binned sums carry a third-order remainder <= ~3e-8 of |P| + |L| (bin
         // width 3.4e-4, x Ymax >= -0.9) and fp64 rounding: a 1e-6 bound leaves a
@@ -1371,6 +1391,9 @@ __device__ void setup_grid(FitState *f) {
       f->bin_cl = 64 - __clzll((long long)f->nt);   // N_t < 2^cl
       f->use_bins = 1;
       f->nbins = min(kMaxBins, (int)ceil(oct * bk) + 1);
+      // the first bin of the exactly summed high Y: bins from log2(Ymax / 2)
+      f->bin_cb = (int)fmin(fmax(floor((log2(ymax) - 1.0 - l0) * bk), 0.0), (double)f->nbins);
+      f->pole_hybrid = (n64 <= kMaxPole) ? 1 : 0;
     }
   }
 }
@@ -1517,7 +1540,7 @@ template <bool kDeriv>
 __device__ __forceinline__ void eval_bins(const unsigned long long *bins, int j0, int j1,
                                           const double (&x)[4], int nu,
                                           double (&acc)[4][kSums], const LogTab &T, double l0,
-                                          double bk, int cl) {
+                                          double bk, int cl, unsigned pole_mask = 0u, int cb = 0) {
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -1537,7 +1560,7 @@ __device__ __forceinline__ void eval_bins(const unsigned long long *bins, int j0
     const double s2 = fmax(qd - sd * dm, 0.0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (u < nu) {
+      if (u < nu && !(((pole_mask >> u) & 1u) && b >= cb)) {   // pole points: bins < cb only
         const double xm = x[u] * m;
         const double v = 1.0 + xm;
         const double r = rcp_nr(v);
@@ -1570,6 +1593,8 @@ struct FitShared {
   int scratch[32];
   double sred[kMaxPts][kSums];   // per warp item partial sums [slice * npts + pt][k]
   double powp[kPotWarps][kPow];  // PH_GRID32: per-warp power sums of Y / Ymax
+  double plist[kPotWarps][kPoleList];   // PH_GRID32: the warp's high Y awaiting evaluation
+  double pacc[kPotWarps][kMaxPole][2];  // PH_GRID32: per-warp exact P, L sums of the pole points
   double red[kSums][kMaxPts];    // grid totals after the barrier
 };
 
@@ -1709,8 +1734,11 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
   // bundles of 4 list points (PH_GRID32: the fp64 points; the rest of the grid
   // is evaluated over the bins).  Warp items = (bundle, Y slice); the points are
   // spread evenly over the bundles (a refine pass's 6 points: 3 + 3, not 4 + 2)
+  // (PH_GRID32 with hybrid pole points: no warp items -- the pole points' exact
+  // high-Y part is summed in the mixed loop below)
+  const bool hybrid = mixed && f.pole_hybrid;
 #ifndef ENOVA_AB_NOPOLE   // diagnostic A/B only (results invalid without the pole points)
-  const int n64 = mixed ? f.n64 : npts;
+  const int n64 = mixed ? (hybrid ? 0 : f.n64) : npts;
 #else
   const int n64 = mixed ? 0 : npts;
 #endif
@@ -1731,8 +1759,12 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
       eval_bundle<true>(Y, s0, s1, x, nu, acc, S.tab);
     else if (phase == PH_BREFINE)
       eval_bins<true>(bins, (int)s0, (int)s1, x, nu, acc, S.tab, f.bin_l0, f.bin_k, f.bin_cl);
-    else if (binned)
-      eval_bins<false>(bins, (int)s0, (int)s1, x, nu, acc, S.tab, f.bin_l0, f.bin_k, f.bin_cl);
+    else if (binned) {
+      unsigned pm = 0u;   // PH_GRIDBIN list points that are hybrid pole points
+      for (int u = 0; u < nu; ++u) pm |= (f.gmode[f.gidx[base + u]] == 4 ? 1u : 0u) << u;
+      eval_bins<false>(bins, (int)s0, (int)s1, x, nu, acc, S.tab, f.bin_l0, f.bin_k, f.bin_cl,
+                       pm, f.bin_cb);
+    }
     else
       eval_bundle<false>(Y, s0, s1, x, nu, acc, S.tab);
     if (lane == 0) {
@@ -1751,24 +1783,71 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
     double q[kPow];
 #pragma unroll
     for (int m = 0; m < kPow; ++m) q[m] = 0.0;
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const double y = Y[i];
-      const double u = y * iy;
-      double pw_ = u;
+    const int np = hybrid ? f.n64 : 0, cb = f.bin_cb;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int i = lane; i < 2 * kMaxPole; i += 32) (&S.pacc[warp][0][0])[i] = 0.0;
+    __syncwarp();
+    double *lst = S.plist[warp];
+    int cnt = 0;   // warp-uniform: high Y in the warp's list
+    // the list's contributions to every pole point (list order; lanes over items,
+    // fixed xor tree, added to the warp's sums in flush order)
+    auto flush = [&]() {
+      for (int u = 0; u < np; ++u) {
+        const double x = f.xs[u];
+        double aP = 0.0, aL = 0.0;
+        for (int j = lane; j < cnt; j += 32) {
+          const double yv = lst[j];
+          const double xy = x * yv, v = 1.0 + xy, r = rcp_nr(v);
+          aP -= xy * r;
+          aL += log1p_fast(xy, v, r, S.tab);
+        }
 #pragma unroll
-      for (int m = 0; m < kPow; ++m) {
-        q[m] += pw_;
-        pw_ *= u;
+        for (int o = 16; o; o >>= 1) {
+          aP += __shfl_xor_sync(0xffffffffu, aP, o);
+          aL += __shfl_xor_sync(0xffffffffu, aL, o);
+        }
+        if (lane == 0) {
+          S.pacc[warp][u][0] += aP;
+          S.pacc[warp][u][1] += aL;
+        }
       }
-      float lg;
-      asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"((float)y));
-      const int bi = min(max(__float2int_rd((lg - l0f) * bkf), 0), nbn - 1);
+      __syncwarp();
+      cnt = 0;
+    };
+    // thread (warp, lane) takes i = c0 + tid + k blockDim as before (power-sum order
+    // unchanged); the warp-uniform trip count lets the warp ballot its high Y
+    for (int64_t i0 = c0 + (int64_t)warp * 32; i0 < c1; i0 += blockDim.x) {
+      const int64_t i = i0 + lane;
+      const bool ok = i < c1;
+      const double y = ok ? Y[i] : 0.0;
+      int bi = -1;
+      if (ok) {
+        const double u = y * iy;
+        double pw_ = u;
+#pragma unroll
+        for (int m = 0; m < kPow; ++m) {
+          q[m] += pw_;
+          pw_ *= u;
+        }
+        float lg;
+        asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"((float)y));
+        bi = min(max(__float2int_rd((lg - l0f) * bkf), 0), nbn - 1);
 #ifndef ENOVA_AB_NOBIN   // diagnostic A/B only (results invalid without the bins)
-      bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
+        bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
 #else
-      if (bi == -7) bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
+        if (bi == -7) bin_add(bins, bi, y, f.bin_l0, f.bin_k, f.bin_cl);
 #endif
+      }
+      const bool hi = np > 0 && bi >= cb;
+      const unsigned bal = __ballot_sync(0xffffffffu, hi);
+      if (bal) {
+        if (cnt + 32 > kPoleList) flush();
+        if (hi) lst[cnt + __popc(bal & lt)] = y;
+        __syncwarp();
+        cnt += __popc(bal);
+      }
     }
+    if (cnt) flush();
 #pragma unroll
     for (int m = 0; m < kPow; ++m) {
 #pragma unroll
@@ -1782,11 +1861,16 @@ __device__ void fit_eval_partials(FitShared &S, const double *Y, int64_t c0, int
     for (int w = 0; w < kPotWarps; ++w) sp += S.powp[w][threadIdx.x];
     pw[((size_t)2 * kMaxPts + threadIdx.x) * kMaxCtas + blockIdx.x] = sp;
   }
-  // CTA partial per (k, point): slices summed in order
+  // CTA partial per (k, point): slices summed in order (hybrid PH_GRID32: the
+  // pole points' exact high-Y sums, warps summed in order)
   for (int i = threadIdx.x; i < nk * npts; i += blockDim.x) {
     const int k = i / npts, pt = i % npts;
     double s = 0.0;
-    for (int sl = 0; sl < sA; ++sl) s += S.sred[sl * npts + pt][k];
+    if (hybrid) {
+      for (int w = 0; w < kPotWarps; ++w) s += S.pacc[w][pt][k];
+    } else {
+      for (int sl = 0; sl < sA; ++sl) s += S.sred[sl * npts + pt][k];
+    }
     pw[((size_t)k * kMaxPts + pt) * kMaxCtas + blockIdx.x] = s;
   }
 }
