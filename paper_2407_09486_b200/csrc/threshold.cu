@@ -65,6 +65,12 @@ enum { PH_GRID = 0, PH_REFINE = 1, PH_FINAL = 2, PH_DONE = 3, PH_GRID32 = 4, PH_
 // within rounding of it and the next pass certifies it -- two passes over Y
 // instead of five from the grid's secant point.
 constexpr int kMaxBinRefine = 4;
+// a binned Halley step below this (relative) ends the binned passes: the
+// iterate it produced is then within the binned model's error of the root
+#ifndef ENOVA_BREF_TOL
+#define ENOVA_BREF_TOL 1e-10
+#endif
+constexpr double kBrefTol = ENOVA_BREF_TOL;
 // evaluation sums per point of a pass: P, L (+ first and second derivatives)
 __device__ __forceinline__ int phase_sums(int phase) {
   return (phase == PH_REFINE || phase == PH_BREFINE) ? kSums : 2;
@@ -1131,7 +1137,7 @@ __device__ void controller(FitState *f, int *scratch) {
       const double den = 2.0 * dw * dw - w * ddw;
       xn = (den != 0.0 && isfinite(den)) ? x - 2.0 * w * dw / den : (dw != 0.0 ? x - w / dw : x);
       if (!(xn > a && xn < b)) xn = (xn <= a) ? 0.5 * (x + a) : 0.5 * (x + b);
-      conv = fabs(xn - x) <= 1e-10 * fabs(x);
+      conv = fabs(xn - x) <= kBrefTol * fabs(x);
     }
     const int all_conv = __syncthreads_and(conv);   // every read of xs / w done
     const bool done = all_conv || it + 1 >= kMaxBinRefine;
