@@ -158,6 +158,8 @@ struct FitState {
   // binned part
   int bin_cb, pole_hybrid;
   double gP[kMaxPts], gL[kMaxPts];
+  double bdiag[kMaxBinRefine][4];   // diagnostic build (ENOVA_FIT_STAMPS): binned Halley steps
+  int bdiag_nr, pad_bd;
   int rdone[kMaxSlots];       // refine slot converged (triple mode)
   double lo[kMaxSlots], hi[kMaxSlots], wlo[kMaxSlots], whi[kMaxSlots];
   int exact[kMaxSlots];
@@ -1136,8 +1138,13 @@ __device__ void controller(FitState *f, int *scratch) {
       const double a = fmin(f->lo[sidx], f->hi[sidx]), b = fmax(f->lo[sidx], f->hi[sidx]);
       const double den = 2.0 * dw * dw - w * ddw;
       xn = (den != 0.0 && isfinite(den)) ? x - 2.0 * w * dw / den : (dw != 0.0 ? x - w / dw : x);
-      if (!(xn > a && xn < b)) xn = (xn <= a) ? 0.5 * (x + a) : 0.5 * (x + b);
+      const bool clamped = !(xn > a && xn < b);
+      if (clamped) xn = (xn <= a) ? 0.5 * (x + a) : 0.5 * (x + b);
       conv = fabs(xn - x) <= kBrefTol * fabs(x);
+#ifdef ENOVA_FIT_STAMPS   // diagnostic: per pass and root, the relative step (negative if clamped)
+      if (it < kMaxBinRefine && tid < 4) f->bdiag[it][tid] = (clamped ? -1.0 : 1.0) * fabs(xn - x) / fabs(x);
+      if (tid == 0) f->bdiag_nr = nr;
+#endif
     }
     const int all_conv = __syncthreads_and(conv);   // every read of xs / w done
     const bool done = all_conv || it + 1 >= kMaxBinRefine;
@@ -1951,6 +1958,11 @@ __device__ void fit_finish_pass(FitShared &S) {
 // the fit's result -> PotGlobal (CTA 0, thread 0)
 __device__ void fit_publish(const PotArgs &a, const FitState &f) {
   PotGlobal *g = a.g;
+#ifdef ENOVA_FIT_STAMPS   // diagnostic: the binned Halley steps into the stamp slots 72..88
+  for (int i = 0; i < kMaxBinRefine * 4; ++i)
+    g->stamps[72 + i] = (unsigned long long)__double_as_longlong((&f.bdiag[0][0])[i]);
+  g->stamps[88] = (unsigned long long)f.bdiag_nr;
+#endif
   g->gamma = f.gamma;
   g->sigma = f.sigma;
   g->z_q = f.z_q;
