@@ -334,7 +334,7 @@ def run_streaming(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def run(k0, e2e, gate=False, per_tick=True):
+    def run(k0, e2e, gate=False, per_tick=True, direct=False):
         starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
         flags_h = torch.empty(n, dtype=torch.int8).pin_memory()
         if gate:
@@ -349,6 +349,8 @@ def run_streaming(args, rank, world, local_rank):
             if e2e:
                 stage.copy_(S_h[k], non_blocking=True)
                 graphs[(t_hist + k) % W].replay()
+            elif direct:   # the fused kernel launched straight through the C ABI
+                ring.step(S[k], t_hist + k, thr_dev, out=(flags, scores, md))
             else:
                 tick_graphs[k - k0].replay()
             if e2e:
@@ -368,6 +370,7 @@ def run_streaming(args, rank, world, local_rank):
         # throughput: the same back-to-back ticks with events only around the
         # timed region (per-tick event records add ~1 us of stream gaps each)
         _, tot = run(0, False, gate=True, per_tick=False)
+        _, tot_direct = run(0, False, gate=True, per_tick=False, direct=True)
     # validate the last tick against a batch scoring of the same windows
     t_last = t_hist + ticks - 1
     fb, sb, mb = E.detect(X[:, t_last - W + 1:t_last + 1].contiguous(), det, mean, std, thr,
@@ -489,6 +492,7 @@ def run_streaming(args, rank, world, local_rank):
                                            "note": "each tick's graph launched from the Python loop "
                                                    "as the previous one is queued: includes the "
                                                    "host launch rate"},
+            "tick_direct_launch_us": 1e3 * tot_direct / args.steps,
             "tick_latency_us": {"p50": 1e3 * _pct(lat, 50), "p99": 1e3 * _pct(lat, 99),
                                 "max": 1e3 * max(lat), "mean_per_tick_events": 1e3 * tot_ev / args.steps,
                                 "note": "events around every tick (a separate back-to-back run); "
