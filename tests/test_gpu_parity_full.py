@@ -445,13 +445,14 @@ def test_binned_fit_deterministic(E):
 
 
 # --------------------------------------------- binned grid pass (N_t >= 1e5) ----
-@pytest.mark.parametrize("kind", ["exp", "gpd_heavy", "gpd_neg", "ties", "wide"])
+@pytest.mark.parametrize("kind", ["exp", "gpd_heavy", "gpd_neg", "gpd_neg45", "ties", "wide"])
 def test_binned_grid_fit_matches_oracle(E, kind):
     """The fit's binned grid pass (k_pot PH_GRIDBIN: N_t >= 1e5 peaks; the non-pole
     grid points evaluated over a log2 histogram of Y with the second-order
     correction, certified signs, uncertain points re-evaluated in fp64 -- R-13)
     on tails of different shapes: exponential, heavy (xi = 0.5), bounded
-    (xi = -0.2), heavy ties, and a tail spanning ~30 octaves.  6M scores ->
+    (xi = -0.2 and -0.45: roots near the pole, many Y in the hybrid pole points'
+    exact high bins), heavy ties, and a tail spanning ~30 octaves.  6M scores ->
     120k peaks; t, N_t and the method exact, z_q within 1e-9 of the oracle's
     fp64 scan + bisection."""
     n = 6_000_000
@@ -462,6 +463,8 @@ def test_binned_grid_fit_matches_oracle(E, kind):
         s = 2.0 / 0.5 * (r.uniform(size=n) ** -0.5 - 1.0)
     elif kind == "gpd_neg":
         s = 2.0 / -0.2 * (r.uniform(size=n) ** 0.2 - 1.0)
+    elif kind == "gpd_neg45":     # strongly bounded: the root near the pole x -> -1/Ymax,
+        s = 2.0 / -0.45 * (r.uniform(size=n) ** 0.45 - 1.0)   # many Y in the exact high bins
     elif kind == "ties":
         s = np.round(r.exponential(1.0, n), 3)
     else:   # tail values from ~1e-6 to ~1e3 above t
