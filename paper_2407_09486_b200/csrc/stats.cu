@@ -53,6 +53,7 @@ constexpr int kStatsMaxGrid = 512;   // <= 256 SMs x 2 (workspace sizing)
 #define ENOVA_STATS_CHUNK 65536
 #endif
 constexpr int kStatsStages = ENOVA_STATS_STAGES;
+constexpr int kStatsDefer = 64;   // segments whose ticket / combine wait for finalize()
 constexpr uint32_t kStatsChunkBytes = ENOVA_STATS_CHUNK;
 
 // contributors of one instance: a CTA range holds >= floor(N T / nb) >= 64
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     unsigned int *ticket, double *slots, int64_t max_contrib, unsigned long long *tr) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t full[kStatsStages], empty[kStatsStages];
-  __shared__ bool last;
+  __shared__ long long dinst[kStatsDefer];   // deferred segments: their instances
+  __shared__ int dlast[kStatsDefer];         //   and whether this CTA is the last contributor
   __shared__ int bad_any;
   double *red = reinterpret_cast<double *>(sm + kStatsStages * kStatsChunkBytes);  // [rows][2][M]
   const int G = M / 4;
@@ -141,6 +143,55 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
     return;   // the consumers never wait on the producer warp with a CTA barrier
   }
   // ---------------- consumers ----------------
+  // finalize(): for every deferred segment (instance inst, this CTA's slot
+  // written), the instance's ticket -- an acq_rel RMW at gpu scope after the
+  // CTA barrier: it releases this CTA's slot writes (cumulative over the
+  // barrier) and, for the last contributor, acquires every other contributor's
+  // (no full fences) -- then the last contributor combines the slots in
+  // contributor order: mean = K + S1/n, var = S2/n - (S1/n)^2
+  int ndef = 0;   // uniform over the consumer threads
+  auto finalize = [&]() {
+    named_bar_sync(1, kStatsThreads);
+    for (int q = tid; q < ndef; q += kStatsThreads) {
+      const int64_t inst = dinst[q];
+      const int64_t first = cta_of(inst * T_cal, S, nb);
+      const int64_t ncontrib = cta_of((inst + 1) * T_cal - 1, S, nb) - first + 1;
+      unsigned int old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "l"(ticket + inst)
+                   : "memory");
+      dlast[q] = (old == (unsigned)ncontrib - 1) ? 1 : 0;
+    }
+    named_bar_sync(1, kStatsThreads);
+    for (int w = tid; w < ndef * M; w += kStatsThreads) {
+      const int q = w / M, j = w % M;
+      if (!dlast[q]) continue;
+      const int64_t inst = dinst[q];
+      const int64_t first = cta_of(inst * T_cal, S, nb);
+      const int64_t ncontrib = cta_of((inst + 1) * T_cal - 1, S, nb) - first + 1;
+      const double *p0 = slots + (size_t)inst * max_contrib * 2 * M;
+      double s1 = 0, s2 = 0;
+      for (int64_t c = 0; c < ncontrib; ++c) {
+        s1 += *(volatile const double *)(p0 + (size_t)c * 2 * M + j);
+        s2 += *(volatile const double *)(p0 + (size_t)c * 2 * M + M + j);
+      }
+      const double n = (double)T_cal;
+      const double kj = (double)__ldg(X + inst * ld + j);
+      const double m1 = s1 / n;
+      double var = s2 / n - m1 * m1;
+      if (var < 0) var = 0;
+      double sd = sqrt(var);
+      if (sd < 1e-6) {
+        atomicAdd(diag + 0, 1ull);
+        sd = 1e-6;
+      }
+      mean_out[inst * M + j] = (float)(kj + m1);
+      std_out[inst * M + j] = (float)sd;
+    }
+    named_bar_sync(1, kStatsThreads);   // dinst / dlast are reused
+    ndef = 0;
+  };
   const int g = tid % G;
   const int slot = tid / G;
   const bool act = tid < active;
@@ -221,46 +272,18 @@ __global__ void __launch_bounds__(kStatsBlock, 1) k_series_stats(
       for (int q = 0; q < nred; ++q) sacc += red[(size_t)q * 2 * M + e];
       pc[e] = sacc;
     }
-    // the last contributor of this instance combines the slots in order: the
-    // ticket is an acq_rel RMW at gpu scope after the CTA barrier -- it releases
-    // this CTA's slot writes (cumulative over the barrier) and, for the last
-    // contributor, acquires every other contributor's (no full fences)
-    named_bar_sync(1, kStatsThreads);
-    if (tid == 0) {
-      unsigned int old;
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                   : "=r"(old)
-                   : "l"(ticket + inst)
-                   : "memory");
-      last = (old == (unsigned)ncontrib - 1);
-    }
-    named_bar_sync(1, kStatsThreads);
-    if (last) {
-      for (int j = tid; j < M; j += kStatsThreads) {
-        const double *p0 = slots + (size_t)inst * max_contrib * 2 * M;
-        double s1 = 0, s2 = 0;
-        for (int64_t q = 0; q < ncontrib; ++q) {
-          s1 += *(volatile const double *)(p0 + (size_t)q * 2 * M + j);
-          s2 += *(volatile const double *)(p0 + (size_t)q * 2 * M + M + j);
-        }
-        const double n = (double)T_cal;
-        const double kj = (double)__ldg(X + inst * ld + j);
-        const double m1 = s1 / n;
-        double var = s2 / n - m1 * m1;
-        if (var < 0) var = 0;
-        double sd = sqrt(var);
-        if (sd < 1e-6) {
-          atomicAdd(diag + 0, 1ull);
-          sd = 1e-6;
-        }
-        mean_out[inst * M + j] = (float)(kj + m1);
-        std_out[inst * M + j] = (float)sd;
-      }
-    }
-    named_bar_sync(1, kStatsThreads);   // red[] and `last` are reused by the next segment
+    // the tickets and the last contributors' combines of this CTA's segments
+    // are deferred to the end of its range (or to a full list): one round of
+    // tickets and one of combines instead of two dependent global round trips
+    // per segment on the streaming path
+    if (tid == 0) dinst[ndef] = inst;
+    ++ndef;
+    named_bar_sync(1, kStatsThreads);   // red[] is reused by the next segment
+    if (ndef == kStatsDefer) finalize();
     if (tid == 0) k1_stamp(tr, 65 + 2 * min(seg, 7));
     ++seg;
   }
+  if (ndef) finalize();
   if (bad) atomicOr(&bad_any, 1);
   named_bar_sync(1, kStatsThreads);
   if (tid == 0 && bad_any) atomicAdd(diag + 1, 1ull);   // CTAs with a non-finite sample
