@@ -486,7 +486,10 @@ def test_async_failures_are_reported_on_device(E):
 def test_stats_chunked_one_pass_matches_oracle(E):
     """One-pass shifted sums over time chunks: many instances (1 chunk each) and
     few long ones (up to 16 chunks), incl. a degenerate and an offset series."""
-    for N, T, M in ((1, 20000, 8), (3, 9000, 32), (700, 300, 16)):
+    # (20000, 100, 8) and (5000, 80, 24): > 64 instance segments per CTA, so the
+    # deferred tickets / combines are flushed mid-range (kStatsDefer) as well as
+    # at the end; M = 24 takes the non-power-of-two reduction
+    for N, T, M in ((1, 20000, 8), (3, 9000, 32), (700, 300, 16), (20000, 100, 8), (5000, 80, 24)):
         X = synth.metric_trace(N, T, M, seed=53 + N)
         X[0, :, 1] = 7.25                                    # constant -> floored
         X[-1, :, 0] += 1e4                                   # large offset vs spread
