@@ -69,6 +69,7 @@ struct RowBars {
   uint64_t w_full[kMaxWStages], w_empty[kMaxWStages], a_full[kRAStages], a_empty[kRAStages];
   uint64_t wimg, g1_done, h_full, g2_done, mu_full, g3_done;
   uint64_t e3_done;   // split epilogue (stream kernel): the helpers' E3 partials are in smem
+  uint64_t e2_done;   // split epilogue, ZP = 16: the helpers' KL terms z = 8..15 are in smem
   uint32_t tmem_slot, pad;
 };
 
@@ -162,7 +163,8 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
                                               const float *wbarm_s = nullptr,
                                               const float *xsum = nullptr,
                                               const float *bbarm = nullptr, float *md_metric = nullptr,
-                                              int M = 0, int W = 0, float *e3part = nullptr) {
+                                              int M = 0, int W = 0, float *e3part = nullptr,
+                                              float *e2part = nullptr) {
   auto stamp = [&](int slot) {   // diagnostic; compiled in with -DENOVA_TRACE only
 #ifdef ENOVA_TRACE
     if (tr && r == 0) {
@@ -202,6 +204,42 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
     __syncwarp();
     if (lane == 0) mbar_arrive(&B.h_full);
     stamp(7);
+    if constexpr (kPart == 2 && ZP == 16) {
+      // helper: E2 for z = 8..15 -- the KL terms into e2part (the row thread sums
+      // all 16 in z order), mu's hi / lo pairs of that K half into the GEMM3 image
+      mbar_wait_sleep(&B.g2_done, 0, 32);
+      tc_fence_after();
+      float vm[8], vl[8];
+      tmem_ld8(lane_addr + H + 8, vm);
+      tmem_ld8(lane_addr + H + ZP + 8, vl);
+      tmem_wait_ld();
+      float mz[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const float m = vm[z] + bmls[8 + z];
+        const float t = kl_term2(m, vl[z] + bmls[ZP + 8 + z]);
+        mz[z] = 8 + z < Z ? m : 0.f;
+        e2part[z * kRR + r] = 8 + z < Z ? t : 0.f;
+      }
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int z = 0; z < 8; z += 2) {
+        const uint32_t hp = cvt_pack_f16x2(mz[z], mz[z + 1]);
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
+        hi[z >> 1] = hp;
+        lo[z >> 1] = cvt_pack_f16x2(mz[z] - hf.x, mz[z + 1] - hf.y);
+      }
+      const size_t off1 = kmajor_step_offset(r, 8, kRR);
+      *reinterpret_cast<uint4 *>(mubuf + off1) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off1) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&B.mu_full);
+        mbar_arrive(&B.e2_done);
+      }
+    }
     if constexpr (kPart == 2) {
       // helper: E3 chains 2, 3 -> e3part
       mbar_wait_sleep(&B.g3_done, 0, 32);
@@ -247,20 +285,19 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
       // every term first (branch-free: independent chains the scheduler can
       // interleave), then the sum in z order (the same additions as before:
       // + 0.f for z >= Z leaves kl unchanged, kl >= +0)
+      // (split, ZP = 16: this thread takes z = 0..7, its helper z = 8..15)
+      constexpr int kZ1 = (kPart == 1 && ZP == 16) ? 8 : ZP;
       float mz[ZP], tz[ZP];
 #pragma unroll
-      for (int z = 0; z < ZP; ++z) {
+      for (int z = 0; z < kZ1; ++z) {
         const float m = vm[z] + bmls[z];
         const float t = kl_term2(m, vl[z] + bmls[ZP + z]);
         mz[z] = z < Z ? m : 0.f;
         tz[z] = z < Z ? t : 0.f;
       }
-      float kl = 0.f;
-#pragma unroll
-      for (int z = 0; z < ZP; ++z) kl += tz[z];
       uint32_t hi[8], lo[8];
 #pragma unroll
-      for (int z = 0; z < ZP; z += 2) {
+      for (int z = 0; z < kZ1; z += 2) {
         const float m2[2] = {mz[z], mz[z + 1]};
         const uint32_t hp = cvt_pack_f16x2(m2[0], m2[1]);
         const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
@@ -270,19 +307,27 @@ __device__ __forceinline__ void rows_epilogue(uint32_t tmem, int warp, int lane,
       const size_t off0 = kmajor_step_offset(r, 0, kRR);
       *reinterpret_cast<uint4 *>(mubuf + off0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if constexpr (ZP == 16) {
+      if constexpr (ZP == 16 && kZ1 == ZP) {
         const size_t off1 = kmajor_step_offset(r, 8, kRR);
         *reinterpret_cast<uint4 *>(mubuf + off1) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
         *reinterpret_cast<uint4 *>(mubuf + kRR * 32 + off1) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
       }
+      stamp(13);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      stamp(14);
+      if (lane == 0) mbar_arrive(&B.mu_full);
+      if constexpr (kZ1 < ZP) {   // the helper's terms, then the sum in z order
+        mbar_wait(&B.e2_done, 0);
+#pragma unroll
+        for (int z = kZ1; z < ZP; ++z) tz[z] = e2part[(z - kZ1) * kRR + r];
+      }
+      float kl = 0.f;
+#pragma unroll
+      for (int z = 0; z < ZP; ++z) kl += tz[z];
       score = fmaxf(0.5f * kl, 0.f);
     }
-    stamp(13);
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    stamp(14);
-    if (lane == 0) mbar_arrive(&B.mu_full);
     stamp(9);
 
     // ---- E3: MD by the column-sum identity; flag ----
@@ -814,6 +859,11 @@ constexpr int kSThreads = kRThreads + 32 + kRowThreads;
 __device__ __forceinline__ float *e3part_of(uint8_t *smem, const RowLayoutSm &SL) {
   return reinterpret_cast<float *>(smem + SL.mubuf);
 }
+// the helpers' KL terms z = 8..15 ([8][128] floats) in the explain-only w_bar
+// region, unused by the stream kernel
+__device__ __forceinline__ float *e2part_of(uint8_t *smem, const RowLayoutSm &SL) {
+  return reinterpret_cast<float *>(smem + SL.wbarm);
+}
 constexpr uint32_t kSAStageBytes = kRR * 32 * kSAK;
 
 struct StreamParams {
@@ -956,9 +1006,10 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
     mbar_init(&B.g1_done, 1);
     mbar_init(&B.h_full, 2 * kRowThreads / 32);   // row warps + helper warps (E1 halves)
     mbar_init(&B.g2_done, 1);
-    mbar_init(&B.mu_full, kRowThreads / 32);
+    mbar_init(&B.mu_full, (ZP == 16 ? 2 : 1) * kRowThreads / 32);   // + the helpers' E2 half
     mbar_init(&B.g3_done, 1);
     mbar_init(&B.e3_done, kRowThreads / 32);
+    mbar_init(&B.e2_done, kRowThreads / 32);
     fence_mbar_init();
   }
   __syncthreads();
@@ -1097,7 +1148,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
       rows_epilogue<H, ZP, RowBars, decltype(no_sx) &, 2>(
           tmem, q4, lane, r, row0 + r, row0 + r < p.n, no_sx, region, mubuf, b1s, b3s, wbs, bmls, B,
           p.Z, p.D, p.bbar, nullptr, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr,
-          nullptr, nullptr, 0, 0, e3part_of(smem, SL));
+          nullptr, nullptr, 0, 0, e3part_of(smem, SL), e2part_of(smem, SL));
     } else {
       // ---------------- row threads: the fused ingest, window sums, the epilogues ----------------
       const int r = tid;
@@ -1169,7 +1220,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_stream_rows(const StreamParams
       rows_epilogue<H, ZP, RowBars, decltype(sx_get) &, 1>(
           tmem, warp, lane, r, row, valid, sx_get, region, mubuf, b1s, b3s, wbs, bmls, B, p.Z, p.D,
           p.bbar, p.scores, p.md, p.flags, 0.0, p.z_q_dev, tr, nullptr, nullptr, nullptr, nullptr, 0,
-          0, e3part_of(smem, SL));
+          0, e3part_of(smem, SL), e2part_of(smem, SL));
     }
   }
   tc_fence_before();
